@@ -1,0 +1,20 @@
+"""B200-native (sm_100a) implementation of the GMRES operator-apply hot path of
+the reference Laplace-Beltrami package `lapbel` (arXiv:2111.10743).
+
+The public names mirror `lapbel/__init__.py:37-50` for the hot path: the point
+sums (FmmSources, FmmResult, evaluate_direct, evaluate_fmm, FmmPlan), the
+operator set (LayerOperatorSet, DensityVector) and the solver (gmres,
+solve_laplace_beltrami, SolveConfig, SolveReport).  All arithmetic runs in
+libb200lb.so; there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .fmm import (FmmCapacityError, FmmPlan, FmmResult, FmmSources,
+                  evaluate_direct, evaluate_fmm, order_for_eps)
+from ._pointsum import run_grouped_direct
+
+__all__ = [
+    "FmmSources", "FmmResult", "FmmCapacityError", "FmmPlan",
+    "evaluate_direct", "evaluate_fmm", "order_for_eps", "run_grouped_direct",
+]

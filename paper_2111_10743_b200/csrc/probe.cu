@@ -1,0 +1,56 @@
+// Hardware probes used by bench.py / tests to state rooflines from measured
+// numbers: an FP64 FMA-pipe peak kernel and a dump of the MUFU.RSQ64H seed
+// (its accuracy decides how many refinement steps inv_sqrt_skip needs).
+#include "lb_common.cuh"
+
+namespace lb {
+
+// 8 independent DFMA chains per thread; each iteration = 8 DFMA = 16 flop
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+__global__ void rsqrt_seed_kernel(const double* x, double* y, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = rsqrt_seed(x[i]);
+}
+
+__global__ void inv_sqrt_kernel(const double* x, double* y, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = inv_sqrt_skip(x[i]);
+}
+
+}  // namespace lb
+
+extern "C" {
+
+// flops executed = blocks * 256 * iters * 16 * 8 * 2
+int lb_probe_dfma(double* scratch, int blocks, int iters, void* stream) {
+  lb::dfma_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 0.999999, 1e-7);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+// mode 0: raw MUFU.RSQ64H seed; mode 1: refined inv_sqrt_skip
+int lb_probe_rsqrt(const double* x, double* y, int64_t n, int mode, void* stream) {
+  if (n <= 0) return LB_OK;
+  unsigned g = (unsigned)lb::ceil_div(n, 256);
+  if (mode == 0)
+    lb::rsqrt_seed_kernel<<<g, 256, 0, lb::as_stream(stream)>>>(x, y, n);
+  else
+    lb::inv_sqrt_kernel<<<g, 256, 0, lb::as_stream(stream)>>>(x, y, n);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+}  // extern "C"
