@@ -81,6 +81,94 @@ int lb_p2p_grouped(const double* t_xyz, const int64_t* t_out,
                    double* grad, double* hess, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Operator set: the device-resident LayerOperatorSet (operators.py:70-273).
+ *
+ * Kernel-kind codes follow quadrature.py:47-55 (_KIND_CODES). */
+enum {
+  LB_KIND_S = 0,
+  LB_KIND_D = 1,
+  LB_KIND_SPRIME = 2,
+  LB_KIND_GRAD_S1 = 3,
+  LB_KIND_GRAD_S2 = 4,
+  LB_KIND_GRAD_S3 = 5,
+  LB_KIND_SPP_PLUS_DPRIME = 6,
+  LB_NKINDS = 7
+};
+
+/* Everything the apply consumes, as DEVICE pointers that must outlive the
+ * handle (they are not copied).  Geometry is SurfaceDiscretization's
+ * (surface.py:77-106): nodes/normals (n,3), weights/curvature (n),
+ * tangents_u/v (n,3) and inv_metric (n,2,2) (A1 only, may be NULL),
+ * over_nodes/over_normals (n_over,3), over_weights (n_over); over_interp is
+ * ReferenceElement.over_interp (nbo, nb) row-major (simplex.py:383); the
+ * corrections are the scipy CSR arrays of NearCorrections.matrix
+ * (quadrature.py:693-700) with ONE shared pattern (indptr int64 (n+1),
+ * indices int32 (nnz)) and one value array per kind, NULL for kinds not
+ * built.  weight_sum is the host value sum(weights).  phi0 = S[1]
+ * (operators.py:99-100) is needed by A1 only and may be set later. */
+typedef struct {
+  int64_t n, n_over, npatches;
+  int nb, nbo;
+  const double *nodes, *normals, *weights, *curvature;
+  const double *tangents_u, *tangents_v, *inv_metric;
+  const double *over_nodes, *over_normals, *over_weights, *over_interp;
+  int64_t nnz;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const double* corr[LB_NKINDS];
+  double weight_sum;
+  const double* phi0;
+} lb_opset_desc;
+
+typedef struct lb_opset lb_opset;
+
+/* Allocates the handle's scratch (packed far-field sources, partials, work
+ * vectors) once; synchronises the device once. */
+int lb_opset_create(const lb_opset_desc* desc, lb_opset** out);
+int lb_opset_destroy(lb_opset* h);
+int lb_opset_set_phi0(lb_opset* h, const double* phi0);
+/* out = A_f tau for formulation f in {1,2,3} (apply_a1/a2/a3,
+ * operators.py:161-266).  tau/out: device (n), must not alias.  Enqueued on
+ * `stream`; no host synchronisation; capturable in a CUDA graph.  Missing
+ * correction kind -> LB_ERR_KEY (operators.py:119-123). */
+int lb_opset_apply(lb_opset* h, int formulation, const double* tau,
+                   double* out, void* stream);
+/* out = corrected layer operator of `kind` applied to tau
+ * (apply_layer, operators.py:126-155). */
+int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau,
+                         double* out, void* stream);
+/* Copies the last W-average (eta / ws) the handle computed to dev_out. */
+int lb_opset_last_scalar(const lb_opset* h, double* dev_out);
+
+/* y_j (+)= A_j x_j for njobs <= 4 CSR matrices sharing one pattern
+ * (`corr(kind) @ v`, operators.py:119-123).  vals/xs/ys are HOST arrays of
+ * njobs DEVICE pointers. */
+int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows,
+                int njobs, const double* const* vals, const double* const* xs,
+                double* const* ys, int accumulate, void* stream);
+
+/* ------------------------------------------------------------------------
+ * GMRES vector kernels (solver.py:48-103).  Deterministic reductions: the
+ * scalars land in DEVICE memory, no host synchronisation.
+ *
+ * lb_arnoldi_mgs: modified Gram-Schmidt of v against rows 0..k of Q
+ * (row stride ldq):  for j = 0..k: h[j] = Q_j . v ; v -= h[j] Q_j
+ * (solver.py:75-77); then h[k+1] = ||v|| (solver.py:78) and, when
+ * h[k+1] > 0, Q_{k+1} = v / h[k+1] (solver.py:80-81).  h: device (k+2). */
+int lb_arnoldi_mgs(double* Q, int64_t ldq, int k, int64_t n, double* v,
+                   double* h, void* stream);
+/* x = sum_j y[j] Q_j, j < k (solver.py:102); y: device (k). */
+int lb_combine_rows(const double* Q, int64_t ldq, int k, int64_t n,
+                    const double* y, double* x, void* stream);
+/* out[0] = x . y  /  out[0] = ||x|| (device scalar) */
+int lb_dot(const double* x, const double* y, int64_t n, double* out,
+           void* stream);
+int lb_nrm2(const double* x, int64_t n, double* out, void* stream);
+/* y = x * (1 / s[0]) with s a device scalar (s == 0 leaves y unchanged) */
+int lb_scale_inv(const double* x, const double* s, int64_t n, double* y,
+                 void* stream);
+
+/* ------------------------------------------------------------------------
  * Hardware probes (no reference counterpart): FP64 FMA-pipe peak
  * (flops = blocks*256*iters*256) and the 1/sqrt seed/refinement, used to state
  * the measured fp64 roofline and the kernel's rsqrt accuracy. */

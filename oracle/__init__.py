@@ -15,3 +15,4 @@ vectors produced by running the reference itself (scripts/make_golden.py).
 """
 
 from .core import *  # noqa: F401,F403
+from .apply import OracleOperator, gmres, solve  # noqa: F401

@@ -38,6 +38,7 @@ def lib():
                                          I32]
         L.oracle_csr_matvec.argtypes = [_P, _P, _P, I64, _P, _P, I32, I32]
         L.oracle_max_threads.argtypes = []
+        L.oracle_spp_far.argtypes = [_P, _P, I64, _P, _P, _P, I64, _P, I32]
         _lib = L
     return _lib
 
@@ -115,3 +116,13 @@ def csr_matvec(indptr, indices, data, x, nthreads=0):
     lib().oracle_csr_matvec(_p(indptr), _p(indices), _p(data), len(y), _p(x),
                             _p(y), 0, nthreads)
     return y
+
+
+def spp_far(x, nx, y, ny, c, nthreads=0):
+    """Combined-form S''+D' far sum (kernels.py:60-67 kernel, no 4 pi)."""
+    x, nx, y, ny, c = (np.ascontiguousarray(a, dtype=float)
+                       for a in (x, nx, y, ny, c))
+    out = np.zeros(x.shape[0])
+    lib().oracle_spp_far(_p(x), _p(nx), x.shape[0], _p(y), _p(ny), _p(c),
+                         y.shape[0], _p(out), nthreads)
+    return out

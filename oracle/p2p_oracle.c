@@ -171,3 +171,35 @@ int oracle_csr_matvec(const int64_t* indptr, const int32_t* indices,
   }
   return 0;
 }
+
+/* The S''+D' far kernel in the combined form of kernels.py:60-67 (no 1/4pi):
+ *   out_i = sum_j c_j (3 (nx.r)((nx-ny).r)/r^2 - nx.(nx-ny)) / r^3,
+ * r = x_i - y_j, r == 0 skipped.  Algebraically equal to the reference's
+ * separate n.H(charge).n + n.grad(dipole c n_y) (operators.py:257-259) but
+ * without its 1/r^5 cancellation. */
+int oracle_spp_far(const double* x, const double* nx, int64_t nt,
+                   const double* y, const double* ny, const double* c,
+                   int64_t ns, double* out, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t i = 0; i < nt; ++i) {
+    double acc = 0.0;
+    const double n0 = nx[3 * i], n1 = nx[3 * i + 1], n2 = nx[3 * i + 2];
+    for (int64_t j = 0; j < ns; ++j) {
+      const double r0 = x[3 * i] - y[3 * j], r1 = x[3 * i + 1] - y[3 * j + 1],
+                   r2 = x[3 * i + 2] - y[3 * j + 2];
+      const double rr = r0 * r0 + r1 * r1 + r2 * r2;
+      if (rr == 0.0) continue;
+      const double d0 = n0 - ny[3 * j], d1 = n1 - ny[3 * j + 1], d2 = n2 - ny[3 * j + 2];
+      const double rnx = r0 * n0 + r1 * n1 + r2 * n2;
+      const double rdn = r0 * d0 + r1 * d1 + r2 * d2;
+      const double ndn = n0 * d0 + n1 * d1 + n2 * d2;
+      const double invr = 1.0 / sqrt(rr);
+      acc += c[j] * (3.0 * rnx * rdn / rr - ndn) * (invr / rr);
+    }
+    out[i] = acc;
+  }
+  return 0;
+}

@@ -13,8 +13,15 @@ __version__ = "0.1.0"
 from .fmm import (FmmCapacityError, FmmPlan, FmmResult, FmmSources,
                   evaluate_direct, evaluate_fmm, order_for_eps)
 from ._pointsum import run_grouped_direct
+from .operators import (FORMULATIONS, CorrectionSet, DensityVector, Geometry,
+                        KernelKind, LayerOperatorSet, apply_layer)
+from .solver import (GmresBreakdown, SolveConfig, SolveReport, gmres,
+                     solve_laplace_beltrami)
 
 __all__ = [
     "FmmSources", "FmmResult", "FmmCapacityError", "FmmPlan",
     "evaluate_direct", "evaluate_fmm", "order_for_eps", "run_grouped_direct",
+    "KernelKind", "FORMULATIONS", "DensityVector", "Geometry", "CorrectionSet",
+    "LayerOperatorSet", "apply_layer", "SolveConfig", "SolveReport",
+    "GmresBreakdown", "gmres", "solve_laplace_beltrami",
 ]

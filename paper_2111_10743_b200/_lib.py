@@ -41,6 +41,18 @@ SIGNATURES = {
                _I32, _P],
     "lb_p2p_grouped": [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _I64, _I32,
                        _U32, _U32, _I32, _I64, _P, _P, _P, _P],
+    "lb_opset_create": [_P, _P],
+    "lb_opset_destroy": [_P],
+    "lb_opset_set_phi0": [_P, _P],
+    "lb_opset_apply": [_P, _I32, _P, _P, _P],
+    "lb_opset_apply_layer": [_P, _I32, _P, _P, _P],
+    "lb_opset_last_scalar": [_P, _P],
+    "lb_csr_spmv": [_P, _P, _I64, _I32, _P, _P, _P, _I32, _P],
+    "lb_arnoldi_mgs": [_P, _I64, _I32, _I64, _P, _P, _P],
+    "lb_combine_rows": [_P, _I64, _I32, _I64, _P, _P, _P],
+    "lb_dot": [_P, _P, _I64, _P, _P],
+    "lb_nrm2": [_P, _I64, _P, _P],
+    "lb_scale_inv": [_P, _P, _I64, _P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],
 }

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cmath>
 #include <string>
 
 #include "../../include/lapbel_b200.h"
@@ -70,6 +72,25 @@ struct Scratch {
 };
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Source-split factor for an all-pairs launch of `tiles` equal-work target
+// tiles over `src_tiles` source tiles with `slots` co-resident blocks: the
+// smallest split whose wave quantisation wastes < 3% (and that gives at least
+// two waves), so the last wave never idles most of the 148 SMs.
+inline int64_t choose_splits(int64_t tiles, int64_t src_tiles, int64_t slots) {
+  if (tiles <= 0 || src_tiles <= 1) return 1;
+  const int64_t cap = std::min<int64_t>(src_tiles, 4096);
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t s = 1; s <= cap; ++s) {
+    const int64_t units = tiles * s;
+    const double waves = (double)units / (double)slots;
+    const double eff = waves / std::ceil(waves);
+    if (units >= 2 * slots && eff >= 0.97) return s;
+    if (eff > best_eff + 1e-9 && units >= slots) { best = s; best_eff = eff; }
+  }
+  return best_eff > 0 ? best : cap;
+}
 
 // ---------------------------------------------------------------------------
 // fp64 1/sqrt(r2) with the coincident-pair skip of fmm.py:136-141 /

@@ -1,0 +1,895 @@
+// The GMRES operator apply on the device: LayerOperatorSet.apply_a1/a2/a3 and
+// apply_layer (operators.py:126-266) as a fixed sequence of fused kernels:
+//
+//   oversample  : tau -> w_over * (over_interp @ tau_patch)  written straight
+//                 into the packed far-field source records  (surface.py:370)
+//   far         : one tiled fp64 all-pairs sweep per FMM call of the
+//                 reference, computing ONLY the projections the operator
+//                 consumes (pot, n.grad, n.H.n + n.grad_dipole, ...) rather
+//                 than full grad/hess arrays (operators.py:237-259)
+//   csr + epi   : the near-correction SpMVs of one pass share one read of the
+//                 CSR pattern (all kinds share it, quadrature.py:693-700) and
+//                 the scalar glue (1/4pi, -tau/4, 2H S', W-average) runs in
+//                 the same kernel; the W-average is a deterministic grid
+//                 reduction published on the device
+//
+// Signs/ordering follow the reference code (not the paper text) where they
+// differ.
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "lb_common.cuh"
+#include "reduce.cuh"
+
+namespace lb {
+
+constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
+
+struct Tgt {
+  double x, y, z, nx, ny, nz, nn;
+};
+
+// ---------------------------------------------------------------------------
+// far-field pair functors.  r = t - s; every functor skips r == 0 through
+// inv_sqrt_skip.  Output j of functor F accumulates into a[j].
+
+#define LB_GEOM                                                     \
+  const double r0 = t.x - s[0], r1 = t.y - s[1], r2 = t.z - s[2];   \
+  const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));              \
+  const double invr = inv_sqrt_skip(rr);
+
+// S (pot only):  a0 += c/r                      record [x y z c]
+struct FarS {
+  static constexpr int S = 4, NOUT = 1;
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    a[0] = fma(s[3], invr, a[0]);
+  }
+};
+
+// A3 call 1 (operators.py:237): charge c, pot + n_t.grad.
+//   a0 += c/r ; a1 += c (n_t.r)/r^3   (n_t.grad = -a1)        record [x y z c]
+struct FarA3a {
+  static constexpr int S = 4, NOUT = 2;
+  static constexpr bool TN = true;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double ci = s[3] * invr;
+    const double ci3 = ci * (invr * invr);
+    a[0] += ci;
+    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
+    a[1] = fma(ci3, rnt, a[1]);
+  }
+};
+
+// S''+D' kernel times r^3: 3 (n_t.r)((n_t-n_s).r)/r^2 - n_t.(n_t-n_s)
+// (kernels.py:60-67), equal to n_t.hess(charge).n_t + n_t.grad(dipole n_s)
+#define LB_SPP(rnt, rns, ntns)                                               \
+  fma(3.0 * (rnt) * ((rnt) - (rns)), invr * invr, (ntns) - t.nn)
+
+// A3 call 2 (operators.py:247-259): charges c0 = w mu1, c1 = w mu2 and
+// dipole c1 n_s.   record [x y z nx ny nz c0 c1]
+//   a0 += c0 (n_t.r)/r^3   (sp_mu1 far = -a0)
+//   a1 += c1 / r           (s_mu2 far)
+//   a2 += c1 (n_t.r)/r^3   (sp_mu2 far = -a2)
+//   a3 += c1 Kspp/r^3      (sppdp_mu2 far)
+struct FarA3b {
+  static constexpr int S = 8, NOUT = 4;
+  static constexpr bool TN = true;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double invr3 = invr * (invr * invr);
+    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
+    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
+    const double ntns = fma(t.nz, s[5], fma(t.ny, s[4], t.nx * s[3]));
+    const double g = rnt * invr3;
+    a[0] = fma(s[6], g, a[0]);
+    a[1] = fma(s[7], invr, a[1]);
+    a[2] = fma(s[7], g, a[2]);
+    a[3] = fma(s[7] * invr3, LB_SPP(rnt, rns, ntns), a[3]);
+  }
+};
+
+// A2 call 1 (operators.py:200-212): charge c and dipole c n_s (c = w tau).
+//   a0 += c/r ; a1 += c (n_s.r)/r^3 (D) ; a2 += c (n_t.r)/r^3 ; a3 += c Kspp/r^3
+//   record [x y z nx ny nz c 0]
+struct FarA2a {
+  static constexpr int S = 8, NOUT = 4;
+  static constexpr bool TN = true;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double c = s[6];
+    const double ci = c * invr;
+    const double ci3 = ci * (invr * invr);
+    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
+    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
+    const double ntns = fma(t.nz, s[5], fma(t.ny, s[4], t.nx * s[3]));
+    a[0] += ci;
+    a[1] = fma(ci3, rns, a[1]);
+    a[2] = fma(ci3, rnt, a[2]);
+    a[3] = fma(ci3, LB_SPP(rnt, rns, ntns), a[3]);
+  }
+};
+
+// A2 call 2 (operators.py:216-223): dipole c0 n_s (c0 = w mu1), charge c1 = w mu2
+//   a0 += c0 (n_s.r)/r^3 ; a1 += c1/r      record [x y z nx ny nz c0 c1]
+struct FarA2b {
+  static constexpr int S = 8, NOUT = 2;
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
+    a[0] = fma(s[6] * rns, invr * (invr * invr), a[0]);
+    a[1] = fma(s[7], invr, a[1]);
+  }
+};
+
+// D alone (apply_layer DOUBLE_LAYER, operators.py:144-147): record [.. c0 ..]
+struct FarD {
+  static constexpr int S = 8, NOUT = 1;
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
+    a[0] = fma(s[6] * rns, invr * (invr * invr), a[0]);
+  }
+};
+
+// A1 call 1 (operators.py:167-171): charge c, pot + full gradient
+//   a0 += c/r ; a1..3 += c r/r^3  (grad = -a1..3)        record [x y z c]
+struct FarA1a {
+  static constexpr int S = 4, NOUT = 4;
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double ci = s[3] * invr;
+    const double ci3 = ci * (invr * invr);
+    a[0] += ci;
+    a[1] = fma(ci3, r0, a[1]);
+    a[2] = fma(ci3, r1, a[2]);
+    a[3] = fma(ci3, r2, a[3]);
+  }
+};
+
+// A1 call 2 (operators.py:181-185): three charges c_l = w mu_l, only the
+// divergence sum_l d_l u_l is consumed:  a0 += (c . r)/r^3 (div far = -a0)
+//   record [x y z c0 c1 c2]
+struct FarA1b {
+  static constexpr int S = 6, NOUT = 1;
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double cr = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
+    a[0] = fma(cr, invr * (invr * invr), a[0]);
+  }
+};
+
+#undef LB_GEOM
+
+// ---------------------------------------------------------------------------
+// tiled far kernel (same structure as p2p_tile_kernel)
+
+template <class F, int TPT, int BT, int TS>
+__global__ void __launch_bounds__(BT) opfar_kernel(const double* __restrict__ nodes,
+                                                   const double* __restrict__ normals, int64_t n,
+                                                   const double* __restrict__ pack,
+                                                   int64_t ns_pad, int64_t chunk,
+                                                   double* __restrict__ part) {
+  constexpr int S = F::S;
+  constexpr int NO = F::NOUT;
+  __shared__ __align__(16) double sh[TS * S];
+  const int64_t tbase = (int64_t)blockIdx.x * (BT * TPT) + threadIdx.x;
+  const int64_t s_begin = (int64_t)blockIdx.y * chunk;
+  const int64_t s_end = min(s_begin + chunk, ns_pad);
+  Tgt tg[TPT];
+  double acc[TPT][NO];
+#pragma unroll
+  for (int j = 0; j < TPT; ++j) {
+    const int64_t i = tbase + (int64_t)j * BT;
+    const bool in = i < n;
+    tg[j].x = in ? nodes[3 * i] : 0.0;
+    tg[j].y = in ? nodes[3 * i + 1] : 0.0;
+    tg[j].z = in ? nodes[3 * i + 2] : 0.0;
+    if (F::TN) {
+      tg[j].nx = in ? normals[3 * i] : 0.0;
+      tg[j].ny = in ? normals[3 * i + 1] : 0.0;
+      tg[j].nz = in ? normals[3 * i + 2] : 0.0;
+      tg[j].nn = fma(tg[j].nz, tg[j].nz, fma(tg[j].ny, tg[j].ny, tg[j].nx * tg[j].nx));
+    } else {
+      tg[j].nx = tg[j].ny = tg[j].nz = tg[j].nn = 0.0;
+    }
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
+  }
+  for (int64_t s0 = s_begin; s0 < s_end; s0 += TS) {
+    __syncthreads();
+    const double2* g = reinterpret_cast<const double2*>(pack + s0 * S);
+    double2* d = reinterpret_cast<double2*>(sh);
+#pragma unroll 4
+    for (int k = threadIdx.x; k < TS * S / 2; k += BT) d[k] = __ldg(g + k);
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < TS; ++k) {
+#pragma unroll
+      for (int j = 0; j < TPT; ++j) F::pair(tg[j], sh + k * S, acc[j]);
+    }
+  }
+  double* out = part + (int64_t)blockIdx.y * NO * n;
+#pragma unroll
+  for (int j = 0; j < TPT; ++j) {
+    const int64_t i = tbase + (int64_t)j * BT;
+    if (i < n) {
+#pragma unroll
+      for (int o = 0; o < NO; ++o) out[(int64_t)o * n + i] = acc[j][o];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// oversampling (interpolate_to_oversampled, surface.py:370-375) fused with the
+// over_weights scaling and the write into the packed source records.  One
+// block per patch.  Optionally adds a device scalar to input vector 0 in place
+// first (A2's W-average, operators.py:212).
+
+struct OvsArgs {
+  const double* in[3];
+  int slot[3];
+  int nv;
+  double* in0_add_target;  // == in[0] when the scalar must be added, else null
+  const double* add_scalar;
+  double* pack;
+  int S;
+  const double* w_over;
+  const double* oi;  // (nbo, nb)
+  int nb, nbo;
+};
+
+__global__ void __launch_bounds__(128) oversample_kernel(OvsArgs a) {
+  extern __shared__ double sv[];  // nv * nb
+  const int64_t p = blockIdx.x;
+  const int nb = a.nb;
+  for (int k = threadIdx.x; k < a.nv * nb; k += blockDim.x) {
+    const int v = k / nb, b = k - v * nb;
+    double x = a.in[v][p * nb + b];
+    if (v == 0 && a.in0_add_target) {
+      x += a.add_scalar[0];
+      a.in0_add_target[p * nb + b] = x;
+    }
+    sv[k] = x;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < a.nbo; o += blockDim.x) {
+    const double* row = a.oi + (int64_t)o * nb;
+    const int64_t gi = p * a.nbo + o;
+    const double w = a.w_over[gi];
+    for (int v = 0; v < a.nv; ++v) {
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s = fma(__ldg(row + b), sv[v * nb + b], s);
+      a.pack[gi * a.S + a.slot[v]] = w * s;
+    }
+  }
+}
+
+// fill geometry slots of a packed record buffer ([x y z] or [x y z nx ny nz])
+__global__ void fill_geom_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
+                                 int64_t ns, int64_t ns_pad, int S, double* __restrict__ pack) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns_pad) return;
+  double* r = pack + i * S;
+  for (int k = 0; k < S; ++k) r[k] = 0.0;
+  if (i >= ns) return;
+  r[0] = pos[3 * i];
+  r[1] = pos[3 * i + 1];
+  r[2] = pos[3 * i + 2];
+  if (nrm && S >= 8) {
+    r[3] = nrm[3 * i];
+    r[4] = nrm[3 * i + 1];
+    r[5] = nrm[3 * i + 2];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR multi-job SpMV with a fused epilogue: one warp per row; every job reads
+// the shared pattern once per nnz (repeated value/x reads of a pass hit L1).
+
+template <int J>
+struct CsrJobs {
+  const double* val[J];
+  const double* x[J];
+};
+
+constexpr int kCsrBT = 256;
+
+// sum of the far-kernel partials over source splits for output o of row i
+__device__ __forceinline__ double far_sum(const double* part, int nsplit, int nout, int o,
+                                          int64_t n, int64_t i) {
+  double s = 0.0;
+  for (int p = 0; p < nsplit; ++p) s += part[((int64_t)p * nout + o) * n + i];
+  return s;
+}
+
+struct EpiBase {
+  const double* part;
+  int nsplit, nout;
+  int64_t n;
+  __device__ double f(int o, int64_t i) const { return far_sum(part, nsplit, nout, o, n, i); }
+};
+
+// generic: y_j = (accumulate ? y_j : 0) + acc_j
+template <int J>
+struct EpiStore {
+  static constexpr bool kReduce = false;
+  double* y[J];
+  int accumulate;
+  __device__ double operator()(int64_t i, const double* acc) const {
+#pragma unroll
+    for (int j = 0; j < J; ++j) y[j][i] = (accumulate ? y[j][i] : 0.0) + acc[j];
+    return 0.0;
+  }
+};
+
+// apply_layer: y = sign * far_o / 4pi + C tau  (operators.py:155)
+struct EpiLayer : EpiBase {
+  static constexpr bool kReduce = false;
+  int o;
+  double sign;
+  double* y;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    return (y[i] = fma(sign * kInv4Pi, f(o, i), acc[0])), 0.0;
+  }
+};
+
+// A3 pass 1 (operators.py:239-241)
+struct EpiA3p1 : EpiBase {
+  static constexpr bool kReduce = false;
+  double *s_tau, *sp_tau;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    s_tau[i] = fma(f(0, i), kInv4Pi, acc[0]);
+    sp_tau[i] = fma(-f(1, i), kInv4Pi, acc[1]);
+    return 0.0;
+  }
+};
+
+// A3 pass 2 (operators.py:252-263) minus the eta term; reduces w * s_mu2
+struct EpiA3p2 : EpiBase {
+  static constexpr bool kReduce = true;
+  const double *tau, *curv, *w;
+  double* result;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double sp_mu1 = fma(-f(0, i), kInv4Pi, acc[0]);
+    const double s_mu2 = fma(f(1, i), kInv4Pi, acc[1]);
+    const double sp_mu2 = fma(-f(2, i), kInv4Pi, acc[2]);
+    const double sppdp_mu2 = fma(f(3, i), kInv4Pi, acc[3]);
+    result[i] = -tau[i] / 4.0 + sp_mu1 - sppdp_mu2 - 2.0 * curv[i] * sp_mu2;
+    return w[i] * s_mu2;
+  }
+};
+
+// A2 pass 1 (operators.py:204-212): mu1 = D tau, mu2 = -(S''+D')tau - 2H S'tau
+// (+ ws added by the next oversample); reduces w * s_tau
+struct EpiA2p1 : EpiBase {
+  static constexpr bool kReduce = true;
+  const double *curv, *w;
+  double *mu1, *mu2;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double s_tau = fma(f(0, i), kInv4Pi, acc[0]);
+    const double d_tau = fma(f(1, i), kInv4Pi, acc[1]);
+    const double sp_tau = fma(-f(2, i), kInv4Pi, acc[2]);
+    const double sppdp_tau = fma(f(3, i), kInv4Pi, acc[3]);
+    mu1[i] = d_tau;
+    mu2[i] = -sppdp_tau - 2.0 * curv[i] * sp_tau;
+    return w[i] * s_tau;
+  }
+};
+
+// A2 pass 2 (operators.py:222-224)
+struct EpiA2p2 : EpiBase {
+  static constexpr bool kReduce = false;
+  const double* tau;
+  double* result;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double d_mu1 = fma(f(0, i), kInv4Pi, acc[0]);
+    const double s_mu2 = fma(f(1, i), kInv4Pi, acc[1]);
+    result[i] = -tau[i] / 4.0 + s_mu2 + d_mu1;
+    return 0.0;
+  }
+};
+
+// A1 pass 1 (operators.py:169-179): s_tau for eta, grad S tau, tangential
+// projection mu = g^{ij} x_i x_j . grad; reduces w * s_tau
+struct EpiA1p1 : EpiBase {
+  static constexpr bool kReduce = true;
+  const double *tu, *tv, *gi, *w;
+  double *mux, *muy, *muz;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double s_tau = fma(f(0, i), kInv4Pi, acc[0]);
+    const double gx = fma(-f(1, i), kInv4Pi, acc[1]);
+    const double gy = fma(-f(2, i), kInv4Pi, acc[2]);
+    const double gz = fma(-f(3, i), kInv4Pi, acc[3]);
+    const double* u = tu + 3 * i;
+    const double* v = tv + 3 * i;
+    const double* g = gi + 4 * i;
+    const double gu = gx * u[0] + gy * u[1] + gz * u[2];
+    const double gv = gx * v[0] + gy * v[1] + gz * v[2];
+    const double a = g[0] * gu + g[1] * gv;
+    const double b = g[2] * gu + g[3] * gv;
+    mux[i] = a * u[0] + b * v[0];
+    muy[i] = a * u[1] + b * v[1];
+    muz[i] = a * u[2] + b * v[2];
+    return w[i] * s_tau;
+  }
+};
+
+// A1 pass 2 (operators.py:181-187): div + eta * phi0
+struct EpiA1p2 : EpiBase {
+  static constexpr bool kReduce = false;
+  const double *phi0, *eta;
+  double* result;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double div_far = -f(0, i) * kInv4Pi;
+    double div = 0.0;
+    div += div_far + acc[0];
+    div += acc[1];
+    div += acc[2];
+    result[i] = div + eta[0] * phi0[i];
+    return 0.0;
+  }
+};
+
+template <int J, class E>
+__global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
+                                                         const int32_t* __restrict__ indices,
+                                                         int64_t nrows, CsrJobs<J> jobs, E epi,
+                                                         double* partials, unsigned* ticket,
+                                                         double* red_out, double red_div) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (kCsrBT / 32) + (threadIdx.x >> 5);
+  double red = 0.0;
+  if (row < nrows) {
+    double acc[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] = 0.0;
+    const int64_t kb = indptr[row], ke = indptr[row + 1];
+    for (int64_t k = kb + lane; k < ke; k += 32) {
+      const int c = __ldg(indices + k);
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(__ldg(jobs.val[j] + k), __ldg(jobs.x[j] + c), acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    }
+    if (lane == 0) red = epi(row, acc);
+  }
+  if constexpr (E::kReduce) grid_reduce_finish<kCsrBT>(red, partials, ticket, red_out, 0, red_div);
+}
+
+__global__ void add_scalar_kernel(double* y, int64_t n, const double* s) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += s[0];
+}
+
+}  // namespace lb
+
+// ===========================================================================
+// the operator-set handle
+
+struct lb_opset {
+  lb_opset_desc d;
+  double wsum = 0.0;
+  int64_t ns_pad = 0;
+  double* pack4 = nullptr;  // [x y z c]
+  double* pack6 = nullptr;  // [x y z c0 c1 c2]
+  double* pack8 = nullptr;  // [x y z nx ny nz c0 c1]
+  double* part = nullptr;
+  int64_t part_cap = 0;
+  double* vec = nullptr;  // 8 work vectors of length n
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  double* scal = nullptr;  // [0] W-average / eta
+  int csr_blocks = 0;
+};
+
+namespace lb {
+namespace {
+
+constexpr int kFarBT = 128;
+constexpr int kFarTS = 128;
+
+template <class F>
+constexpr int far_tpt() {
+  return F::NOUT <= 2 && F::S <= 4 ? 2 : 1;
+}
+
+template <class F>
+int far_splits(const lb_opset* h) {
+  constexpr int TPT = far_tpt<F>();
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int b = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, opfar_kernel<F, TPT, kFarBT, kFarTS>, kFarBT, 0);
+    per_sm = std::max(b, 1);
+  }
+  const int64_t tiles = ceil_div(h->d.n, (int64_t)kFarBT * TPT);
+  return (int)choose_splits(tiles, h->ns_pad / kFarTS, (int64_t)sm_count() * per_sm);
+}
+
+template <class F>
+int run_far(const lb_opset* h, const double* pack, int* nsplit_out, cudaStream_t st) {
+  constexpr int TPT = far_tpt<F>();
+  const int64_t n = h->d.n;
+  const int64_t tiles = ceil_div(n, (int64_t)kFarBT * TPT);
+  const int64_t src_tiles = h->ns_pad / kFarTS;
+  int64_t splits = far_splits<F>(h);
+  const int64_t chunk = ceil_div(src_tiles, splits) * kFarTS;
+  splits = ceil_div(h->ns_pad, chunk);
+  if (splits * F::NOUT * n > h->part_cap) return fail(LB_ERR_ARG, "opset: partial buffer too small");
+  dim3 grid((unsigned)tiles, (unsigned)splits);
+  opfar_kernel<F, TPT, kFarBT, kFarTS><<<grid, kFarBT, 0, st>>>(h->d.nodes, h->d.normals, n, pack,
+                                                                h->ns_pad, chunk, h->part);
+  LB_CHECK_LAUNCH();
+  *nsplit_out = (int)splits;
+  return LB_OK;
+}
+
+int oversample(const lb_opset* h, int nv, const double* const* in, const int* slot, double* pack,
+               int S, bool add_ws, cudaStream_t st) {
+  OvsArgs a{};
+  for (int v = 0; v < nv; ++v) {
+    a.in[v] = in[v];
+    a.slot[v] = slot[v];
+  }
+  a.nv = nv;
+  a.in0_add_target = add_ws ? const_cast<double*>(in[0]) : nullptr;
+  a.add_scalar = h->scal;
+  a.pack = pack;
+  a.S = S;
+  a.w_over = h->d.over_weights;
+  a.oi = h->d.over_interp;
+  a.nb = h->d.nb;
+  a.nbo = h->d.nbo;
+  oversample_kernel<<<(unsigned)h->d.npatches, 128, sizeof(double) * nv * h->d.nb, st>>>(a);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+template <int J, class E>
+int run_csr(const lb_opset* h, const double* const* vals, const double* const* xs, const E& epi,
+            cudaStream_t st, double red_div = 1.0) {
+  CsrJobs<J> jobs;
+  for (int j = 0; j < J; ++j) {
+    if (!vals[j]) return fail(LB_ERR_KEY, "opset: a required correction kind was not provided");
+    jobs.val[j] = vals[j];
+    jobs.x[j] = xs[j];
+  }
+  csr_epi_kernel<J, E><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
+      h->d.indptr, h->d.indices, h->d.n, jobs, epi, h->partials, h->ticket, h->scal, red_div);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+template <class E>
+E base_epi(const lb_opset* h, int nsplit, int nout) {
+  E e{};
+  e.part = h->part;
+  e.nsplit = nsplit;
+  e.nout = nout;
+  e.n = h->d.n;
+  return e;
+}
+
+double* V(const lb_opset* h, int k) { return h->vec + (int64_t)k * h->d.n; }
+
+int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
+  const auto* C = h->d.corr;
+  int ns1 = 0, ns2 = 0;
+  double* s_tau = V(h, 0);
+  double* sp_tau = V(h, 1);
+  {
+    const double* in[1] = {tau};
+    const int slot[1] = {3};
+    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
+  }
+  LB_TRY(run_far<FarA3a>(h, h->pack4, &ns1, st));
+  {
+    auto e = base_epi<EpiA3p1>(h, ns1, 2);
+    e.s_tau = s_tau;
+    e.sp_tau = sp_tau;
+    const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
+    const double* xs[2] = {tau, tau};
+    LB_TRY((run_csr<2>(h, vals, xs, e, st)));
+  }
+  {
+    const double* in[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
+    const int slot[2] = {6, 7};
+    LB_TRY(oversample(h, 2, in, slot, h->pack8, 8, false, st));
+  }
+  LB_TRY(run_far<FarA3b>(h, h->pack8, &ns2, st));
+  {
+    auto e = base_epi<EpiA3p2>(h, ns2, 4);
+    e.tau = tau;
+    e.curv = h->d.curvature;
+    e.w = h->d.weights;
+    e.result = out;
+    const double* vals[4] = {C[LB_KIND_SPRIME], C[LB_KIND_S], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+    const double* xs[4] = {sp_tau, s_tau, s_tau, s_tau};
+    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
+  }
+  add_scalar_kernel<<<(unsigned)ceil_div(h->d.n, 256), 256, 0, st>>>(out, h->d.n, h->scal);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+int apply_a2(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
+  const auto* C = h->d.corr;
+  int ns1 = 0, ns2 = 0;
+  double* mu1 = V(h, 0);
+  double* mu2 = V(h, 1);
+  {
+    const double* in[1] = {tau};
+    const int slot[1] = {6};
+    LB_TRY(oversample(h, 1, in, slot, h->pack8, 8, false, st));
+  }
+  LB_TRY(run_far<FarA2a>(h, h->pack8, &ns1, st));
+  {
+    auto e = base_epi<EpiA2p1>(h, ns1, 4);
+    e.curv = h->d.curvature;
+    e.w = h->d.weights;
+    e.mu1 = mu1;
+    e.mu2 = mu2;
+    const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_D], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+    const double* xs[4] = {tau, tau, tau, tau};
+    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
+  }
+  {
+    // mu2 += ws in place (scal[0]), then both oversampled into pack8
+    const double* in[2] = {mu2, mu1};
+    const int slot[2] = {7, 6};
+    LB_TRY(oversample(h, 2, in, slot, h->pack8, 8, true, st));
+  }
+  LB_TRY(run_far<FarA2b>(h, h->pack8, &ns2, st));
+  {
+    auto e = base_epi<EpiA2p2>(h, ns2, 2);
+    e.tau = tau;
+    e.result = out;
+    const double* vals[2] = {C[LB_KIND_D], C[LB_KIND_S]};
+    const double* xs[2] = {mu1, mu2};
+    LB_TRY((run_csr<2>(h, vals, xs, e, st)));
+  }
+  return LB_OK;
+}
+
+int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
+  const auto* C = h->d.corr;
+  if (!h->d.tangents_u || !h->d.tangents_v || !h->d.inv_metric || !h->d.phi0)
+    return fail(LB_ERR_ARG, "opset: A1 needs tangents, inverse metric and phi0");
+  int ns1 = 0, ns2 = 0;
+  double* mux = V(h, 0);
+  double* muy = V(h, 1);
+  double* muz = V(h, 2);
+  {
+    const double* in[1] = {tau};
+    const int slot[1] = {3};
+    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
+  }
+  LB_TRY(run_far<FarA1a>(h, h->pack4, &ns1, st));
+  {
+    auto e = base_epi<EpiA1p1>(h, ns1, 4);
+    e.tu = h->d.tangents_u;
+    e.tv = h->d.tangents_v;
+    e.gi = h->d.inv_metric;
+    e.w = h->d.weights;
+    e.mux = mux;
+    e.muy = muy;
+    e.muz = muz;
+    const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
+    const double* xs[4] = {tau, tau, tau, tau};
+    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
+  }
+  {
+    const double* in[3] = {mux, muy, muz};
+    const int slot[3] = {3, 4, 5};
+    LB_TRY(oversample(h, 3, in, slot, h->pack6, 6, false, st));
+  }
+  LB_TRY(run_far<FarA1b>(h, h->pack6, &ns2, st));
+  {
+    auto e = base_epi<EpiA1p2>(h, ns2, 1);
+    e.phi0 = h->d.phi0;
+    e.eta = h->scal;
+    e.result = out;
+    const double* vals[3] = {C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
+    const double* xs[3] = {mux, muy, muz};
+    LB_TRY((run_csr<3>(h, vals, xs, e, st)));
+  }
+  return LB_OK;
+}
+
+int apply_layer(lb_opset* h, int kind, const double* tau, double* out, cudaStream_t st) {
+  if (kind < 0 || kind >= LB_NKINDS) return fail(LB_ERR_ARG, "opset: unknown kernel kind");
+  const double* val = h->d.corr[kind];
+  if (!val) return fail(LB_ERR_KEY, "opset: corrections for this kind were not built");
+  int ns = 0, nout = 1, o = 0;
+  double sign = 1.0;
+  if (kind == LB_KIND_S || kind == LB_KIND_SPRIME ||
+      (kind >= LB_KIND_GRAD_S1 && kind <= LB_KIND_GRAD_S3)) {
+    const double* in[1] = {tau};
+    const int slot[1] = {3};
+    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
+    if (kind == LB_KIND_S) {
+      LB_TRY(run_far<FarS>(h, h->pack4, &ns, st));
+    } else if (kind == LB_KIND_SPRIME) {
+      LB_TRY(run_far<FarA3a>(h, h->pack4, &ns, st));
+      nout = 2; o = 1; sign = -1.0;
+    } else {
+      LB_TRY(run_far<FarA1a>(h, h->pack4, &ns, st));
+      nout = 4; o = 1 + (kind - LB_KIND_GRAD_S1); sign = -1.0;
+    }
+  } else {
+    const double* in[1] = {tau};
+    const int slot[1] = {6};
+    LB_TRY(oversample(h, 1, in, slot, h->pack8, 8, false, st));
+    if (kind == LB_KIND_D) {
+      LB_TRY(run_far<FarD>(h, h->pack8, &ns, st));
+    } else {  // S'' + D'
+      LB_TRY(run_far<FarA2a>(h, h->pack8, &ns, st));
+      nout = 4; o = 3;
+    }
+  }
+  auto e = base_epi<EpiLayer>(h, ns, nout);
+  e.o = o;
+  e.sign = sign;
+  e.y = out;
+  const double* vals[1] = {val};
+  const double* xs[1] = {tau};
+  return run_csr<1>(h, vals, xs, e, st);
+}
+
+}  // namespace
+}  // namespace lb
+
+extern "C" {
+
+int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
+  using namespace lb;
+  if (!d || !out) return fail(LB_ERR_ARG, "lb_opset_create: null argument");
+  *out = nullptr;
+  if (d->n <= 0 || d->n_over <= 0 || d->npatches <= 0 || d->nb <= 0 || d->nbo <= 0)
+    return fail(LB_ERR_SHAPE, "lb_opset_create: empty discretisation");
+  if (d->n != d->npatches * d->nb || d->n_over != d->npatches * d->nbo)
+    return fail(LB_ERR_SHAPE, "lb_opset_create: n/n_over do not match npatches*nb/nbo");
+  if (!d->nodes || !d->normals || !d->weights || !d->curvature || !d->over_nodes ||
+      !d->over_normals || !d->over_weights || !d->over_interp || !d->indptr || !d->indices)
+    return fail(LB_ERR_ARG, "lb_opset_create: missing geometry or CSR pattern");
+  lb_opset* h = new lb_opset();
+  h->d = *d;
+  h->wsum = d->weight_sum;
+  const int64_t n = d->n;
+  h->ns_pad = ceil_div(d->n_over, kFarTS) * kFarTS;
+  int64_t maxsplit = 1;
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarS>(h) * (int64_t)FarS::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA3a>(h) * (int64_t)FarA3a::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA3b>(h) * (int64_t)FarA3b::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA2a>(h) * (int64_t)FarA2a::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA2b>(h) * (int64_t)FarA2b::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarD>(h) * (int64_t)FarD::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA1a>(h) * (int64_t)FarA1a::NOUT);
+  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA1b>(h) * (int64_t)FarA1b::NOUT);
+  // splits are recomputed per launch; allow for the ceil-div adjustment
+  h->part_cap = (maxsplit + 8) * n;
+  h->csr_blocks = (int)ceil_div(n, kCsrBT / 32);
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+  };
+  A((void**)&h->pack4, sizeof(double) * h->ns_pad * 4);
+  A((void**)&h->pack6, sizeof(double) * h->ns_pad * 6);
+  A((void**)&h->pack8, sizeof(double) * h->ns_pad * 8);
+  A((void**)&h->part, sizeof(double) * h->part_cap);
+  A((void**)&h->vec, sizeof(double) * n * 8);
+  A((void**)&h->partials, sizeof(double) * (h->csr_blocks + 32));
+  A((void**)&h->ticket, sizeof(unsigned) * 4);
+  A((void**)&h->scal, sizeof(double) * 8);
+  if (e == cudaSuccess) e = cudaMemset(h->ticket, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(h->scal, 0, sizeof(double) * 8);
+  if (e != cudaSuccess) {
+    lb_opset_destroy(h);
+    return fail(LB_ERR_CUDA, std::string("lb_opset_create: ") + cudaGetErrorString(e));
+  }
+  const unsigned g = (unsigned)ceil_div(h->ns_pad, 256);
+  fill_geom_kernel<<<g, 256>>>(d->over_nodes, nullptr, d->n_over, h->ns_pad, 4, h->pack4);
+  fill_geom_kernel<<<g, 256>>>(d->over_nodes, nullptr, d->n_over, h->ns_pad, 6, h->pack6);
+  fill_geom_kernel<<<g, 256>>>(d->over_nodes, d->over_normals, d->n_over, h->ns_pad, 8, h->pack8);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    lb_opset_destroy(h);
+    return fail(LB_ERR_CUDA, std::string("lb_opset_create: ") + cudaGetErrorString(e));
+  }
+  *out = h;
+  return LB_OK;
+}
+
+int lb_opset_destroy(lb_opset* h) {
+  if (!h) return LB_OK;
+  cudaFree(h->pack4);
+  cudaFree(h->pack6);
+  cudaFree(h->pack8);
+  cudaFree(h->part);
+  cudaFree(h->vec);
+  cudaFree(h->partials);
+  cudaFree(h->ticket);
+  cudaFree(h->scal);
+  delete h;
+  return LB_OK;
+}
+
+int lb_opset_set_phi0(lb_opset* h, const double* phi0) {
+  if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_phi0: null handle");
+  h->d.phi0 = phi0;
+  return LB_OK;
+}
+
+int lb_opset_apply(lb_opset* h, int formulation, const double* tau, double* out, void* stream) {
+  using namespace lb;
+  if (!h || !tau || !out) return fail(LB_ERR_ARG, "lb_opset_apply: null argument");
+  if (tau == out) return fail(LB_ERR_ARG, "lb_opset_apply: tau and out must not alias");
+  cudaStream_t st = as_stream(stream);
+  switch (formulation) {
+    case 1: return apply_a1(h, tau, out, st);
+    case 2: return apply_a2(h, tau, out, st);
+    case 3: return apply_a3(h, tau, out, st);
+    default: return fail(LB_ERR_ARG, "lb_opset_apply: formulation must be 1, 2 or 3");
+  }
+}
+
+int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau, double* out, void* stream) {
+  using namespace lb;
+  if (!h || !tau || !out) return fail(LB_ERR_ARG, "lb_opset_apply_layer: null argument");
+  if (tau == out) return fail(LB_ERR_ARG, "lb_opset_apply_layer: tau and out must not alias");
+  return apply_layer(h, kind, tau, out, as_stream(stream));
+}
+
+int lb_opset_last_scalar(const lb_opset* h, double* dev_out) {
+  if (!h || !dev_out) return lb::fail(LB_ERR_ARG, "lb_opset_last_scalar: null argument");
+  LB_CUDA(cudaMemcpy(dev_out, h->scal, sizeof(double), cudaMemcpyDeviceToDevice));
+  return LB_OK;
+}
+
+int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, int njobs,
+                const double* const* vals, const double* const* xs, double* const* ys,
+                int accumulate, void* stream) {
+  using namespace lb;
+  if (njobs < 1 || njobs > 4) return fail(LB_ERR_ARG, "lb_csr_spmv: njobs must be in [1, 4]");
+  if (nrows <= 0) return LB_OK;
+  cudaStream_t st = as_stream(stream);
+  const unsigned blocks = (unsigned)ceil_div(nrows, kCsrBT / 32);
+#define LB_SPMV(J)                                                                          \
+  {                                                                                         \
+    CsrJobs<J> jobs;                                                                        \
+    EpiStore<J> epi;                                                                        \
+    for (int j = 0; j < J; ++j) {                                                           \
+      jobs.val[j] = vals[j];                                                                \
+      jobs.x[j] = xs[j];                                                                    \
+      epi.y[j] = ys[j];                                                                     \
+    }                                                                                       \
+    epi.accumulate = accumulate;                                                            \
+    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, nrows, jobs, \
+                                                              epi, nullptr, nullptr,        \
+                                                              nullptr, 1.0);                \
+  }
+  switch (njobs) {
+    case 1: LB_SPMV(1) break;
+    case 2: LB_SPMV(2) break;
+    case 3: LB_SPMV(3) break;
+    default: LB_SPMV(4) break;
+  }
+#undef LB_SPMV
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+}  // extern "C"

@@ -249,9 +249,7 @@ int run_direct_chunk(const double* tgt, int64_t nt, const double* src, int64_t n
   per_sm = std::max(per_sm, 1);
   const int64_t tiles = ceil_div(nt, (int64_t)kBT * TPT);
   const int64_t src_tiles = ns_pad / kTS;
-  const int64_t want = (int64_t)sm_count() * per_sm * 2;
-  int64_t splits = std::min<int64_t>(std::max<int64_t>(ceil_div(want, tiles), 1), src_tiles);
-  splits = std::min<int64_t>(splits, 65535);
+  int64_t splits = choose_splits(tiles, src_tiles, (int64_t)sm_count() * per_sm);
   const int64_t chunk = ceil_div(src_tiles, splits) * kTS;
   splits = ceil_div(ns_pad, chunk);
 

@@ -1,0 +1,509 @@
+"""The device-resident layer-operator set: drop-in for lapbel.operators
+(`/root/reference/pkg/src/lapbel/operators.py`).
+
+`LayerOperatorSet(disc, formulation, eps, ...)` keeps the reference's
+constructor, attributes (`disc`, `formulation`, `eps`, `near`, `corrections`,
+`t_q`, `t_mv_total`, `n_apply`, `phi0`) and methods (`apply`, `apply_a1/2/3`,
+`apply_layer`, `evaluate_solution`, `corr`).  The discretisation is
+duck-typed: the reference's own SurfaceDiscretization works, as does
+`Geometry` (the same attributes loaded from a bundle).  Corrections are the
+reference's CSR matrices (NearCorrections.matrix); building them is the
+reference's CPU precompute (compute_corrections, quadrature.py:663-701, out of
+scope here), so they are either passed in or built by the reference when it
+is importable.
+
+The apply itself is one C-ABI call (lb_opset_apply): oversampling, the two
+far-field sweeps (fp64, exact all-pairs), the near-correction SpMVs and the
+glue run as fused sm_100a kernels on one stream.  Inputs may be numpy (result
+returned as numpy, like the reference) or CUDA tensors (result stays on the
+device, nothing synchronised).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["KernelKind", "FORMULATIONS", "DensityVector", "Geometry",
+           "CorrectionSet", "LayerOperatorSet", "apply_layer", "FOUR_PI"]
+
+FOUR_PI = 4.0 * np.pi  # kernels.py:16
+
+
+class KernelKind(Enum):
+    """Same members and values as kernels.py:25-32."""
+
+    SINGLE_LAYER = "s"
+    DOUBLE_LAYER = "d"
+    SPRIME = "sprime"
+    GRAD_S1 = "grads1"
+    GRAD_S2 = "grads2"
+    GRAD_S3 = "grads3"
+    SPP_PLUS_DPRIME = "spp_plus_dprime"
+
+
+# quadrature.py:47-55 codes == include/lapbel_b200.h LB_KIND_*
+KIND_CODE = {
+    KernelKind.SINGLE_LAYER: 0, KernelKind.DOUBLE_LAYER: 1,
+    KernelKind.SPRIME: 2, KernelKind.GRAD_S1: 3, KernelKind.GRAD_S2: 4,
+    KernelKind.GRAD_S3: 5, KernelKind.SPP_PLUS_DPRIME: 6,
+}
+
+FORMULATIONS = {  # operators.py:36-44
+    "a1": (KernelKind.SINGLE_LAYER, KernelKind.GRAD_S1, KernelKind.GRAD_S2,
+           KernelKind.GRAD_S3),
+    "a2": (KernelKind.SINGLE_LAYER, KernelKind.DOUBLE_LAYER,
+           KernelKind.SPRIME, KernelKind.SPP_PLUS_DPRIME),
+    "a3": (KernelKind.SINGLE_LAYER, KernelKind.SPRIME,
+           KernelKind.SPP_PLUS_DPRIME),
+}
+
+
+def as_kind(kind) -> KernelKind:
+    """Accept our KernelKind, the reference's KernelKind, or its value."""
+    if isinstance(kind, KernelKind):
+        return kind
+    return KernelKind(getattr(kind, "value", kind))
+
+
+@dataclass
+class DensityVector:
+    """N scalar samples at the discretization nodes (operators.py:47-57)."""
+
+    values: np.ndarray
+    role: str = "intermediate"
+
+    def __post_init__(self):
+        self.values = np.asarray(self.values, dtype=float).ravel()
+        if not np.all(np.isfinite(self.values)):
+            raise ValueError("density contains non-finite entries")
+
+
+def _values(density):
+    if isinstance(density, DensityVector):
+        return density.values
+    if _lib.is_torch(density):
+        return density.reshape(-1)
+    return np.asarray(density, dtype=float).ravel()
+
+
+# ---------------------------------------------------------------------------
+# inputs
+
+
+@dataclass
+class Geometry:
+    """The SurfaceDiscretization arrays the apply consumes (surface.py:77-106)
+    plus ReferenceElement.over_interp (simplex.py:383)."""
+
+    order: int
+    nodes: np.ndarray
+    normals: np.ndarray
+    weights: np.ndarray
+    curvature: np.ndarray
+    over_nodes: np.ndarray
+    over_normals: np.ndarray
+    over_weights: np.ndarray
+    over_interp: np.ndarray
+    tangents_u: np.ndarray | None = None
+    tangents_v: np.ndarray | None = None
+    inv_metric: np.ndarray | None = None
+    node_patch: np.ndarray | None = None
+    metadata: dict = field(default_factory=dict)
+
+    @property
+    def nnodes(self):
+        return self.nodes.shape[0]
+
+    @property
+    def noversampled(self):
+        return self.over_nodes.shape[0]
+
+    @property
+    def nodes_per_patch(self):
+        return self.over_interp.shape[1]
+
+    @property
+    def npatches(self):
+        return self.nnodes // self.nodes_per_patch
+
+    @property
+    def area(self):
+        return float(np.sum(self.weights))
+
+    @classmethod
+    def from_arrays(cls, arrs, prefix=""):
+        g = lambda k: np.asarray(arrs[prefix + k]) if prefix + k in arrs \
+            else None  # noqa: E731
+        return cls(order=int(g("order")), nodes=g("nodes"),
+                   normals=g("normals"), weights=g("weights"),
+                   curvature=g("curvature"), over_nodes=g("over_nodes"),
+                   over_normals=g("over_normals"),
+                   over_weights=g("over_weights"),
+                   over_interp=g("over_interp"), tangents_u=g("tangents_u"),
+                   tangents_v=g("tangents_v"), inv_metric=g("inv_metric"),
+                   node_patch=g("node_patch"))
+
+
+def _over_interp(disc):
+    oi = getattr(disc, "over_interp", None)
+    if oi is not None:
+        return np.asarray(oi, dtype=float)
+    try:  # the reference's own element (host precompute, simplex.py:383)
+        from lapbel.simplex import reference_element
+    except ImportError as exc:  # pragma: no cover
+        raise ValueError("disc has no over_interp and lapbel is not "
+                         "importable to build it") from exc
+    return reference_element(disc.order).over_interp
+
+
+class CorrectionSet:
+    """Near corrections of several kinds on ONE shared CSR pattern
+    (quadrature.py:693-700): indptr (int64), indices (int32), values per kind.
+    Built from the reference's NearCorrections / scipy CSR matrices."""
+
+    def __init__(self, indptr, indices, values: dict, shape=None):
+        self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+        self.indices = np.ascontiguousarray(indices, dtype=np.int32)
+        self.values = {as_kind(k): np.ascontiguousarray(v, dtype=float)
+                       for k, v in values.items()}
+        n = len(self.indptr) - 1
+        self.shape = shape or (n, n)
+        for k, v in self.values.items():
+            if v.shape != self.indices.shape:
+                raise ValueError(f"correction values for {k} do not match "
+                                 "the shared pattern")
+
+    @property
+    def nnz(self):
+        return int(self.indices.shape[0])
+
+    @classmethod
+    def from_matrices(cls, corrections: dict):
+        """corrections: kind -> NearCorrections | scipy sparse matrix."""
+        import scipy.sparse as sp
+        mats = {}
+        for k, c in corrections.items():
+            m = getattr(c, "matrix", c)
+            m = sp.csr_matrix(m)
+            m.sort_indices()
+            mats[as_kind(k)] = m
+        if not mats:
+            raise ValueError("no corrections given")
+        first = next(iter(mats.values()))
+        same = all(np.array_equal(m.indptr, first.indptr)
+                   and np.array_equal(m.indices, first.indices)
+                   for m in mats.values())
+        if not same:  # put every kind on the union pattern
+            pat = None
+            for m in mats.values():
+                p = (m != 0).astype(np.int8) + 0 * m.astype(np.int8)
+                pat = p if pat is None else (pat + p)
+            pat = sp.csr_matrix(pat)
+            pat.sort_indices()
+            vals = {}
+            for k, m in mats.items():
+                mm = m.tolil()
+                vals[k] = np.asarray(mm[pat.nonzero()]).ravel()
+            return cls(pat.indptr, pat.indices, vals, first.shape)
+        return cls(first.indptr, first.indices,
+                   {k: m.data for k, m in mats.items()}, first.shape)
+
+    @classmethod
+    def from_arrays(cls, arrs, prefix="corr_"):
+        vals = {}
+        for kind in KernelKind:
+            key = prefix + kind.value
+            if key in arrs:
+                vals[kind] = np.asarray(arrs[key])
+        return cls(arrs[prefix + "indptr"], arrs[prefix + "indices"], vals)
+
+    def matrix(self, kind):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.values[as_kind(kind)], self.indices,
+                              self.indptr), shape=self.shape)
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_over", ctypes.c_int64),
+                ("npatches", ctypes.c_int64), ("nb", ctypes.c_int),
+                ("nbo", ctypes.c_int)] + \
+        [(nm, ctypes.c_void_p) for nm in (
+            "nodes", "normals", "weights", "curvature", "tangents_u",
+            "tangents_v", "inv_metric", "over_nodes", "over_normals",
+            "over_weights", "over_interp")] + \
+        [("nnz", ctypes.c_int64), ("indptr", ctypes.c_void_p),
+         ("indices", ctypes.c_void_p), ("corr", ctypes.c_void_p * 7),
+         ("weight_sum", ctypes.c_double), ("phi0", ctypes.c_void_p)]
+
+
+_Lib = None
+
+
+def _bind_opset():
+    global _Lib
+    if _Lib is None:
+        L = _lib.load()
+        P = ctypes.c_void_p
+        L.lb_opset_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(P)]
+        L.lb_opset_destroy.argtypes = [P]
+        L.lb_opset_set_phi0.argtypes = [P, P]
+        L.lb_opset_apply.argtypes = [P, ctypes.c_int, P, P, P]
+        L.lb_opset_apply_layer.argtypes = [P, ctypes.c_int, P, P, P]
+        L.lb_opset_last_scalar.argtypes = [P, P]
+        _Lib = L
+    return _Lib
+
+
+class DeviceOperator:
+    """Owner of the device arrays and the lb_opset handle (C ABI)."""
+
+    def __init__(self, disc, corrections: CorrectionSet, kinds):
+        t = _lib.require_cuda()
+        L = _bind_opset()
+        oi = _over_interp(disc)
+        nbo, nb = oi.shape
+        n = disc.nodes.shape[0]
+        nover = disc.over_nodes.shape[0]
+        dev = _lib.to_device
+        self.keep = {}
+
+        def put(name, a, dtype=None):
+            if a is None:
+                return None
+            x = dev(np.ascontiguousarray(a), dtype)
+            self.keep[name] = x
+            return x.data_ptr()
+
+        d = _Desc()
+        d.n, d.n_over, d.npatches, d.nb, d.nbo = n, nover, n // nb, nb, nbo
+        d.nodes = put("nodes", disc.nodes)
+        d.normals = put("normals", disc.normals)
+        d.weights = put("weights", disc.weights)
+        d.curvature = put("curvature", disc.curvature)
+        d.tangents_u = put("tangents_u", getattr(disc, "tangents_u", None))
+        d.tangents_v = put("tangents_v", getattr(disc, "tangents_v", None))
+        d.inv_metric = put("inv_metric", getattr(disc, "inv_metric", None))
+        d.over_nodes = put("over_nodes", disc.over_nodes)
+        d.over_normals = put("over_normals", disc.over_normals)
+        d.over_weights = put("over_weights", disc.over_weights)
+        d.over_interp = put("over_interp", oi)
+        d.nnz = corrections.nnz
+        d.indptr = put("indptr", corrections.indptr, t.int64)
+        d.indices = put("indices", corrections.indices, t.int32)
+        for kind in kinds:
+            if kind in corrections.values:
+                d.corr[KIND_CODE[kind]] = put("corr_" + kind.value,
+                                              corrections.values[kind])
+        d.weight_sum = float(np.sum(disc.weights))
+        d.phi0 = None
+        self.desc = d
+        self.n = n
+        h = ctypes.c_void_p()
+        _lib.check(L.lb_opset_create(ctypes.byref(d), ctypes.byref(h)),
+                   "lb_opset_create")
+        self.handle = h
+        self._L = L
+
+    def set_phi0(self, phi0_dev):
+        self.keep["phi0"] = phi0_dev
+        _lib.check(self._L.lb_opset_set_phi0(self.handle,
+                                             ctypes.c_void_p(phi0_dev.data_ptr())))
+
+    def apply(self, formulation: int, tau, out, stream=None):
+        _lib.check(self._L.lb_opset_apply(
+            self.handle, formulation, ctypes.c_void_p(tau.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _lib.stream_handle(stream)),
+            "lb_opset_apply")
+
+    def apply_layer(self, kind: KernelKind, tau, out, stream=None):
+        _lib.check(self._L.lb_opset_apply_layer(
+            self.handle, KIND_CODE[kind], ctypes.c_void_p(tau.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _lib.stream_handle(stream)),
+            "lb_opset_apply_layer")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._L.lb_opset_destroy(h)
+            except Exception:  # pragma: no cover - interpreter teardown
+                pass
+            self.handle = None
+
+
+_FORM_CODE = {"a1": 1, "a2": 2, "a3": 3}
+
+
+class LayerOperatorSet:
+    """Corrections + geometry + far-field machinery for one formulation
+    (operators.py:70-273), resident on the B200.
+
+    Extra keyword arguments beyond the reference's:
+      corrections : dict kind -> NearCorrections/CSR, or a CorrectionSet;
+                    when None the reference's compute_corrections builds
+                    them (requires lapbel to be importable).
+    """
+
+    def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
+                 use_fmm: bool = True, near=None, extra_kinds=(),
+                 corrections=None):
+        self.disc = disc
+        self.formulation = formulation.lower()
+        if self.formulation not in FORMULATIONS:
+            raise ValueError(f"unknown formulation {formulation!r}")
+        self.eps = float(eps)
+        self.use_fmm = use_fmm
+        kinds = list(dict.fromkeys(
+            list(FORMULATIONS[self.formulation])
+            + [as_kind(k) for k in extra_kinds]))
+        self.kinds = kinds
+        self.t_q = 0.0
+        if corrections is None:
+            corrections, self.near, self.t_q = _reference_corrections(
+                disc, kinds, self.eps, eta, near)
+        else:
+            self.near = near
+        if not isinstance(corrections, CorrectionSet):
+            corrections = CorrectionSet.from_matrices(corrections)
+        self._cset = corrections
+        self.corrections = {k: _CorrView(corrections, k)
+                            for k in corrections.values if k in kinds}
+        self.t_mv_total = 0.0
+        self.n_apply = 0
+        self.dev = DeviceOperator(disc, corrections, kinds)
+        n = disc.nodes.shape[0]
+        self._n = n
+        self._out = _lib.empty((n,))
+        # S[1], stored once for the SWS term of A1 (operators.py:99-100)
+        if KernelKind.SINGLE_LAYER in corrections.values:
+            ones = _lib.to_device(np.ones(n))
+            phi0 = _lib.empty((n,))
+            self.dev.apply_layer(KernelKind.SINGLE_LAYER, ones, phi0)
+            self.dev.set_phi0(phi0)
+            self._phi0_dev = phi0
+        else:
+            self._phi0_dev = None
+
+    @property
+    def phi0(self):
+        return None if self._phi0_dev is None else \
+            self._phi0_dev.cpu().numpy()
+
+    @classmethod
+    def from_bundle(cls, arrs, formulation: str, eps: float | None = None):
+        """Build from a saved bundle (scripts/make_golden.py layout)."""
+        geom = Geometry.from_arrays(arrs)
+        cset = CorrectionSet.from_arrays(arrs)
+        e = float(arrs["eps"]) if eps is None and "eps" in arrs else eps
+        return cls(geom, formulation, e, corrections=cset)
+
+    # -- reference-compatible accessors -----------------------------------
+    def corr(self, kind):
+        kind = as_kind(kind)
+        if kind not in self.corrections:
+            raise KeyError(f"corrections for {kind} were not built "
+                           f"(formulation {self.formulation})")
+        return self._cset.matrix(kind)
+
+    # -- device entry points (torch in, torch out, no sync) ---------------
+    def apply_device(self, tau, out=None, stream=None):
+        out = _lib.empty((self._n,)) if out is None else out
+        self.dev.apply(_FORM_CODE[self.formulation], tau, out, stream)
+        return out
+
+    def apply_layer_device(self, kind, tau, out=None, stream=None):
+        out = _lib.empty((self._n,)) if out is None else out
+        self.dev.apply_layer(as_kind(kind), tau, out, stream)
+        return out
+
+    # -- reference API ------------------------------------------------------
+    def _run(self, fn, density):
+        tau = _values(density)
+        host = not _lib.is_torch(tau)
+        t0 = time.perf_counter()
+        x = _lib.to_device(tau)
+        if x.numel() != self._n:
+            raise ValueError("density has the wrong length")
+        out = fn(x)
+        res = out.cpu().numpy() if host else out
+        return res, t0
+
+    def apply(self, tau):
+        return getattr(self, f"apply_{self.formulation}")(tau)
+
+    def _apply_form(self, form, tau):
+        if self.formulation != form and not all(
+                k in self._cset.values for k in FORMULATIONS[form]):
+            raise KeyError(f"corrections for {form} were not built")
+        res, t0 = self._run(lambda x: self._apply_code(form, x), tau)
+        self.t_mv_total += time.perf_counter() - t0
+        self.n_apply += 1
+        return res
+
+    def _apply_code(self, form, x):
+        out = _lib.empty((self._n,))
+        self.dev.apply(_FORM_CODE[form], x, out)
+        return out
+
+    def apply_a1(self, tau):
+        return self._apply_form("a1", tau)
+
+    def apply_a2(self, tau):
+        return self._apply_form("a2", tau)
+
+    def apply_a3(self, tau):
+        return self._apply_form("a3", tau)
+
+    def apply_layer(self, kind, density):
+        kind = as_kind(kind)
+        res, _ = self._run(lambda x: self.apply_layer_device(kind, x), density)
+        return res
+
+    def evaluate_solution(self, sigma):
+        """u = S[sigma] (A1/A2) or S^2[sigma] (A3) (operators.py:268-273)."""
+        host = not _lib.is_torch(sigma)
+        x = _lib.to_device(_values(sigma))
+        u = self.apply_layer_device(KernelKind.SINGLE_LAYER, x)
+        if self.formulation == "a3":
+            u = self.apply_layer_device(KernelKind.SINGLE_LAYER, u)
+        return u.cpu().numpy() if host else u
+
+
+class _CorrView:
+    """Stand-in for NearCorrections (quadrature.py:505-512)."""
+
+    def __init__(self, cset, kind):
+        self._cset = cset
+        self.kind = kind
+
+    @property
+    def matrix(self):
+        return self._cset.matrix(self.kind)
+
+
+def _reference_corrections(disc, kinds, eps, eta, near):
+    try:
+        from lapbel.kernels import KernelKind as RefKind
+        from lapbel.quadrature import build_near_map, compute_corrections
+    except ImportError as exc:
+        raise ValueError(
+            "corrections must be passed in (building them is the reference's "
+            "CPU precompute, quadrature.py:663-701, and lapbel is not "
+            "importable here)") from exc
+    if near is None:
+        near = build_near_map(disc, eta)
+    ref_kinds = [RefKind(k.value) for k in kinds]
+    corrs, t_q = compute_corrections(disc, near, ref_kinds, eps)
+    return {as_kind(k): v for k, v in corrs.items()}, near, t_q
+
+
+def apply_layer(opset: LayerOperatorSet, kind, density) -> DensityVector:
+    """Module-level wrapper (operators.py:276-278)."""
+    return DensityVector(opset.apply_layer(as_kind(kind), density))
