@@ -28,7 +28,7 @@ namespace lb {
 constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
 
 struct Tgt {
-  double x, y, z, nx, ny, nz, nn;
+  double x, y, z, nx, ny, nz;
 };
 
 // ---------------------------------------------------------------------------
@@ -65,10 +65,19 @@ struct FarA3a {
   }
 };
 
-// S''+D' kernel times r^3: 3 (n_t.r)((n_t-n_s).r)/r^2 - n_t.(n_t-n_s)
-// (kernels.py:60-67), equal to n_t.hess(charge).n_t + n_t.grad(dipole n_s)
-#define LB_SPP(rnt, rns, ntns)                                               \
-  fma(3.0 * (rnt) * ((rnt) - (rns)), invr * invr, (ntns) - t.nn)
+// S''+D' kernel times r^3, in the form of kernels.py:60-67:
+//   3 (n_t.r)(dn.r)/r^2 - n_t.dn,   dn = n_t - n_s.
+// dn is formed FIRST: for nearby nodes n_t - n_s is exact (Sterbenz), so
+// n_t.dn = O(r^2) keeps its relative accuracy; the algebraically equal
+// |n_t|^2 - n_t.n_s (or the reference's separate n.H.n + n.grad_dipole,
+// operators.py:257-259) loses ~eps/r^2 of it.  The sum equals
+// n_t.hess(charge).n_t + n_t.grad(dipole n_s).
+#define LB_SPP_TERMS                                                       \
+  const double dn0 = t.nx - s[3], dn1 = t.ny - s[4], dn2 = t.nz - s[5];    \
+  const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));              \
+  const double rdn = fma(dn2, r2, fma(dn1, r1, dn0 * r0));                 \
+  const double ndn = fma(t.nz, dn2, fma(t.ny, dn1, t.nx * dn0));           \
+  const double kspp = fma(3.0 * rnt * rdn, invr * invr, -ndn);
 
 // A3 call 2 (operators.py:247-259): charges c0 = w mu1, c1 = w mu2 and
 // dipole c1 n_s.   record [x y z nx ny nz c0 c1]
@@ -82,14 +91,12 @@ struct FarA3b {
   __device__ static void pair(const Tgt& t, const double* s, double* a) {
     LB_GEOM
     const double invr3 = invr * (invr * invr);
-    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
-    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
-    const double ntns = fma(t.nz, s[5], fma(t.ny, s[4], t.nx * s[3]));
+    LB_SPP_TERMS
     const double g = rnt * invr3;
     a[0] = fma(s[6], g, a[0]);
     a[1] = fma(s[7], invr, a[1]);
     a[2] = fma(s[7], g, a[2]);
-    a[3] = fma(s[7] * invr3, LB_SPP(rnt, rns, ntns), a[3]);
+    a[3] = fma(s[7] * invr3, kspp, a[3]);
   }
 };
 
@@ -104,13 +111,12 @@ struct FarA2a {
     const double c = s[6];
     const double ci = c * invr;
     const double ci3 = ci * (invr * invr);
-    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
-    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
-    const double ntns = fma(t.nz, s[5], fma(t.ny, s[4], t.nx * s[3]));
+    LB_SPP_TERMS
+    const double rns = rnt - rdn;  // n_s.r
     a[0] += ci;
     a[1] = fma(ci3, rns, a[1]);
     a[2] = fma(ci3, rnt, a[2]);
-    a[3] = fma(ci3, LB_SPP(rnt, rns, ntns), a[3]);
+    a[3] = fma(ci3, kspp, a[3]);
   }
 };
 
@@ -197,9 +203,8 @@ __global__ void __launch_bounds__(BT) opfar_kernel(const double* __restrict__ no
       tg[j].nx = in ? normals[3 * i] : 0.0;
       tg[j].ny = in ? normals[3 * i + 1] : 0.0;
       tg[j].nz = in ? normals[3 * i + 2] : 0.0;
-      tg[j].nn = fma(tg[j].nz, tg[j].nz, fma(tg[j].ny, tg[j].ny, tg[j].nx * tg[j].nx));
     } else {
-      tg[j].nx = tg[j].ny = tg[j].nz = tg[j].nn = 0.0;
+      tg[j].nx = tg[j].ny = tg[j].nz = 0.0;
     }
 #pragma unroll
     for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;

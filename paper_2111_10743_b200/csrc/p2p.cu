@@ -337,6 +337,7 @@ int lb_p2p(const double* tgt, int64_t nt, const double* src, int64_t ns, const d
   if (nd <= 0 || nd > 32) return fail(LB_ERR_SHAPE, "lb_p2p: nd must be in [1, 32]");
   if (level < 0 || level > 2) return fail(LB_ERR_ARG, "lb_p2p: level must be 0, 1 or 2");
   if (nt < 0 || ns < 0) return fail(LB_ERR_SHAPE, "lb_p2p: negative sizes");
+  if (nt == 0) return LB_OK;
   if (!pot || (level >= 1 && !grad) || (level >= 2 && !hess))
     return fail(LB_ERR_ARG, "lb_p2p: missing output buffer for the requested level");
   if ((cmask && !charges) || (dmask && !dipoles))

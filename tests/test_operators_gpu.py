@@ -1,6 +1,10 @@
 """Device operator set (lb_opset_*) and GMRES (lb_arnoldi_mgs ...) vs
   (1) the CPU oracle evaluating the SAME arithmetic (combined S''+D' kernel):
-      kernel correctness, 1e-10 relative (summation order only);
+      kernel correctness.  Tolerance ORACLE_TOL = 1e-10 relative: these coarse
+      fixtures put oversampled nodes 2.5e-4 from targets, where n_t.r of an
+      almost tangent r keeps only eps/r^2 relative accuracy (S' sums move by
+      ~1e-11 between two correct fp64 summation orders); single-layer sums
+      match to 1e-12;
   (2) the reference's own outputs (golden vectors): bounded by the reference's
       measured cancellation noise in its S''+D' far sum (see
       tests/test_oracle_golden.py REF_NOISE).
@@ -17,6 +21,7 @@ from test_oracle_golden import REF_NOISE
 
 pytestmark = pytest.mark.gpu
 
+ORACLE_TOL = 1e-10
 FIXTURES = [("opset_sphere_o3.npz", ("a1", "a2", "a3")),
             ("opset_torus_o3.npz", ("a3",))]
 
@@ -37,7 +42,7 @@ def test_apply_vs_oracle_and_reference(cuda, fixture, forms):
     for form in forms:
         op = LayerOperatorSet.from_bundle(g, form)
         got = op.apply(g["tau"])
-        assert _rel(got, orc.apply(form, g["tau"])) < 1e-10, form
+        assert _rel(got, orc.apply(form, g["tau"])) < ORACLE_TOL, form
         assert _rel(got, g[f"{form}_apply"]) < REF_NOISE[form], form
         assert _rel(op.phi0, g[f"{form}_phi0"]) < 1e-12
         assert op.n_apply == 1
@@ -52,9 +57,10 @@ def test_apply_layer_every_kind(cuda, fixture, forms):
         op = LayerOperatorSet.from_bundle(g, form)
         for kind in op.corrections:
             got = op.apply_layer(kind, g["tau"])
-            assert _rel(got, orc.apply_layer(kind.value, g["tau"])) < 1e-10, kind
+            tol = 1e-12 if kind.value == "s" else ORACLE_TOL
+            assert _rel(got, orc.apply_layer(kind.value, g["tau"])) < tol, kind
             ref = g[f"{form}_layer_{kind.value}"]
-            tol = 5e-7 if kind.value == "spp_plus_dprime" else 5e-11
+            tol = 5e-7 if kind.value == "spp_plus_dprime" else 2e-10
             assert _rel(got, ref) < tol, kind
 
 
