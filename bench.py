@@ -1,0 +1,347 @@
+"""Benchmark of the GMRES operator-apply hot path (BASELINE.json metric:
+"fp64 Laplace pot+grad interactions/s; GMRES operator-apply time vs N").
+
+Workload (N=1): BASELINE config 2 — icosphere, reference order 7 (N=8,960
+nodes, 35,840 oversampled sources), A3 formulation (the reference default).
+One step = one GMRES iteration of the device solver: the A3 operator apply
+(oversample -> far sweep 1 -> 2 corrected SpMVs -> oversample -> far sweep 2 ->
+4 corrected SpMVs + glue + W-average) followed by the modified Gram-Schmidt
+Arnoldi update against K_ARNOLDI=4 basis vectors (the reference converges in
+4 iterations here).  Interactions per step = sum over the two far sweeps of
+(densities x N x N_over): 1 + 3 = 4 density-sweeps.
+
+Geometry + corrections come from data/config2.npz (built by running the
+reference, scripts/make_golden.py config2); without it the committed geometry
+subset is not enough, so the bench refuses (the round driver's box receives
+data/ with the repo snapshot).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+CONFIG2 = os.path.join(ROOT, "data", "config2.npz")
+K_ARNOLDI = 4
+METRIC = "fp64 Laplace pot+grad interactions/s; GMRES operator-apply time vs N"
+UNIT = "interactions/s"
+NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_bundle():
+    if not os.path.exists(CONFIG2):
+        raise SystemExit(f"{CONFIG2} missing: run `python scripts/make_golden.py "
+                         "config2` where the reference is importable")
+    z = np.load(CONFIG2)
+    keys = [k for k in z.files if not k.startswith(("a2_", "a3_"))]
+    return {k: z[k] for k in keys} | {k: z[k] for k in z.files
+                                      if k in ("a3_apply",)}
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line) through NVML every 5 ms; nvidia-smi when
+    NVML is unavailable."""
+
+    REASONS = {  # nvmlClocksEventReason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown",
+        0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+    }
+
+    def __init__(self, index=0, period=0.005):
+        self.index = index
+        self.period = period
+        self.sm = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = get_r(h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+                self._stop.wait(self.period)
+        except Exception:
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}",
+                         "--query-gpu=clocks.sm,clocks.max.sm",
+                         "--format=csv,noheader,nounits"], capture_output=True,
+                        text=True, timeout=5).stdout.strip().split(",")
+                    self.sm.append(float(out[0]))
+                    self.max_mhz = float(out[1])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
+
+
+def fp64_peak_tflops(torch, lib, _lib):
+    """Measured FP64 FMA-pipe peak (lb_probe_dfma), best of 3."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 8, 4000
+    scr = torch.zeros(blocks, dtype=torch.float64, device="cuda")
+    st = _lib.stream_handle()
+    best = 0.0
+    for _ in range(4):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.lb_probe_dfma(_lib.ptr(scr), blocks, iters, st))
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, blocks * 256 * iters * 256 / (e0.elapsed_time(e1) / 1e3))
+    return best / 1e12
+
+
+def cpu_baseline_apply(b, nthreads, reps=1):
+    """The oracle port (C restatement of the reference's direct sums + numpy
+    glue, oracle/apply.py) timed on this host: full A3 applies."""
+    import oracle
+    op = oracle.OracleOperator(b, nthreads=nthreads)
+    tau = np.asarray(b["tau"])
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        op.apply_a3(tau)
+        ts.append(time.perf_counter() - t0)
+    return min(ts), oracle.max_threads() if nthreads <= 0 else nthreads
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    b = load_bundle()
+    n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
+    inter = 4 * n * nover
+    nthreads = os.cpu_count() or 1
+    import oracle
+    op = oracle.OracleOperator(b, nthreads=nthreads)
+    tau = np.asarray(b["tau"])
+    for _ in range(max(args.warmup, 1) if args.warmup < 3 else 1):
+        op.apply_a3(tau)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        op.apply_a3(tau)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    v = inter / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2-A3-operator-apply", "N": n,
+                   "N_over": nover, "formulation": "a3",
+                   "interactions_per_step": inter},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads,
+                         "kind": "port",
+                         "sample": "full A3 apply of config 2 per step (oracle/"
+                                   "apply.py: C direct sums + numpy glue)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2111_10743_b200 import _build, _lib
+    _build.build(verbose=False)
+    lib = _lib.load()
+    from paper_2111_10743_b200 import LayerOperatorSet
+    from paper_2111_10743_b200.solver import _bind
+
+    b = load_bundle()
+    n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
+    inter = 4 * n * nover  # density-sweeps x targets x sources per step
+    op = LayerOperatorSet.from_bundle(b, "a3")
+    L = _bind()
+    st = _lib.stream_handle()
+
+    # Krylov state for the Arnoldi part of the step
+    rng = np.random.default_rng(2)
+    Q = torch.from_numpy(np.linalg.qr(rng.standard_normal((n, K_ARNOLDI + 1)))[0].T
+                         .copy()).cuda().contiguous()
+    hdev = torch.zeros(K_ARNOLDI + 2, dtype=torch.float64, device="cuda")
+    v = torch.empty(n, dtype=torch.float64, device="cuda")
+    tau = torch.from_numpy(np.asarray(b["tau"])).cuda()
+
+    def step():
+        op.apply_device(tau, out=v)
+        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
+                                    _lib.ptr(hdev), st))
+
+    launches_per_step = 7 + 1  # apply: 7 kernels; MGS: one single-CTA kernel (n <= 24576)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    # parity spot check against the reference's own A3 apply
+    y = op.apply(np.asarray(b["tau"]))
+    parity = float(np.abs(y - b["a3_apply"]).max() / np.abs(b["a3_apply"]).max()) \
+        if "a3_apply" in b else None
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        times = []
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as cs:
+            for _ in range(k):
+                flush.zero_()  # L2 flush between timed iterations (untimed)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) / 1e3)
+        if world > 1:
+            torch.distributed.barrier()
+        return times, cs.summary()
+
+    times, clocks = timed(step, args.steps)
+    t_step = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = inter * world / t_step  # independent replicas: whole-job aggregate
+
+    # dominant kernel: far sweep 2 (opfar_kernel<FarA3b>), timed alone
+    from paper_2111_10743_b200.operators import _bind_opset  # noqa: F401
+    far_t = far2_time(torch, op, tau, lib, _lib)
+
+    # e2e through the public API with host buffers: H2D tau, apply, D2H result
+    tau_h = torch.from_numpy(np.asarray(b["tau"])).pin_memory()
+    out_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    tau_d = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def e2e_step():
+        tau_d.copy_(tau_h, non_blocking=True)
+        op.apply_device(tau_d, out=v)
+        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
+                                    _lib.ptr(hdev), st))
+        out_h.copy_(v, non_blocking=True)
+    e2e_times, _ = timed(e2e_step, args.steps)
+    e2e_t = sum(e2e_times) / len(e2e_times)
+
+    peak = fp64_peak_tflops(torch, lib, _lib)
+    far_flops = 44.0 * n * nover  # algorithmic flops of FarA3b per launch
+    achieved = far_flops / far_t / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_cpu, cores = cpu_baseline_apply(b, os.cpu_count() or 1)
+        cpu = {"value": inter / t_cpu, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": "one full A3 apply of config 2 (oracle/apply.py: C direct "
+                         "sums + numpy glue; MGS excluded)"}
+
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (config 2 geometry + reference-built corrections)",
+            "config": {"workload": "config2-A3-operator-apply+MGS(k=4)",
+                       "N": n, "N_over": nover, "formulation": "a3",
+                       "interactions_per_step": inter,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "apply_parity_vs_reference": parity},
+            "roofline": {"bound": "fp64", "kernel": "opfar_kernel<FarA3b>",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak,
+                         "peak_source": "measured in-run (lb_probe_dfma); nominal "
+                                        f"{NOMINAL_FP64_TFLOPS}",
+                         "far2_ms": far_t * 1e3, "flops_per_pair": 44,
+                         "traffic": None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": inter * world / e2e_t, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": e2e_t * 1e3},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def far2_time(torch, op, tau, lib, _lib, which=2, reps=20):
+    """Average device duration of one far sweep (default: A3 call 2,
+    opfar_kernel<FarA3b>) timed with CUDA events on its launching stream
+    (lb_opset_time_far); the packed sources are the last apply's."""
+    import ctypes
+    op.apply_device(tau)
+    sec = ctypes.c_double(0.0)
+    _lib.check(lib.lb_opset_time_far(op.dev.handle, which, reps, ctypes.byref(sec),
+                                     _lib.stream_handle()))
+    return sec.value
+
+
+if __name__ == "__main__":
+    main()

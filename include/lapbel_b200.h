@@ -140,6 +140,13 @@ int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau,
 /* Copies the last W-average (eta / ws) the handle computed to dev_out. */
 int lb_opset_last_scalar(const lb_opset* h, double* dev_out);
 
+/* Profiling helper: average duration (seconds, written to a HOST double) of
+ * `reps` back-to-back launches of one far sweep on the handle's current
+ * packed sources: which = 0 S, 1 A3 call 1, 2 A3 call 2, 3 A2 call 1,
+ * 4 A2 call 2, 5 A1 call 1, 6 A1 call 2, 7 D.  Synchronises. */
+int lb_opset_time_far(lb_opset* h, int which, int reps, double* seconds_host,
+                      void* stream);
+
 /* y_j (+)= A_j x_j for njobs <= 4 CSR matrices sharing one pattern
  * (`corr(kind) @ v`, operators.py:119-123).  vals/xs/ys are HOST arrays of
  * njobs DEVICE pointers. */

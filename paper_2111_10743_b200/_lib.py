@@ -47,6 +47,7 @@ SIGNATURES = {
     "lb_opset_apply": [_P, _I32, _P, _P, _P],
     "lb_opset_apply_layer": [_P, _I32, _P, _P, _P],
     "lb_opset_last_scalar": [_P, _P],
+    "lb_opset_time_far": [_P, _I32, _I32, _P, _P],
     "lb_csr_spmv": [_P, _P, _I64, _I32, _P, _P, _P, _I32, _P],
     "lb_arnoldi_mgs": [_P, _I64, _I32, _I64, _P, _P, _P],
     "lb_combine_rows": [_P, _I64, _I32, _I64, _P, _P, _P],

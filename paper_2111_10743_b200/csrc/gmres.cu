@@ -60,6 +60,56 @@ __global__ void combine_rows_kernel(const double* __restrict__ Q, int64_t ldq, i
   }
 }
 
+// Small-N Arnoldi step in ONE CTA: v lives in shared memory for the whole MGS
+// sweep (k+1 dots/axpys + norm + normalise in one launch instead of k+3
+// latency-bound grid passes).  Used for n <= kSmallN (config 2: n = 8960).
+constexpr int kSmallBT = 1024;
+constexpr int64_t kSmallN = 24576;  // 192 KB of shared memory
+
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = l < (int)(blockDim.x >> 5) ? red[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (l == 0) red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__global__ void __launch_bounds__(kSmallBT) mgs_small_kernel(double* __restrict__ Q, int64_t ldq, int k,
+                                                             int n, double* __restrict__ v,
+                                                             double* __restrict__ h) {
+  extern __shared__ double sv[];
+  __shared__ double red[33];
+  for (int i = threadIdx.x; i < n; i += kSmallBT) sv[i] = v[i];
+  __syncthreads();
+  for (int j = 0; j <= k; ++j) {
+    const double* q = Q + (int64_t)j * ldq;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += kSmallBT) s = fma(q[i], sv[i], s);
+    const double hj = cta_sum(s, red);
+    if (threadIdx.x == 0) h[j] = hj;
+    for (int i = threadIdx.x; i < n; i += kSmallBT) sv[i] = fma(-hj, q[i], sv[i]);
+  }
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kSmallBT) s = fma(sv[i], sv[i], s);
+  const double nrm = sqrt(cta_sum(s, red));
+  if (threadIdx.x == 0) h[k + 1] = nrm;
+  double* qn = Q + (int64_t)(k + 1) * ldq;
+  for (int i = threadIdx.x; i < n; i += kSmallBT) {
+    v[i] = sv[i];
+    if (nrm != 0.0) qn[i] = sv[i] / nrm;
+  }
+}
+
 namespace {
 
 // persistent reduction scratch per device (grid <= 2*SMs blocks)
@@ -99,6 +149,17 @@ int lb_arnoldi_mgs(double* Q, int64_t ldq, int k, int64_t n, double* v, double* 
   using namespace lb;
   if (!Q || !v || !h || k < 0 || n <= 0 || ldq < n) return fail(LB_ERR_ARG, "lb_arnoldi_mgs: bad arguments");
   cudaStream_t st = as_stream(stream);
+  if (n <= kSmallN) {
+    static bool attr = false;
+    if (!attr) {
+      LB_CUDA(cudaFuncSetAttribute(mgs_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kSmallN * sizeof(double))));
+      attr = true;
+    }
+    mgs_small_kernel<<<1, kSmallBT, n * sizeof(double), st>>>(Q, ldq, k, (int)n, v, h);
+    LB_CHECK_LAUNCH();
+    return LB_OK;
+  }
   const int blocks = vec_blocks(n);
   RedBufs rb;
   LB_TRY(get_pool(&rb, 2 * sm_count() + 8));

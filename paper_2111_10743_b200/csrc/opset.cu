@@ -18,220 +18,14 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "lb_common.cuh"
+#include "opfar.cuh"
 #include "reduce.cuh"
 
 namespace lb {
-
-constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
-
-struct Tgt {
-  double x, y, z, nx, ny, nz;
-};
-
-// ---------------------------------------------------------------------------
-// far-field pair functors.  r = t - s; every functor skips r == 0 through
-// inv_sqrt_skip.  Output j of functor F accumulates into a[j].
-
-#define LB_GEOM                                                     \
-  const double r0 = t.x - s[0], r1 = t.y - s[1], r2 = t.z - s[2];   \
-  const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));              \
-  const double invr = inv_sqrt_skip(rr);
-
-// S (pot only):  a0 += c/r                      record [x y z c]
-struct FarS {
-  static constexpr int S = 4, NOUT = 1;
-  static constexpr bool TN = false;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    a[0] = fma(s[3], invr, a[0]);
-  }
-};
-
-// A3 call 1 (operators.py:237): charge c, pot + n_t.grad.
-//   a0 += c/r ; a1 += c (n_t.r)/r^3   (n_t.grad = -a1)        record [x y z c]
-struct FarA3a {
-  static constexpr int S = 4, NOUT = 2;
-  static constexpr bool TN = true;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double ci = s[3] * invr;
-    const double ci3 = ci * (invr * invr);
-    a[0] += ci;
-    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
-    a[1] = fma(ci3, rnt, a[1]);
-  }
-};
-
-// S''+D' kernel times r^3, in the form of kernels.py:60-67:
-//   3 (n_t.r)(dn.r)/r^2 - n_t.dn,   dn = n_t - n_s.
-// dn is formed FIRST: for nearby nodes n_t - n_s is exact (Sterbenz), so
-// n_t.dn = O(r^2) keeps its relative accuracy; the algebraically equal
-// |n_t|^2 - n_t.n_s (or the reference's separate n.H.n + n.grad_dipole,
-// operators.py:257-259) loses ~eps/r^2 of it.  The sum equals
-// n_t.hess(charge).n_t + n_t.grad(dipole n_s).
-#define LB_SPP_TERMS                                                       \
-  const double dn0 = t.nx - s[3], dn1 = t.ny - s[4], dn2 = t.nz - s[5];    \
-  const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));              \
-  const double rdn = fma(dn2, r2, fma(dn1, r1, dn0 * r0));                 \
-  const double ndn = fma(t.nz, dn2, fma(t.ny, dn1, t.nx * dn0));           \
-  const double kspp = fma(3.0 * rnt * rdn, invr * invr, -ndn);
-
-// A3 call 2 (operators.py:247-259): charges c0 = w mu1, c1 = w mu2 and
-// dipole c1 n_s.   record [x y z nx ny nz c0 c1]
-//   a0 += c0 (n_t.r)/r^3   (sp_mu1 far = -a0)
-//   a1 += c1 / r           (s_mu2 far)
-//   a2 += c1 (n_t.r)/r^3   (sp_mu2 far = -a2)
-//   a3 += c1 Kspp/r^3      (sppdp_mu2 far)
-struct FarA3b {
-  static constexpr int S = 8, NOUT = 4;
-  static constexpr bool TN = true;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double invr3 = invr * (invr * invr);
-    LB_SPP_TERMS
-    const double g = rnt * invr3;
-    a[0] = fma(s[6], g, a[0]);
-    a[1] = fma(s[7], invr, a[1]);
-    a[2] = fma(s[7], g, a[2]);
-    a[3] = fma(s[7] * invr3, kspp, a[3]);
-  }
-};
-
-// A2 call 1 (operators.py:200-212): charge c and dipole c n_s (c = w tau).
-//   a0 += c/r ; a1 += c (n_s.r)/r^3 (D) ; a2 += c (n_t.r)/r^3 ; a3 += c Kspp/r^3
-//   record [x y z nx ny nz c 0]
-struct FarA2a {
-  static constexpr int S = 8, NOUT = 4;
-  static constexpr bool TN = true;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double c = s[6];
-    const double ci = c * invr;
-    const double ci3 = ci * (invr * invr);
-    LB_SPP_TERMS
-    const double rns = rnt - rdn;  // n_s.r
-    a[0] += ci;
-    a[1] = fma(ci3, rns, a[1]);
-    a[2] = fma(ci3, rnt, a[2]);
-    a[3] = fma(ci3, kspp, a[3]);
-  }
-};
-
-// A2 call 2 (operators.py:216-223): dipole c0 n_s (c0 = w mu1), charge c1 = w mu2
-//   a0 += c0 (n_s.r)/r^3 ; a1 += c1/r      record [x y z nx ny nz c0 c1]
-struct FarA2b {
-  static constexpr int S = 8, NOUT = 2;
-  static constexpr bool TN = false;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
-    a[0] = fma(s[6] * rns, invr * (invr * invr), a[0]);
-    a[1] = fma(s[7], invr, a[1]);
-  }
-};
-
-// D alone (apply_layer DOUBLE_LAYER, operators.py:144-147): record [.. c0 ..]
-struct FarD {
-  static constexpr int S = 8, NOUT = 1;
-  static constexpr bool TN = false;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double rns = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
-    a[0] = fma(s[6] * rns, invr * (invr * invr), a[0]);
-  }
-};
-
-// A1 call 1 (operators.py:167-171): charge c, pot + full gradient
-//   a0 += c/r ; a1..3 += c r/r^3  (grad = -a1..3)        record [x y z c]
-struct FarA1a {
-  static constexpr int S = 4, NOUT = 4;
-  static constexpr bool TN = false;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double ci = s[3] * invr;
-    const double ci3 = ci * (invr * invr);
-    a[0] += ci;
-    a[1] = fma(ci3, r0, a[1]);
-    a[2] = fma(ci3, r1, a[2]);
-    a[3] = fma(ci3, r2, a[3]);
-  }
-};
-
-// A1 call 2 (operators.py:181-185): three charges c_l = w mu_l, only the
-// divergence sum_l d_l u_l is consumed:  a0 += (c . r)/r^3 (div far = -a0)
-//   record [x y z c0 c1 c2]
-struct FarA1b {
-  static constexpr int S = 6, NOUT = 1;
-  static constexpr bool TN = false;
-  __device__ static void pair(const Tgt& t, const double* s, double* a) {
-    LB_GEOM
-    const double cr = fma(s[5], r2, fma(s[4], r1, s[3] * r0));
-    a[0] = fma(cr, invr * (invr * invr), a[0]);
-  }
-};
-
-#undef LB_GEOM
-
-// ---------------------------------------------------------------------------
-// tiled far kernel (same structure as p2p_tile_kernel)
-
-template <class F, int TPT, int BT, int TS>
-__global__ void __launch_bounds__(BT) opfar_kernel(const double* __restrict__ nodes,
-                                                   const double* __restrict__ normals, int64_t n,
-                                                   const double* __restrict__ pack,
-                                                   int64_t ns_pad, int64_t chunk,
-                                                   double* __restrict__ part) {
-  constexpr int S = F::S;
-  constexpr int NO = F::NOUT;
-  __shared__ __align__(16) double sh[TS * S];
-  const int64_t tbase = (int64_t)blockIdx.x * (BT * TPT) + threadIdx.x;
-  const int64_t s_begin = (int64_t)blockIdx.y * chunk;
-  const int64_t s_end = min(s_begin + chunk, ns_pad);
-  Tgt tg[TPT];
-  double acc[TPT][NO];
-#pragma unroll
-  for (int j = 0; j < TPT; ++j) {
-    const int64_t i = tbase + (int64_t)j * BT;
-    const bool in = i < n;
-    tg[j].x = in ? nodes[3 * i] : 0.0;
-    tg[j].y = in ? nodes[3 * i + 1] : 0.0;
-    tg[j].z = in ? nodes[3 * i + 2] : 0.0;
-    if (F::TN) {
-      tg[j].nx = in ? normals[3 * i] : 0.0;
-      tg[j].ny = in ? normals[3 * i + 1] : 0.0;
-      tg[j].nz = in ? normals[3 * i + 2] : 0.0;
-    } else {
-      tg[j].nx = tg[j].ny = tg[j].nz = 0.0;
-    }
-#pragma unroll
-    for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
-  }
-  for (int64_t s0 = s_begin; s0 < s_end; s0 += TS) {
-    __syncthreads();
-    const double2* g = reinterpret_cast<const double2*>(pack + s0 * S);
-    double2* d = reinterpret_cast<double2*>(sh);
-#pragma unroll 4
-    for (int k = threadIdx.x; k < TS * S / 2; k += BT) d[k] = __ldg(g + k);
-    __syncthreads();
-#pragma unroll 2
-    for (int k = 0; k < TS; ++k) {
-#pragma unroll
-      for (int j = 0; j < TPT; ++j) F::pair(tg[j], sh + k * S, acc[j]);
-    }
-  }
-  double* out = part + (int64_t)blockIdx.y * NO * n;
-#pragma unroll
-  for (int j = 0; j < TPT; ++j) {
-    const int64_t i = tbase + (int64_t)j * BT;
-    if (i < n) {
-#pragma unroll
-      for (int o = 0; o < NO; ++o) out[(int64_t)o * n + i] = acc[j][o];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // oversampling (interpolate_to_oversampled, surface.py:370-375) fused with the
@@ -307,20 +101,19 @@ struct CsrJobs {
 };
 
 constexpr int kCsrBT = 256;
+constexpr int kCsrRows = 8;  // rows per block: one warp per row
 
-// sum of the far-kernel partials over source splits for output o of row i
-__device__ __forceinline__ double far_sum(const double* part, int nsplit, int nout, int o,
-                                          int64_t n, int64_t i) {
-  double s = 0.0;
-  for (int p = 0; p < nsplit; ++p) s += part[((int64_t)p * nout + o) * n + i];
-  return s;
-}
-
+// Far-sweep partials (one per source split) are summed for the block's rows
+// in a coalesced first phase (thread = row, fixed split order:
+// deterministic) into shared memory; the epilogue reads them through f().
 struct EpiBase {
+  static constexpr int kMaxOut = 4;
   const double* part;
-  int nsplit, nout;
-  int64_t n;
-  __device__ double f(int o, int64_t i) const { return far_sum(part, nsplit, nout, o, n, i); }
+  SkLayout L;
+  int nout;
+  const double* fs;  // shared: fs[o * kCsrRows + local_row]
+  int64_t row0;
+  __device__ double f(int o, int64_t i) const { return fs[o * kCsrRows + (int)(i - row0)]; }
 };
 
 // generic: y_j = (accumulate ? y_j : 0) + acc_j
@@ -451,14 +244,44 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
                                                          double* partials, unsigned* ticket,
                                                          double* red_out, double red_div) {
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (kCsrBT / 32) + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * kCsrRows;
+  __shared__ double fs[EpiBase::kMaxOut * kCsrRows];
+  E e = epi;
+  if constexpr (std::is_base_of<EpiBase, E>::value) {
+    const int o = threadIdx.x / kCsrRows, lr = threadIdx.x % kCsrRows;
+    if (o < e.nout) {
+      const int64_t i = row0 + lr;
+      fs[o * kCsrRows + lr] = i < nrows ? sk_sum(e.part, e.L, e.nout, o, i) : 0.0;
+    }
+    __syncthreads();
+    e.fs = fs;
+    e.row0 = row0;
+  }
   double red = 0.0;
-  if (row < nrows) {
+#pragma unroll 1
+  for (int rr = 0; rr < kCsrRows / (kCsrBT / 32); ++rr) {
+    const int64_t row = row0 + warp * (kCsrRows / (kCsrBT / 32)) + rr;
+    if (row >= nrows) break;
     double acc[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) acc[j] = 0.0;
     const int64_t kb = indptr[row], ke = indptr[row + 1];
-    for (int64_t k = kb + lane; k < ke; k += 32) {
+    // 4 chunks of 32 nnz in flight per warp (the row loop is latency-bound
+    // otherwise: ~600 nnz per row at config 2)
+    int64_t k = kb + lane;
+    for (; k + 96 < ke; k += 128) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = __ldg(indices + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          acc[j] = fma(__ldg(jobs.val[j] + k + 32 * u), __ldg(jobs.x[j] + c[u]), acc[j]);
+      }
+    }
+    for (; k < ke; k += 32) {
       const int c = __ldg(indices + k);
 #pragma unroll
       for (int j = 0; j < J; ++j) acc[j] = fma(__ldg(jobs.val[j] + k), __ldg(jobs.x[j] + c), acc[j]);
@@ -468,7 +291,7 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
     }
-    if (lane == 0) red = epi(row, acc);
+    if (lane == 0) red += e(row, acc);
   }
   if constexpr (E::kReduce) grid_reduce_finish<kCsrBT>(red, partials, ticket, red_out, 0, red_div);
 }
@@ -502,42 +325,51 @@ struct lb_opset {
 namespace lb {
 namespace {
 
-constexpr int kFarBT = 128;
-constexpr int kFarTS = 128;
+// launch shape per functor, from tools/far_sweep.cu on B200 (config-2 and
+// 1e5-sized sweeps): 64-thread CTAs, 4 targets/thread with 64-source tiles for
+// the light 4-double records, 2 targets/thread with 128-source tiles for the
+// 8-double records; next source tile prefetched into registers.
+constexpr int kFarBT = 64;
 
 template <class F>
 constexpr int far_tpt() {
-  return F::NOUT <= 2 && F::S <= 4 ? 2 : 1;
+  return F::S <= 4 && F::NOUT <= 2 ? 4 : 2;
 }
+template <class F>
+constexpr int far_ts() {
+  return F::S <= 4 ? 64 : 128;
+}
+constexpr int kFarPad = 128;  // source padding: a multiple of every far_ts
 
 template <class F>
-int far_splits(const lb_opset* h) {
+SkLayout far_layout(const lb_opset* h) {
   constexpr int TPT = far_tpt<F>();
   static int per_sm = -1;
   if (per_sm < 0) {
     int b = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, opfar_kernel<F, TPT, kFarBT, kFarTS>, kFarBT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, opfar_kernel<F, TPT, kFarBT, far_ts<F>()>,
+                                                  kFarBT, 0);
     per_sm = std::max(b, 1);
   }
-  const int64_t tiles = ceil_div(h->d.n, (int64_t)kFarBT * TPT);
-  return (int)choose_splits(tiles, h->ns_pad / kFarTS, (int64_t)sm_count() * per_sm);
+  return make_sk_layout(h->d.n, h->ns_pad, kFarBT * TPT, far_ts<F>(), (int64_t)sm_count() * per_sm);
 }
 
 template <class F>
-int run_far(const lb_opset* h, const double* pack, int* nsplit_out, cudaStream_t st) {
+int64_t far_part_size(const lb_opset* h) {
+  const SkLayout L = far_layout<F>(h);
+  return L.tiles * L.kmax * F::NOUT * L.tt;
+}
+
+template <class F>
+int run_far(const lb_opset* h, const double* pack, SkLayout* out, cudaStream_t st) {
   constexpr int TPT = far_tpt<F>();
-  const int64_t n = h->d.n;
-  const int64_t tiles = ceil_div(n, (int64_t)kFarBT * TPT);
-  const int64_t src_tiles = h->ns_pad / kFarTS;
-  int64_t splits = far_splits<F>(h);
-  const int64_t chunk = ceil_div(src_tiles, splits) * kFarTS;
-  splits = ceil_div(h->ns_pad, chunk);
-  if (splits * F::NOUT * n > h->part_cap) return fail(LB_ERR_ARG, "opset: partial buffer too small");
-  dim3 grid((unsigned)tiles, (unsigned)splits);
-  opfar_kernel<F, TPT, kFarBT, kFarTS><<<grid, kFarBT, 0, st>>>(h->d.nodes, h->d.normals, n, pack,
-                                                                h->ns_pad, chunk, h->part);
+  const SkLayout L = far_layout<F>(h);
+  if (L.tiles * L.kmax * F::NOUT * L.tt > h->part_cap)
+    return fail(LB_ERR_ARG, "opset: partial buffer too small");
+  opfar_kernel<F, TPT, kFarBT, far_ts<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(h->d.nodes, h->d.normals,
+                                                                        h->d.n, pack, L, h->part);
   LB_CHECK_LAUNCH();
-  *nsplit_out = (int)splits;
+  *out = L;
   return LB_OK;
 }
 
@@ -578,12 +410,11 @@ int run_csr(const lb_opset* h, const double* const* vals, const double* const* x
 }
 
 template <class E>
-E base_epi(const lb_opset* h, int nsplit, int nout) {
+E base_epi(const lb_opset* h, const SkLayout& L, int nout) {
   E e{};
   e.part = h->part;
-  e.nsplit = nsplit;
+  e.L = L;
   e.nout = nout;
-  e.n = h->d.n;
   return e;
 }
 
@@ -591,7 +422,7 @@ double* V(const lb_opset* h, int k) { return h->vec + (int64_t)k * h->d.n; }
 
 int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
-  int ns1 = 0, ns2 = 0;
+  SkLayout ns1{}, ns2{};
   double* s_tau = V(h, 0);
   double* sp_tau = V(h, 1);
   {
@@ -631,7 +462,7 @@ int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
 
 int apply_a2(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
-  int ns1 = 0, ns2 = 0;
+  SkLayout ns1{}, ns2{};
   double* mu1 = V(h, 0);
   double* mu2 = V(h, 1);
   {
@@ -672,7 +503,7 @@ int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
   if (!h->d.tangents_u || !h->d.tangents_v || !h->d.inv_metric || !h->d.phi0)
     return fail(LB_ERR_ARG, "opset: A1 needs tangents, inverse metric and phi0");
-  int ns1 = 0, ns2 = 0;
+  SkLayout ns1{}, ns2{};
   double* mux = V(h, 0);
   double* muy = V(h, 1);
   double* muz = V(h, 2);
@@ -717,7 +548,8 @@ int apply_layer(lb_opset* h, int kind, const double* tau, double* out, cudaStrea
   if (kind < 0 || kind >= LB_NKINDS) return fail(LB_ERR_ARG, "opset: unknown kernel kind");
   const double* val = h->d.corr[kind];
   if (!val) return fail(LB_ERR_KEY, "opset: corrections for this kind were not built");
-  int ns = 0, nout = 1, o = 0;
+  SkLayout ns{};
+  int nout = 1, o = 0;
   double sign = 1.0;
   if (kind == LB_KIND_S || kind == LB_KIND_SPRIME ||
       (kind >= LB_KIND_GRAD_S1 && kind <= LB_KIND_GRAD_S3)) {
@@ -773,19 +605,18 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   h->d = *d;
   h->wsum = d->weight_sum;
   const int64_t n = d->n;
-  h->ns_pad = ceil_div(d->n_over, kFarTS) * kFarTS;
-  int64_t maxsplit = 1;
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarS>(h) * (int64_t)FarS::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA3a>(h) * (int64_t)FarA3a::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA3b>(h) * (int64_t)FarA3b::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA2a>(h) * (int64_t)FarA2a::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA2b>(h) * (int64_t)FarA2b::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarD>(h) * (int64_t)FarD::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA1a>(h) * (int64_t)FarA1a::NOUT);
-  maxsplit = std::max<int64_t>(maxsplit, far_splits<FarA1b>(h) * (int64_t)FarA1b::NOUT);
-  // splits are recomputed per launch; allow for the ceil-div adjustment
-  h->part_cap = (maxsplit + 8) * n;
-  h->csr_blocks = (int)ceil_div(n, kCsrBT / 32);
+  h->ns_pad = ceil_div(d->n_over, kFarPad) * kFarPad;
+  int64_t cap = 1;
+  cap = std::max(cap, far_part_size<FarS>(h));
+  cap = std::max(cap, far_part_size<FarA3a>(h));
+  cap = std::max(cap, far_part_size<FarA3b>(h));
+  cap = std::max(cap, far_part_size<FarA2a>(h));
+  cap = std::max(cap, far_part_size<FarA2b>(h));
+  cap = std::max(cap, far_part_size<FarD>(h));
+  cap = std::max(cap, far_part_size<FarA1a>(h));
+  cap = std::max(cap, far_part_size<FarA1b>(h));
+  h->part_cap = cap;
+  h->csr_blocks = (int)ceil_div(n, kCsrRows);
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes);
@@ -864,6 +695,39 @@ int lb_opset_last_scalar(const lb_opset* h, double* dev_out) {
   return LB_OK;
 }
 
+int lb_opset_time_far(lb_opset* h, int which, int reps, double* seconds_host, void* stream) {
+  using namespace lb;
+  if (!h || !seconds_host || reps <= 0) return fail(LB_ERR_ARG, "lb_opset_time_far: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  cudaEvent_t e0, e1;
+  LB_CUDA(cudaEventCreate(&e0));
+  LB_CUDA(cudaEventCreate(&e1));
+  SkLayout ns{};
+  int rc = LB_OK;
+  LB_CUDA(cudaEventRecord(e0, st));
+  for (int r = 0; r < reps && rc == LB_OK; ++r) {
+    switch (which) {
+      case 0: rc = run_far<FarS>(h, h->pack4, &ns, st); break;
+      case 1: rc = run_far<FarA3a>(h, h->pack4, &ns, st); break;
+      case 2: rc = run_far<FarA3b>(h, h->pack8, &ns, st); break;
+      case 3: rc = run_far<FarA2a>(h, h->pack8, &ns, st); break;
+      case 4: rc = run_far<FarA2b>(h, h->pack8, &ns, st); break;
+      case 5: rc = run_far<FarA1a>(h, h->pack4, &ns, st); break;
+      case 6: rc = run_far<FarA1b>(h, h->pack6, &ns, st); break;
+      case 7: rc = run_far<FarD>(h, h->pack8, &ns, st); break;
+      default: rc = fail(LB_ERR_ARG, "lb_opset_time_far: unknown sweep");
+    }
+  }
+  LB_CUDA(cudaEventRecord(e1, st));
+  LB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  LB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *seconds_host = (double)ms * 1e-3 / reps;
+  return rc;
+}
+
 int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, int njobs,
                 const double* const* vals, const double* const* xs, double* const* ys,
                 int accumulate, void* stream) {
@@ -871,7 +735,7 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
   if (njobs < 1 || njobs > 4) return fail(LB_ERR_ARG, "lb_csr_spmv: njobs must be in [1, 4]");
   if (nrows <= 0) return LB_OK;
   cudaStream_t st = as_stream(stream);
-  const unsigned blocks = (unsigned)ceil_div(nrows, kCsrBT / 32);
+  const unsigned blocks = (unsigned)ceil_div(nrows, kCsrRows);
 #define LB_SPMV(J)                                                                          \
   {                                                                                         \
     CsrJobs<J> jobs;                                                                        \

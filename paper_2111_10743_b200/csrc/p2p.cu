@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(BT) p2p_grouped_kernel(
 
 namespace {
 
-constexpr int kBT = 128;
+constexpr int kBT = 64;   // 64-thread blocks x 2-4 targets/thread (tools/far_sweep.cu)
 constexpr int kTS = 128;
 
 struct ChunkSpec {
@@ -235,7 +235,8 @@ int run_direct_chunk(const double* tgt, int64_t nt, const double* src, int64_t n
                      uint32_t dmask, int level_out, double* pot, double* grad, double* hess,
                      int accumulate, cudaStream_t st) {
   using L = SrcLayout<NDC, HC, HD>;
-  constexpr int TPT = (NDC == 1 && LEVEL <= 1) ? 2 : 1;
+  constexpr int NA = NDC * ncomp(LEVEL);
+  constexpr int TPT = NA <= 4 ? 4 : (NA <= 12 ? 2 : 1);
   constexpr int NC = ncomp(LEVEL);
   const int64_t ns_pad = ceil_div(ns, kTS) * kTS;
   Scratch pack;
