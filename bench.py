@@ -232,7 +232,7 @@ def main():
         _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
                                     _lib.ptr(hdev), st))
 
-    launches_per_step = 7 + 1  # apply: 7 kernels; MGS: one single-CTA kernel (n <= 24576)
+    launches_per_step = 7 + 1  # apply: 7 kernels; MGS: one single-CTA kernel (n <= 12288)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
 
     # parity spot check against the reference's own A3 apply

@@ -60,11 +60,11 @@ __global__ void combine_rows_kernel(const double* __restrict__ Q, int64_t ldq, i
   }
 }
 
-// Small-N Arnoldi step in ONE CTA: v lives in shared memory for the whole MGS
+// Small-N Arnoldi step in ONE CTA: v lives in registers for the whole MGS
 // sweep (k+1 dots/axpys + norm + normalise in one launch instead of k+3
 // latency-bound grid passes).  Used for n <= kSmallN (config 2: n = 8960).
 constexpr int kSmallBT = 1024;
-constexpr int64_t kSmallN = 24576;  // 192 KB of shared memory
+constexpr int64_t kSmallN = 12288;  // 12 doubles of v per thread, in registers
 
 __device__ __forceinline__ double cta_sum(double v, double* red) {
 #pragma unroll
@@ -87,26 +87,51 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
 __global__ void __launch_bounds__(kSmallBT) mgs_small_kernel(double* __restrict__ Q, int64_t ldq, int k,
                                                              int n, double* __restrict__ v,
                                                              double* __restrict__ h) {
-  extern __shared__ double sv[];
+  // each thread owns elements threadIdx.x + e*kSmallBT, e < kPer, kept in
+  // registers; every basis row is loaded with all kPer loads in flight
+  constexpr int kPer = (int)(kSmallN / kSmallBT);
   __shared__ double red[33];
-  for (int i = threadIdx.x; i < n; i += kSmallBT) sv[i] = v[i];
-  __syncthreads();
+  double x[kPer];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int i = threadIdx.x + e * kSmallBT;
+    x[e] = i < n ? v[i] : 0.0;
+  }
   for (int j = 0; j <= k; ++j) {
     const double* q = Q + (int64_t)j * ldq;
     double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += kSmallBT) s = fma(q[i], sv[i], s);
+#pragma unroll
+    for (int e0 = 0; e0 < kPer; e0 += 4) {  // 4 loads in flight per chunk
+      double qv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = threadIdx.x + (e0 + e) * kSmallBT;
+        qv[e] = i < n ? q[i] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s = fma(qv[e], x[e0 + e], s);
+    }
     const double hj = cta_sum(s, red);
     if (threadIdx.x == 0) h[j] = hj;
-    for (int i = threadIdx.x; i < n; i += kSmallBT) sv[i] = fma(-hj, q[i], sv[i]);
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {  // second read of Q_j hits L1
+      const int i = threadIdx.x + e * kSmallBT;
+      if (i < n) x[e] = fma(-hj, q[i], x[e]);
+    }
   }
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += kSmallBT) s = fma(sv[i], sv[i], s);
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) s = fma(x[e], x[e], s);
   const double nrm = sqrt(cta_sum(s, red));
   if (threadIdx.x == 0) h[k + 1] = nrm;
   double* qn = Q + (int64_t)(k + 1) * ldq;
-  for (int i = threadIdx.x; i < n; i += kSmallBT) {
-    v[i] = sv[i];
-    if (nrm != 0.0) qn[i] = sv[i] / nrm;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int i = threadIdx.x + e * kSmallBT;
+    if (i < n) {
+      v[i] = x[e];
+      if (nrm != 0.0) qn[i] = x[e] / nrm;
+    }
   }
 }
 
@@ -150,13 +175,7 @@ int lb_arnoldi_mgs(double* Q, int64_t ldq, int k, int64_t n, double* v, double* 
   if (!Q || !v || !h || k < 0 || n <= 0 || ldq < n) return fail(LB_ERR_ARG, "lb_arnoldi_mgs: bad arguments");
   cudaStream_t st = as_stream(stream);
   if (n <= kSmallN) {
-    static bool attr = false;
-    if (!attr) {
-      LB_CUDA(cudaFuncSetAttribute(mgs_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(kSmallN * sizeof(double))));
-      attr = true;
-    }
-    mgs_small_kernel<<<1, kSmallBT, n * sizeof(double), st>>>(Q, ldq, k, (int)n, v, h);
+    mgs_small_kernel<<<1, kSmallBT, 0, st>>>(Q, ldq, k, (int)n, v, h);
     LB_CHECK_LAUNCH();
     return LB_OK;
   }

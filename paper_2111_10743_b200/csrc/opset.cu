@@ -101,7 +101,7 @@ struct CsrJobs {
 };
 
 constexpr int kCsrBT = 256;
-constexpr int kCsrRows = 8;  // rows per block: one warp per row
+constexpr int kCsrRows = 8;  // rows per block: one warp per row (power of 2)
 
 // Far-sweep partials (one per source split) are summed for the block's rows
 // in a coalesced first phase (thread = row, fixed split order:
@@ -237,51 +237,70 @@ struct EpiA1p2 : EpiBase {
   }
 };
 
+// One block = 8 warps = RB rows x W warps per row (W = wpr in {1,2,4,8},
+// picked from the mean row length so every warp has ~4 chunks of 32 nnz in
+// flight: the row loop is latency-bound otherwise).  Segment warps of a row
+// combine their partial sums in a fixed order through shared memory.
 template <int J, class E>
 __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
                                                          const int32_t* __restrict__ indices,
-                                                         int64_t nrows, CsrJobs<J> jobs, E epi,
-                                                         double* partials, unsigned* ticket,
+                                                         int64_t nrows, int wpr, CsrJobs<J> jobs,
+                                                         E epi, double* partials, unsigned* ticket,
                                                          double* red_out, double red_div) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * kCsrRows;
+  const int rb = (kCsrBT / 32) / wpr;
+  const int64_t row0 = (int64_t)blockIdx.x * rb;
   __shared__ double fs[EpiBase::kMaxOut * kCsrRows];
+  __shared__ double wacc[kCsrBT / 32][J];
   E e = epi;
   if constexpr (std::is_base_of<EpiBase, E>::value) {
-    const int o = threadIdx.x / kCsrRows, lr = threadIdx.x % kCsrRows;
-    if (o < e.nout) {
-      const int64_t i = row0 + lr;
-      fs[o * kCsrRows + lr] = i < nrows ? sk_sum(e.part, e.L, e.nout, o, i) : 0.0;
+    // all 256 threads: (row lr, output o) x 8 slot-lanes sl, then a fixed-order
+    // 8-way reduction through shared memory (latency-bound otherwise)
+    __shared__ double red8[8][EpiBase::kMaxOut * kCsrRows];
+    const int lr = threadIdx.x & (kCsrRows - 1);
+    const int o = (threadIdx.x >> 3) & 3;
+    const int sl = threadIdx.x >> 5;
+    double v = 0.0;
+    const int64_t i = row0 + lr;
+    if (lr < rb && o < e.nout && i < nrows) {
+      const int64_t t = i / e.L.tt;
+      const int lt = (int)(i - t * e.L.tt);
+      const int64_t nseg = e.L.blast(t) - e.L.bfirst(t) + 1;
+      for (int64_t k = sl; k < nseg; k += 8) v += e.part[e.L.idx(t, k, o, e.nout, lt)];
     }
+    red8[sl][o * kCsrRows + lr] = v;
     __syncthreads();
+    if (threadIdx.x < EpiBase::kMaxOut * kCsrRows) {
+      double s8 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s8 += red8[q][threadIdx.x];
+      fs[threadIdx.x] = s8;
+    }
     e.fs = fs;
     e.row0 = row0;
   }
-  double red = 0.0;
-#pragma unroll 1
-  for (int rr = 0; rr < kCsrRows / (kCsrBT / 32); ++rr) {
-    const int64_t row = row0 + warp * (kCsrRows / (kCsrBT / 32)) + rr;
-    if (row >= nrows) break;
-    double acc[J];
+  const int rloc = warp / wpr, seg = warp - rloc * wpr;
+  const int64_t row = row0 + rloc;
+  double acc[J];
 #pragma unroll
-    for (int j = 0; j < J; ++j) acc[j] = 0.0;
+  for (int j = 0; j < J; ++j) acc[j] = 0.0;
+  if (row < nrows) {
     const int64_t kb = indptr[row], ke = indptr[row + 1];
-    // 4 chunks of 32 nnz in flight per warp (the row loop is latency-bound
-    // otherwise: ~600 nnz per row at config 2)
-    int64_t k = kb + lane;
-    for (; k + 96 < ke; k += 128) {
+    const int64_t stride = 32 * wpr;
+    int64_t k = kb + seg * 32 + lane;
+    for (; k + 3 * stride < ke; k += 4 * stride) {
       int c[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = __ldg(indices + k + 32 * u);
+      for (int u = 0; u < 4; ++u) c[u] = __ldg(indices + k + stride * u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
 #pragma unroll
         for (int j = 0; j < J; ++j)
-          acc[j] = fma(__ldg(jobs.val[j] + k + 32 * u), __ldg(jobs.x[j] + c[u]), acc[j]);
+          acc[j] = fma(__ldg(jobs.val[j] + k + stride * u), __ldg(jobs.x[j] + c[u]), acc[j]);
       }
     }
-    for (; k < ke; k += 32) {
+    for (; k < ke; k += stride) {
       const int c = __ldg(indices + k);
 #pragma unroll
       for (int j = 0; j < J; ++j) acc[j] = fma(__ldg(jobs.val[j] + k), __ldg(jobs.x[j] + c), acc[j]);
@@ -291,9 +310,31 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
     }
-    if (lane == 0) red += e(row, acc);
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) wacc[warp][j] = acc[j];
+    }
+  }
+  __syncthreads();
+  double red = 0.0;
+  if (row < nrows && seg == 0 && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < wpr; ++q) t += wacc[warp + q][j];
+      acc[j] = t;
+    }
+    red = e(row, acc);
   }
   if constexpr (E::kReduce) grid_reduce_finish<kCsrBT>(red, partials, ticket, red_out, 0, red_div);
+}
+
+// warps per row from the mean row length.  Measured on B200 at config 2
+// (617 nnz/row): 1 warp/row 33.6 us vs 4 warps/row 50 us for pass 1, so rows
+// are only split when they are very long.
+inline int csr_wpr(int64_t nnz, int64_t nrows) {
+  const int64_t avg = nrows > 0 ? nnz / nrows : 0;
+  return avg >= 8192 ? 4 : avg >= 4096 ? 2 : 1;
 }
 
 __global__ void add_scalar_kernel(double* y, int64_t n, const double* s) {
@@ -320,6 +361,7 @@ struct lb_opset {
   unsigned* ticket = nullptr;
   double* scal = nullptr;  // [0] W-average / eta
   int csr_blocks = 0;
+  int csr_wpr = 1;
 };
 
 namespace lb {
@@ -404,7 +446,8 @@ int run_csr(const lb_opset* h, const double* const* vals, const double* const* x
     jobs.x[j] = xs[j];
   }
   csr_epi_kernel<J, E><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
-      h->d.indptr, h->d.indices, h->d.n, jobs, epi, h->partials, h->ticket, h->scal, red_div);
+      h->d.indptr, h->d.indices, h->d.n, h->csr_wpr, jobs, epi, h->partials, h->ticket, h->scal,
+      red_div);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }
@@ -616,7 +659,8 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   cap = std::max(cap, far_part_size<FarA1a>(h));
   cap = std::max(cap, far_part_size<FarA1b>(h));
   h->part_cap = cap;
-  h->csr_blocks = (int)ceil_div(n, kCsrRows);
+  h->csr_wpr = csr_wpr(d->nnz, n);
+  h->csr_blocks = (int)ceil_div(n, (kCsrBT / 32) / h->csr_wpr);
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes);
@@ -735,7 +779,10 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
   if (njobs < 1 || njobs > 4) return fail(LB_ERR_ARG, "lb_csr_spmv: njobs must be in [1, 4]");
   if (nrows <= 0) return LB_OK;
   cudaStream_t st = as_stream(stream);
-  const unsigned blocks = (unsigned)ceil_div(nrows, kCsrRows);
+  int64_t nnz = 0;
+  LB_CUDA(cudaMemcpy(&nnz, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  const int wpr = csr_wpr(nnz, nrows);
+  const unsigned blocks = (unsigned)ceil_div(nrows, (kCsrBT / 32) / wpr);
 #define LB_SPMV(J)                                                                          \
   {                                                                                         \
     CsrJobs<J> jobs;                                                                        \
@@ -746,7 +793,7 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
       epi.y[j] = ys[j];                                                                     \
     }                                                                                       \
     epi.accumulate = accumulate;                                                            \
-    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, nrows, jobs, \
+    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, nrows, wpr, jobs, \
                                                               epi, nullptr, nullptr,        \
                                                               nullptr, 1.0);                \
   }
