@@ -176,6 +176,70 @@ int lb_scale_inv(const double* x, const double* s, int64_t n, double* y,
                  void* stream);
 
 /* ------------------------------------------------------------------------
+ * FMM plan: FmmPlan (fmm.py:722-990) on the device.
+ *
+ * lb_fmm_plan_create builds the adaptive octree over vstack([spos, tpos]) and
+ * the colleague/V/U/W/X lists, bit-exact with _build_tree/_build_lists
+ * (fmm.py:559-715): same Morton keys, stable order, DFS-LIFO box ids, list
+ * order.  spos/tpos are HOST pointers (plan-time).  flags: LB_FMM_DEVICE_SORT
+ * computes the keys and radix-sorts them on the GPU (otherwise host).
+ * Capacity overflow -> LB_ERR_CAPACITY (FmmCapacityError, fmm.py:606-609). */
+typedef struct lb_fmm_plan lb_fmm_plan;
+#define LB_FMM_DEVICE_SORT 1
+
+enum {
+  LB_TREE_LEVEL = 0, LB_TREE_IJK, LB_TREE_PARENT, LB_TREE_IS_LEAF, LB_TREE_NSRC,
+  LB_TREE_CHILDREN_OFF, LB_TREE_CHILDREN, LB_TREE_SRC_SORTED, LB_TREE_TGT_SORTED,
+  LB_TREE_SRC_LO, LB_TREE_SRC_HI, LB_TREE_TGT_LO, LB_TREE_TGT_HI,
+  LB_TREE_COLLEAGUES_OFF, LB_TREE_COLLEAGUES, LB_TREE_V_OFF, LB_TREE_V,
+  LB_TREE_U_OFF, LB_TREE_U, LB_TREE_W_OFF, LB_TREE_W, LB_TREE_X_OFF, LB_TREE_X
+};
+
+int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos,
+                       int64_t nt, int ncrit, int buffer, int flags,
+                       lb_fmm_plan** out);
+int lb_fmm_plan_destroy(lb_fmm_plan* plan);
+/* sizes[10] = {nbox, nlevels, ns, nt, |children|, |colleagues|, |V|, |U|,
+ * |W|, |X|}; geom[4] = {center x y z, half} (HOST arrays, either may be NULL) */
+int lb_fmm_plan_info(const lb_fmm_plan* plan, int64_t* sizes, double* geom);
+/* copy one int64 tree/list array (LB_TREE_*) into a HOST buffer sized from
+ * lb_fmm_plan_info (per-box arrays: nbox; *_OFF: nbox+1; IJK: 3*nbox) */
+int lb_fmm_plan_export(const lb_fmm_plan* plan, int what, int64_t* dst);
+
+/* Unit-box translation operators (HOST arrays), as _unit_operators
+ * (fmm.py:287-354, rep = 0 "surface": pts = expansion_grid(m) (nrep,3),
+ * pinv_up/pinv_dn (nrep,nrep), m2m/l2l 8 x (nrep,nrep) in octant order
+ * 4*ox+2*oy+oz) or _unit_operators_grid (fmm.py:431-481, rep = 1 "grid":
+ * pts = Chebyshev tensor grid (n^3,3), m2m = m2m_1d 2 x (n,n), vinv (n,n),
+ * pinv_up/pinv_dn/l2l unused).  canon: ncanon canonical M2L matrices
+ * (nrep,nrep); per lattice offset d (noff of them, off_vec (noff,3)):
+ * off_key = its canonical matrix, off_perm (nrep) with
+ * K_d[i,j] = canon[off_key][perm[i], perm[j]]. */
+typedef struct {
+  int rep, m, nrep;
+  const double *pts, *pinv_up, *pinv_dn, *m2m, *l2l;
+  int ncanon;
+  const double* canon;
+  int noff;
+  const int32_t *off_vec, *off_key, *off_perm;
+  const double* vinv;
+} lb_fmm_ops;
+int lb_fmm_plan_set_operators(lb_fmm_plan* plan, const lb_fmm_ops* ops);
+/* FmmPlan.apply (fmm.py:784-990): charges (nd,ns) / dipoles (nd,ns,3) in the
+ * plan's source order (DEVICE; NULL when the mask is 0), outputs pot (nd,nt),
+ * grad (nd,nt,3), hess (nd,nt,3,3) in target order (DEVICE, overwritten).
+ * level 0/1/2 as lb_p2p.  nd <= 32 (processed in chunks of 4). */
+int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
+                 const double* dipoles, int nd, uint32_t cmask, uint32_t dmask,
+                 int level, double* pot, double* grad, double* hess,
+                 void* stream);
+/* device time of each stage of the last apply, ms (HOST double[8]):
+ * gather+P2M, M2M, M2L, X, L2L, leaf (L2T+W+U), scatter, total.  Recorded
+ * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */
+int lb_fmm_plan_set_timing(lb_fmm_plan* plan, int on);
+int lb_fmm_stage_times(const lb_fmm_plan* plan, double* ms);
+
+/* ------------------------------------------------------------------------
  * Hardware probes (no reference counterpart): FP64 FMA-pipe peak
  * (flops = blocks*256*iters*256) and the 1/sqrt seed/refinement, used to state
  * the measured fp64 roofline and the kernel's rsqrt accuracy. */

@@ -33,11 +33,13 @@ def _nvcc():
 
 
 def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) +
+                  glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
 def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + \
+        sorted(glob.glob(os.path.join(CSRC, "*.h"))) + \
         sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
@@ -52,7 +54,8 @@ def build(force=False, verbose=True, extra=()):
     if not force and not needs_build():
         return LIB
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *sources(), "-lcudart"]
+           "-o", LIB + ".tmp", *sources(), "-lcudart", "-lcublas",
+           "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -1,0 +1,1035 @@
+// FmmPlan.apply (fmm.py:784-990) on the B200.
+//
+//   gather   : charges/dipoles into Morton-sorted source order (one pass)
+//   P2M      : surface: check potentials at the UC lattice of every source
+//              leaf (pairwise kernel) then one DGEMM with pinv_up;
+//              grid: Lagrange anterpolation kernel (charges + dipole terms)
+//   M2M      : per (level, octant) DGEMM (surface) / separable 3x1-D kernel
+//              (grid), children accumulated in octant order like fmm.py:853-871
+//   M2L      : pairs grouped by CANONICAL offset across all levels: gather with
+//              the inverse cube-symmetry permutation (and 1/h), ONE DGEMM with
+//              the canonical matrix, deterministic per-target accumulation
+//              through the forward permutation (no permuted matrix is ever
+//              built; the reference spends most of a config-2 apply there)
+//   X        : source leaves -> downward check points (pairwise kernel)
+//   L2L      : per level DGEMM with pinv_dn (surface; grid: local = dcheck),
+//              per (level, octant) DGEMM / separable kernel into the children
+//   leaf     : grid L2T (value/grad/hess of the Chebyshev interpolant), then ONE
+//              pairwise kernel per target leaf over U-list sources, the own
+//              downward-equivalent charges (surface) and W-list equivalent
+//              charges, exactly the fused leaf stage of fmm.py:937-988
+//   scatter  : sorted targets -> reference layout (pot, grad, full hess)
+//
+// DGEMMs are plain cuBLAS calls; every other stage is a hand-written kernel.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "fmm_plan.h"
+#include "lb_common.cuh"
+#include "p2p_core.cuh"
+
+namespace lb {
+
+#define LB_BLAS(expr)                                                              \
+  do {                                                                             \
+    cublasStatus_t _s = (expr);                                                    \
+    if (_s != CUBLAS_STATUS_SUCCESS)                                               \
+      return fail(LB_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string((int)_s)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// small device helpers
+
+__global__ void gather_sources_kernel(const double* __restrict__ charges,
+                                      const double* __restrict__ dipoles,
+                                      const int64_t* __restrict__ src_sorted, int64_t ns, int nd,
+                                      int d0, uint32_t cmask, uint32_t dmask, double* __restrict__ cs,
+                                      double* __restrict__ vs) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= ns) return;
+  const int64_t o = src_sorted[p];
+  for (int l = 0; l < nd; ++l) {
+    const int d = d0 + l;
+    cs[(int64_t)l * ns + p] = ((cmask >> d) & 1u) ? charges[(int64_t)d * ns + o] : 0.0;
+    const bool on = (dmask >> d) & 1u;
+    for (int k = 0; k < 3; ++k)
+      vs[((int64_t)l * ns + p) * 3 + k] = on ? dipoles[((int64_t)d * ns + o) * 3 + k] : 0.0;
+  }
+}
+
+// dst[cols[c]*ld + r] (+)= src[c*ld + r] for c < ncols, r < ld
+__global__ void scatter_cols_kernel(const double* __restrict__ src, const int64_t* __restrict__ boxes,
+                                    int64_t nbox_list, int nd, int ld, double* __restrict__ dst,
+                                    int add) {
+  const int64_t c = blockIdx.x;  // (box, density) column
+  if (c >= nbox_list * nd) return;
+  const int64_t b = boxes[c / nd];
+  const int l = (int)(c % nd);
+  const double* s = src + c * ld;
+  double* d = dst + (b * nd + l) * (int64_t)ld;
+  for (int r = threadIdx.x; r < ld; r += blockDim.x) d[r] = add ? d[r] + s[r] : s[r];
+}
+
+__global__ void gather_cols_kernel(const double* __restrict__ src, const int64_t* __restrict__ boxes,
+                                   int64_t nbox_list, int nd, int ld, double* __restrict__ dst) {
+  const int64_t c = blockIdx.x;
+  if (c >= nbox_list * nd) return;
+  const int64_t b = boxes[c / nd];
+  const int l = (int)(c % nd);
+  const double* s = src + (b * nd + l) * (int64_t)ld;
+  double* d = dst + c * ld;
+  for (int r = threadIdx.x; r < ld; r += blockDim.x) d[r] = s[r];
+}
+
+// ---------------------------------------------------------------------------
+// potentials at lattice points from real sources (P2M check, X list)
+
+// out[(box_col*nd + l)*nrep + i] (+)= scale * sum_j pot_l(x_i; sources of the
+// listed leaves).  Points x_i = center(box) + fac*half(box)*pts[i].
+template <int ND>
+__global__ void __launch_bounds__(128) lattice_pot_kernel(
+    const int64_t* __restrict__ boxes, const int64_t* __restrict__ src_off,
+    const int64_t* __restrict__ src_boxes, int single, const double* __restrict__ bctr,
+    const double* __restrict__ bhalf, const int64_t* __restrict__ bsrc,
+    const double* __restrict__ spos, const double* __restrict__ cs, const double* __restrict__ vs,
+    int64_t ns, int hd, const double* __restrict__ pts, int nrep, double fac, int scale_by_h,
+    double* __restrict__ out, int out_by_box, int add) {
+  constexpr int TS = 64;
+  __shared__ double sh[TS][3 + 4 * ND];
+  const int64_t bi = blockIdx.x;
+  const int64_t b = boxes[bi];
+  const double h = bhalf[b];
+  const double cx = bctr[3 * b], cy = bctr[3 * b + 1], cz = bctr[3 * b + 2];
+  const int64_t lb = single ? bi : src_off[bi];
+  const int64_t le = single ? bi + 1 : src_off[bi + 1];
+  for (int i0 = 0; i0 < nrep; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool in = i < nrep;
+    const double px = in ? cx + fac * h * pts[3 * i] : 0.0;
+    const double py = in ? cy + fac * h * pts[3 * i + 1] : 0.0;
+    const double pz = in ? cz + fac * h * pts[3 * i + 2] : 0.0;
+    double acc[ND];
+#pragma unroll
+    for (int l = 0; l < ND; ++l) acc[l] = 0.0;
+    for (int64_t q = lb; q < le; ++q) {
+      const int64_t sb = single ? b : src_boxes[q];
+      const int64_t s0 = bsrc[2 * sb], s1 = bsrc[2 * sb + 1];
+      for (int64_t t0 = s0; t0 < s1; t0 += TS) {
+        const int n = (int)min((int64_t)TS, s1 - t0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+          const int64_t j = t0 + k;
+          sh[k][0] = spos[3 * j];
+          sh[k][1] = spos[3 * j + 1];
+          sh[k][2] = spos[3 * j + 2];
+#pragma unroll
+          for (int l = 0; l < ND; ++l) {
+            sh[k][3 + l] = cs[(int64_t)l * ns + j];
+            if (hd) {
+              sh[k][3 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3];
+              sh[k][4 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 1];
+              sh[k][5 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 2];
+            }
+          }
+        }
+        __syncthreads();
+        for (int k = 0; k < n; ++k) {
+          const double r0 = px - sh[k][0], r1 = py - sh[k][1], r2 = pz - sh[k][2];
+          const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+          const double invr = inv_sqrt_skip(rr);
+          const double invr3 = invr * invr * invr;
+#pragma unroll
+          for (int l = 0; l < ND; ++l) {
+            acc[l] = fma(sh[k][3 + l], invr, acc[l]);
+            if (hd) {
+              const double vr = fma(sh[k][5 + ND + 3 * l], r2,
+                                    fma(sh[k][4 + ND + 3 * l], r1, sh[k][3 + ND + 3 * l] * r0));
+              acc[l] = fma(vr, invr3, acc[l]);
+            }
+          }
+        }
+      }
+    }
+    if (in) {
+      const double s = scale_by_h ? h : 1.0;
+      const int64_t col = out_by_box ? b : bi;
+#pragma unroll
+      for (int l = 0; l < ND; ++l) {
+        double* o = out + (col * ND + l) * (int64_t)nrep + i;
+        *o = add ? *o + s * acc[l] : s * acc[l];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Chebyshev-grid representation kernels (fmm.py:389-533)
+
+// Lagrange basis at Chebyshev nodes: L = T @ vinv, with derivatives
+// (fmm.py:393-428); n <= 16
+__device__ void lag_basis(int n, const double* __restrict__ vinv, double x, double* L, double* dL,
+                          double* d2L, int nderiv) {
+  double t[16], dt[16], d2t[16];
+  t[0] = 1.0; dt[0] = 0.0; d2t[0] = 0.0;
+  if (n > 1) { t[1] = x; dt[1] = 1.0; d2t[1] = 0.0; }
+  for (int k = 2; k < n; ++k) {
+    t[k] = 2.0 * x * t[k - 1] - t[k - 2];
+    dt[k] = 2.0 * t[k - 1] + 2.0 * x * dt[k - 1] - dt[k - 2];
+    d2t[k] = 4.0 * dt[k - 1] + 2.0 * x * d2t[k - 1] - d2t[k - 2];
+  }
+  for (int a = 0; a < n; ++a) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double v = vinv[k * n + a];
+      s0 += t[k] * v;
+      if (nderiv >= 1) s1 += dt[k] * v;
+      if (nderiv >= 2) s2 += d2t[k] * v;
+    }
+    L[a] = s0;
+    if (nderiv >= 1) dL[a] = s1;
+    if (nderiv >= 2) d2L[a] = s2;
+  }
+}
+
+// P2M grid anterpolation (fmm.py:484-504): one block per source leaf,
+// W[(a*n+b)*n+c, l] = sum_j Lx Ly Lz q + (1/h) (dLx Ly Lz vx + ...)
+template <int ND>
+__global__ void __launch_bounds__(256) p2m_grid_kernel(
+    const int64_t* __restrict__ leaves, const double* __restrict__ bctr,
+    const double* __restrict__ bhalf, const int64_t* __restrict__ bsrc,
+    const double* __restrict__ spos, const double* __restrict__ cs, const double* __restrict__ vs,
+    int64_t ns, int hd, int n, const double* __restrict__ vinv, double* __restrict__ up) {
+  constexpr int TJ = 16;
+  __shared__ double Ls[TJ][3][16], dLs[TJ][3][16];
+  __shared__ double q[TJ][ND], v[TJ][ND][3];
+  const int64_t b = leaves[blockIdx.x];
+  const double h = bhalf[b], ih = 1.0 / h;
+  const double c[3] = {bctr[3 * b], bctr[3 * b + 1], bctr[3 * b + 2]};
+  const int64_t s0 = bsrc[2 * b], s1 = bsrc[2 * b + 1];
+  const int nrep = n * n * n;
+  for (int o0 = 0; o0 < nrep; o0 += blockDim.x) {
+    const int o = o0 + threadIdx.x;
+    const int ia = o / (n * n), ib = (o / n) % n, ic = o % n;
+    double acc[ND];
+#pragma unroll
+    for (int l = 0; l < ND; ++l) acc[l] = 0.0;
+    for (int64_t j0 = s0; j0 < s1; j0 += TJ) {
+      const int nj = (int)min((int64_t)TJ, s1 - j0);
+      __syncthreads();
+      if (threadIdx.x < nj * 3) {
+        const int jj = threadIdx.x / 3, ax = threadIdx.x % 3;
+        const double tloc = (spos[3 * (j0 + jj) + ax] - c[ax]) / h;  // fmm.py:832
+        double d2[16];
+        lag_basis(n, vinv, tloc, Ls[jj][ax], dLs[jj][ax], d2, hd ? 1 : 0);
+      }
+      if (threadIdx.x < nj * ND) {
+        const int jj = threadIdx.x / ND, l = threadIdx.x % ND;
+        q[jj][l] = cs[(int64_t)l * ns + j0 + jj];
+        for (int k = 0; k < 3; ++k) v[jj][l][k] = hd ? vs[((int64_t)l * ns + j0 + jj) * 3 + k] : 0.0;
+      }
+      __syncthreads();
+      if (o < nrep) {
+        for (int jj = 0; jj < nj; ++jj) {
+          const double lx = Ls[jj][0][ia], ly = Ls[jj][1][ib], lz = Ls[jj][2][ic];
+          const double w = lx * ly * lz;
+#pragma unroll
+          for (int l = 0; l < ND; ++l) {
+            acc[l] = fma(w, q[jj][l], acc[l]);
+            if (hd) {
+              const double g = dLs[jj][0][ia] * ly * lz * v[jj][l][0] +
+                               lx * dLs[jj][1][ib] * lz * v[jj][l][1] +
+                               lx * ly * dLs[jj][2][ic] * v[jj][l][2];
+              acc[l] = fma(ih, g, acc[l]);
+            }
+          }
+        }
+      }
+    }
+    if (o < nrep) {
+#pragma unroll
+      for (int l = 0; l < ND; ++l) up[(b * ND + l) * (int64_t)nrep + o] = acc[l];
+    }
+  }
+}
+
+// separable 3 x 1-D transform of one n^3 block (per (child,parent) pair):
+//   mode 0 (M2M, fmm.py:866-868): dst_p[a,b,c] += sum_def F0[d,a] F1[e,b] F2[f,c] src_c[d,e,f]
+//   mode 1 (L2L, fmm.py:930-932): dst_c[d,e,f] += sum_abc F0[d,a] F1[e,b] F2[f,c] src_p[a,b,c]
+// F_k = m2m_1d[octant bit k] (n x n: child node x parent basis)
+template <int ND>
+__global__ void __launch_bounds__(256) grid_tensor_kernel(const int64_t* __restrict__ child,
+                                                          const int64_t* __restrict__ parent,
+                                                          const int64_t* __restrict__ octant_of,
+                                                          const double* __restrict__ f1d, int n,
+                                                          const double* __restrict__ src,
+                                                          double* __restrict__ dst, int mode) {
+  extern __shared__ double sm[];
+  const int n3 = n * n * n;
+  double* A = sm;        // n^3
+  double* B = sm + n3;   // n^3
+  const int64_t c = child[blockIdx.x], p = parent[blockIdx.x];
+  const int oct = (int)octant_of[c];
+  const double* F[3] = {f1d + (oct & 1) * n * n, f1d + ((oct >> 1) & 1) * n * n,
+                        f1d + ((oct >> 2) & 1) * n * n};
+  const int64_t sbox = mode == 0 ? c : p, dbox = mode == 0 ? p : c;
+  for (int l = 0; l < ND; ++l) {
+    const double* s = src + (sbox * ND + l) * (int64_t)n3;
+    __syncthreads();
+    for (int o = threadIdx.x; o < n3; o += blockDim.x) A[o] = s[o];
+    __syncthreads();
+    // contract axis 2, then 1, then 0; M(u,v) = F[u*n+v] (row = child node)
+    for (int o = threadIdx.x; o < n3; o += blockDim.x) {  // B[i,j,z] over A[i,j,k]
+      const int i = o / (n * n), j = (o / n) % n, z = o % n;
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k)
+        acc += (mode == 0 ? F[2][k * n + z] : F[2][z * n + k]) * A[(i * n + j) * n + k];
+      B[o] = acc;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < n3; o += blockDim.x) {  // A[i,y,z] over B[i,j,z]
+      const int i = o / (n * n), y = (o / n) % n, z = o % n;
+      double acc = 0.0;
+      for (int j = 0; j < n; ++j)
+        acc += (mode == 0 ? F[1][j * n + y] : F[1][y * n + j]) * B[(i * n + j) * n + z];
+      A[o] = acc;
+    }
+    __syncthreads();
+    double* d = dst + (dbox * ND + l) * (int64_t)n3;
+    for (int o = threadIdx.x; o < n3; o += blockDim.x) {  // out[x,y,z] over A[i,y,z]
+      const int x = o / (n * n), yz = o % (n * n);
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i)
+        acc += (mode == 0 ? F[0][i * n + x] : F[0][x * n + i]) * A[i * n * n + yz];
+      d[o] += acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// M2L staging
+
+// X[(pi*nd+l)*nrep + p] = scale(pi) * up[src(pi), l, perm_inv[off(pi), p]]
+__global__ void m2l_gather_kernel(const double* __restrict__ up, const int64_t* __restrict__ vsrc,
+                                  const int32_t* __restrict__ voff, const double* __restrict__ vscale,
+                                  const int32_t* __restrict__ perm_inv, int64_t p0, int64_t np, int nd,
+                                  int nrep, double* __restrict__ X) {
+  const int64_t col = blockIdx.x;  // local pair*nd + l
+  if (col >= np * nd) return;
+  const int64_t pi = p0 + col / nd;
+  const int l = (int)(col % nd);
+  const double* u = up + (vsrc[pi] * nd + l) * (int64_t)nrep;
+  const int32_t* pv = perm_inv + (int64_t)voff[pi] * nrep;
+  const double s = vscale[pi];
+  double* x = X + col * (int64_t)nrep;
+  for (int p = threadIdx.x; p < nrep; p += blockDim.x) x[p] = s * u[pv[p]];
+}
+
+// per unique target t of the chunk: dc[t,l,i] += sum over its pairs (fixed
+// order) of Y[(pi-p0)*nd+l, perm[off(pi), i]]
+__global__ void m2l_accum_kernel(const double* __restrict__ Y, const int64_t* __restrict__ vtgts,
+                                 const int64_t* __restrict__ tpair_off, const int32_t* __restrict__ voff,
+                                 const int32_t* __restrict__ perm, int64_t t0, int64_t p0, int nd,
+                                 int nrep, double* __restrict__ dc) {
+  const int64_t ti = t0 + blockIdx.x;
+  const int64_t tb = vtgts[ti];
+  const int64_t pb = tpair_off[ti], pe = tpair_off[ti + 1];
+  for (int l = 0; l < nd; ++l) {
+    double* d = dc + (tb * nd + l) * (int64_t)nrep;
+    for (int i = threadIdx.x; i < nrep; i += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t pi = pb; pi < pe; ++pi)
+        acc += Y[((pi - p0) * nd + l) * (int64_t)nrep + perm[(int64_t)voff[pi] * nrep + i]];
+      d[i] += acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// leaf stage
+
+// grid L2T (fmm.py:507-533): tout[l, t, comp] += interpolant of local[b]
+template <int ND>
+__global__ void __launch_bounds__(64) l2t_grid_kernel(
+    const int64_t* __restrict__ leaves, const double* __restrict__ bctr,
+    const double* __restrict__ bhalf, const int64_t* __restrict__ btgt,
+    const double* __restrict__ tpos, int64_t nt, int n, const double* __restrict__ vinv,
+    const double* __restrict__ loc, int level, double* __restrict__ tout) {
+  const int64_t b = leaves[blockIdx.x];
+  const double h = bhalf[b], ih = 1.0 / h;
+  const double c[3] = {bctr[3 * b], bctr[3 * b + 1], bctr[3 * b + 2]};
+  const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
+  const int nrep = n * n * n;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    double L[3][3][16];  // [axis][deriv][node]
+    for (int ax = 0; ax < 3; ++ax)
+      lag_basis(n, vinv, (tpos[3 * t + ax] - c[ax]) / h, L[ax][0], L[ax][1], L[ax][2], level);
+    for (int l = 0; l < ND; ++l) {
+      const double* w = loc + (b * ND + l) * (int64_t)nrep;
+      double r[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int ia = 0; ia < n; ++ia) {
+        double s[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // [dy][dz] after y,z contraction
+        for (int ib = 0; ib < n; ++ib) {
+          double z0 = 0, z1 = 0, z2 = 0;
+          const double* wr = w + (ia * n + ib) * n;
+          for (int ic = 0; ic < n; ++ic) {
+            z0 = fma(L[2][0][ic], wr[ic], z0);
+            if (level >= 1) z1 = fma(L[2][1][ic], wr[ic], z1);
+            if (level >= 2) z2 = fma(L[2][2][ic], wr[ic], z2);
+          }
+          s[0][0] = fma(L[1][0][ib], z0, s[0][0]);
+          if (level >= 1) {
+            s[0][1] = fma(L[1][0][ib], z1, s[0][1]);
+            s[1][0] = fma(L[1][1][ib], z0, s[1][0]);
+          }
+          if (level >= 2) {
+            s[0][2] = fma(L[1][0][ib], z2, s[0][2]);
+            s[1][1] = fma(L[1][1][ib], z1, s[1][1]);
+            s[2][0] = fma(L[1][2][ib], z0, s[2][0]);
+          }
+        }
+        r[0] = fma(L[0][0][ia], s[0][0], r[0]);
+        if (level >= 1) {
+          r[1] = fma(L[0][1][ia], s[0][0], r[1]);  // d/dx
+          r[2] = fma(L[0][0][ia], s[1][0], r[2]);  // d/dy
+          r[3] = fma(L[0][0][ia], s[0][1], r[3]);  // d/dz
+        }
+        if (level >= 2) {
+          r[4] = fma(L[0][2][ia], s[0][0], r[4]);  // xx
+          r[5] = fma(L[0][0][ia], s[2][0], r[5]);  // yy
+          r[6] = fma(L[0][0][ia], s[0][2], r[6]);  // zz
+          r[7] = fma(L[0][1][ia], s[1][0], r[7]);  // xy
+          r[8] = fma(L[0][1][ia], s[0][1], r[8]);  // xz
+          r[9] = fma(L[0][0][ia], s[1][1], r[9]);  // yz
+        }
+      }
+      double* o = tout + ((int64_t)l * nt + t) * 10;
+      o[0] += r[0];
+      if (level >= 1)
+        for (int k = 1; k < 4; ++k) o[k] += ih * r[k];
+      if (level >= 2)
+        for (int k = 4; k < 10; ++k) o[k] += ih * ih * r[k];
+    }
+  }
+}
+
+// fused leaf P2P (fmm.py:947-988): U-list real sources, own DE equivalent
+// charges (surface), W-list equivalent charges
+template <int ND, bool HD, int LEVEL>
+__global__ void __launch_bounds__(64) leaf_kernel(
+    const int64_t* __restrict__ leaves, const int64_t* __restrict__ u_off,
+    const int64_t* __restrict__ u_list, const int64_t* __restrict__ w_off,
+    const int64_t* __restrict__ w_list, const double* __restrict__ bctr,
+    const double* __restrict__ bhalf, const int64_t* __restrict__ bsrc,
+    const int64_t* __restrict__ btgt, const double* __restrict__ spos,
+    const double* __restrict__ tpos, const double* __restrict__ cs, const double* __restrict__ vs,
+    int64_t ns, int64_t nt, const double* __restrict__ pts, int nrep, int surface, double de_scale,
+    double ue_scale, const double* __restrict__ loc, const double* __restrict__ up,
+    double* __restrict__ tout) {
+  using Lay = SrcLayout<ND, true, HD>;
+  constexpr int S = Lay::stride;
+  constexpr int NC = ncomp(LEVEL);
+  constexpr int TS = 64;
+  __shared__ __align__(16) double sh[TS * S];
+  const int64_t b = leaves[blockIdx.x];
+  const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
+  const int64_t nu = u_off[blockIdx.x + 1] - u_off[blockIdx.x];
+  const int64_t nw = w_off[blockIdx.x + 1] - w_off[blockIdx.x];
+  for (int64_t tb = t0; tb < t1; tb += blockDim.x) {
+    const int64_t t = tb + threadIdx.x;
+    const bool in = t < t1;
+    const double tx = in ? tpos[3 * t] : 0.0, ty = in ? tpos[3 * t + 1] : 0.0,
+                 tz = in ? tpos[3 * t + 2] : 0.0;
+    double acc[ND * NC];
+#pragma unroll
+    for (int a = 0; a < ND * NC; ++a) acc[a] = 0.0;
+    // source sets: U leaves, then (surface) own DE set, then W sets
+    const int64_t nsets = nu + (surface ? 1 : 0) + nw;
+    for (int64_t q = 0; q < nsets; ++q) {
+      bool real = q < nu;
+      int64_t s0, s1, eb = -1;
+      const double* eq = nullptr;
+      double fac = 0.0;
+      if (real) {
+        const int64_t sb = u_list[u_off[blockIdx.x] + q];
+        s0 = bsrc[2 * sb];
+        s1 = bsrc[2 * sb + 1];
+      } else if (surface && q == nu) {
+        eb = b; eq = loc; fac = de_scale; s0 = 0; s1 = nrep;
+      } else {
+        eb = w_list[w_off[blockIdx.x] + (q - nu - (surface ? 1 : 0))];
+        eq = up; fac = ue_scale; s0 = 0; s1 = nrep;
+      }
+      for (int64_t j0 = s0; j0 < s1; j0 += TS) {
+        const int n = (int)min((int64_t)TS, s1 - j0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+          double* r = sh + k * S;
+          const int64_t j = j0 + k;
+          if (real) {
+            r[0] = spos[3 * j]; r[1] = spos[3 * j + 1]; r[2] = spos[3 * j + 2];
+          } else {
+            const double h = bhalf[eb];
+            r[0] = bctr[3 * eb] + fac * h * pts[3 * j];
+            r[1] = bctr[3 * eb + 1] + fac * h * pts[3 * j + 1];
+            r[2] = bctr[3 * eb + 2] + fac * h * pts[3 * j + 2];
+          }
+          int o = 3;
+#pragma unroll
+          for (int l = 0; l < ND; ++l) {
+            r[o++] = real ? cs[(int64_t)l * ns + j] : eq[(eb * ND + l) * (int64_t)nrep + j];
+            if (HD) {
+              for (int kk = 0; kk < 3; ++kk) r[o++] = real ? vs[((int64_t)l * ns + j) * 3 + kk] : 0.0;
+            }
+          }
+        }
+        __syncthreads();
+        for (int k = 0; k < n; ++k) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+      }
+    }
+    if (in) {
+#pragma unroll
+      for (int l = 0; l < ND; ++l) {
+        double* o = tout + ((int64_t)l * nt + t) * 10;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) o[c] += acc[l * NC + c];
+      }
+    }
+  }
+}
+
+// sorted targets -> reference layout
+__global__ void fmm_scatter_kernel(const double* __restrict__ tout, const int64_t* __restrict__ tgt_sorted,
+                                   int64_t nt, int nd, int d0, int level, double* __restrict__ pot,
+                                   double* __restrict__ grad, double* __restrict__ hess) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nd * nt) return;
+  const int l = (int)(idx / nt);
+  const int64_t t = idx - (int64_t)l * nt;
+  const double* v = tout + idx * 10;
+  const int64_t row = (int64_t)(d0 + l) * nt + tgt_sorted[t];
+  pot[row] = v[0];
+  if (level >= 1)
+    for (int k = 0; k < 3; ++k) grad[row * 3 + k] = v[1 + k];
+  if (level >= 2) {
+    const double hv[9] = {v[4], v[7], v[8], v[7], v[5], v[9], v[8], v[9], v[6]};
+    for (int k = 0; k < 9; ++k) hess[row * 9 + k] = hv[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: device state
+
+namespace {
+
+template <class T>
+int upload(T** dst, const std::vector<T>& v) {
+  cudaError_t e = cudaMalloc((void**)dst, std::max<size_t>(v.size() * sizeof(T), 16));
+  if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("fmm upload: ") + cudaGetErrorString(e));
+  return LB_OK;
+}
+
+int build_device(lb_fmm_plan* P) {
+  FmmTree& t = P->tree;
+  FmmDevice& D = P->dev;
+  const int64_t nb = t.nbox();
+  const int nrep = P->nrep;
+  // slots: boxes level by level (ascending id within a level)
+  P->slot_of.assign(nb, -1);
+  P->id_of.clear();
+  std::vector<int64_t> level_slot_off{0};
+  for (int l = 0; l < t.nlev; ++l) {
+    for (int64_t b : t.levels[l]) {
+      P->slot_of[b] = (int64_t)P->id_of.size();
+      P->id_of.push_back(b);
+    }
+    level_slot_off.push_back((int64_t)P->id_of.size());
+  }
+  const auto& S = P->slot_of;
+  std::vector<double> ctr(3 * nb), hf(nb), spos_s(3 * t.ns), tpos_s(3 * t.nt);
+  std::vector<int64_t> bsrc(2 * nb), btgt(2 * nb), octant(nb, 0);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t s = S[b];
+    t.box_center(b, &ctr[3 * s]);
+    hf[s] = t.box_half(b);
+    bsrc[2 * s] = t.src_lo[b];
+    bsrc[2 * s + 1] = t.src_hi[b];
+    btgt[2 * s] = t.tgt_lo[b];
+    btgt[2 * s + 1] = t.tgt_hi[b];
+    if (b > 0) {
+      const int64_t p = t.parent[b];
+      const int ox = (int)(t.ijk[3 * b] - 2 * t.ijk[3 * p]);
+      const int oy = (int)(t.ijk[3 * b + 1] - 2 * t.ijk[3 * p + 1]);
+      const int oz = (int)(t.ijk[3 * b + 2] - 2 * t.ijk[3 * p + 2]);
+      octant[s] = ox | (oy << 1) | (oz << 2);  // bit k = offset along axis k
+    }
+  }
+  for (int64_t p = 0; p < t.ns; ++p)
+    for (int k = 0; k < 3; ++k) spos_s[3 * p + k] = P->spos[3 * t.src_sorted[p] + k];
+  for (int64_t p = 0; p < t.nt; ++p)
+    for (int k = 0; k < 3; ++k) tpos_s[3 * p + k] = P->tpos[3 * t.tgt_sorted[p] + k];
+  LB_TRY(upload(&D.spos, spos_s));
+  LB_TRY(upload(&D.tpos, tpos_s));
+  LB_TRY(upload(&D.src_sorted, t.src_sorted));
+  LB_TRY(upload(&D.tgt_sorted, t.tgt_sorted));
+  LB_TRY(upload(&D.bctr, ctr));
+  LB_TRY(upload(&D.bhalf, hf));
+  LB_TRY(upload(&D.bsrc, bsrc));
+  LB_TRY(upload(&D.btgt, btgt));
+  int64_t* doct = nullptr;
+  LB_TRY(upload(&doct, octant));
+  D.vinv = nullptr;
+  // operators
+  LB_TRY(upload(&D.pts, P->pts));
+  if (P->rep == 0) {
+    LB_TRY(upload(&D.pinv_up, P->pinv_up));
+    LB_TRY(upload(&D.pinv_dn, P->pinv_dn));
+    LB_TRY(upload(&D.l2l, P->l2l));
+  } else {
+    LB_TRY(upload(&D.vinv, P->vinv));
+  }
+  LB_TRY(upload(&D.m2m, P->m2m));
+  LB_TRY(upload(&D.canon, P->canon));
+  std::vector<int32_t> pinv(P->off_perm.size());
+  for (int d = 0; d < P->noff; ++d)
+    for (int i = 0; i < nrep; ++i) pinv[(int64_t)d * nrep + P->off_perm[(int64_t)d * nrep + i]] = i;
+  LB_TRY(upload(&D.perm, P->off_perm));
+  LB_TRY(upload(&D.perm_inv, pinv));
+  // P2M leaves (fmm.py:826) and M2M / L2L groups per (level, octant)
+  std::vector<int64_t> p2m;
+  for (int64_t b = 0; b < nb; ++b)
+    if (t.is_leaf[b] && t.src_hi[b] > t.src_lo[b]) p2m.push_back(S[b]);
+  D.n_p2m = (int64_t)p2m.size();
+  LB_TRY(upload(&D.p2m_leaves, p2m));
+  std::vector<int64_t> uc, upar, dch, dpar;
+  D.up_off.assign(1, 0);
+  D.dn_off.assign(1, 0);
+  for (int l = 0; l < t.nlev; ++l) {
+    for (int oct = 0; oct < 8; ++oct) {
+      for (int64_t b : (l > 0 ? t.levels[l] : std::vector<int64_t>{})) {
+        const int64_t s = S[b];
+        if (octant[s] != oct) continue;
+        const int64_t p = t.parent[b];
+        if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) {  // fmm.py:855-859
+          uc.push_back(s);
+          upar.push_back(S[p]);
+        }
+        dch.push_back(s);  // fmm.py:923-935: every child
+        dpar.push_back(S[p]);
+      }
+      D.up_off.push_back((int64_t)uc.size());
+      D.dn_off.push_back((int64_t)dch.size());
+    }
+  }
+  LB_TRY(upload(&D.up_child, uc));
+  LB_TRY(upload(&D.up_parent, upar));
+  LB_TRY(upload(&D.dn_child, dch));
+  LB_TRY(upload(&D.dn_parent, dpar));
+  // M2L pairs: offset index of each lattice offset
+  std::map<std::tuple<int, int, int>, int> off_index;
+  for (int d = 0; d < P->noff; ++d)
+    off_index[{P->off_vec[3 * d], P->off_vec[3 * d + 1], P->off_vec[3 * d + 2]}] = d;
+  struct Pair { int64_t tgt, src; int32_t off; double scale; };
+  std::vector<std::vector<Pair>> by_key(P->ncanon);
+  for (int l = 0; l < t.nlev; ++l) {
+    const double hl = t.half / std::ldexp(1.0, l);  // fmm.py:879
+    for (int64_t b : t.levels[l]) {
+      for (int64_t q = 0; q < t.vlist.size(b); ++q) {
+        const int64_t s = t.vlist.row(b)[q];
+        const int dx = (int)(t.ijk[3 * s] - t.ijk[3 * b]);
+        const int dy = (int)(t.ijk[3 * s + 1] - t.ijk[3 * b + 1]);
+        const int dz = (int)(t.ijk[3 * s + 2] - t.ijk[3 * b + 2]);
+        auto it = off_index.find({dx, dy, dz});
+        if (it == off_index.end()) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
+        const int d = it->second;
+        by_key[P->off_key[d]].push_back({S[b], S[s], d, 1.0 / hl});
+      }
+    }
+  }
+  std::vector<int64_t> vsrc, vtgts, tpoff{0};
+  std::vector<int32_t> voff;
+  std::vector<double> vscale;
+  D.v_key_pair_off.assign(1, 0);
+  D.v_key_tgt_off.assign(1, 0);
+  D.max_key_pairs = 0;
+  for (int k = 0; k < P->ncanon; ++k) {
+    auto& v = by_key[k];
+    std::stable_sort(v.begin(), v.end(), [](const Pair& a, const Pair& b) { return a.tgt < b.tgt; });
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (i == 0 || v[i].tgt != v[i - 1].tgt) {
+        if (i > 0) tpoff.push_back((int64_t)vsrc.size());
+        vtgts.push_back(v[i].tgt);
+      }
+      vsrc.push_back(v[i].src);
+      voff.push_back(v[i].off);
+      vscale.push_back(v[i].scale);
+    }
+    if (!v.empty()) tpoff.push_back((int64_t)vsrc.size());
+    D.v_key_pair_off.push_back((int64_t)vsrc.size());
+    D.v_key_tgt_off.push_back((int64_t)vtgts.size());
+    D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, (int64_t)v.size());
+  }
+  LB_TRY(upload(&D.v_src, vsrc));
+  LB_TRY(upload(&D.v_tgts, vtgts));
+  LB_TRY(upload(&D.v_tgt_pair_off, tpoff));
+  D.v_tpoff_host = tpoff;
+  LB_TRY(upload(&D.v_off_idx, voff));
+  LB_TRY(upload(&D.v_scale, vscale));
+  // X list (fmm.py:891-911): boxes with sourceful X entries
+  std::vector<int64_t> xb, xo{0}, xl;
+  for (int64_t b = 0; b < nb; ++b) {
+    bool any = false;
+    for (int64_t q = 0; q < t.xlist.size(b); ++q) {
+      const int64_t x = t.xlist.row(b)[q];
+      if (t.src_hi[x] > t.src_lo[x]) { any = true; xl.push_back(S[x]); }
+    }
+    if (any) { xb.push_back(S[b]); xo.push_back((int64_t)xl.size()); }
+  }
+  D.n_x = (int64_t)xb.size();
+  LB_TRY(upload(&D.x_boxes, xb));
+  LB_TRY(upload(&D.x_off, xo));
+  LB_TRY(upload(&D.x_leaves, xl));
+  // leaf stage (fmm.py:940-988): target leaves, their U (with sources) and W lists
+  std::vector<int64_t> tl, uo{0}, ul, wo{0}, wl;
+  for (int64_t b = 0; b < nb; ++b) {
+    if (!t.is_leaf[b] || t.tgt_hi[b] == t.tgt_lo[b]) continue;
+    tl.push_back(S[b]);
+    for (int64_t q = 0; q < t.ulist.size(b); ++q) {
+      const int64_t u = t.ulist.row(b)[q];
+      if (t.src_hi[u] > t.src_lo[u]) ul.push_back(S[u]);
+    }
+    uo.push_back((int64_t)ul.size());
+    for (int64_t q = 0; q < t.wlist.size(b); ++q) wl.push_back(S[t.wlist.row(b)[q]]);
+    wo.push_back((int64_t)wl.size());
+  }
+  D.n_tleaf = (int64_t)tl.size();
+  LB_TRY(upload(&D.t_leaves, tl));
+  LB_TRY(upload(&D.u_off, uo));
+  LB_TRY(upload(&D.u_list, ul));
+  LB_TRY(upload(&D.w_off, wo));
+  LB_TRY(upload(&D.w_list, wl));
+  // octant per slot is needed by the grid tensor kernel: keep it in bsrc's
+  // companion buffer
+  D.btgt_oct = doct;
+  D.level_slot_off = level_slot_off;
+  if (cublasCreate(&D.blas) != CUBLAS_STATUS_SUCCESS) return fail(LB_ERR_CUDA, "cublasCreate failed");
+  D.ready = true;
+  return LB_OK;
+}
+
+int ensure_work(lb_fmm_plan* P, int nd) {
+  FmmDevice& D = P->dev;
+  if (D.nd_alloc == nd) return LB_OK;
+  cudaFree(D.cs); cudaFree(D.vs); cudaFree(D.up); cudaFree(D.dc); cudaFree(D.loc);
+  cudaFree(D.tmpA); cudaFree(D.tmpB); cudaFree(D.tout);
+  D.cs = D.vs = D.up = D.dc = D.loc = D.tmpA = D.tmpB = D.tout = nullptr;
+  const FmmTree& t = P->tree;
+  const int64_t nb = t.nbox(), nrep = P->nrep;
+  // GEMM staging: the largest of (P2M leaves, any level/octant group, M2L chunk)
+  int64_t cols = std::max<int64_t>(D.n_p2m, 1);
+  for (size_t i = 0; i + 1 < D.up_off.size(); ++i) cols = std::max(cols, D.up_off[i + 1] - D.up_off[i]);
+  for (size_t i = 0; i + 1 < D.dn_off.size(); ++i) cols = std::max(cols, D.dn_off[i + 1] - D.dn_off[i]);
+  const int64_t m2l_cap = std::max<int64_t>(1, std::min<int64_t>(D.max_key_pairs, (int64_t)1 << 17));
+  cols = std::max(cols, m2l_cap);
+  D.tmp_cols = cols;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](double** p, int64_t n) { if (e == cudaSuccess) e = cudaMalloc((void**)p, std::max<int64_t>(n, 2) * 8); };
+  A(&D.cs, (int64_t)nd * t.ns);
+  A(&D.vs, (int64_t)nd * t.ns * 3);
+  A(&D.up, nb * nd * nrep);
+  A(&D.dc, nb * nd * nrep);
+  if (P->rep == 0) A(&D.loc, nb * nd * nrep);
+  A(&D.tmpA, cols * nd * nrep);
+  A(&D.tmpB, cols * nd * nrep);
+  A(&D.tout, (int64_t)nd * t.nt * 10);
+  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("fmm work arrays: ") + cudaGetErrorString(e));
+  if (P->rep == 1) D.loc = D.dc;  // grid: local = dcheck (fmm.py:918)
+  D.nd_alloc = nd;
+  return LB_OK;
+}
+
+// child octant (x | y<<1 | z<<2, the children order of fmm.py:624-628) ->
+// index of the reference's m2m/l2l operator lists, k = 4*ox + 2*oy + oz
+// (fmm.py:307-317, 870, 934)
+inline int ref_octant(int oct) { return ((oct & 1) << 2) | (oct & 2) | ((oct >> 2) & 1); }
+
+// Y(nrep x ncols) = alpha * A(nrep x nrep, row-major) * X(nrep x ncols, col-major)
+int gemm_rm(cublasHandle_t h, const double* A, const double* X, double* Y, int nrep, int64_t ncols,
+            double alpha, double beta) {
+  if (ncols <= 0) return LB_OK;
+  LB_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nrep, (int)ncols, nrep, &alpha, A, nrep, X, nrep,
+                      &beta, Y, nrep));
+  return LB_OK;
+}
+
+template <int ND>
+int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const double* charges,
+                const double* dipoles, int level, double* pot, double* grad, double* hess,
+                cudaStream_t st, std::vector<cudaEvent_t>& ev) {
+  FmmTree& t = P->tree;
+  FmmDevice& D = P->dev;
+  const int nrep = P->nrep;
+  const int64_t nb = t.nbox();
+  const bool surface = P->rep == 0;
+  const int n = P->m;
+  const bool hd = ((dmask >> d0) & ((1u << ND) - 1u)) != 0;
+  auto mark = [&](int i) { if (!ev.empty()) cudaEventRecord(ev[i], st); };
+  mark(0);
+  // gather into sorted source order
+  if (t.ns > 0)
+    gather_sources_kernel<<<(unsigned)ceil_div(t.ns, 256), 256, 0, st>>>(
+        charges, dipoles, D.src_sorted, t.ns, ND, d0, cmask, dmask, D.cs, D.vs);
+  LB_CUDA(cudaMemsetAsync(D.up, 0, sizeof(double) * nb * ND * nrep, st));
+  LB_CUDA(cudaMemsetAsync(D.dc, 0, sizeof(double) * nb * ND * nrep, st));
+  // ---- P2M (fmm.py:823-852)
+  if (D.n_p2m > 0) {
+    if (surface) {
+      lattice_pot_kernel<ND><<<(unsigned)D.n_p2m, 128, 0, st>>>(
+          D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf, D.bsrc, D.spos, D.cs, D.vs, t.ns,
+          hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1, D.tmpA, 0, 0);
+      LB_CHECK_LAUNCH();
+      LB_TRY(gemm_rm(D.blas, D.pinv_up, D.tmpA, D.tmpB, nrep, D.n_p2m * ND, 1.0, 0.0));
+      scatter_cols_kernel<<<(unsigned)(D.n_p2m * ND), 128, 0, st>>>(D.tmpB, D.p2m_leaves, D.n_p2m, ND,
+                                                                    nrep, D.up, 0);
+      LB_CHECK_LAUNCH();
+    } else {
+      p2m_grid_kernel<ND><<<(unsigned)D.n_p2m, 256, 0, st>>>(D.p2m_leaves, D.bctr, D.bhalf, D.bsrc,
+                                                             D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, n,
+                                                             D.vinv, D.up);
+      LB_CHECK_LAUNCH();
+    }
+  }
+  mark(1);
+  // ---- M2M (fmm.py:853-871), deepest level first, octants in order
+  const size_t grid_smem = sizeof(double) * 2 * nrep;
+  for (int l = t.nlev - 1; l >= 1; --l) {
+    for (int oct = 0; oct < 8; ++oct) {
+      const int64_t g0 = D.up_off[8 * l + oct], g1 = D.up_off[8 * l + oct + 1];
+      const int64_t cnt = g1 - g0;
+      if (cnt == 0) continue;
+      if (surface) {
+        gather_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.up, D.up_child + g0, cnt, ND, nrep,
+                                                                D.tmpA);
+        LB_TRY(gemm_rm(D.blas, D.m2m + (int64_t)ref_octant(oct) * nrep * nrep, D.tmpA, D.tmpB, nrep,
+                       cnt * ND, 1.0, 0.0));
+        scatter_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.tmpB, D.up_parent + g0, cnt, ND,
+                                                                 nrep, D.up, 1);
+      } else {
+        grid_tensor_kernel<ND><<<(unsigned)cnt, 256, grid_smem, st>>>(
+            D.up_child + g0, D.up_parent + g0, D.btgt_oct, D.m2m, n, D.up, D.up, 0);
+      }
+      LB_CHECK_LAUNCH();
+    }
+  }
+  mark(2);
+  // ---- M2L (fmm.py:873-886), by canonical key, chunked at target boundaries
+  for (int k = 0; k < P->ncanon; ++k) {
+    const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
+    if (pe == pb) continue;
+    const std::vector<int64_t> tp(D.v_tpoff_host.begin() + D.v_key_tgt_off[k],
+                                  D.v_tpoff_host.begin() + D.v_key_tgt_off[k + 1] + 1);
+    int64_t ti = 0;
+    const int64_t ntg = (int64_t)tp.size() - 1;
+    while (ti < ntg) {
+      int64_t tj = ti;
+      while (tj < ntg && tp[tj + 1] - tp[ti] <= D.tmp_cols) ++tj;
+      if (tj == ti) tj = ti + 1;  // a single target with more pairs than the cap cannot occur (<= 316 offsets)
+      const int64_t p0 = tp[ti], np = tp[tj] - tp[ti];
+      m2l_gather_kernel<<<(unsigned)(np * ND), 128, 0, st>>>(D.up, D.v_src, D.v_off_idx, D.v_scale,
+                                                             D.perm_inv, p0, np, ND, nrep, D.tmpA);
+      LB_CHECK_LAUNCH();
+      LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+      m2l_accum_kernel<<<(unsigned)(tj - ti), 128, 0, st>>>(D.tmpB, D.v_tgts, D.v_tgt_pair_off,
+                                                            D.v_off_idx, D.perm,
+                                                            D.v_key_tgt_off[k] + ti, p0, ND, nrep, D.dc);
+      LB_CHECK_LAUNCH();
+      ti = tj;
+    }
+  }
+  mark(3);
+  // ---- X list (fmm.py:888-911)
+  if (D.n_x > 0) {
+    lattice_pot_kernel<ND><<<(unsigned)D.n_x, 128, 0, st>>>(
+        D.x_boxes, D.x_off, D.x_leaves, 0, D.bctr, D.bhalf, D.bsrc, D.spos, D.cs, D.vs, t.ns,
+        hd ? 1 : 0, D.pts, nrep, surface ? P->dc_scale : 1.0, 0, D.dc, 1, 1);
+    LB_CHECK_LAUNCH();
+  }
+  mark(4);
+  // ---- L2L (fmm.py:913-935)
+  for (int l = 0; l < t.nlev; ++l) {
+    const int64_t s0 = D.level_slot_off[l], s1 = D.level_slot_off[l + 1];
+    if (surface) {
+      const double hl = t.half / std::ldexp(1.0, l);
+      LB_TRY(gemm_rm(D.blas, D.pinv_dn, D.dc + s0 * ND * nrep, D.loc + s0 * ND * nrep, nrep,
+                     (s1 - s0) * ND, hl, 0.0));
+    }
+    if (l + 1 >= t.nlev) break;
+    for (int oct = 0; oct < 8; ++oct) {
+      const int64_t g0 = D.dn_off[8 * (l + 1) + oct], g1 = D.dn_off[8 * (l + 1) + oct + 1];
+      const int64_t cnt = g1 - g0;
+      if (cnt == 0) continue;
+      if (surface) {
+        const double hc = t.half / std::ldexp(1.0, l + 1);
+        gather_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.loc, D.dn_parent + g0, cnt, ND,
+                                                                nrep, D.tmpA);
+        LB_TRY(gemm_rm(D.blas, D.l2l + (int64_t)ref_octant(oct) * nrep * nrep, D.tmpA, D.tmpB, nrep,
+                       cnt * ND, 1.0 / hc, 0.0));
+        scatter_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.tmpB, D.dn_child + g0, cnt, ND,
+                                                                 nrep, D.dc, 1);
+      } else {
+        grid_tensor_kernel<ND><<<(unsigned)cnt, 256, grid_smem, st>>>(
+            D.dn_child + g0, D.dn_parent + g0, D.btgt_oct, D.m2m, n, D.loc, D.dc, 1);
+      }
+      LB_CHECK_LAUNCH();
+    }
+  }
+  mark(5);
+  // ---- leaf stage (fmm.py:937-988)
+  LB_CUDA(cudaMemsetAsync(D.tout, 0, sizeof(double) * ND * t.nt * 10, st));
+  if (D.n_tleaf > 0) {
+    if (!surface) {
+      l2t_grid_kernel<ND><<<(unsigned)D.n_tleaf, 64, 0, st>>>(D.t_leaves, D.bctr, D.bhalf, D.btgt,
+                                                             D.tpos, t.nt, n, D.vinv, D.loc, level,
+                                                             D.tout);
+      LB_CHECK_LAUNCH();
+    }
+#define LB_LEAF(HD, LV)                                                                        \
+  leaf_kernel<ND, HD, LV><<<(unsigned)D.n_tleaf, 64, 0, st>>>(                                 \
+      D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,       \
+      D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,      \
+      surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout)
+    if (hd) {
+      if (level == 0) LB_LEAF(true, 0); else if (level == 1) LB_LEAF(true, 1); else LB_LEAF(true, 2);
+    } else {
+      if (level == 0) LB_LEAF(false, 0); else if (level == 1) LB_LEAF(false, 1); else LB_LEAF(false, 2);
+    }
+#undef LB_LEAF
+    LB_CHECK_LAUNCH();
+  }
+  mark(6);
+  fmm_scatter_kernel<<<(unsigned)ceil_div((int64_t)ND * t.nt, 256), 256, 0, st>>>(
+      D.tout, D.tgt_sorted, t.nt, ND, d0, level, pot, grad, hess);
+  LB_CHECK_LAUNCH();
+  mark(7);
+  return LB_OK;
+}
+
+}  // namespace
+
+void fmm_release_device(lb_fmm_plan* P) {
+  FmmDevice& D = P->dev;
+  void* ptrs[] = {D.spos, D.tpos, D.src_sorted, D.tgt_sorted, D.bctr, D.bhalf, D.bsrc, D.btgt,
+                  D.pts, D.pinv_up, D.pinv_dn, D.m2m, D.l2l, D.canon, D.perm, D.perm_inv, D.vinv,
+                  D.p2m_leaves, D.up_child, D.up_parent, D.dn_child, D.dn_parent, D.v_src,
+                  D.v_tgt_pair_off, D.v_tgts, D.v_off_idx, D.v_scale, D.x_boxes, D.x_off,
+                  D.x_leaves, D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.cs, D.vs, D.up,
+                  D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct};
+  for (void* p : ptrs) cudaFree(p);
+  if (P->rep == 0) cudaFree(D.loc);
+  if (D.blas) cublasDestroy(D.blas);
+  D = FmmDevice();
+}
+
+}  // namespace lb
+
+using namespace lb;
+
+extern "C" {
+
+int lb_fmm_plan_set_operators(lb_fmm_plan* P, const lb_fmm_ops* o) {
+  if (!P || !o) return fail(LB_ERR_ARG, "lb_fmm_plan_set_operators: null argument");
+  if (o->rep != 0 && o->rep != 1) return fail(LB_ERR_ARG, "lb_fmm_plan_set_operators: rep must be 0 or 1");
+  if (o->rep == 1 && (o->m < 2 || o->m > 16)) return fail(LB_ERR_ARG, "grid order must be in [2, 16]");
+  const int nrep = o->nrep;
+  const int64_t nn = (int64_t)nrep * nrep;
+  fmm_release_device(P);
+  P->rep = o->rep;
+  P->m = o->m;
+  P->nrep = nrep;
+  P->pts.assign(o->pts, o->pts + 3 * nrep);
+  if (o->rep == 0) {
+    P->pinv_up.assign(o->pinv_up, o->pinv_up + nn);
+    P->pinv_dn.assign(o->pinv_dn, o->pinv_dn + nn);
+    P->m2m.assign(o->m2m, o->m2m + 8 * nn);
+    P->l2l.assign(o->l2l, o->l2l + 8 * nn);
+  } else {
+    P->m2m.assign(o->m2m, o->m2m + 2 * o->m * o->m);
+    P->vinv.assign(o->vinv, o->vinv + o->m * o->m);
+  }
+  P->ncanon = o->ncanon;
+  P->canon.assign(o->canon, o->canon + (int64_t)o->ncanon * nn);
+  P->noff = o->noff;
+  P->off_vec.assign(o->off_vec, o->off_vec + 3 * o->noff);
+  P->off_key.assign(o->off_key, o->off_key + o->noff);
+  P->off_perm.assign(o->off_perm, o->off_perm + (int64_t)o->noff * nrep);
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_timing(lb_fmm_plan* P, int on) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  P->timing = on != 0;
+  return LB_OK;
+}
+
+int lb_fmm_stage_times(const lb_fmm_plan* P, double* ms) {
+  if (!P || !ms) return fail(LB_ERR_ARG, "null argument");
+  for (int i = 0; i < 8; ++i) ms[i] = i < (int)P->stage_ms.size() ? P->stage_ms[i] : 0.0;
+  return LB_OK;
+}
+
+int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, int nd,
+                 uint32_t cmask, uint32_t dmask, int level, double* pot, double* grad,
+                 double* hess, void* stream) {
+  if (!P) return fail(LB_ERR_ARG, "lb_fmm_apply: null plan");
+  if (P->rep < 0) return fail(LB_ERR_ARG, "lb_fmm_apply: operators not set");
+  if (nd <= 0 || nd > 32) return fail(LB_ERR_SHAPE, "lb_fmm_apply: nd must be in [1, 32]");
+  if (level < 0 || level > 2) return fail(LB_ERR_ARG, "lb_fmm_apply: level must be 0, 1 or 2");
+  if (!pot || (level >= 1 && !grad) || (level >= 2 && !hess))
+    return fail(LB_ERR_ARG, "lb_fmm_apply: missing output buffer");
+  const uint32_t valid = nd == 32 ? 0xffffffffu : ((1u << nd) - 1u);
+  cmask &= valid;
+  dmask &= valid;
+  if ((cmask && !charges) || (dmask && !dipoles))
+    return fail(LB_ERR_ARG, "lb_fmm_apply: active mask without a density array");
+  cudaStream_t st = as_stream(stream);
+  if (!P->dev.ready) LB_TRY(build_device(P));
+  LB_BLAS(cublasSetStream(P->dev.blas, st));
+  std::vector<cudaEvent_t> ev;
+  if (P->timing) {
+    ev.resize(8);
+    for (auto& e : ev) cudaEventCreate(&e);
+  }
+  std::vector<double> acc(8, 0.0);
+  for (int d0 = 0; d0 < nd; d0 += 4) {
+    const int ndc = std::min(4, nd - d0);
+    LB_TRY(ensure_work(P, ndc));
+    int rc;
+    switch (ndc) {
+      case 1: rc = apply_chunk<1>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
+      case 2: rc = apply_chunk<2>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
+      case 3: rc = apply_chunk<3>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
+      default: rc = apply_chunk<4>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
+    }
+    if (rc != LB_OK) return rc;
+    if (P->timing) {
+      cudaEventSynchronize(ev[7]);
+      float t = 0;
+      for (int i = 0; i < 7; ++i) {
+        cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+        acc[i] += t;
+      }
+      cudaEventElapsedTime(&t, ev[0], ev[7]);
+      acc[7] += t;
+    }
+  }
+  if (P->timing) {
+    P->stage_ms = acc;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  return LB_OK;
+}
+
+}  // extern "C"

