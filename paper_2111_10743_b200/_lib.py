@@ -54,6 +54,14 @@ SIGNATURES = {
     "lb_dot": [_P, _P, _I64, _P, _P],
     "lb_nrm2": [_P, _I64, _P, _P],
     "lb_scale_inv": [_P, _P, _I64, _P, _P],
+    "lb_fmm_plan_create": [_P, _I64, _P, _I64, _I32, _I32, _I32, _P],
+    "lb_fmm_plan_destroy": [_P],
+    "lb_fmm_plan_info": [_P, _P, _P],
+    "lb_fmm_plan_export": [_P, _I32, _P],
+    "lb_fmm_plan_set_operators": [_P, _P],
+    "lb_fmm_apply": [_P, _P, _P, _I32, _U32, _U32, _I32, _P, _P, _P, _P],
+    "lb_fmm_plan_set_timing": [_P, _I32],
+    "lb_fmm_stage_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],
 }
