@@ -233,8 +233,8 @@ int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
                  const double* dipoles, int nd, uint32_t cmask, uint32_t dmask,
                  int level, double* pot, double* grad, double* hess,
                  void* stream);
-/* device time of each stage of the last apply, ms (HOST double[8]):
- * gather+P2M, M2M, M2L, X, L2L, leaf (L2T+W+U), scatter, total.  Recorded
+/* device time of each stage of the last apply, ms (HOST double[9]):
+ * gather+P2M, M2M, M2L, X, L2L, L2T (grid), leaf (U+DE+W), scatter, total.  Recorded
  * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */
 int lb_fmm_plan_set_timing(lb_fmm_plan* plan, int on);
 int lb_fmm_stage_times(const lb_fmm_plan* plan, double* ms);

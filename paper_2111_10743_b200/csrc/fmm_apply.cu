@@ -33,6 +33,8 @@
 
 namespace lb {
 
+constexpr int kStages = 8;  // p2m m2m m2l x l2l l2t leaf scatter (+ total)
+
 #define LB_BLAS(expr)                                                              \
   do {                                                                             \
     cublasStatus_t _s = (expr);                                                    \
@@ -350,59 +352,86 @@ __global__ void m2l_accum_kernel(const double* __restrict__ Y, const int64_t* __
 // ---------------------------------------------------------------------------
 // leaf stage
 
-// grid L2T (fmm.py:507-533): tout[l, t, comp] += interpolant of local[b]
+// grid L2T (fmm.py:507-533): tout[l, t, comp] += interpolant of local[b].
+// One block per target leaf, one thread per target; the leaf's local
+// coefficients (n^3) and every thread's 1-D bases (value / d / d2 per axis)
+// live in shared memory, the contraction runs z -> y -> x.
+constexpr int kL2tBT = 64;
+
 template <int ND>
-__global__ void __launch_bounds__(64) l2t_grid_kernel(
+__global__ void __launch_bounds__(kL2tBT) l2t_grid_kernel(
     const int64_t* __restrict__ leaves, const double* __restrict__ bctr,
     const double* __restrict__ bhalf, const int64_t* __restrict__ btgt,
     const double* __restrict__ tpos, int64_t nt, int n, const double* __restrict__ vinv,
     const double* __restrict__ loc, int level, double* __restrict__ tout) {
+  extern __shared__ double sm[];
+  const int n3 = n * n * n;
+  const int nb = 3 * (level + 1) * n;  // bases per thread
+  double* W = sm;                       // n^3
+  double* Bs = sm + n3;                 // kL2tBT * nb
   const int64_t b = leaves[blockIdx.x];
   const double h = bhalf[b], ih = 1.0 / h;
   const double c[3] = {bctr[3 * b], bctr[3 * b + 1], bctr[3 * b + 2]};
   const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
-  const int nrep = n * n * n;
-  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-    double L[3][3][16];  // [axis][deriv][node]
-    for (int ax = 0; ax < 3; ++ax)
-      lag_basis(n, vinv, (tpos[3 * t + ax] - c[ax]) / h, L[ax][0], L[ax][1], L[ax][2], level);
+  double* B = Bs + threadIdx.x * nb;  // [axis][deriv][node]
+  for (int64_t tb = t0; tb < t1; tb += kL2tBT) {
+    const int64_t t = tb + threadIdx.x;
+    const bool in = t < t1;
+    if (in) {
+      for (int ax = 0; ax < 3; ++ax) {
+        double* Lax = B + ax * (level + 1) * n;
+        lag_basis(n, vinv, (tpos[3 * t + ax] - c[ax]) / h, Lax, Lax + n, Lax + 2 * n, level);
+      }
+    }
+    const double* X0 = B;
+    const double* Y0 = B + (level + 1) * n;
+    const double* Z0 = B + 2 * (level + 1) * n;
     for (int l = 0; l < ND; ++l) {
-      const double* w = loc + (b * ND + l) * (int64_t)nrep;
+      __syncthreads();
+      const double* w = loc + (b * ND + l) * (int64_t)n3;
+      for (int o = threadIdx.x; o < n3; o += kL2tBT) W[o] = w[o];
+      __syncthreads();
+      if (!in) continue;
       double r[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
       for (int ia = 0; ia < n; ++ia) {
-        double s[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // [dy][dz] after y,z contraction
+        double s00 = 0, s01 = 0, s10 = 0, s02 = 0, s11 = 0, s20 = 0;
         for (int ib = 0; ib < n; ++ib) {
           double z0 = 0, z1 = 0, z2 = 0;
-          const double* wr = w + (ia * n + ib) * n;
+          const double* wr = W + (ia * n + ib) * n;
           for (int ic = 0; ic < n; ++ic) {
-            z0 = fma(L[2][0][ic], wr[ic], z0);
-            if (level >= 1) z1 = fma(L[2][1][ic], wr[ic], z1);
-            if (level >= 2) z2 = fma(L[2][2][ic], wr[ic], z2);
+            const double wv = wr[ic];
+            z0 = fma(Z0[ic], wv, z0);
+            if (level >= 1) z1 = fma(Z0[n + ic], wv, z1);
+            if (level >= 2) z2 = fma(Z0[2 * n + ic], wv, z2);
           }
-          s[0][0] = fma(L[1][0][ib], z0, s[0][0]);
+          const double y0 = Y0[ib];
+          s00 = fma(y0, z0, s00);
           if (level >= 1) {
-            s[0][1] = fma(L[1][0][ib], z1, s[0][1]);
-            s[1][0] = fma(L[1][1][ib], z0, s[1][0]);
-          }
-          if (level >= 2) {
-            s[0][2] = fma(L[1][0][ib], z2, s[0][2]);
-            s[1][1] = fma(L[1][1][ib], z1, s[1][1]);
-            s[2][0] = fma(L[1][2][ib], z0, s[2][0]);
+            const double y1 = Y0[n + ib];
+            s01 = fma(y0, z1, s01);
+            s10 = fma(y1, z0, s10);
+            if (level >= 2) {
+              s02 = fma(y0, z2, s02);
+              s11 = fma(y1, z1, s11);
+              s20 = fma(Y0[2 * n + ib], z0, s20);
+            }
           }
         }
-        r[0] = fma(L[0][0][ia], s[0][0], r[0]);
+        const double x0 = X0[ia];
+        r[0] = fma(x0, s00, r[0]);
         if (level >= 1) {
-          r[1] = fma(L[0][1][ia], s[0][0], r[1]);  // d/dx
-          r[2] = fma(L[0][0][ia], s[1][0], r[2]);  // d/dy
-          r[3] = fma(L[0][0][ia], s[0][1], r[3]);  // d/dz
-        }
-        if (level >= 2) {
-          r[4] = fma(L[0][2][ia], s[0][0], r[4]);  // xx
-          r[5] = fma(L[0][0][ia], s[2][0], r[5]);  // yy
-          r[6] = fma(L[0][0][ia], s[0][2], r[6]);  // zz
-          r[7] = fma(L[0][1][ia], s[1][0], r[7]);  // xy
-          r[8] = fma(L[0][1][ia], s[0][1], r[8]);  // xz
-          r[9] = fma(L[0][0][ia], s[1][1], r[9]);  // yz
+          const double x1 = X0[n + ia];
+          r[1] = fma(x1, s00, r[1]);  // d/dx
+          r[2] = fma(x0, s10, r[2]);  // d/dy
+          r[3] = fma(x0, s01, r[3]);  // d/dz
+          if (level >= 2) {
+            r[4] = fma(X0[2 * n + ia], s00, r[4]);  // xx
+            r[5] = fma(x0, s20, r[5]);              // yy
+            r[6] = fma(x0, s02, r[6]);              // zz
+            r[7] = fma(x1, s10, r[7]);              // xy
+            r[8] = fma(x1, s01, r[8]);              // xz
+            r[9] = fma(x0, s11, r[9]);              // yz
+          }
         }
       }
       double* o = tout + ((int64_t)l * nt + t) * 10;
@@ -415,10 +444,21 @@ __global__ void __launch_bounds__(64) l2t_grid_kernel(
   }
 }
 
-// fused leaf P2P (fmm.py:947-988): U-list real sources, own DE equivalent
-// charges (surface), W-list equivalent charges
+inline size_t l2t_smem(int n, int level) {
+  return sizeof(double) * ((size_t)n * n * n + (size_t)kL2tBT * 3 * (level + 1) * n);
+}
+
+// Fused leaf P2P (fmm.py:947-988).  The source sets of a target leaf -- its
+// U-list leaves (real charges/dipoles), its own downward-equivalent charges
+// (surface) and its W-list boxes' upward-equivalent charges -- are walked as
+// ONE virtual list so every shared-memory tile is full; the block's threads
+// are split into kSplit source phases per target and combined at the end.
+constexpr int kLeafBT = 128;
+constexpr int kLeafTS = 128;
+constexpr int kLeafMaxSets = 512;
+
 template <int ND, bool HD, int LEVEL>
-__global__ void __launch_bounds__(64) leaf_kernel(
+__global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     const int64_t* __restrict__ leaves, const int64_t* __restrict__ u_off,
     const int64_t* __restrict__ u_list, const int64_t* __restrict__ w_off,
     const int64_t* __restrict__ w_list, const double* __restrict__ bctr,
@@ -431,65 +471,113 @@ __global__ void __launch_bounds__(64) leaf_kernel(
   using Lay = SrcLayout<ND, true, HD>;
   constexpr int S = Lay::stride;
   constexpr int NC = ncomp(LEVEL);
-  constexpr int TS = 64;
-  __shared__ __align__(16) double sh[TS * S];
+  constexpr int NA = ND * NC;
+  constexpr int kTS = S > 8 ? kLeafTS / 2 : kLeafTS;
+  __shared__ __align__(16) double sh[kTS * S];
+  __shared__ int64_t set_end[kLeafMaxSets + 1];
+  __shared__ int64_t set_box[kLeafMaxSets];
+  __shared__ double red[kLeafBT];
   const int64_t b = leaves[blockIdx.x];
   const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
-  const int64_t nu = u_off[blockIdx.x + 1] - u_off[blockIdx.x];
-  const int64_t nw = w_off[blockIdx.x + 1] - w_off[blockIdx.x];
-  for (int64_t tb = t0; tb < t1; tb += blockDim.x) {
-    const int64_t t = tb + threadIdx.x;
+  // leaves hold few targets (~17 on average at ncrit 120): size the target
+  // pass to the leaf and give the remaining threads other source phases
+  int kTgt = 16;
+  while (kTgt < t1 - t0 && kTgt < kLeafBT) kTgt <<= 1;
+  const int kSplit = kLeafBT / kTgt;
+  const int64_t ub = u_off[blockIdx.x], nu = u_off[blockIdx.x + 1] - ub;
+  const int64_t wb = w_off[blockIdx.x], nw = w_off[blockIdx.x + 1] - wb;
+  const int64_t nde = surface ? 1 : 0;
+  const int64_t nsets_all = nu + nde + nw;
+  const int ti = threadIdx.x % kTgt, ph = threadIdx.x / kTgt;
+  for (int64_t tb = t0; tb < t1; tb += kTgt) {
+    const int64_t t = tb + ti;
     const bool in = t < t1;
     const double tx = in ? tpos[3 * t] : 0.0, ty = in ? tpos[3 * t + 1] : 0.0,
                  tz = in ? tpos[3 * t + 2] : 0.0;
-    double acc[ND * NC];
+    double acc[NA];
 #pragma unroll
-    for (int a = 0; a < ND * NC; ++a) acc[a] = 0.0;
-    // source sets: U leaves, then (surface) own DE set, then W sets
-    const int64_t nsets = nu + (surface ? 1 : 0) + nw;
-    for (int64_t q = 0; q < nsets; ++q) {
-      bool real = q < nu;
-      int64_t s0, s1, eb = -1;
-      const double* eq = nullptr;
-      double fac = 0.0;
-      if (real) {
-        const int64_t sb = u_list[u_off[blockIdx.x] + q];
-        s0 = bsrc[2 * sb];
-        s1 = bsrc[2 * sb + 1];
-      } else if (surface && q == nu) {
-        eb = b; eq = loc; fac = de_scale; s0 = 0; s1 = nrep;
-      } else {
-        eb = w_list[w_off[blockIdx.x] + (q - nu - (surface ? 1 : 0))];
-        eq = up; fac = ue_scale; s0 = 0; s1 = nrep;
-      }
-      for (int64_t j0 = s0; j0 < s1; j0 += TS) {
-        const int n = (int)min((int64_t)TS, s1 - j0);
-        __syncthreads();
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
-          double* r = sh + k * S;
-          const int64_t j = j0 + k;
-          if (real) {
-            r[0] = spos[3 * j]; r[1] = spos[3 * j + 1]; r[2] = spos[3 * j + 2];
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    for (int64_t sb0 = 0; sb0 < nsets_all; sb0 += kLeafMaxSets) {
+      const int nsets = (int)min((int64_t)kLeafMaxSets, nsets_all - sb0);
+      __syncthreads();
+      if (threadIdx.x == 0) {  // prefix sizes of this batch of source sets
+        int64_t e = 0;
+        for (int q = 0; q < nsets; ++q) {
+          const int64_t g = sb0 + q;
+          int64_t box, cnt;
+          if (g < nu) {
+            box = u_list[ub + g];
+            cnt = bsrc[2 * box + 1] - bsrc[2 * box];
+          } else if (g < nu + nde) {
+            box = -1 - b;  // own DE set
+            cnt = nrep;
           } else {
-            const double h = bhalf[eb];
-            r[0] = bctr[3 * eb] + fac * h * pts[3 * j];
-            r[1] = bctr[3 * eb + 1] + fac * h * pts[3 * j + 1];
-            r[2] = bctr[3 * eb + 2] + fac * h * pts[3 * j + 2];
+            box = -1 - w_list[wb + (g - nu - nde)];
+            cnt = nrep;
           }
+          set_box[q] = box;
+          e += cnt;
+          set_end[q] = e;
+        }
+      }
+      __syncthreads();
+      const int64_t total = set_end[nsets - 1];
+      for (int64_t v0 = 0; v0 < total; v0 += kTS) {
+        const int n = (int)min((int64_t)kTS, total - v0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < n; k += kLeafBT) {
+          const int64_t v = v0 + k;
+          int lo = 0, hi = nsets - 1;  // first set with set_end > v
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (set_end[mid] > v) hi = mid; else lo = mid + 1;
+          }
+          const int64_t off = v - (lo ? set_end[lo - 1] : 0);
+          const int64_t box = set_box[lo];
+          double* r = sh + k * S;
           int o = 3;
+          if (box >= 0) {  // real sources of a U-list leaf
+            const int64_t j = bsrc[2 * box] + off;
+            r[0] = spos[3 * j]; r[1] = spos[3 * j + 1]; r[2] = spos[3 * j + 2];
 #pragma unroll
-          for (int l = 0; l < ND; ++l) {
-            r[o++] = real ? cs[(int64_t)l * ns + j] : eq[(eb * ND + l) * (int64_t)nrep + j];
-            if (HD) {
-              for (int kk = 0; kk < 3; ++kk) r[o++] = real ? vs[((int64_t)l * ns + j) * 3 + kk] : 0.0;
+            for (int l = 0; l < ND; ++l) {
+              r[o++] = cs[(int64_t)l * ns + j];
+              if (HD)
+                for (int kk = 0; kk < 3; ++kk) r[o++] = vs[((int64_t)l * ns + j) * 3 + kk];
+            }
+          } else {  // equivalent charges: own DE set (loc) or a W box (up)
+            const int64_t eb = -1 - box;
+            const bool de = eb == b && surface && (lo + sb0) == nu;
+            const double fac = de ? de_scale : ue_scale;
+            const double* eq = de ? loc : up;
+            const double h = bhalf[eb];
+            r[0] = bctr[3 * eb] + fac * h * pts[3 * off];
+            r[1] = bctr[3 * eb + 1] + fac * h * pts[3 * off + 1];
+            r[2] = bctr[3 * eb + 2] + fac * h * pts[3 * off + 2];
+#pragma unroll
+            for (int l = 0; l < ND; ++l) {
+              r[o++] = eq[(eb * ND + l) * (int64_t)nrep + off];
+              if (HD)
+                for (int kk = 0; kk < 3; ++kk) r[o++] = 0.0;
             }
           }
         }
         __syncthreads();
-        for (int k = 0; k < n; ++k) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+        for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
       }
     }
-    if (in) {
+    // combine the source phases (fixed order), one component at a time
+    if (kSplit > 1) {
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        __syncthreads();
+        red[threadIdx.x] = acc[a];
+        __syncthreads();
+        if (ph == 0)
+          for (int q = 1; q < kSplit; ++q) acc[a] += red[q * kTgt + ti];
+      }
+    }
+    if (in && ph == 0) {
 #pragma unroll
       for (int l = 0; l < ND; ++l) {
         double* o = tout + ((int64_t)l * nt + t) * 10;
@@ -891,13 +979,17 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   LB_CUDA(cudaMemsetAsync(D.tout, 0, sizeof(double) * ND * t.nt * 10, st));
   if (D.n_tleaf > 0) {
     if (!surface) {
-      l2t_grid_kernel<ND><<<(unsigned)D.n_tleaf, 64, 0, st>>>(D.t_leaves, D.bctr, D.bhalf, D.btgt,
-                                                             D.tpos, t.nt, n, D.vinv, D.loc, level,
-                                                             D.tout);
+      const size_t sm = l2t_smem(n, level);
+      LB_CUDA(cudaFuncSetAttribute(l2t_grid_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)l2t_smem(16, 2)));
+      l2t_grid_kernel<ND><<<(unsigned)D.n_tleaf, kL2tBT, sm, st>>>(D.t_leaves, D.bctr, D.bhalf,
+                                                                  D.btgt, D.tpos, t.nt, n, D.vinv,
+                                                                  D.loc, level, D.tout);
       LB_CHECK_LAUNCH();
     }
+    mark(6);
 #define LB_LEAF(HD, LV)                                                                        \
-  leaf_kernel<ND, HD, LV><<<(unsigned)D.n_tleaf, 64, 0, st>>>(                                 \
+  leaf_kernel<ND, HD, LV><<<(unsigned)D.n_tleaf, kLeafBT, 0, st>>>(                                 \
       D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,       \
       D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,      \
       surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout)
@@ -909,11 +1001,12 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
 #undef LB_LEAF
     LB_CHECK_LAUNCH();
   }
-  mark(6);
+  if (D.n_tleaf == 0) mark(6);
+  mark(7);
   fmm_scatter_kernel<<<(unsigned)ceil_div((int64_t)ND * t.nt, 256), 256, 0, st>>>(
       D.tout, D.tgt_sorted, t.nt, ND, d0, level, pot, grad, hess);
   LB_CHECK_LAUNCH();
-  mark(7);
+  mark(8);
   return LB_OK;
 }
 
@@ -976,7 +1069,7 @@ int lb_fmm_plan_set_timing(lb_fmm_plan* P, int on) {
 
 int lb_fmm_stage_times(const lb_fmm_plan* P, double* ms) {
   if (!P || !ms) return fail(LB_ERR_ARG, "null argument");
-  for (int i = 0; i < 8; ++i) ms[i] = i < (int)P->stage_ms.size() ? P->stage_ms[i] : 0.0;
+  for (int i = 0; i <= kStages; ++i) ms[i] = i < (int)P->stage_ms.size() ? P->stage_ms[i] : 0.0;
   return LB_OK;
 }
 
@@ -999,10 +1092,10 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
   LB_BLAS(cublasSetStream(P->dev.blas, st));
   std::vector<cudaEvent_t> ev;
   if (P->timing) {
-    ev.resize(8);
+    ev.resize(kStages + 1);
     for (auto& e : ev) cudaEventCreate(&e);
   }
-  std::vector<double> acc(8, 0.0);
+  std::vector<double> acc(kStages + 1, 0.0);
   for (int d0 = 0; d0 < nd; d0 += 4) {
     const int ndc = std::min(4, nd - d0);
     LB_TRY(ensure_work(P, ndc));
@@ -1015,14 +1108,14 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
     }
     if (rc != LB_OK) return rc;
     if (P->timing) {
-      cudaEventSynchronize(ev[7]);
+      cudaEventSynchronize(ev[kStages]);
       float t = 0;
-      for (int i = 0; i < 7; ++i) {
+      for (int i = 0; i < kStages; ++i) {
         cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
         acc[i] += t;
       }
-      cudaEventElapsedTime(&t, ev[0], ev[7]);
-      acc[7] += t;
+      cudaEventElapsedTime(&t, ev[0], ev[kStages]);
+      acc[kStages] += t;
     }
   }
   if (P->timing) {

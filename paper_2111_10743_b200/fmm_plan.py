@@ -385,11 +385,11 @@ class FmmPlan:
         _lib.check(self._L.lb_fmm_plan_set_timing(self._h, 1 if on else 0))
 
     def stage_times(self):
-        """Device ms of gather+P2M, M2M, M2L, X, L2L, leaf, scatter, total."""
-        ms = np.zeros(8)
+        """Device ms of gather+P2M, M2M, M2L, X, L2L, L2T, leaf, scatter, total."""
+        ms = np.zeros(9)
         _lib.check(self._L.lb_fmm_stage_times(self._h, ms.ctypes.data_as(ctypes.c_void_p)))
-        return dict(zip(("p2m", "m2m", "m2l", "x", "l2l", "leaf", "scatter",
-                         "total"), ms.tolist()))
+        return dict(zip(("p2m", "m2m", "m2l", "x", "l2l", "l2t", "leaf",
+                         "scatter", "total"), ms.tolist()))
 
     def apply_device(self, charges, dipoles, nd, cmask, dmask, level, pot,
                      grad=None, hess=None, stream=None):
