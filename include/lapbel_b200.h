@@ -127,6 +127,12 @@ typedef struct lb_opset lb_opset;
 int lb_opset_create(const lb_opset_desc* desc, lb_opset** out);
 int lb_opset_destroy(lb_opset* h);
 int lb_opset_set_phi0(lb_opset* h, const double* phi0);
+/* Route every far-field call of the handle through an FMM plan built on
+ * (over_nodes, nodes) (the reference's use_fmm=True path, operators.py:104-112)
+ * instead of the exact all-pairs sweeps; NULL restores the sweeps.  The plan
+ * must outlive the handle's use of it. */
+struct lb_fmm_plan;
+int lb_opset_set_fmm(lb_opset* h, struct lb_fmm_plan* plan);
 /* out = A_f tau for formulation f in {1,2,3} (apply_a1/a2/a3,
  * operators.py:161-266).  tau/out: device (n), must not alias.  Enqueued on
  * `stream`; no host synchronisation; capturable in a CUDA graph.  Missing

@@ -811,7 +811,8 @@ int build_device(lb_fmm_plan* P) {
 int ensure_work(lb_fmm_plan* P, int nd) {
   FmmDevice& D = P->dev;
   if (D.nd_alloc == nd) return LB_OK;
-  cudaFree(D.cs); cudaFree(D.vs); cudaFree(D.up); cudaFree(D.dc); cudaFree(D.loc);
+  if (D.loc != D.dc) cudaFree(D.loc);  // grid: loc aliases dc
+  cudaFree(D.cs); cudaFree(D.vs); cudaFree(D.up); cudaFree(D.dc);
   cudaFree(D.tmpA); cudaFree(D.tmpB); cudaFree(D.tout);
   D.cs = D.vs = D.up = D.dc = D.loc = D.tmpA = D.tmpB = D.tout = nullptr;
   const FmmTree& t = P->tree;
@@ -850,6 +851,11 @@ int gemm_rm(cublasHandle_t h, const double* A, const double* X, double* Y, int n
   if (ncols <= 0) return LB_OK;
   LB_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nrep, (int)ncols, nrep, &alpha, A, nrep, X, nrep,
                       &beta, Y, nrep));
+  // cuBLAS reports through its status; do not let an internal runtime error
+  // it tolerated surface at our next launch check
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(LB_ERR_CUDA, std::string("after cublasDgemm: ") + cudaGetErrorString(e));
   return LB_OK;
 }
 
@@ -867,9 +873,11 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   auto mark = [&](int i) { if (!ev.empty()) cudaEventRecord(ev[i], st); };
   mark(0);
   // gather into sorted source order
-  if (t.ns > 0)
+  if (t.ns > 0) {
     gather_sources_kernel<<<(unsigned)ceil_div(t.ns, 256), 256, 0, st>>>(
         charges, dipoles, D.src_sorted, t.ns, ND, d0, cmask, dmask, D.cs, D.vs);
+    LB_CHECK_LAUNCH();
+  }
   LB_CUDA(cudaMemsetAsync(D.up, 0, sizeof(double) * nb * ND * nrep, st));
   LB_CUDA(cudaMemsetAsync(D.dc, 0, sizeof(double) * nb * ND * nrep, st));
   // ---- P2M (fmm.py:823-852)
@@ -1088,6 +1096,12 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
   if ((cmask && !charges) || (dmask && !dipoles))
     return fail(LB_ERR_ARG, "lb_fmm_apply: active mask without a density array");
   cudaStream_t st = as_stream(stream);
+  {
+    const cudaError_t stale = cudaGetLastError();
+    if (stale != cudaSuccess)
+      return fail(LB_ERR_CUDA, std::string("lb_fmm_apply: error pending before the call: ") +
+                                   cudaGetErrorString(stale));
+  }
   if (!P->dev.ready) LB_TRY(build_device(P));
   LB_BLAS(cublasSetStream(P->dev.blas, st));
   std::vector<cudaEvent_t> ev;

@@ -33,7 +33,9 @@ int fail(int code, const std::string& msg);
   do {                                                                       \
     cudaError_t _e = cudaGetLastError();                                     \
     if (_e != cudaSuccess)                                                   \
-      return ::lb::fail(LB_ERR_CUDA, std::string("kernel launch: ") +       \
+      return ::lb::fail(LB_ERR_CUDA, std::string("kernel launch (") +       \
+                                         __FILE__ + ":" +                    \
+                                         std::to_string(__LINE__) + "): " +  \
                                          cudaGetErrorString(_e));            \
   } while (0)
 

@@ -362,6 +362,10 @@ struct lb_opset {
   double* scal = nullptr;  // [0] W-average / eta
   int csr_blocks = 0;
   int csr_wpr = 1;
+  // optional FMM far field (lb_opset_set_fmm) and its scratch
+  lb_fmm_plan* fmm = nullptr;
+  double *f_ch = nullptr, *f_ch3 = nullptr, *f_dp = nullptr;
+  double *f_pot = nullptr, *f_grad = nullptr, *f_hess = nullptr;
 };
 
 namespace lb {
@@ -463,33 +467,174 @@ E base_epi(const lb_opset* h, const SkLayout& L, int nout) {
 
 double* V(const lb_opset* h, int k) { return h->vec + (int64_t)k * h->d.n; }
 
+// ---------------------------------------------------------------------------
+// one far-field call of the reference (a `_far` call, operators.py:103-114):
+// oversample the input vector(s) and run the sweep, either exact all-pairs
+// (opfar_kernel) or through the attached FMM plan (lb_fmm_apply + a
+// projection to the same per-target outputs), returning the partial layout
+// the CSR epilogue reads.
+
+enum FarKind { FK_S, FK_A3A, FK_A3B, FK_A2A, FK_A2B, FK_A1A, FK_A1B, FK_D };
+
+struct FarSpec {
+  double* pack;
+  int S;
+  int slot[3];
+};
+
+FarSpec far_spec(lb_opset* h, FarKind k) {
+  switch (k) {
+    case FK_S: case FK_A3A: case FK_A1A: return {h->pack4, 4, {3, 0, 0}};
+    case FK_A3B: return {h->pack8, 8, {6, 7, 0}};
+    case FK_A2A: case FK_D: return {h->pack8, 8, {6, 0, 0}};
+    case FK_A2B: return {h->pack8, 8, {7, 6, 0}};
+    default: return {h->pack6, 6, {3, 4, 5}};  // FK_A1B
+  }
+}
+
+int far_nout(FarKind k) {
+  switch (k) {
+    case FK_S: case FK_A1B: case FK_D: return 1;
+    case FK_A3A: case FK_A2B: return 2;
+    default: return 4;
+  }
+}
+
+// c * n_over dipoles for FMM densities
+__global__ void dipole_kernel(const double* __restrict__ c, const double* __restrict__ nrm, int64_t ns,
+                              double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  for (int k = 0; k < 3; ++k) out[3 * i + k] = c[i] * nrm[3 * i + k];
+}
+
+// FMM outputs -> the functor outputs, written as a one-segment stream-K layout
+__global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t n,
+                               const double* __restrict__ pot, const double* __restrict__ grad,
+                               const double* __restrict__ hess, SkLayout L, int nout,
+                               double* __restrict__ part) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double nx = nrm[3 * i], ny = nrm[3 * i + 1], nz = nrm[3 * i + 2];
+  auto ng = [&](int l) {  // n . grad_l
+    const double* g = grad + ((int64_t)l * n + i) * 3;
+    return nx * g[0] + ny * g[1] + nz * g[2];
+  };
+  auto nhn = [&](int l) {  // n . hess_l . n
+    const double* H = hess + ((int64_t)l * n + i) * 9;
+    return nx * (H[0] * nx + H[1] * ny + H[2] * nz) + ny * (H[3] * nx + H[4] * ny + H[5] * nz) +
+           nz * (H[6] * nx + H[7] * ny + H[8] * nz);
+  };
+  double a[4] = {0, 0, 0, 0};
+  switch (kind) {
+    case FK_S: case FK_D: a[0] = pot[i]; break;
+    case FK_A3A: a[0] = pot[i]; a[1] = -ng(0); break;
+    case FK_A3B: a[0] = -ng(0); a[1] = pot[n + i]; a[2] = -ng(1); a[3] = nhn(1) + ng(2); break;
+    case FK_A2A: a[0] = pot[i]; a[1] = pot[n + i]; a[2] = -ng(0); a[3] = nhn(0) + ng(1); break;
+    case FK_A2B: a[0] = pot[i]; a[1] = pot[n + i]; break;
+    case FK_A1A:
+      a[0] = pot[i];
+      for (int k = 0; k < 3; ++k) a[1 + k] = -grad[i * 3 + k];
+      break;
+    case FK_A1B:
+      a[0] = -(grad[(0 * n + i) * 3 + 0] + grad[(1 * n + i) * 3 + 1] + grad[(2 * n + i) * 3 + 2]);
+      break;
+  }
+  const int64_t t = i / L.tt;
+  const int lt = (int)(i - t * L.tt);
+  for (int o = 0; o < nout; ++o) part[L.idx(t, 0, o, nout, lt)] = a[o];
+}
+
+int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool add_ws, SkLayout* L,
+              cudaStream_t st) {
+  if (!h->fmm) {
+    const FarSpec sp = far_spec(h, kind);
+    LB_TRY(oversample(h, nv, in, sp.slot, sp.pack, sp.S, add_ws, st));
+    switch (kind) {
+      case FK_S: return run_far<FarS>(h, sp.pack, L, st);
+      case FK_A3A: return run_far<FarA3a>(h, sp.pack, L, st);
+      case FK_A3B: return run_far<FarA3b>(h, sp.pack, L, st);
+      case FK_A2A: return run_far<FarA2a>(h, sp.pack, L, st);
+      case FK_A2B: return run_far<FarA2b>(h, sp.pack, L, st);
+      case FK_A1A: return run_far<FarA1a>(h, sp.pack, L, st);
+      case FK_A1B: return run_far<FarA1b>(h, sp.pack, L, st);
+      default: return run_far<FarD>(h, sp.pack, L, st);
+    }
+  }
+  // FMM path: plain charge arrays c_v = w_over * oversample(in_v)
+  const int64_t no = h->d.n_over, n = h->d.n;
+  const int slot[3] = {0, (int)no, (int)(2 * no)};
+  LB_TRY(oversample(h, nv, in, slot, h->f_ch, 1, add_ws, st));
+  double* c0 = h->f_ch;
+  double* c1 = h->f_ch + no;
+  double* ch = h->f_ch3;  // (3, no) densities handed to the FMM
+  double* dp = h->f_dp;   // (3, no, 3)
+  const unsigned g = (unsigned)ceil_div(no, 256);
+  int nd = 1, level = 0;
+  uint32_t cm = 0, dm = 0;
+  const double* chp = c0;
+  const double* dpp = nullptr;
+  switch (kind) {
+    case FK_S: nd = 1; cm = 1; level = 0; break;
+    case FK_D:
+      dipole_kernel<<<g, 256, 0, st>>>(c0, h->d.over_normals, no, dp);
+      nd = 1; dm = 1; level = 0; chp = nullptr; dpp = dp; break;
+    case FK_A3A: case FK_A1A: nd = 1; cm = 1; level = 1; break;
+    case FK_A3B:  // charges [c0, c1, 0], dipoles [0, 0, c1 n]
+      LB_CUDA(cudaMemcpyAsync(ch, c0, sizeof(double) * no, cudaMemcpyDeviceToDevice, st));
+      LB_CUDA(cudaMemcpyAsync(ch + no, c1, sizeof(double) * no, cudaMemcpyDeviceToDevice, st));
+      dipole_kernel<<<g, 256, 0, st>>>(c1, h->d.over_normals, no, dp + 2 * no * 3);
+      nd = 3; cm = 3; dm = 4; level = 2; chp = ch; dpp = dp; break;
+    case FK_A2A:  // charge c0 on density 0, dipole c0 n on density 1
+      dipole_kernel<<<g, 256, 0, st>>>(c0, h->d.over_normals, no, dp + no * 3);
+      nd = 2; cm = 1; dm = 2; level = 2; chp = c0; dpp = dp; break;
+    case FK_A2B:  // dipole (w mu1) n on density 0, charge (w mu2) on density 1
+      // in = {mu2, mu1}: c0 = w mu2, c1 = w mu1
+      dipole_kernel<<<g, 256, 0, st>>>(c1, h->d.over_normals, no, dp);
+      LB_CUDA(cudaMemcpyAsync(ch + no, c0, sizeof(double) * no, cudaMemcpyDeviceToDevice, st));
+      nd = 2; cm = 2; dm = 1; level = 0; chp = ch; dpp = dp; break;
+    case FK_A1B: nd = 3; cm = 7; level = 1; chp = c0; break;
+  }
+  LB_CHECK_LAUNCH();
+  {
+    int rc = lb_fmm_apply(h->fmm, chp, dpp, nd, cm, dm, level, h->f_pot, h->f_grad, h->f_hess, st);
+    if (rc != LB_OK) return fail(rc, std::string("far_stage(kind ") + std::to_string((int)kind) +
+                                         "): " + lb_last_error_string());
+  }
+  SkLayout l1{};
+  l1.tt = 64;
+  l1.tiles = ceil_div(n, l1.tt);
+  l1.C = 1;
+  l1.U = l1.tiles;
+  l1.G = l1.tiles;
+  l1.kmax = 1;
+  const int nout = far_nout(kind);
+  project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals, n, h->f_pot,
+                                                             h->f_grad, h->f_hess, l1, nout, h->part);
+  LB_CHECK_LAUNCH();
+  *L = l1;
+  return LB_OK;
+}
+
 int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
-  SkLayout ns1{}, ns2{};
+  SkLayout L1{}, L2{};
   double* s_tau = V(h, 0);
   double* sp_tau = V(h, 1);
+  const double* in1[1] = {tau};
+  LB_TRY(far_stage(h, FK_A3A, 1, in1, false, &L1, st));
   {
-    const double* in[1] = {tau};
-    const int slot[1] = {3};
-    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
-  }
-  LB_TRY(run_far<FarA3a>(h, h->pack4, &ns1, st));
-  {
-    auto e = base_epi<EpiA3p1>(h, ns1, 2);
+    auto e = base_epi<EpiA3p1>(h, L1, 2);
     e.s_tau = s_tau;
     e.sp_tau = sp_tau;
     const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
     const double* xs[2] = {tau, tau};
     LB_TRY((run_csr<2>(h, vals, xs, e, st)));
   }
+  const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
+  LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L2, st));
   {
-    const double* in[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
-    const int slot[2] = {6, 7};
-    LB_TRY(oversample(h, 2, in, slot, h->pack8, 8, false, st));
-  }
-  LB_TRY(run_far<FarA3b>(h, h->pack8, &ns2, st));
-  {
-    auto e = base_epi<EpiA3p2>(h, ns2, 4);
+    auto e = base_epi<EpiA3p2>(h, L2, 4);
     e.tau = tau;
     e.curv = h->d.curvature;
     e.w = h->d.weights;
@@ -505,17 +650,13 @@ int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
 
 int apply_a2(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
-  SkLayout ns1{}, ns2{};
+  SkLayout L1{}, L2{};
   double* mu1 = V(h, 0);
   double* mu2 = V(h, 1);
+  const double* in1[1] = {tau};
+  LB_TRY(far_stage(h, FK_A2A, 1, in1, false, &L1, st));
   {
-    const double* in[1] = {tau};
-    const int slot[1] = {6};
-    LB_TRY(oversample(h, 1, in, slot, h->pack8, 8, false, st));
-  }
-  LB_TRY(run_far<FarA2a>(h, h->pack8, &ns1, st));
-  {
-    auto e = base_epi<EpiA2p1>(h, ns1, 4);
+    auto e = base_epi<EpiA2p1>(h, L1, 4);
     e.curv = h->d.curvature;
     e.w = h->d.weights;
     e.mu1 = mu1;
@@ -524,15 +665,11 @@ int apply_a2(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
     const double* xs[4] = {tau, tau, tau, tau};
     LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
   }
+  // mu2 += ws in place (scal[0]) while both are oversampled
+  const double* in2[2] = {mu2, mu1};
+  LB_TRY(far_stage(h, FK_A2B, 2, in2, true, &L2, st));
   {
-    // mu2 += ws in place (scal[0]), then both oversampled into pack8
-    const double* in[2] = {mu2, mu1};
-    const int slot[2] = {7, 6};
-    LB_TRY(oversample(h, 2, in, slot, h->pack8, 8, true, st));
-  }
-  LB_TRY(run_far<FarA2b>(h, h->pack8, &ns2, st));
-  {
-    auto e = base_epi<EpiA2p2>(h, ns2, 2);
+    auto e = base_epi<EpiA2p2>(h, L2, 2);
     e.tau = tau;
     e.result = out;
     const double* vals[2] = {C[LB_KIND_D], C[LB_KIND_S]};
@@ -546,18 +683,14 @@ int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
   if (!h->d.tangents_u || !h->d.tangents_v || !h->d.inv_metric || !h->d.phi0)
     return fail(LB_ERR_ARG, "opset: A1 needs tangents, inverse metric and phi0");
-  SkLayout ns1{}, ns2{};
+  SkLayout L1{}, L2{};
   double* mux = V(h, 0);
   double* muy = V(h, 1);
   double* muz = V(h, 2);
+  const double* in1[1] = {tau};
+  LB_TRY(far_stage(h, FK_A1A, 1, in1, false, &L1, st));
   {
-    const double* in[1] = {tau};
-    const int slot[1] = {3};
-    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
-  }
-  LB_TRY(run_far<FarA1a>(h, h->pack4, &ns1, st));
-  {
-    auto e = base_epi<EpiA1p1>(h, ns1, 4);
+    auto e = base_epi<EpiA1p1>(h, L1, 4);
     e.tu = h->d.tangents_u;
     e.tv = h->d.tangents_v;
     e.gi = h->d.inv_metric;
@@ -569,14 +702,10 @@ int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
     const double* xs[4] = {tau, tau, tau, tau};
     LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
   }
+  const double* in2[3] = {mux, muy, muz};
+  LB_TRY(far_stage(h, FK_A1B, 3, in2, false, &L2, st));
   {
-    const double* in[3] = {mux, muy, muz};
-    const int slot[3] = {3, 4, 5};
-    LB_TRY(oversample(h, 3, in, slot, h->pack6, 6, false, st));
-  }
-  LB_TRY(run_far<FarA1b>(h, h->pack6, &ns2, st));
-  {
-    auto e = base_epi<EpiA1p2>(h, ns2, 1);
+    auto e = base_epi<EpiA1p2>(h, L2, 1);
     e.phi0 = h->d.phi0;
     e.eta = h->scal;
     e.result = out;
@@ -591,35 +720,20 @@ int apply_layer(lb_opset* h, int kind, const double* tau, double* out, cudaStrea
   if (kind < 0 || kind >= LB_NKINDS) return fail(LB_ERR_ARG, "opset: unknown kernel kind");
   const double* val = h->d.corr[kind];
   if (!val) return fail(LB_ERR_KEY, "opset: corrections for this kind were not built");
-  SkLayout ns{};
+  FarKind fk;
   int nout = 1, o = 0;
   double sign = 1.0;
-  if (kind == LB_KIND_S || kind == LB_KIND_SPRIME ||
-      (kind >= LB_KIND_GRAD_S1 && kind <= LB_KIND_GRAD_S3)) {
-    const double* in[1] = {tau};
-    const int slot[1] = {3};
-    LB_TRY(oversample(h, 1, in, slot, h->pack4, 4, false, st));
-    if (kind == LB_KIND_S) {
-      LB_TRY(run_far<FarS>(h, h->pack4, &ns, st));
-    } else if (kind == LB_KIND_SPRIME) {
-      LB_TRY(run_far<FarA3a>(h, h->pack4, &ns, st));
-      nout = 2; o = 1; sign = -1.0;
-    } else {
-      LB_TRY(run_far<FarA1a>(h, h->pack4, &ns, st));
-      nout = 4; o = 1 + (kind - LB_KIND_GRAD_S1); sign = -1.0;
-    }
-  } else {
-    const double* in[1] = {tau};
-    const int slot[1] = {6};
-    LB_TRY(oversample(h, 1, in, slot, h->pack8, 8, false, st));
-    if (kind == LB_KIND_D) {
-      LB_TRY(run_far<FarD>(h, h->pack8, &ns, st));
-    } else {  // S'' + D'
-      LB_TRY(run_far<FarA2a>(h, h->pack8, &ns, st));
-      nout = 4; o = 3;
-    }
+  switch (kind) {
+    case LB_KIND_S: fk = FK_S; break;
+    case LB_KIND_SPRIME: fk = FK_A3A; nout = 2; o = 1; sign = -1.0; break;
+    case LB_KIND_D: fk = FK_D; break;
+    case LB_KIND_SPP_PLUS_DPRIME: fk = FK_A2A; nout = 4; o = 3; break;
+    default: fk = FK_A1A; nout = 4; o = 1 + (kind - LB_KIND_GRAD_S1); sign = -1.0; break;
   }
-  auto e = base_epi<EpiLayer>(h, ns, nout);
+  SkLayout L{};
+  const double* in[1] = {tau};
+  LB_TRY(far_stage(h, fk, 1, in, false, &L, st));
+  auto e = base_epi<EpiLayer>(h, L, nout);
   e.o = o;
   e.sign = sign;
   e.y = out;
@@ -703,7 +817,48 @@ int lb_opset_destroy(lb_opset* h) {
   cudaFree(h->partials);
   cudaFree(h->ticket);
   cudaFree(h->scal);
+  cudaFree(h->f_ch);
+  cudaFree(h->f_ch3);
+  cudaFree(h->f_dp);
+  cudaFree(h->f_pot);
+  cudaFree(h->f_grad);
+  cudaFree(h->f_hess);
   delete h;
+  return LB_OK;
+}
+
+int lb_opset_set_fmm(lb_opset* h, lb_fmm_plan* plan) {
+  using namespace lb;
+  if (!h) return fail(LB_ERR_ARG, "lb_opset_set_fmm: null handle");
+  h->fmm = plan;
+  if (!plan || h->f_ch) return LB_OK;
+  int64_t sizes[10];
+  LB_TRY(lb_fmm_plan_info(plan, sizes, nullptr));
+  if (sizes[2] != h->d.n_over || sizes[3] != h->d.n) {
+    h->fmm = nullptr;
+    return fail(LB_ERR_SHAPE, "lb_opset_set_fmm: plan sources/targets must be over_nodes/nodes");
+  }
+  const int64_t no = h->d.n_over, n = h->d.n;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](double** p, int64_t k) { if (e == cudaSuccess) e = cudaMalloc((void**)p, sizeof(double) * k); };
+  A(&h->f_ch, 3 * no);
+  A(&h->f_ch3, 3 * no);
+  A(&h->f_dp, 9 * no);
+  A(&h->f_pot, 3 * n);
+  A(&h->f_grad, 9 * n);
+  A(&h->f_hess, 27 * n);
+  if (e == cudaSuccess) e = cudaMemset(h->f_ch3, 0, sizeof(double) * 3 * no);
+  if (e == cudaSuccess) e = cudaMemset(h->f_dp, 0, sizeof(double) * 9 * no);
+  if (e == cudaSuccess) e = cudaMemset(h->f_ch, 0, sizeof(double) * 3 * no);
+  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("lb_opset_set_fmm: ") + cudaGetErrorString(e));
+  // the one-segment projection layout must fit the partial buffer
+  const int64_t need = ceil_div(n, 64) * 64 * 4;
+  if (need > h->part_cap) {
+    cudaFree(h->part);
+    h->part = nullptr;
+    LB_CUDA(cudaMalloc(&h->part, sizeof(double) * need));
+    h->part_cap = need;
+  }
   return LB_OK;
 }
 

@@ -254,6 +254,7 @@ def _bind_opset():
         L.lb_opset_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(P)]
         L.lb_opset_destroy.argtypes = [P]
         L.lb_opset_set_phi0.argtypes = [P, P]
+        L.lb_opset_set_fmm.argtypes = [P, P]
         L.lb_opset_apply.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_apply_layer.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_last_scalar.argtypes = [P, P]
@@ -311,6 +312,13 @@ class DeviceOperator:
         self.handle = h
         self._L = L
 
+    def set_fmm(self, plan):
+        """Attach an FmmPlan on (over_nodes, nodes) (None detaches)."""
+        self.keep["fmm"] = plan
+        _lib.check(self._L.lb_opset_set_fmm(
+            self.handle, plan._h if plan is not None else ctypes.c_void_p(0)),
+            "lb_opset_set_fmm")
+
     def set_phi0(self, phi0_dev):
         self.keep["phi0"] = phi0_dev
         _lib.check(self._L.lb_opset_set_phi0(self.handle,
@@ -349,11 +357,19 @@ class LayerOperatorSet:
       corrections : dict kind -> NearCorrections/CSR, or a CorrectionSet;
                     when None the reference's compute_corrections builds
                     them (requires lapbel to be importable).
+      far         : "auto" (default), "direct" or "fmm".  use_fmm=False
+                    always means exact all-pairs sweeps (the reference's
+                    evaluate_direct path).  With use_fmm=True, "auto" keeps
+                    the exact fp64 sweeps while N * N_over <= FMM_CROSSOVER
+                    (they are both faster and more accurate than the FMM
+                    there on a B200) and builds the FmmPlan at eps beyond it.
     """
+
+    FMM_CROSSOVER = 2.0e10  # target-source pairs per sweep
 
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
-                 corrections=None):
+                 corrections=None, far: str = "auto"):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -379,6 +395,18 @@ class LayerOperatorSet:
         self.n_apply = 0
         self.dev = DeviceOperator(disc, corrections, kinds)
         n = disc.nodes.shape[0]
+        nover = disc.over_nodes.shape[0]
+        if far not in ("auto", "direct", "fmm"):
+            raise ValueError("far must be 'auto', 'direct' or 'fmm'")
+        self.far = "direct"
+        if use_fmm and (far == "fmm" or (far == "auto" and
+                                         n * nover > self.FMM_CROSSOVER)):
+            from .fmm_plan import FmmPlan
+            self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps)
+            self.dev.set_fmm(self._plan)
+            self.far = "fmm"
+        else:
+            self._plan = None
         self._n = n
         self._out = _lib.empty((n,))
         # S[1], stored once for the SWS term of A1 (operators.py:99-100)
@@ -397,12 +425,13 @@ class LayerOperatorSet:
             self._phi0_dev.cpu().numpy()
 
     @classmethod
-    def from_bundle(cls, arrs, formulation: str, eps: float | None = None):
+    def from_bundle(cls, arrs, formulation: str, eps: float | None = None,
+                    **kw):
         """Build from a saved bundle (scripts/make_golden.py layout)."""
         geom = Geometry.from_arrays(arrs)
         cset = CorrectionSet.from_arrays(arrs)
         e = float(arrs["eps"]) if eps is None and "eps" in arrs else eps
-        return cls(geom, formulation, e, corrections=cset)
+        return cls(geom, formulation, e, corrections=cset, **kw)
 
     # -- reference-compatible accessors -----------------------------------
     def corr(self, kind):
