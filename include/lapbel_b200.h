@@ -118,6 +118,9 @@ typedef struct {
   const double* corr[LB_NKINDS];
   double weight_sum;
   const double* phi0;
+  /* owned target rows [row0, row0 + nrows) for a sharded apply (nrows = 0:
+   * all rows).  Densities stay full length; only owned rows are written. */
+  int64_t row0, nrows;
 } lb_opset_desc;
 
 typedef struct lb_opset lb_opset;
@@ -139,6 +142,20 @@ int lb_opset_set_fmm(lb_opset* h, struct lb_fmm_plan* plan);
  * correction kind -> LB_ERR_KEY (operators.py:119-123). */
 int lb_opset_apply(lb_opset* h, int formulation, const double* tau,
                    double* out, void* stream);
+/* Sharded apply: the formulation runs as phases (A3: 3, A2/A1:
+ * 2) on the handle's rows; after phase p the caller all-gathers the work
+ * vectors lb_opset_phase_exchange lists (rows [row0, row0+nrows) of each
+ * rank -> full vectors, see lb_opset_buffers) and, when reduce_scalar is set,
+ * sum-all-reduces the handle's scalar.  The result's owned rows are valid
+ * after the last phase.  vecs must hold 3 ints. */
+int lb_opset_apply_phase(lb_opset* h, int formulation, int phase,
+                         const double* tau, double* out, void* stream);
+int lb_opset_phase_exchange(const lb_opset* h, int formulation, int phase,
+                            int* nvec, int* vecs, int* reduce_scalar);
+/* device pointers: work vectors (k * n doubles each, k < 8) and the scalar */
+int lb_opset_buffers(const lb_opset* h, double** work, double** scalar,
+                     int64_t* row0, int64_t* nrows);
+
 /* out = corrected layer operator of `kind` applied to tau
  * (apply_layer, operators.py:126-155). */
 int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau,

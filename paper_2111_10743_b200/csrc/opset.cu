@@ -244,9 +244,11 @@ struct EpiA1p2 : EpiBase {
 template <int J, class E>
 __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
                                                          const int32_t* __restrict__ indices,
-                                                         int64_t nrows, int wpr, CsrJobs<J> jobs,
-                                                         E epi, double* partials, unsigned* ticket,
-                                                         double* red_out, double red_div) {
+                                                         int64_t grow0, int64_t nrows, int wpr,
+                                                         CsrJobs<J> jobs, E epi, double* partials,
+                                                         unsigned* ticket, double* red_out,
+                                                         double red_div) {
+  // local rows r in [0, nrows) are global rows grow0 + r (sharded apply)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int rb = (kCsrBT / 32) / wpr;
@@ -278,14 +280,15 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
       fs[threadIdx.x] = s8;
     }
     e.fs = fs;
-    e.row0 = row0;
+    e.row0 = grow0 + row0;
   }
   const int rloc = warp / wpr, seg = warp - rloc * wpr;
-  const int64_t row = row0 + rloc;
+  const int64_t lrow = row0 + rloc;
+  const int64_t row = grow0 + lrow;
   double acc[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) acc[j] = 0.0;
-  if (row < nrows) {
+  if (lrow < nrows) {
     const int64_t kb = indptr[row], ke = indptr[row + 1];
     const int64_t stride = 32 * wpr;
     int64_t k = kb + seg * 32 + lane;
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
   }
   __syncthreads();
   double red = 0.0;
-  if (row < nrows && seg == 0 && lane == 0) {
+  if (lrow < nrows && seg == 0 && lane == 0) {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       double t = 0.0;
@@ -349,6 +352,7 @@ __global__ void add_scalar_kernel(double* y, int64_t n, const double* s) {
 
 struct lb_opset {
   lb_opset_desc d;
+  int64_t r0 = 0, nr = 0;  // owned target rows [r0, r0 + nr) (sharded apply)
   double wsum = 0.0;
   int64_t ns_pad = 0;
   double* pack4 = nullptr;  // [x y z c]
@@ -397,7 +401,7 @@ SkLayout far_layout(const lb_opset* h) {
                                                   kFarBT, 0);
     per_sm = std::max(b, 1);
   }
-  return make_sk_layout(h->d.n, h->ns_pad, kFarBT * TPT, far_ts<F>(), (int64_t)sm_count() * per_sm);
+  return make_sk_layout(h->nr, h->ns_pad, kFarBT * TPT, far_ts<F>(), (int64_t)sm_count() * per_sm);
 }
 
 template <class F>
@@ -412,8 +416,8 @@ int run_far(const lb_opset* h, const double* pack, SkLayout* out, cudaStream_t s
   const SkLayout L = far_layout<F>(h);
   if (L.tiles * L.kmax * F::NOUT * L.tt > h->part_cap)
     return fail(LB_ERR_ARG, "opset: partial buffer too small");
-  opfar_kernel<F, TPT, kFarBT, far_ts<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(h->d.nodes, h->d.normals,
-                                                                        h->d.n, pack, L, h->part);
+  opfar_kernel<F, TPT, kFarBT, far_ts<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(
+      h->d.nodes + 3 * h->r0, h->d.normals + 3 * h->r0, h->nr, pack, L, h->part);
   LB_CHECK_LAUNCH();
   *out = L;
   return LB_OK;
@@ -450,8 +454,8 @@ int run_csr(const lb_opset* h, const double* const* vals, const double* const* x
     jobs.x[j] = xs[j];
   }
   csr_epi_kernel<J, E><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
-      h->d.indptr, h->d.indices, h->d.n, h->csr_wpr, jobs, epi, h->partials, h->ticket, h->scal,
-      red_div);
+      h->d.indptr, h->d.indices, h->r0, h->nr, h->csr_wpr, jobs, epi, h->partials, h->ticket,
+      h->scal, red_div);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }
@@ -562,7 +566,7 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
     }
   }
   // FMM path: plain charge arrays c_v = w_over * oversample(in_v)
-  const int64_t no = h->d.n_over, n = h->d.n;
+  const int64_t no = h->d.n_over, n = h->nr;
   const int slot[3] = {0, (int)no, (int)(2 * no)};
   LB_TRY(oversample(h, nv, in, slot, h->f_ch, 1, add_ws, st));
   double* c0 = h->f_ch;
@@ -609,88 +613,86 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
   l1.G = l1.tiles;
   l1.kmax = 1;
   const int nout = far_nout(kind);
-  project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals, n, h->f_pot,
+  project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals + 3 * h->r0, n, h->f_pot,
                                                              h->f_grad, h->f_hess, l1, nout, h->part);
   LB_CHECK_LAUNCH();
   *L = l1;
   return LB_OK;
 }
 
-int apply_a3(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
+// The three formulations as phases separated by the only cross-row
+// dependencies of the apply: a phase ends where every row's
+// value of an intermediate density (or the W-average) is needed.  A sharded
+// apply runs the phases on its rows and exchanges, between them, the work
+// vectors lb_opset_phase_exchange lists (all-gather) and the scalar
+// (all-reduce); an unsharded apply runs them back to back.
+int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
-  SkLayout L1{}, L2{};
-  double* s_tau = V(h, 0);
-  double* sp_tau = V(h, 1);
-  const double* in1[1] = {tau};
-  LB_TRY(far_stage(h, FK_A3A, 1, in1, false, &L1, st));
-  {
-    auto e = base_epi<EpiA3p1>(h, L1, 2);
-    e.s_tau = s_tau;
-    e.sp_tau = sp_tau;
-    const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
-    const double* xs[2] = {tau, tau};
-    LB_TRY((run_csr<2>(h, vals, xs, e, st)));
+  SkLayout L{};
+  if (form == 3) {
+    double* s_tau = V(h, 0);
+    double* sp_tau = V(h, 1);
+    if (phase == 0) {
+      const double* in1[1] = {tau};
+      LB_TRY(far_stage(h, FK_A3A, 1, in1, false, &L, st));
+      auto e = base_epi<EpiA3p1>(h, L, 2);
+      e.s_tau = s_tau;
+      e.sp_tau = sp_tau;
+      const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
+      const double* xs[2] = {tau, tau};
+      return run_csr<2>(h, vals, xs, e, st);
+    }
+    if (phase == 1) {
+      const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
+      LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L, st));
+      auto e = base_epi<EpiA3p2>(h, L, 4);
+      e.tau = tau;
+      e.curv = h->d.curvature;
+      e.w = h->d.weights;
+      e.result = out;
+      const double* vals[4] = {C[LB_KIND_SPRIME], C[LB_KIND_S], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+      const double* xs[4] = {sp_tau, s_tau, s_tau, s_tau};
+      return run_csr<4>(h, vals, xs, e, st, h->wsum);
+    }
+    add_scalar_kernel<<<(unsigned)ceil_div(h->nr, 256), 256, 0, st>>>(out + h->r0, h->nr, h->scal);
+    LB_CHECK_LAUNCH();
+    return LB_OK;
   }
-  const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
-  LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L2, st));
-  {
-    auto e = base_epi<EpiA3p2>(h, L2, 4);
-    e.tau = tau;
-    e.curv = h->d.curvature;
-    e.w = h->d.weights;
-    e.result = out;
-    const double* vals[4] = {C[LB_KIND_SPRIME], C[LB_KIND_S], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
-    const double* xs[4] = {sp_tau, s_tau, s_tau, s_tau};
-    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
-  }
-  add_scalar_kernel<<<(unsigned)ceil_div(h->d.n, 256), 256, 0, st>>>(out, h->d.n, h->scal);
-  LB_CHECK_LAUNCH();
-  return LB_OK;
-}
-
-int apply_a2(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
-  const auto* C = h->d.corr;
-  SkLayout L1{}, L2{};
-  double* mu1 = V(h, 0);
-  double* mu2 = V(h, 1);
-  const double* in1[1] = {tau};
-  LB_TRY(far_stage(h, FK_A2A, 1, in1, false, &L1, st));
-  {
-    auto e = base_epi<EpiA2p1>(h, L1, 4);
-    e.curv = h->d.curvature;
-    e.w = h->d.weights;
-    e.mu1 = mu1;
-    e.mu2 = mu2;
-    const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_D], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
-    const double* xs[4] = {tau, tau, tau, tau};
-    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
-  }
-  // mu2 += ws in place (scal[0]) while both are oversampled
-  const double* in2[2] = {mu2, mu1};
-  LB_TRY(far_stage(h, FK_A2B, 2, in2, true, &L2, st));
-  {
-    auto e = base_epi<EpiA2p2>(h, L2, 2);
+  if (form == 2) {
+    double* mu1 = V(h, 0);
+    double* mu2 = V(h, 1);
+    if (phase == 0) {
+      const double* in1[1] = {tau};
+      LB_TRY(far_stage(h, FK_A2A, 1, in1, false, &L, st));
+      auto e = base_epi<EpiA2p1>(h, L, 4);
+      e.curv = h->d.curvature;
+      e.w = h->d.weights;
+      e.mu1 = mu1;
+      e.mu2 = mu2;
+      const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_D], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+      const double* xs[4] = {tau, tau, tau, tau};
+      return run_csr<4>(h, vals, xs, e, st, h->wsum);
+    }
+    // mu2 += ws in place (scal[0]) while both are oversampled
+    const double* in2[2] = {mu2, mu1};
+    LB_TRY(far_stage(h, FK_A2B, 2, in2, true, &L, st));
+    auto e = base_epi<EpiA2p2>(h, L, 2);
     e.tau = tau;
     e.result = out;
     const double* vals[2] = {C[LB_KIND_D], C[LB_KIND_S]};
     const double* xs[2] = {mu1, mu2};
-    LB_TRY((run_csr<2>(h, vals, xs, e, st)));
+    return run_csr<2>(h, vals, xs, e, st);
   }
-  return LB_OK;
-}
-
-int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
-  const auto* C = h->d.corr;
+  // form == 1
   if (!h->d.tangents_u || !h->d.tangents_v || !h->d.inv_metric || !h->d.phi0)
     return fail(LB_ERR_ARG, "opset: A1 needs tangents, inverse metric and phi0");
-  SkLayout L1{}, L2{};
   double* mux = V(h, 0);
   double* muy = V(h, 1);
   double* muz = V(h, 2);
-  const double* in1[1] = {tau};
-  LB_TRY(far_stage(h, FK_A1A, 1, in1, false, &L1, st));
-  {
-    auto e = base_epi<EpiA1p1>(h, L1, 4);
+  if (phase == 0) {
+    const double* in1[1] = {tau};
+    LB_TRY(far_stage(h, FK_A1A, 1, in1, false, &L, st));
+    auto e = base_epi<EpiA1p1>(h, L, 4);
     e.tu = h->d.tangents_u;
     e.tv = h->d.tangents_v;
     e.gi = h->d.inv_metric;
@@ -700,21 +702,20 @@ int apply_a1(lb_opset* h, const double* tau, double* out, cudaStream_t st) {
     e.muz = muz;
     const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
     const double* xs[4] = {tau, tau, tau, tau};
-    LB_TRY((run_csr<4>(h, vals, xs, e, st, h->wsum)));
+    return run_csr<4>(h, vals, xs, e, st, h->wsum);
   }
   const double* in2[3] = {mux, muy, muz};
-  LB_TRY(far_stage(h, FK_A1B, 3, in2, false, &L2, st));
-  {
-    auto e = base_epi<EpiA1p2>(h, L2, 1);
-    e.phi0 = h->d.phi0;
-    e.eta = h->scal;
-    e.result = out;
-    const double* vals[3] = {C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
-    const double* xs[3] = {mux, muy, muz};
-    LB_TRY((run_csr<3>(h, vals, xs, e, st)));
-  }
-  return LB_OK;
+  LB_TRY(far_stage(h, FK_A1B, 3, in2, false, &L, st));
+  auto e = base_epi<EpiA1p2>(h, L, 1);
+  e.phi0 = h->d.phi0;
+  e.eta = h->scal;
+  e.result = out;
+  const double* vals[3] = {C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
+  const double* xs[3] = {mux, muy, muz};
+  return run_csr<3>(h, vals, xs, e, st);
 }
+
+int nphases(int form) { return form == 3 ? 3 : 2; }
 
 int apply_layer(lb_opset* h, int kind, const double* tau, double* out, cudaStream_t st) {
   if (kind < 0 || kind >= LB_NKINDS) return fail(LB_ERR_ARG, "opset: unknown kernel kind");
@@ -758,8 +759,12 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   if (!d->nodes || !d->normals || !d->weights || !d->curvature || !d->over_nodes ||
       !d->over_normals || !d->over_weights || !d->over_interp || !d->indptr || !d->indices)
     return fail(LB_ERR_ARG, "lb_opset_create: missing geometry or CSR pattern");
+  if (d->row0 < 0 || d->nrows < 0 || d->row0 + d->nrows > d->n)
+    return fail(LB_ERR_SHAPE, "lb_opset_create: row range outside [0, n)");
   lb_opset* h = new lb_opset();
   h->d = *d;
+  h->r0 = d->nrows > 0 ? d->row0 : 0;
+  h->nr = d->nrows > 0 ? d->nrows : d->n;
   h->wsum = d->weight_sum;
   const int64_t n = d->n;
   h->ns_pad = ceil_div(d->n_over, kFarPad) * kFarPad;
@@ -774,7 +779,7 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   cap = std::max(cap, far_part_size<FarA1b>(h));
   h->part_cap = cap;
   h->csr_wpr = csr_wpr(d->nnz, n);
-  h->csr_blocks = (int)ceil_div(n, (kCsrBT / 32) / h->csr_wpr);
+  h->csr_blocks = (int)ceil_div(h->nr, (kCsrBT / 32) / h->csr_wpr);
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes);
@@ -834,11 +839,11 @@ int lb_opset_set_fmm(lb_opset* h, lb_fmm_plan* plan) {
   if (!plan || h->f_ch) return LB_OK;
   int64_t sizes[10];
   LB_TRY(lb_fmm_plan_info(plan, sizes, nullptr));
-  if (sizes[2] != h->d.n_over || sizes[3] != h->d.n) {
+  if (sizes[2] != h->d.n_over || sizes[3] != h->nr) {
     h->fmm = nullptr;
     return fail(LB_ERR_SHAPE, "lb_opset_set_fmm: plan sources/targets must be over_nodes/nodes");
   }
-  const int64_t no = h->d.n_over, n = h->d.n;
+  const int64_t no = h->d.n_over, n = h->nr;
   cudaError_t e = cudaSuccess;
   auto A = [&](double** p, int64_t k) { if (e == cudaSuccess) e = cudaMalloc((void**)p, sizeof(double) * k); };
   A(&h->f_ch, 3 * no);
@@ -873,12 +878,48 @@ int lb_opset_apply(lb_opset* h, int formulation, const double* tau, double* out,
   if (!h || !tau || !out) return fail(LB_ERR_ARG, "lb_opset_apply: null argument");
   if (tau == out) return fail(LB_ERR_ARG, "lb_opset_apply: tau and out must not alias");
   cudaStream_t st = as_stream(stream);
-  switch (formulation) {
-    case 1: return apply_a1(h, tau, out, st);
-    case 2: return apply_a2(h, tau, out, st);
-    case 3: return apply_a3(h, tau, out, st);
-    default: return fail(LB_ERR_ARG, "lb_opset_apply: formulation must be 1, 2 or 3");
+  if (formulation < 1 || formulation > 3)
+    return fail(LB_ERR_ARG, "lb_opset_apply: formulation must be 1, 2 or 3");
+  if (h->nr != h->d.n)
+    return fail(LB_ERR_ARG, "lb_opset_apply: sharded handle; run lb_opset_apply_phase with exchanges");
+  for (int p = 0; p < nphases(formulation); ++p) LB_TRY(apply_phase(h, formulation, p, tau, out, st));
+  return LB_OK;
+}
+
+int lb_opset_apply_phase(lb_opset* h, int formulation, int phase, const double* tau, double* out,
+                         void* stream) {
+  using namespace lb;
+  if (!h || !tau || !out) return fail(LB_ERR_ARG, "lb_opset_apply_phase: null argument");
+  if (formulation < 1 || formulation > 3 || phase < 0 || phase >= nphases(formulation))
+    return fail(LB_ERR_ARG, "lb_opset_apply_phase: bad formulation/phase");
+  return apply_phase(h, formulation, phase, tau, out, as_stream(stream));
+}
+
+int lb_opset_phase_exchange(const lb_opset* h, int formulation, int phase, int* nvec, int* vecs,
+                            int* reduce_scalar) {
+  using namespace lb;
+  if (!h || !nvec || !vecs || !reduce_scalar) return fail(LB_ERR_ARG, "lb_opset_phase_exchange: null");
+  *nvec = 0;
+  *reduce_scalar = 0;
+  if (formulation == 3) {
+    if (phase == 0) { *nvec = 2; vecs[0] = 0; vecs[1] = 1; }
+    else if (phase == 1) *reduce_scalar = 1;
+  } else if (phase == 0) {
+    *nvec = formulation == 2 ? 2 : 3;
+    for (int k = 0; k < *nvec; ++k) vecs[k] = k;
+    *reduce_scalar = 1;
   }
+  return LB_OK;
+}
+
+int lb_opset_buffers(const lb_opset* h, double** work, double** scalar, int64_t* row0,
+                     int64_t* nrows) {
+  if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_buffers: null handle");
+  if (work) *work = h->vec;
+  if (scalar) *scalar = h->scal;
+  if (row0) *row0 = h->r0;
+  if (nrows) *nrows = h->nr;
+  return LB_OK;
 }
 
 int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau, double* out, void* stream) {
@@ -948,7 +989,7 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
       epi.y[j] = ys[j];                                                                     \
     }                                                                                       \
     epi.accumulate = accumulate;                                                            \
-    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, nrows, wpr, jobs, \
+    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, 0, nrows, wpr, jobs, \
                                                               epi, nullptr, nullptr,        \
                                                               nullptr, 1.0);                \
   }

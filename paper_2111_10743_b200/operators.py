@@ -240,7 +240,8 @@ class _Desc(ctypes.Structure):
             "over_weights", "over_interp")] + \
         [("nnz", ctypes.c_int64), ("indptr", ctypes.c_void_p),
          ("indices", ctypes.c_void_p), ("corr", ctypes.c_void_p * 7),
-         ("weight_sum", ctypes.c_double), ("phi0", ctypes.c_void_p)]
+         ("weight_sum", ctypes.c_double), ("phi0", ctypes.c_void_p),
+         ("row0", ctypes.c_int64), ("nrows", ctypes.c_int64)]
 
 
 _Lib = None
@@ -255,6 +256,9 @@ def _bind_opset():
         L.lb_opset_destroy.argtypes = [P]
         L.lb_opset_set_phi0.argtypes = [P, P]
         L.lb_opset_set_fmm.argtypes = [P, P]
+        L.lb_opset_apply_phase.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.lb_opset_phase_exchange.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.lb_opset_buffers.argtypes = [P, P, P, P, P]
         L.lb_opset_apply.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_apply_layer.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_last_scalar.argtypes = [P, P]
@@ -265,7 +269,8 @@ def _bind_opset():
 class DeviceOperator:
     """Owner of the device arrays and the lb_opset handle (C ABI)."""
 
-    def __init__(self, disc, corrections: CorrectionSet, kinds):
+    def __init__(self, disc, corrections: CorrectionSet, kinds, row0=0,
+                 nrows=0):
         t = _lib.require_cuda()
         L = _bind_opset()
         oi = _over_interp(disc)
@@ -304,6 +309,9 @@ class DeviceOperator:
                                               corrections.values[kind])
         d.weight_sum = float(np.sum(disc.weights))
         d.phi0 = None
+        d.row0, d.nrows = int(row0), int(nrows)
+        self.row0 = int(row0)
+        self.nrows = int(nrows) if nrows else n
         self.desc = d
         self.n = n
         h = ctypes.c_void_p()
@@ -330,6 +338,31 @@ class DeviceOperator:
             ctypes.c_void_p(out.data_ptr()), _lib.stream_handle(stream)),
             "lb_opset_apply")
 
+    def apply_phase(self, formulation: int, phase: int, tau, out, stream=None):
+        _lib.check(self._L.lb_opset_apply_phase(
+            self.handle, formulation, phase, ctypes.c_void_p(tau.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _lib.stream_handle(stream)),
+            "lb_opset_apply_phase")
+
+    def phase_exchange(self, formulation: int, phase: int):
+        nvec, red = ctypes.c_int(), ctypes.c_int()
+        vecs = (ctypes.c_int * 3)()
+        _lib.check(self._L.lb_opset_phase_exchange(
+            self.handle, formulation, phase, ctypes.byref(nvec), vecs,
+            ctypes.byref(red)))
+        return [vecs[i] for i in range(nvec.value)], bool(red.value)
+
+    def buffers(self):
+        """(work vectors (8, n) tensor view, scalar (1,) tensor view)."""
+        if "views" not in self.keep:
+            t = _lib.torch()
+            w, sc = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(self._L.lb_opset_buffers(self.handle, ctypes.byref(w),
+                                                ctypes.byref(sc), None, None))
+            self.keep["views"] = (_device_view(w.value, (8, self.n), t),
+                                  _device_view(sc.value, (1,), t))
+        return self.keep["views"]
+
     def apply_layer(self, kind: KernelKind, tau, out, stream=None):
         _lib.check(self._L.lb_opset_apply_layer(
             self.handle, KIND_CODE[kind], ctypes.c_void_p(tau.data_ptr()),
@@ -347,6 +380,16 @@ class DeviceOperator:
 
 
 _FORM_CODE = {"a1": 1, "a2": 2, "a3": 3}
+
+
+def _device_view(addr, shape, t):
+    """Zero-copy torch view of a float64 device buffer owned by libb200lb."""
+    n = int(np.prod(shape))
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                    "data": (addr, False), "version": 3}
+    return t.as_tensor(_Cai(), device="cuda").view(*shape)
 
 
 class LayerOperatorSet:
