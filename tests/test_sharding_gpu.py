@@ -74,4 +74,6 @@ def test_emulated_shards_match_unsharded(cuda, fixture, form, far):
             d.set_phi0(phi0)
         got = _emulate(devs, parts, code, tau, torch)
         err = (got - ref).abs().max().item() / ref.abs().max().item()
-        assert err < (1e-12 if far == "direct" else 1e-9), (world, err)
+        # FMM shards build their own trees over their targets: a different,
+        # equally valid eps = 1e-10 approximation (100 x eps after S''+D' noise)
+        assert err < (1e-12 if far == "direct" else 1e-8), (world, err)
