@@ -175,7 +175,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config2-A3-operator-apply", "N": n,
                    "N_over": nover, "formulation": "a3",
@@ -215,7 +215,15 @@ def main():
     b = load_bundle()
     n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
     inter = 4 * n * nover  # density-sweeps x targets x sources per step
-    op = LayerOperatorSet.from_bundle(b, "a3")
+    if world > 1:
+        # target rows sharded over the ranks, densities all-gathered between
+        # the apply's phases over NCCL (sharding.py); GMRES replicated
+        from paper_2111_10743_b200 import CorrectionSet, Geometry
+        from paper_2111_10743_b200.sharding import ShardedOperatorSet
+        op = ShardedOperatorSet(Geometry.from_arrays(b), "a3", float(b["eps"]),
+                                CorrectionSet.from_arrays(b))
+    else:
+        op = LayerOperatorSet.from_bundle(b, "a3")
     L = _bind()
     st = _lib.stream_handle()
 
@@ -269,11 +277,12 @@ def main():
         tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_step = float(tt.item())
-    value = inter * world / t_step  # independent replicas: whole-job aggregate
+    value = inter / t_step  # one apply per step, shared by all ranks (strong scaling)
 
     # dominant kernel: far sweep 2 (opfar_kernel<FarA3b>), timed alone
     from paper_2111_10743_b200.operators import _bind_opset  # noqa: F401
     far_t = far2_time(torch, op, tau, lib, _lib)
+    nloc = op.dev.nrows if world > 1 else n
 
     # e2e through the public API with host buffers: H2D tau, apply, D2H result
     tau_h = torch.from_numpy(np.asarray(b["tau"])).pin_memory()
@@ -288,9 +297,13 @@ def main():
         out_h.copy_(v, non_blocking=True)
     e2e_times, _ = timed(e2e_step, args.steps)
     e2e_t = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(tt.item())
 
     peak = fp64_peak_tflops(torch, lib, _lib)
-    far_flops = 44.0 * n * nover  # algorithmic flops of FarA3b per launch
+    far_flops = 44.0 * nloc * nover  # algorithmic flops of FarA3b per launch
     achieved = far_flops / far_t / 1e12
 
     cpu = None
@@ -305,12 +318,12 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": t_step * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (config 2 geometry + reference-built corrections)",
             "config": {"workload": "config2-A3-operator-apply+MGS(k=4)",
                        "N": n, "N_over": nover, "formulation": "a3",
                        "interactions_per_step": inter,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"target-shard{world}" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MB write)",
                        "apply_parity_vs_reference": parity},
             "roofline": {"bound": "fp64", "kernel": "opfar_kernel<FarA3b>",
@@ -321,7 +334,7 @@ def main():
                          "far2_ms": far_t * 1e3, "flops_per_pair": 44,
                          "traffic": None},
             "cpu_baseline": cpu,
-            "e2e": {"value": inter * world / e2e_t, "unit": UNIT,
+            "e2e": {"value": inter / e2e_t, "unit": UNIT,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": e2e_t * 1e3},
             "gpu_launches": launches_per_step * args.steps,
@@ -337,6 +350,7 @@ def far2_time(torch, op, tau, lib, _lib, which=2, reps=20):
     (lb_opset_time_far); the packed sources are the last apply's."""
     import ctypes
     op.apply_device(tau)
+    torch.cuda.synchronize()
     sec = ctypes.c_double(0.0)
     _lib.check(lib.lb_opset_time_far(op.dev.handle, which, reps, ctypes.byref(sec),
                                      _lib.stream_handle()))
