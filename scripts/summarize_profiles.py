@@ -1,0 +1,106 @@
+"""Summarise ncu outputs from gpurun_out/ into profiles/round1/ (tracked)."""
+import csv
+import json
+import os
+import re
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "profiles", "round1")
+G = os.path.join(ROOT, "gpurun_out")
+os.makedirs(OUT, exist_ok=True)
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    for i, r in enumerate(rows):
+        if "Kernel Name" in r:
+            hdr, start = r, i
+            break
+    ki, mi, vi, ui, idi = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value",
+                                                    "Metric Unit", "ID"))
+    recs = defaultdict(dict)
+    names = {}
+    for r in rows[start + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        u = r[ui]
+        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3,
+                 "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        recs[r[idi]][r[mi]] = v * scale
+        names[r[idi]] = re.sub(r"\(.*", "", r[ki])[:80]
+    return [(names[k], recs[k]) for k in sorted(recs, key=int)]
+
+
+def step_summary():
+    L = launches(os.path.join(G, "launches_step.csv"))
+    tot = sum(m["gpu__time_duration.sum"] for _, m in L)
+    lines = ["# Config 2 bench step (A3 apply + MGS k=4): ncu launch list",
+             "", "Cold-cache, serialised (ncu); compare SHARES, not absolute times "
+             "(bench.py times the step with CUDA events).", "",
+             "| # | kernel | us | share | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|---|"]
+    for i, (nm, m) in enumerate(L):
+        t = m["gpu__time_duration.sum"]
+        lines.append(f"| {i} | `{nm}` | {t:.1f} | {100 * t / tot:.1f}% | "
+                     f"{m.get('dram__bytes_read.sum', 0) / 1e6:.1f} | "
+                     f"{m.get('dram__bytes_write.sum', 0) / 1e6:.1f} |")
+    lines.append(f"| | total | {tot:.1f} | 100% | | |")
+    open(os.path.join(OUT, "config2_step_launches.md"), "w").write("\n".join(lines) + "\n")
+    return L
+
+
+def fmm_summary():
+    L = launches(os.path.join(G, "launches_fmm.csv"))
+    agg = defaultdict(lambda: [0, 0.0])
+    for nm, m in L:
+        key = re.sub(r"<.*", "", nm.replace("void ", "")).strip()
+        agg[key][0] += 1
+        agg[key][1] += m["gpu__time_duration.sum"]
+    tot = sum(v[1] for v in agg.values())
+    lines = ["# FMM apply, N = 1e6 uniform on the sphere, eps 1e-6 (surface m=8), nd=1 pot+grad",
+             "", "ncu launch list aggregated by kernel (cold-cache, serialised).", "",
+             "| kernel | launches | ms | share |", "|---|---|---|---|"]
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| `{k}` | {c} | {t / 1e3:.2f} | {100 * t / tot:.1f}% |")
+    lines.append(f"| total | {sum(v[0] for v in agg.values())} | {tot / 1e3:.2f} | |")
+    open(os.path.join(OUT, "fmm_1e6_eps1e-6_launches.md"), "w").write("\n".join(lines) + "\n")
+
+
+def full_summary(rep, out_name):
+    raw = subprocess.run(["ncu", "-i", os.path.join(G, rep), "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+            "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+            "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:90]}
+        for w in want:
+            if w in hdr:
+                d[w] = r[hdr.index(w)] + " " + units[hdr.index(w)]
+        res.append(d)
+    json.dump(res, open(os.path.join(OUT, out_name), "w"), indent=1)
+    return res
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["step", "fmm", "full"]
+    if "step" in what:
+        step_summary()
+    if "fmm" in what:
+        fmm_summary()
+    if "full" in what:
+        full_summary("prof_step2.ncu-rep", "ncu_full_config2_far_csr.json")
+    print("written to", OUT)
