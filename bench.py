@@ -303,6 +303,18 @@ def main():
         e2e_t = float(tt.item())
 
     peak = fp64_peak_tflops(torch, lib, _lib)
+    traffic = None  # dram read+write bytes per launch of the dominant kernel (ncu --set full)
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "round1",
+                                           "ncu_full_config2_far_csr.json")))
+        for k in prof:
+            if "FarA3b" in k["kernel"]:
+                tb = [float(k[m].split()[0]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+                                                "Gbyte": 1e9}[k[m].split()[1]]
+                      for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")]
+                traffic = sum(tb)
+    except (OSError, KeyError, ValueError):
+        pass
     far_flops = 44.0 * nloc * nover  # algorithmic flops of FarA3b per launch
     achieved = far_flops / far_t / 1e12
 
@@ -332,7 +344,10 @@ def main():
                          "peak_source": "measured in-run (lb_probe_dfma); nominal "
                                         f"{NOMINAL_FP64_TFLOPS}",
                          "far2_ms": far_t * 1e3, "flops_per_pair": 44,
-                         "traffic": None},
+                         "traffic": traffic,
+                         "traffic_note": "bytes/launch from profiles/round1 ncu --set full: "
+                                         "the kernel is FP64-bound, DRAM traffic is the "
+                                         "2.3 MB packed source array plus outputs"},
             "cpu_baseline": cpu,
             "e2e": {"value": inter / e2e_t, "unit": UNIT,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
