@@ -160,6 +160,11 @@ int lb_opset_buffers(const lb_opset* h, double** work, double** scalar,
  * (apply_layer, operators.py:126-155). */
 int lb_opset_apply_layer(lb_opset* h, int kind, const double* tau,
                          double* out, void* stream);
+/* Per-stage device timing of lb_opset_apply (events between stages; off by
+ * default): ms[0..] = consecutive stage durations (far 1, SpMV pass 1, far 2,
+ * SpMV pass 2 + glue ...), ms[7] = total (HOST double[8]). */
+int lb_opset_set_timing(lb_opset* h, int on);
+int lb_opset_stage_times(lb_opset* h, double* ms);
 /* Copies the last W-average (eta / ws) the handle computed to dev_out. */
 int lb_opset_last_scalar(const lb_opset* h, double* dev_out);
 

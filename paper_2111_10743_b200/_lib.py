@@ -48,6 +48,8 @@ SIGNATURES = {
     "lb_opset_apply_phase": [_P, _I32, _I32, _P, _P, _P],
     "lb_opset_phase_exchange": [_P, _I32, _I32, _P, _P, _P],
     "lb_opset_buffers": [_P, _P, _P, _P, _P],
+    "lb_opset_set_timing": [_P, _I32],
+    "lb_opset_stage_times": [_P, _P],
     "lb_opset_apply": [_P, _I32, _P, _P, _P],
     "lb_opset_apply_layer": [_P, _I32, _P, _P, _P],
     "lb_opset_last_scalar": [_P, _P],

@@ -202,8 +202,8 @@ __device__ __forceinline__ double sk_sum(const double* __restrict__ part, const 
   return v;
 }
 
-template <class F, int TPT, int BT, int TS, bool PF = true>
-__global__ void __launch_bounds__(BT) opfar_kernel(const double* __restrict__ nodes,
+template <class F, int TPT, int BT, int TS, bool PF = true, int UR = 4, int MINB = 1>
+__global__ void __launch_bounds__(BT, MINB) opfar_kernel(const double* __restrict__ nodes,
                                                    const double* __restrict__ normals, int64_t n,
                                                    const double* __restrict__ pack, SkLayout L,
                                                    double* __restrict__ part) {
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(BT) opfar_kernel(const double* __restrict__ no
           if (k < TS * S / 2) pf[q] = __ldg(g + k);
         }
       }
-#pragma unroll 2
+#pragma unroll UR
       for (int k = 0; k < TS; ++k) {
 #pragma unroll
         for (int j = 0; j < TPT; ++j) F::pair(tg[j], sh + k * S, acc[j]);

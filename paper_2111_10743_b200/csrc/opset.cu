@@ -368,6 +368,10 @@ struct lb_opset {
   int csr_wpr = 1;
   // optional FMM far field (lb_opset_set_fmm) and its scratch
   lb_fmm_plan* fmm = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[16] = {};
+  int nev = 0;
+  double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double *f_ch = nullptr, *f_ch3 = nullptr, *f_dp = nullptr;
   double *f_pot = nullptr, *f_grad = nullptr, *f_hess = nullptr;
 };
@@ -626,15 +630,22 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
 // apply runs the phases on its rows and exchanges, between them, the work
 // vectors lb_opset_phase_exchange lists (all-gather) and the scalar
 // (all-reduce); an unsharded apply runs them back to back.
+void tmark(lb_opset* h, cudaStream_t st) {
+  if (h->timing && h->nev < 16) cudaEventRecord(h->ev[h->nev++], st);
+}
+
 int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
   SkLayout L{};
+  if (phase == 0) h->nev = 0;
+  tmark(h, st);
   if (form == 3) {
     double* s_tau = V(h, 0);
     double* sp_tau = V(h, 1);
     if (phase == 0) {
       const double* in1[1] = {tau};
       LB_TRY(far_stage(h, FK_A3A, 1, in1, false, &L, st));
+      tmark(h, st);
       auto e = base_epi<EpiA3p1>(h, L, 2);
       e.s_tau = s_tau;
       e.sp_tau = sp_tau;
@@ -645,6 +656,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
     if (phase == 1) {
       const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
       LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L, st));
+      tmark(h, st);
       auto e = base_epi<EpiA3p2>(h, L, 4);
       e.tau = tau;
       e.curv = h->d.curvature;
@@ -664,6 +676,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
     if (phase == 0) {
       const double* in1[1] = {tau};
       LB_TRY(far_stage(h, FK_A2A, 1, in1, false, &L, st));
+      tmark(h, st);
       auto e = base_epi<EpiA2p1>(h, L, 4);
       e.curv = h->d.curvature;
       e.w = h->d.weights;
@@ -676,6 +689,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
     // mu2 += ws in place (scal[0]) while both are oversampled
     const double* in2[2] = {mu2, mu1};
     LB_TRY(far_stage(h, FK_A2B, 2, in2, true, &L, st));
+      tmark(h, st);
     auto e = base_epi<EpiA2p2>(h, L, 2);
     e.tau = tau;
     e.result = out;
@@ -692,6 +706,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
   if (phase == 0) {
     const double* in1[1] = {tau};
     LB_TRY(far_stage(h, FK_A1A, 1, in1, false, &L, st));
+      tmark(h, st);
     auto e = base_epi<EpiA1p1>(h, L, 4);
     e.tu = h->d.tangents_u;
     e.tv = h->d.tangents_v;
@@ -706,6 +721,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
   }
   const double* in2[3] = {mux, muy, muz};
   LB_TRY(far_stage(h, FK_A1B, 3, in2, false, &L, st));
+      tmark(h, st);
   auto e = base_epi<EpiA1p2>(h, L, 1);
   e.phi0 = h->d.phi0;
   e.eta = h->scal;
@@ -828,6 +844,8 @@ int lb_opset_destroy(lb_opset* h) {
   cudaFree(h->f_pot);
   cudaFree(h->f_grad);
   cudaFree(h->f_hess);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
   delete h;
   return LB_OK;
 }
@@ -873,6 +891,31 @@ int lb_opset_set_phi0(lb_opset* h, const double* phi0) {
   return LB_OK;
 }
 
+int lb_opset_set_timing(lb_opset* h, int on) {
+  if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_timing: null handle");
+  if (on && !h->ev[0])
+    for (auto& e : h->ev) LB_CUDA(cudaEventCreate(&e));
+  h->timing = on != 0;
+  return LB_OK;
+}
+
+// ms between consecutive marks of the last apply: [far 1, csr 1, far 2,
+// csr 2 (+ glue)], total in ms[7]
+int lb_opset_stage_times(lb_opset* h, double* ms) {
+  if (!h || !ms) return lb::fail(LB_ERR_ARG, "lb_opset_stage_times: null argument");
+  for (int i = 0; i < 8; ++i) ms[i] = 0.0;
+  if (!h->timing || h->nev < 2) return LB_OK;
+  LB_CUDA(cudaEventSynchronize(h->ev[h->nev - 1]));
+  float t = 0;
+  for (int i = 0; i + 1 < h->nev && i < 7; ++i) {
+    cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]);
+    ms[i] = t;
+  }
+  cudaEventElapsedTime(&t, h->ev[0], h->ev[h->nev - 1]);
+  ms[7] = t;
+  return LB_OK;
+}
+
 int lb_opset_apply(lb_opset* h, int formulation, const double* tau, double* out, void* stream) {
   using namespace lb;
   if (!h || !tau || !out) return fail(LB_ERR_ARG, "lb_opset_apply: null argument");
@@ -883,6 +926,7 @@ int lb_opset_apply(lb_opset* h, int formulation, const double* tau, double* out,
   if (h->nr != h->d.n)
     return fail(LB_ERR_ARG, "lb_opset_apply: sharded handle; run lb_opset_apply_phase with exchanges");
   for (int p = 0; p < nphases(formulation); ++p) LB_TRY(apply_phase(h, formulation, p, tau, out, st));
+  tmark(h, st);
   return LB_OK;
 }
 

@@ -169,14 +169,21 @@ class CorrectionSet:
     Built from the reference's NearCorrections / scipy CSR matrices."""
 
     def __init__(self, indptr, indices, values: dict, shape=None):
-        self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
-        self.indices = np.ascontiguousarray(indices, dtype=np.int32)
-        self.values = {as_kind(k): np.ascontiguousarray(v, dtype=float)
-                       for k, v in values.items()}
+        if _lib.is_torch(indices):  # already on the device (large patterns)
+            t = _lib.torch()
+            self.indptr = indptr.to(dtype=t.int64).contiguous()
+            self.indices = indices.to(dtype=t.int32).contiguous()
+            self.values = {as_kind(k): v.to(dtype=t.float64).contiguous()
+                           for k, v in values.items()}
+        else:
+            self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+            self.indices = np.ascontiguousarray(indices, dtype=np.int32)
+            self.values = {as_kind(k): np.ascontiguousarray(v, dtype=float)
+                           for k, v in values.items()}
         n = len(self.indptr) - 1
         self.shape = shape or (n, n)
         for k, v in self.values.items():
-            if v.shape != self.indices.shape:
+            if tuple(v.shape) != tuple(self.indices.shape):
                 raise ValueError(f"correction values for {k} do not match "
                                  "the shared pattern")
 
@@ -259,6 +266,8 @@ def _bind_opset():
         L.lb_opset_apply_phase.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
         L.lb_opset_phase_exchange.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
         L.lb_opset_buffers.argtypes = [P, P, P, P, P]
+        L.lb_opset_set_timing.argtypes = [P, ctypes.c_int]
+        L.lb_opset_stage_times.argtypes = [P, P]
         L.lb_opset_apply.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_apply_layer.argtypes = [P, ctypes.c_int, P, P, P]
         L.lb_opset_last_scalar.argtypes = [P, P]
@@ -283,7 +292,7 @@ class DeviceOperator:
         def put(name, a, dtype=None):
             if a is None:
                 return None
-            x = dev(np.ascontiguousarray(a), dtype)
+            x = dev(a if _lib.is_torch(a) else np.ascontiguousarray(a), dtype)
             self.keep[name] = x
             return x.data_ptr()
 
@@ -351,6 +360,15 @@ class DeviceOperator:
             self.handle, formulation, phase, ctypes.byref(nvec), vecs,
             ctypes.byref(red)))
         return [vecs[i] for i in range(nvec.value)], bool(red.value)
+
+    def set_timing(self, on=True):
+        _lib.check(self._L.lb_opset_set_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self):
+        ms = np.zeros(8)
+        _lib.check(self._L.lb_opset_stage_times(self.handle,
+                                                ms.ctypes.data_as(ctypes.c_void_p)))
+        return ms
 
     def buffers(self):
         """(work vectors (8, n) tensor view, scalar (1,) tensor view)."""

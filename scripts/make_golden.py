@@ -492,6 +492,21 @@ def config2(eps=1e-10):
     print("total", time.time() - t0)
 
 
+def config3():
+    """BASELINE config 3 geometry (build_torus(7, 64, 32, 2, 1): N = 114,688)
+    and its near map (eta 2, cap raised to 256: the default 128 raises
+    NearMapCapError here).  Corrections are NOT built (the reference's t_q is
+    hours at this size): timing runs put synthetic values on this exact
+    sparsity pattern and say so."""
+    t0 = time.time()
+    disc = shapes.build_torus(7, 64, 32, 2.0, 1.0)
+    near = build_near_map(disc, 2.0, cap=256)
+    out = dict(geometry_arrays(disc))
+    out.update(near_arrays(near))
+    savez(os.path.join(DATA, "config3_geom.npz"), **out)
+    print("config3", disc.nnodes, disc.noversampled, time.time() - t0)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":

@@ -17,10 +17,10 @@ int fail(int c, const std::string& m) { g_err = m; return c; }
 int sm_count() { int n = 0; cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, 0); return n; }
 }  // namespace lb
 
-template <class F, int TPT, int BT, int TS = 128, bool PF = true>
+template <class F, int TPT, int BT, int TS = 128, bool PF = true, int UR = 2, int MINB = 1>
 void run(const char* name, const double* nodes, const double* normals, int64_t n, const double* pack,
          int64_t ns_pad, double* part, int grid_mult) {
-  auto kern = opfar_kernel<F, TPT, BT, TS, PF>;
+  auto kern = opfar_kernel<F, TPT, BT, TS, PF, UR, MINB>;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BT, 0);
   const SkLayout L = make_sk_layout(n, ns_pad, BT * TPT, TS, (int64_t)sm_count() * per_sm * grid_mult);
@@ -37,7 +37,10 @@ void run(const char* name, const double* nodes, const double* normals, int64_t n
   cudaEventElapsedTime(&ms, e0, e1);
   const double t = ms / reps * 1e-3;
   const double pairs = (double)n * (ns_pad);
-  printf("%-8s PF=%d TS=%d TPT=%d BT=%d gridx%d per_sm=%d G=%lld kmax=%lld  %.1f us  %.3e pairs/s\n", name, (int)PF, TS, TPT, BT,
+  int regs = 0;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) regs = fa.numRegs;
+  printf("%-8s UR=%d MINB=%d regs=%d PF=%d TS=%d TPT=%d BT=%d gridx%d per_sm=%d G=%lld kmax=%lld  %.1f us  %.3e pairs/s\n", name, UR, MINB, regs, (int)PF, TS, TPT, BT,
          grid_mult, per_sm, (long long)L.G, (long long)L.kmax, t * 1e6, pairs / t);
 }
 
@@ -70,17 +73,23 @@ int main(int argc, char** argv) {
   cudaMemcpy(dp, pack.data(), 8 * 8 * ns_pad, cudaMemcpyHostToDevice);
   // A3 call 2 uses the 8-double record; A3 call 1 reads the first 4 doubles
   // of a 4-double record: reuse the buffer (layout-only timing)
-  for (int w : {1, 2, 4}) {
-    run<FarA3b, 1, 128, 128, false>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3b, 1, 128, 128, true>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3b, 2, 64, 128, true>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3b, 2, 64, 64, true>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3b, 2, 128, 64, true>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3a, 4, 64, 128, false>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3a, 4, 64, 128, true>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3a, 2, 128, 128, true>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3a, 4, 64, 64, true>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-    run<FarA3a, 1, 128, 128, true>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+  for (int w : {1}) {
+    run<FarA3b, 2, 64, 128, true, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 2, 64, 128, true, 4, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 2, 64, 128, true, 1, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 2, 64, 128, false, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 2, 64, 128, false, 2, 12>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 2, 128, 128, true, 2, 5>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 3, 64, 128, true, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 1, 128, 128, false, 4, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3b, 1, 256, 128, false, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 4, 64, 64, true, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 4, 64, 64, true, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 4, 64, 64, true, 1, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 4, 64, 64, false, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 2, 128, 64, false, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 2, 64, 64, false, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 6, 64, 64, true, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
