@@ -809,8 +809,12 @@ int build_device(lb_fmm_plan* P) {
 }
 
 int ensure_work(lb_fmm_plan* P, int nd) {
+  // work arrays are sized for the largest density chunk seen so far and never
+  // shrunk: callers alternate nd (the operator apply uses 1 then 3), and a
+  // cudaFree/cudaMalloc pair per call would serialise the device
   FmmDevice& D = P->dev;
-  if (D.nd_alloc == nd) return LB_OK;
+  if (D.nd_alloc >= nd) return LB_OK;
+  nd = std::max(nd, std::min(4, 2 * std::max(D.nd_alloc, 1)));
   if (D.loc != D.dc) cudaFree(D.loc);  // grid: loc aliases dc
   cudaFree(D.cs); cudaFree(D.vs); cudaFree(D.up); cudaFree(D.dc);
   cudaFree(D.tmpA); cudaFree(D.tmpB); cudaFree(D.tout);

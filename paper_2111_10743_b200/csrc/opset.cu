@@ -96,8 +96,29 @@ __global__ void fill_geom_kernel(const double* __restrict__ pos, const double* _
 
 template <int J>
 struct CsrJobs {
-  const double* val[J];
-  const double* x[J];
+  const double* val[J];  // the DISTINCT value arrays (Mix::K of them)
+  const double* x[J];    // the DISTINCT densities (Mix::X of them)
+};
+
+// Job j of a pass multiplies value array vi(j) by density xi(j).  Distinct
+// arrays are loaded once per nnz (A3's second pass reads S' for two densities
+// and mu2 for three kinds: 3 value loads + 2 gathers instead of 4 + 4).
+template <int J>
+struct MixId {
+  static constexpr int K = J, X = J;
+  __host__ __device__ static constexpr int vi(int j) { return j; }
+  __host__ __device__ static constexpr int xi(int j) { return j; }
+};
+template <int J>
+struct MixOneX {  // J kinds applied to one density
+  static constexpr int K = J, X = 1;
+  __host__ __device__ static constexpr int vi(int j) { return j; }
+  __host__ __device__ static constexpr int xi(int) { return 0; }
+};
+struct MixA3p2 {  // [S' mu1, S mu2, S' mu2, (S''+D') mu2]; vals {S', S, S''+D'}, xs {mu1, mu2}
+  static constexpr int K = 3, X = 2;
+  __host__ __device__ static constexpr int vi(int j) { return j == 0 ? 0 : (j == 1 ? 1 : (j == 2 ? 0 : 2)); }
+  __host__ __device__ static constexpr int xi(int j) { return j == 0 ? 0 : 1; }
 };
 
 constexpr int kCsrBT = 256;
@@ -241,7 +262,7 @@ struct EpiA1p2 : EpiBase {
 // picked from the mean row length so every warp has ~4 chunks of 32 nnz in
 // flight: the row loop is latency-bound otherwise).  Segment warps of a row
 // combine their partial sums in a fixed order through shared memory.
-template <int J, class E>
+template <int J, class E, class Mix = MixId<J>>
 __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
                                                          const int32_t* __restrict__ indices,
                                                          int64_t grow0, int64_t nrows, int wpr,
@@ -292,21 +313,31 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
     const int64_t kb = indptr[row], ke = indptr[row + 1];
     const int64_t stride = 32 * wpr;
     int64_t k = kb + seg * 32 + lane;
+    constexpr int K = Mix::K, X = Mix::X;
     for (; k + 3 * stride < ke; k += 4 * stride) {
       int c[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) c[u] = __ldg(indices + k + stride * u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        double v[K], xv[X];
 #pragma unroll
-        for (int j = 0; j < J; ++j)
-          acc[j] = fma(__ldg(jobs.val[j] + k + stride * u), __ldg(jobs.x[j] + c[u]), acc[j]);
+        for (int q = 0; q < K; ++q) v[q] = __ldg(jobs.val[q] + k + stride * u);
+#pragma unroll
+        for (int q = 0; q < X; ++q) xv[q] = __ldg(jobs.x[q] + c[u]);
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma(v[Mix::vi(j)], xv[Mix::xi(j)], acc[j]);
       }
     }
     for (; k < ke; k += stride) {
       const int c = __ldg(indices + k);
+      double v[K], xv[X];
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = fma(__ldg(jobs.val[j] + k), __ldg(jobs.x[j] + c), acc[j]);
+      for (int q = 0; q < K; ++q) v[q] = __ldg(jobs.val[q] + k);
+#pragma unroll
+      for (int q = 0; q < X; ++q) xv[q] = __ldg(jobs.x[q] + c);
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(v[Mix::vi(j)], xv[Mix::xi(j)], acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -448,16 +479,18 @@ int oversample(const lb_opset* h, int nv, const double* const* in, const int* sl
   return LB_OK;
 }
 
-template <int J, class E>
+// vals: the pass's per-job value arrays, xs: per-job densities (J each);
+// Mix collapses them to the distinct ones (the caller's order must match Mix)
+template <int J, class E, class Mix = MixId<J>>
 int run_csr(const lb_opset* h, const double* const* vals, const double* const* xs, const E& epi,
             cudaStream_t st, double red_div = 1.0) {
-  CsrJobs<J> jobs;
+  CsrJobs<J> jobs{};
   for (int j = 0; j < J; ++j) {
     if (!vals[j]) return fail(LB_ERR_KEY, "opset: a required correction kind was not provided");
-    jobs.val[j] = vals[j];
-    jobs.x[j] = xs[j];
+    jobs.val[Mix::vi(j)] = vals[j];
+    jobs.x[Mix::xi(j)] = xs[j];
   }
-  csr_epi_kernel<J, E><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
+  csr_epi_kernel<J, E, Mix><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
       h->d.indptr, h->d.indices, h->r0, h->nr, h->csr_wpr, jobs, epi, h->partials, h->ticket,
       h->scal, red_div);
   LB_CHECK_LAUNCH();
@@ -651,7 +684,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
       e.sp_tau = sp_tau;
       const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
       const double* xs[2] = {tau, tau};
-      return run_csr<2>(h, vals, xs, e, st);
+      return run_csr<2, EpiA3p1>(h, vals, xs, e, st);  // MixOneX<2> measured slower (1.39 vs 1.19 ms, config 3)
     }
     if (phase == 1) {
       const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
@@ -664,7 +697,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
       e.result = out;
       const double* vals[4] = {C[LB_KIND_SPRIME], C[LB_KIND_S], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
       const double* xs[4] = {sp_tau, s_tau, s_tau, s_tau};
-      return run_csr<4>(h, vals, xs, e, st, h->wsum);
+      return run_csr<4, EpiA3p2, MixA3p2>(h, vals, xs, e, st, h->wsum);
     }
     add_scalar_kernel<<<(unsigned)ceil_div(h->nr, 256), 256, 0, st>>>(out + h->r0, h->nr, h->scal);
     LB_CHECK_LAUNCH();
@@ -684,7 +717,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
       e.mu2 = mu2;
       const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_D], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
       const double* xs[4] = {tau, tau, tau, tau};
-      return run_csr<4>(h, vals, xs, e, st, h->wsum);
+      return run_csr<4, EpiA2p1>(h, vals, xs, e, st, h->wsum);
     }
     // mu2 += ws in place (scal[0]) while both are oversampled
     const double* in2[2] = {mu2, mu1};
@@ -717,7 +750,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
     e.muz = muz;
     const double* vals[4] = {C[LB_KIND_S], C[LB_KIND_GRAD_S1], C[LB_KIND_GRAD_S2], C[LB_KIND_GRAD_S3]};
     const double* xs[4] = {tau, tau, tau, tau};
-    return run_csr<4>(h, vals, xs, e, st, h->wsum);
+    return run_csr<4, EpiA1p1>(h, vals, xs, e, st, h->wsum);
   }
   const double* in2[3] = {mux, muy, muz};
   LB_TRY(far_stage(h, FK_A1B, 3, in2, false, &L, st));
@@ -1033,7 +1066,7 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
       epi.y[j] = ys[j];                                                                     \
     }                                                                                       \
     epi.accumulate = accumulate;                                                            \
-    csr_epi_kernel<J, EpiStore<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, 0, nrows, wpr, jobs, \
+    csr_epi_kernel<J, EpiStore<J>, MixId<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, 0, nrows, wpr, jobs, \
                                                               epi, nullptr, nullptr,        \
                                                               nullptr, 1.0);                \
   }

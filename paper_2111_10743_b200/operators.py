@@ -424,13 +424,17 @@ class LayerOperatorSet:
                     the exact fp64 sweeps while N * N_over <= FMM_CROSSOVER
                     (they are both faster and more accurate than the FMM
                     there on a B200) and builds the FmmPlan at eps beyond it.
+      fmm_ncrit   : leaf capacity of that plan (120 = the reference's
+                    default, fmm.py:730, so the far field is the reference's
+                    approximation; ~300 is ~2x faster on a B200 for surface
+                    point sets, tools: scripts/fmm_ncrit_probe.py).
     """
 
     FMM_CROSSOVER = 2.0e10  # target-source pairs per sweep
 
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
-                 corrections=None, far: str = "auto"):
+                 corrections=None, far: str = "auto", fmm_ncrit: int = 120):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -463,7 +467,8 @@ class LayerOperatorSet:
         if use_fmm and (far == "fmm" or (far == "auto" and
                                          n * nover > self.FMM_CROSSOVER)):
             from .fmm_plan import FmmPlan
-            self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps)
+            self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps,
+                                 ncrit=fmm_ncrit)
             self.dev.set_fmm(self._plan)
             self.far = "fmm"
         else:

@@ -40,9 +40,9 @@ def pattern_from_near(g, dev="cuda"):
     return indptr, cols.to(torch.int32)
 
 
-def run(name, g, cset, eps, far, reps=5, synthetic=False):
+def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120):
     geom = Geometry.from_arrays(g)
-    op = LayerOperatorSet(geom, "a3", eps, corrections=cset, far=far)
+    op = LayerOperatorSet(geom, "a3", eps, corrections=cset, far=far, fmm_ncrit=ncrit)
     n = geom.nnodes
     tau = torch.from_numpy(np.random.default_rng(2).standard_normal(n)).cuda()
     out = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -62,7 +62,7 @@ def run(name, g, cset, eps, far, reps=5, synthetic=False):
     nnz = int(cset.indices.shape[0])
     b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
     b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
-    print(json.dumps({"case": name, "far": op.far, "eps": eps, "N": n,
+    print(json.dumps({"case": name, "far": op.far, "eps": eps, "fmm_ncrit": ncrit, "N": n,
                       "N_over": geom.noversampled, "nnz_per_kind": nnz,
                       "synthetic_corrections": synthetic, "apply_ms": best,
                       "stages_ms": {"far1": st[0], "spmv1": st[1], "far2": st[2],
@@ -92,4 +92,6 @@ if __name__ == "__main__":
                 for k in ("s", "sprime", "spp_plus_dprime")}
         cset = CorrectionSet(indptr, idx, vals)
         run("config3", g, cset, 5e-8, "fmm", synthetic=True)
+        run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300)
+        run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300)
         run("config3", g, cset, 5e-8, "direct", reps=2, synthetic=True)
