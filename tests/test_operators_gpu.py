@@ -186,3 +186,26 @@ def test_apply_with_fmm_far_field(cuda, fixture, forms):
                 k, floor = (50.0, 5e-7) if kind.value == "spp_plus_dprime" else (10.0, 0.0)
                 assert np.abs(fast.apply_layer(kind, g["tau"]) - r).max() <= \
                     (k * eps + floor) * max(1.0, np.abs(r).max()), (form, kind, eps)
+
+
+def test_two_far_calls_with_four_densities_through_the_seam(cuda):
+    """The reference's seam contract (test_operators.py:71-93): patching the
+    instance's _far sees exactly two calls per apply whose densities sum to
+    4, for every formulation, and the unfused result equals the fused one."""
+    from paper_2111_10743_b200 import LayerOperatorSet
+    g = golden("opset_sphere_o3.npz")
+    for form in ("a1", "a2", "a3"):
+        for far in ("direct", "fmm"):
+            op = LayerOperatorSet.from_bundle(g, form, eps=1e-10, far=far)
+            fused = op.apply(g["tau"])
+            calls = []
+            original = op._far
+
+            def spy(c, d, out, original=original):
+                calls.append(c.shape[0] if c is not None else d.shape[0])
+                return original(c, d, out)
+            op._far = spy
+            got = op.apply(g["tau"])
+            assert len(calls) == 2 and sum(calls) == 4, (form, far, calls)
+            tol = 1e-10 if far == "direct" else 1e-7
+            assert np.abs(got - fused).max() <= tol * np.abs(fused).max() + 2e-7 * (form != "a1"), (form, far)
