@@ -75,25 +75,6 @@ struct Scratch {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Source-split factor for an all-pairs launch of `tiles` equal-work target
-// tiles over `src_tiles` source tiles with `slots` co-resident blocks: the
-// smallest split giving at least `min_waves` waves with >= 90% of the slot
-// grid busy.  Measured on B200 (tools/far_sweep.cu): the fp64 sweeps need
-// ~8 waves before block start-up/drain stops showing (1 wave: 69% of the FP64
-// pipe, 8 waves: 87-90%); the partial sums this creates are reduced by the
-// consumer with coalesced loads.
-inline int64_t choose_splits(int64_t tiles, int64_t src_tiles, int64_t slots,
-                             int64_t min_waves = 8) {
-  if (tiles <= 0 || src_tiles <= 1) return 1;
-  const int64_t cap = std::min<int64_t>(src_tiles, 4096);
-  for (int64_t s = 1; s <= cap; ++s) {
-    const int64_t units = tiles * s;
-    const int64_t waves = (units + slots - 1) / slots;
-    if (waves >= min_waves && (double)units / (double)(waves * slots) >= 0.90) return s;
-  }
-  return cap;
-}
-
 // ---------------------------------------------------------------------------
 // fp64 1/sqrt(r2) with the coincident-pair skip of fmm.py:136-141 /
 // _pointsum.py:41-42 folded in (returns 0 when r2 == 0).

@@ -9,16 +9,18 @@
 //     thread reads each record as a warp-wide broadcast;
 //   * each thread owns TPT targets and keeps all accumulators in registers;
 //   * 1/r: MUFU.RSQ64H seed + one 2nd-order fp64 refinement (lb_common.cuh);
-//   * when there are too few target tiles to fill 148 SMs the source range
-//     is split across blockIdx.y; partial sums land in a component-major
-//     scratch and one finalize kernel reduces them in a fixed order
-//     (deterministic, no fp64 atomics) while scattering into the reference
-//     layout (pot (nd,Nt), grad (nd,Nt,3), hess (nd,Nt,3,3)).
+//   * the sweep is decomposed stream-K (opfar.cuh): one persistent wave of
+//     CTAs takes equal shares of the (target tile x source tile) units, so
+//     small problems still fill the 148 SMs; per-(tile, CTA) partials are
+//     reduced in a fixed order (deterministic, no fp64 atomics) by a finalize
+//     kernel that also scatters into the reference layout (pot (nd,Nt),
+//     grad (nd,Nt,3), hess (nd,Nt,3,3)).
 #include <algorithm>
 #include <string>
 #include <vector>
 
 #include "lb_common.cuh"
+#include "opfar.cuh"
 #include "p2p_core.cuh"
 
 namespace lb {
@@ -58,93 +60,6 @@ __global__ void pack_sources_kernel(const double* __restrict__ pos, int64_t ns, 
     }
   }
   for (; o < L::stride; ++o) rec[o] = 0.0;
-}
-
-// ---------------------------------------------------------------------------
-// tiled all-pairs kernel: block (tile of BT*TPT targets) x (source split)
-
-template <int NDC, bool HC, bool HD, int LEVEL, int TPT, int BT, int TS>
-__global__ void __launch_bounds__(BT) p2p_tile_kernel(const double* __restrict__ tgt, int64_t nt,
-                                                      const double* __restrict__ pack,
-                                                      int64_t ns_pad, int64_t chunk,
-                                                      double* __restrict__ part) {
-  using L = SrcLayout<NDC, HC, HD>;
-  constexpr int S = L::stride;
-  constexpr int NC = ncomp(LEVEL);
-  constexpr int NA = NDC * NC;
-  __shared__ __align__(16) double sh[TS * S];
-
-  const int64_t tbase = (int64_t)blockIdx.x * (BT * TPT) + threadIdx.x;
-  const int64_t s_begin = (int64_t)blockIdx.y * chunk;
-  const int64_t s_end = min(s_begin + chunk, ns_pad);
-
-  double tx[TPT], ty[TPT], tz[TPT];
-  double acc[TPT][NA];
-#pragma unroll
-  for (int j = 0; j < TPT; ++j) {
-    const int64_t t = tbase + (int64_t)j * BT;
-    const bool in = t < nt;
-    tx[j] = in ? tgt[3 * t + 0] : 0.0;
-    ty[j] = in ? tgt[3 * t + 1] : 0.0;
-    tz[j] = in ? tgt[3 * t + 2] : 0.0;
-#pragma unroll
-    for (int a = 0; a < NA; ++a) acc[j][a] = 0.0;
-  }
-
-  for (int64_t s0 = s_begin; s0 < s_end; s0 += TS) {
-    __syncthreads();
-    const double2* g = reinterpret_cast<const double2*>(pack + s0 * S);
-    double2* d = reinterpret_cast<double2*>(sh);
-#pragma unroll 4
-    for (int k = threadIdx.x; k < TS * S / 2; k += BT) d[k] = __ldg(g + k);
-    __syncthreads();
-#pragma unroll 2
-    for (int k = 0; k < TS; ++k) {
-      const double* rec = sh + k * S;
-#pragma unroll
-      for (int j = 0; j < TPT; ++j) pair_generic<NDC, HC, HD, LEVEL>(tx[j], ty[j], tz[j], rec, acc[j]);
-    }
-  }
-
-  double* out = part + (int64_t)blockIdx.y * NA * nt;
-#pragma unroll
-  for (int j = 0; j < TPT; ++j) {
-    const int64_t t = tbase + (int64_t)j * BT;
-    if (t < nt) {
-#pragma unroll
-      for (int a = 0; a < NA; ++a) out[(int64_t)a * nt + t] = acc[j][a];
-    }
-  }
-}
-
-// sum partials over splits (fixed order) and scatter into the reference layout
-__global__ void p2p_finalize_kernel(const double* __restrict__ part, int nsplit, int64_t nt, int ndc,
-                                    int nc, int d0, int level, double* __restrict__ pot,
-                                    double* __restrict__ grad, double* __restrict__ hess,
-                                    int accumulate) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)ndc * nt) return;
-  const int l = (int)(idx / nt);
-  const int64_t i = idx - (int64_t)l * nt;
-  const int na = ndc * nc;
-  double v[10];
-  for (int c = 0; c < nc; ++c) {
-    double s = 0.0;
-    for (int p = 0; p < nsplit; ++p) s += part[((int64_t)p * na + l * nc + c) * nt + i];
-    v[c] = s;
-  }
-  const int64_t row = (int64_t)(d0 + l) * nt + i;
-  if (accumulate) pot[row] += v[0]; else pot[row] = v[0];
-  if (level >= 1) {
-    double* g = grad + row * 3;
-    for (int k = 0; k < 3; ++k) { if (accumulate) g[k] += v[1 + k]; else g[k] = v[1 + k]; }
-  }
-  if (level >= 2) {
-    // component order xx yy zz xy xz yz -> full symmetric 3x3
-    const double hv[9] = {v[4], v[7], v[8], v[7], v[5], v[9], v[8], v[9], v[6]};
-    double* h = hess + row * 9;
-    for (int k = 0; k < 9; ++k) { if (accumulate) h[k] += hv[k]; else h[k] = hv[k]; }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -229,39 +144,75 @@ int launch_pack(const double* src, int64_t ns, int64_t ns_pad, const double* cha
   return LB_OK;
 }
 
+// the generic pair as an opfar functor: the direct sum reuses the stream-K
+// sweep (one persistent wave, register-prefetched source tiles) of the
+// operator far field
+template <int NDC, bool HC, bool HD, int LEVEL>
+struct GenericPairF {
+  static constexpr int S = SrcLayout<NDC, HC, HD>::stride;
+  static constexpr int NOUT = NDC * ncomp(LEVEL);
+  static constexpr bool TN = false;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    pair_generic<NDC, HC, HD, LEVEL>(t.x, t.y, t.z, s, a);
+  }
+};
+
+// stream-K partials -> reference layout (pot, grad, full hess), fixed order
+__global__ void p2p_sk_finalize_kernel(const double* __restrict__ part, SkLayout L, int64_t nt,
+                                       int ndc, int nc, int d0, int level, double* __restrict__ pot,
+                                       double* __restrict__ grad, double* __restrict__ hess,
+                                       int accumulate) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)ndc * nt) return;
+  const int l = (int)(idx / nt);
+  const int64_t i = idx - (int64_t)l * nt;
+  const int na = ndc * nc;
+  double v[10];
+  for (int c = 0; c < nc; ++c) v[c] = sk_sum(part, L, na, l * nc + c, i);
+  const int64_t row = (int64_t)(d0 + l) * nt + i;
+  if (accumulate) pot[row] += v[0]; else pot[row] = v[0];
+  if (level >= 1) {
+    double* g = grad + row * 3;
+    for (int k = 0; k < 3; ++k) { if (accumulate) g[k] += v[1 + k]; else g[k] = v[1 + k]; }
+  }
+  if (level >= 2) {
+    const double hv[9] = {v[4], v[7], v[8], v[7], v[5], v[9], v[8], v[9], v[6]};
+    double* h = hess + row * 9;
+    for (int k = 0; k < 9; ++k) { if (accumulate) h[k] += hv[k]; else h[k] = hv[k]; }
+  }
+}
+
 template <int NDC, bool HC, bool HD, int LEVEL>
 int run_direct_chunk(const double* tgt, int64_t nt, const double* src, int64_t ns,
                      const double* charges, const double* dipoles, int d0, uint32_t cmask,
                      uint32_t dmask, int level_out, double* pot, double* grad, double* hess,
                      int accumulate, cudaStream_t st) {
-  using L = SrcLayout<NDC, HC, HD>;
-  constexpr int NA = NDC * ncomp(LEVEL);
-  constexpr int TPT = NA <= 4 ? 4 : (NA <= 12 ? 2 : 1);
+  using F = GenericPairF<NDC, HC, HD, LEVEL>;
+  constexpr int NA = F::NOUT;
   constexpr int NC = ncomp(LEVEL);
-  const int64_t ns_pad = ceil_div(ns, kTS) * kTS;
+  constexpr int TPT = NA <= 4 ? 4 : (NA <= 12 ? 2 : 1);
+  constexpr int TS = F::S <= 4 ? 64 : 128;  // tools/far_sweep.cu shapes
+  constexpr int BT = 64;
+  const int64_t ns_pad = ceil_div(ns, kTS) * kTS;  // kTS = 128 is a multiple of TS
   Scratch pack;
-  LB_TRY(pack.alloc(sizeof(double) * ns_pad * L::stride, st));
+  LB_TRY(pack.alloc(sizeof(double) * ns_pad * F::S, st));
   LB_TRY((launch_pack<NDC, HC, HD>(src, ns, ns_pad, charges, dipoles, d0, cmask, dmask,
                                    pack.as<double>(), st)));
-
-  auto kern = p2p_tile_kernel<NDC, HC, HD, LEVEL, TPT, kBT, kTS>;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBT, 0);
-  per_sm = std::max(per_sm, 1);
-  const int64_t tiles = ceil_div(nt, (int64_t)kBT * TPT);
-  const int64_t src_tiles = ns_pad / kTS;
-  int64_t splits = choose_splits(tiles, src_tiles, (int64_t)sm_count() * per_sm);
-  const int64_t chunk = ceil_div(src_tiles, splits) * kTS;
-  splits = ceil_div(ns_pad, chunk);
-
+  auto kern = opfar_kernel<F, TPT, BT, TS>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int b = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, BT, 0);
+    per_sm = std::max(b, 1);
+  }
+  const SkLayout L = make_sk_layout(nt, ns_pad, BT * TPT, TS, (int64_t)sm_count() * per_sm);
   Scratch part;
-  LB_TRY(part.alloc(sizeof(double) * splits * NDC * NC * nt, st));
-  dim3 grid((unsigned)tiles, (unsigned)splits);
-  kern<<<grid, kBT, 0, st>>>(tgt, nt, pack.as<double>(), ns_pad, chunk, part.as<double>());
+  LB_TRY(part.alloc(sizeof(double) * L.tiles * L.kmax * NA * L.tt, st));
+  kern<<<(unsigned)L.G, BT, 0, st>>>(tgt, nullptr, nt, pack.as<double>(), L, part.as<double>());
   LB_CHECK_LAUNCH();
   const int64_t nfin = (int64_t)NDC * nt;
-  p2p_finalize_kernel<<<(unsigned)ceil_div(nfin, 256), 256, 0, st>>>(
-      part.as<double>(), (int)splits, nt, NDC, NC, d0, level_out, pot, grad, hess, accumulate);
+  p2p_sk_finalize_kernel<<<(unsigned)ceil_div(nfin, 256), 256, 0, st>>>(
+      part.as<double>(), L, nt, NDC, NC, d0, level_out, pot, grad, hess, accumulate);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }

@@ -76,14 +76,15 @@ def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120):
 
 
 if __name__ == "__main__":
+    only = sys.argv[1:]
     c2 = os.path.join(ROOT, "data", "config2.npz")
-    if os.path.exists(c2):
+    if os.path.exists(c2) and (not only or "config2" in only):
         g = dict(np.load(c2))
         cset = CorrectionSet.from_arrays(g)
         run("config2", g, cset, 1e-10, "direct")
         run("config2", g, cset, 1e-10, "fmm")
     c3 = os.path.join(ROOT, "data", "config3_geom.npz")
-    if os.path.exists(c3):
+    if os.path.exists(c3) and (not only or "config3" in only):
         g = dict(np.load(c3))
         indptr, idx = pattern_from_near(g)
         gen = torch.Generator(device="cuda").manual_seed(3)
@@ -95,3 +96,16 @@ if __name__ == "__main__":
         run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300)
         run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300)
         run("config3", g, cset, 5e-8, "direct", reps=2, synthetic=True)
+    c4 = os.path.join(ROOT, "data", "config4_geom.npz")
+    if os.path.exists(c4) and (not only or "config4" in only):
+        g = dict(np.load(c4))
+        indptr, idx = pattern_from_near(g)
+        gen = torch.Generator(device="cuda").manual_seed(4)
+        vals = {k: 1e-4 * torch.randn(idx.numel(), dtype=torch.float64, device="cuda",
+                                      generator=gen)
+                for k in ("s", "sprime", "spp_plus_dprime")}
+        cset = CorrectionSet(indptr, idx, vals)
+        del indptr
+        torch.cuda.empty_cache()
+        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=300)
+        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=120)

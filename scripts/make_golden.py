@@ -507,6 +507,52 @@ def config3():
     print("config3", disc.nnodes, disc.noversampled, time.time() - t0)
 
 
+def wavy_torus(order=9, nu=82, nv=163):
+    """BASELINE config 4 surface: tube radius r(theta, phi) = 1 + 0.25 cos(5 phi)
+    sin(3 theta) around the R = 2 torus; theta poloidal (u axis), phi toroidal
+    (v axis), triangles from the reference's own parameter grid with the
+    outward (flip=True) orientation (shapes.py:106-129), sampled with its
+    _sample_patches and built through build_from_samples (surface.py:310)."""
+    def chart(p):
+        th, ph = p[:, 0], p[:, 1]
+        rho = 1.0 + 0.25 * np.cos(5 * ph) * np.sin(3 * th)
+        rho_t = 0.75 * np.cos(5 * ph) * np.cos(3 * th)
+        rho_p = -1.25 * np.sin(5 * ph) * np.sin(3 * th)
+        er = np.column_stack([np.cos(ph), np.sin(ph), np.zeros_like(ph)])
+        ep = np.column_stack([-np.sin(ph), np.cos(ph), np.zeros_like(ph)])
+        ez = np.array([0.0, 0.0, 1.0])[None, :]
+        ring = 2.0 + rho * np.cos(th)
+        x = ring[:, None] * er + (rho * np.sin(th))[:, None] * ez
+        xt = (rho_t * np.cos(th) - rho * np.sin(th))[:, None] * er \
+            + (rho_t * np.sin(th) + rho * np.cos(th))[:, None] * ez
+        xp = (rho_p * np.cos(th))[:, None] * er + ring[:, None] * ep \
+            + (rho_p * np.sin(th))[:, None] * ez
+        return x, xt, xp
+    xs, xus, xvs = shapes._sample_patches(
+        order, shapes._param_grid_triangles(nu, nv, flip=True), chart)
+    disc = build_from_samples(order, xs, xus, xvs,
+                              metadata={"geometry": "wavy-torus", "nu": nu, "nv": nv})
+    shapes._check_outward(disc, "wavy-torus")
+    return disc
+
+
+def config4():
+    """BASELINE config 4 geometry (N = 1,202,940 at reference order 9) and its
+    near map (eta 2).  Corrections are not built (a day of reference CPU
+    time); timing runs put synthetic values on this pattern.  A1-only arrays
+    are dropped to keep the file small."""
+    t0 = time.time()
+    disc = wavy_torus()
+    print("config4 geometry", disc.nnodes, disc.noversampled, time.time() - t0, flush=True)
+    near = build_near_map(disc, 2.0, cap=256)
+    print("near map", time.time() - t0, flush=True)
+    out = {k: v for k, v in geometry_arrays(disc).items()
+           if k not in ("tangents_u", "tangents_v", "inv_metric")}
+    out.update(near_arrays(near))
+    savez(os.path.join(DATA, "config4_geom.npz"), **out)
+    print("config4", time.time() - t0)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
