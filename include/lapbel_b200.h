@@ -261,6 +261,14 @@ int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
                  const double* dipoles, int nd, uint32_t cmask, uint32_t dmask,
                  int level, double* pot, double* grad, double* hess,
                  void* stream);
+/* M2L arithmetic (no reference counterpart: the reference multiplies in
+ * fp64).  slices = 0: fp64 DGEMM.  slices = S in [3, 8]: the M2L products run
+ * on the tcgen05 tensor cores as int8 GEMMs of S-slice (7 bits each) Ozaki
+ * splittings of the canonical matrices and the gathered multipoles, exact
+ * int32 accumulation, fp64 recombination; relative error of each M2L product
+ * about 1e3 * 2^(-7S) of max|K| max|x| (S = 8: fp64 roundoff).  Needs
+ * nrep <= 2048. */
+int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
 /* device time of each stage of the last apply, ms (HOST double[9]):
  * gather+P2M, M2M, M2L, X, L2L, L2T (grid), leaf (U+DE+W), scatter, total.  Recorded
  * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "lb_fmm_plan_set_operators": [_P, _P],
     "lb_fmm_apply": [_P, _P, _P, _I32, _U32, _U32, _I32, _P, _P, _P, _P],
     "lb_fmm_plan_set_timing": [_P, _I32],
+    "lb_fmm_plan_set_m2l": [_P, _I32],
     "lb_fmm_stage_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],

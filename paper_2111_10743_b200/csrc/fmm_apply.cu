@@ -29,6 +29,7 @@
 
 #include "fmm_plan.h"
 #include "lb_common.cuh"
+#include "ozaki.cuh"
 #include "p2p_core.cuh"
 
 namespace lb {
@@ -844,6 +845,43 @@ int ensure_work(lb_fmm_plan* P, int nd) {
   return LB_OK;
 }
 
+// tcgen05 M2L state: A packs of every canonical matrix for the current slice
+// count, column-pack capacity for the largest M2L chunk of nd densities
+int ensure_oz(lb_fmm_plan* P, int nd, cudaStream_t st) {
+  FmmDevice& D = P->dev;
+  const int S = P->m2l_slices, nrep = P->nrep;
+  if (S <= 0) return LB_OK;
+  if (nrep > 2048) return fail(LB_ERR_ARG, "tensor-core M2L needs nrep <= 2048 (set m2l slices to 0)");
+  if (D.oz_S != S) {
+    cudaFree(D.oz_a);
+    cudaFree(D.oz_rs);
+    D.oz_a = nullptr;
+    D.oz_rs = nullptr;
+    D.oz_S = 0;
+    const int mpad = ceil_div(nrep, oz::kBM) * oz::kBM;
+    LB_CUDA(cudaMalloc((void**)&D.oz_a, oz::pack_rows_bytes(nrep, S) * std::max(P->ncanon, 1)));
+    LB_CUDA(cudaMalloc((void**)&D.oz_rs, sizeof(double) * mpad * std::max(P->ncanon, 1)));
+    if (P->ncanon > 0) {
+      oz::pack_rows_kernel<<<dim3((unsigned)mpad, (unsigned)P->ncanon), 256, 0, st>>>(D.canon, nrep, S, D.oz_a,
+                                                                                       D.oz_rs);
+      LB_CHECK_LAUNCH();
+    }
+    D.oz_S = S;
+  }
+  const int64_t need = D.tmp_cols * nd;
+  if (D.oz_cols < need) {
+    cudaFree(D.oz_b);
+    cudaFree(D.oz_cs);
+    D.oz_b = nullptr;
+    D.oz_cs = nullptr;
+    D.oz_cols = 0;
+    LB_CUDA(cudaMalloc((void**)&D.oz_b, oz::pack_cols_bytes(nrep, 8, need)));
+    LB_CUDA(cudaMalloc((void**)&D.oz_cs, sizeof(double) * need));
+    D.oz_cols = need;
+  }
+  return LB_OK;
+}
+
 // child octant (x | y<<1 | z<<2, the children order of fmm.py:624-628) ->
 // index of the reference's m2m/l2l operator lists, k = 4*ox + 2*oy + oz
 // (fmm.py:307-317, 870, 934)
@@ -926,6 +964,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   }
   mark(2);
   // ---- M2L (fmm.py:873-886), by canonical key, chunked at target boundaries
+  LB_TRY(ensure_oz(P, ND, st));
   for (int k = 0; k < P->ncanon; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
     if (pe == pb) continue;
@@ -938,10 +977,19 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       while (tj < ntg && tp[tj + 1] - tp[ti] <= D.tmp_cols) ++tj;
       if (tj == ti) tj = ti + 1;  // a single target with more pairs than the cap cannot occur (<= 316 offsets)
       const int64_t p0 = tp[ti], np = tp[tj] - tp[ti];
-      m2l_gather_kernel<<<(unsigned)(np * ND), 128, 0, st>>>(D.up, D.v_src, D.v_off_idx, D.v_scale,
-                                                             D.perm_inv, p0, np, ND, nrep, D.tmpA);
-      LB_CHECK_LAUNCH();
-      LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+      if (P->m2l_slices > 0) {
+        // gather + slice straight into the int8 column pack, tcgen05 GEMM
+        const oz::ColGather g{D.up, D.v_src, D.v_off_idx, D.v_scale, D.perm_inv, p0, ND};
+        const cudaError_t e = oz::m2l_gemm(P->m2l_slices, D.oz_a + (int64_t)k * oz::pack_rows_bytes(nrep, D.oz_S),
+                                           D.oz_rs + (int64_t)k * ceil_div(nrep, oz::kBM) * oz::kBM, g, nrep,
+                                           np * ND, D.oz_b, D.oz_cs, D.tmpB, st);
+        if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("m2l tcgen05 gemm: ") + cudaGetErrorString(e));
+      } else {
+        m2l_gather_kernel<<<(unsigned)(np * ND), 128, 0, st>>>(D.up, D.v_src, D.v_off_idx, D.v_scale,
+                                                               D.perm_inv, p0, np, ND, nrep, D.tmpA);
+        LB_CHECK_LAUNCH();
+        LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+      }
       m2l_accum_kernel<<<(unsigned)(tj - ti), 128, 0, st>>>(D.tmpB, D.v_tgts, D.v_tgt_pair_off,
                                                             D.v_off_idx, D.perm,
                                                             D.v_key_tgt_off[k] + ti, p0, ND, nrep, D.dc);
@@ -1034,6 +1082,10 @@ void fmm_release_device(lb_fmm_plan* P) {
                   D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct};
   for (void* p : ptrs) cudaFree(p);
   if (P->rep == 0) cudaFree(D.loc);
+  cudaFree(D.oz_a);
+  cudaFree(D.oz_rs);
+  cudaFree(D.oz_b);
+  cudaFree(D.oz_cs);
   if (D.blas) cublasDestroy(D.blas);
   D = FmmDevice();
 }
@@ -1070,6 +1122,16 @@ int lb_fmm_plan_set_operators(lb_fmm_plan* P, const lb_fmm_ops* o) {
   P->off_vec.assign(o->off_vec, o->off_vec + 3 * o->noff);
   P->off_key.assign(o->off_key, o->off_key + o->noff);
   P->off_perm.assign(o->off_perm, o->off_perm + (int64_t)o->noff * nrep);
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_m2l(lb_fmm_plan* P, int slices) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  if (slices != 0 && (slices < 3 || slices > 8))
+    return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: slices must be 0 (fp64) or in [3, 8]");
+  if (slices != 0 && P->nrep > 2048)
+    return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: tensor-core M2L needs nrep <= 2048");
+  P->m2l_slices = slices;
   return LB_OK;
 }
 

@@ -61,6 +61,13 @@ struct FmmDevice {
   int64_t* btgt_oct = nullptr;               // octant (x | y<<1 | z<<2) of every slot
   std::vector<int64_t> level_slot_off;       // slot range of every level
   std::vector<int64_t> v_tpoff_host;         // host copy of v_tgt_pair_off
+  // emulated-fp64 M2L on the tensor cores (ozaki.cuh), built on first use
+  int oz_S = 0;                              // slices the A packs were built for
+  uint8_t* oz_a = nullptr;                   // (ncanon, MT, KC, S, 4096) int8 slices
+  double* oz_rs = nullptr;                   // (ncanon, MT*128) row scales
+  uint8_t* oz_b = nullptr;                   // column slices of one M2L chunk
+  double* oz_cs = nullptr;                   // column scales of one M2L chunk
+  int64_t oz_cols = 0;                       // column capacity of oz_b / oz_cs
 };
 
 }  // namespace lb
@@ -81,6 +88,7 @@ struct lb_fmm_plan {
   std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
   std::vector<double> stage_ms;             // last apply's per-stage device times
   bool timing = false;
+  int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices
 };
 
 namespace lb {

@@ -48,6 +48,20 @@ def order_for_eps(eps: float):
     return "grid", 11, 2
 
 
+def m2l_slices_for(eps: float, nrep: int) -> int:
+    """Int8 slice count of the tensor-core M2L for a tolerance (B200 design
+    choice, no reference counterpart).  With S slices of 7 bits the FMM
+    result moves from the fp64-M2L result by about 2^(-7S) / 4 relative
+    (measured: S=4 2.8e-10, S=5 7e-12 (grid) .. 4e-11 (surface), S=6 6e-14,
+    scripts/m2l_probe.py); S is the smallest count with 2^(-7S) <= eps / 128,
+    i.e. a deviation near eps / 500, and at most 8 (fp64 roundoff).  0 (fp64
+    DGEMM) when the expansion is too large for the kernel (nrep > 2048)."""
+    if nrep > 2048:
+        return 0
+    s = int(np.ceil((np.log2(1.0 / eps) + 7.0) / 7.0))
+    return int(min(8, max(3, s)))
+
+
 # ---------------------------------------------------------------------------
 # unit-box operators (host precompute, cached like the reference's lru_cache)
 
@@ -296,7 +310,7 @@ class FmmPlan:
     def __init__(self, source_positions, target_positions, eps,
                  ncrit: int = 120, m: int | None = None,
                  buffer: int | None = None, rep: str | None = None,
-                 device_sort: bool | None = None):
+                 device_sort: bool | None = None, m2l="auto"):
         self.spos = np.ascontiguousarray(_host(source_positions), dtype=float)
         self.tpos = np.ascontiguousarray(_host(target_positions), dtype=float)
         self.eps = float(eps)
@@ -324,6 +338,20 @@ class FmmPlan:
             self.nrep = self.m ** 3
         self._set_operators()
         self._tree = None
+        self.set_m2l(m2l)
+
+    def set_m2l(self, m2l="auto"):
+        """M2L arithmetic: "fp64" (DGEMM, the reference's arithmetic), "auto"
+        (tcgen05 int8 slices sized from eps, m2l_slices_for) or an explicit
+        slice count in [3, 8] (8 = fp64 roundoff)."""
+        if m2l == "fp64":
+            s = 0
+        elif m2l == "auto":
+            s = m2l_slices_for(self.eps, self.nrep)
+        else:
+            s = int(m2l)
+        _lib.check(self._L.lb_fmm_plan_set_m2l(self._h, s), "lb_fmm_plan_set_m2l")
+        self.m2l_slices = s
 
     def _set_operators(self):
         o = self.ops
@@ -447,7 +475,8 @@ def _host(a):
     return a
 
 
-def evaluate_fmm(sources, targets, eps, outputs=("pot",), ncrit: int = 120):
+def evaluate_fmm(sources, targets, eps, outputs=("pot",), ncrit: int = 120,
+                 m2l="auto"):
     """FMM evaluation matching evaluate_direct to relative tolerance eps
     (fmm.py:993-1011): eps in [1e-12, 1e-3] else ValueError; all-zero input
     returns zeros without building a plan."""
@@ -463,7 +492,7 @@ def evaluate_fmm(sources, targets, eps, outputs=("pot",), ncrit: int = 120):
             if x is not None:
                 x.zero_()
         return _finish(want, pot, grad, hess, host)
-    plan = FmmPlan(sources.positions, targets, eps, ncrit=ncrit)
+    plan = FmmPlan(sources.positions, targets, eps, ncrit=ncrit, m2l=m2l)
     res = plan.apply(sources.charges, sources.dipoles, outputs,
                      sources.charge_active, sources.dipole_active)
     if _lib.is_torch(targets) and not _lib.is_torch(res.pot):

@@ -434,13 +434,17 @@ class LayerOperatorSet:
                     default, fmm.py:730, so the far field is the reference's
                     approximation; ~300 is ~2x faster on a B200 for surface
                     point sets, tools: scripts/fmm_ncrit_probe.py).
+      fmm_m2l     : M2L arithmetic of that plan (FmmPlan.set_m2l): "auto"
+                    (tcgen05 int8 slices sized from eps), "fp64" (DGEMM) or
+                    a slice count in [3, 8].
     """
 
     FMM_CROSSOVER = 2.0e10  # target-source pairs per sweep
 
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
-                 corrections=None, far: str = "auto", fmm_ncrit: int = 120):
+                 corrections=None, far: str = "auto", fmm_ncrit: int = 120,
+                 fmm_m2l="auto"):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -474,7 +478,7 @@ class LayerOperatorSet:
                                          n * nover > self.FMM_CROSSOVER)):
             from .fmm_plan import FmmPlan
             self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps,
-                                 ncrit=fmm_ncrit)
+                                 ncrit=fmm_ncrit, m2l=fmm_m2l)
             self.dev.set_fmm(self._plan)
             self.far = "fmm"
         else:

@@ -21,22 +21,57 @@ def _cloud(m, nt, seed=0):
     return rng, rng.uniform(0, 1, (m, 3)), rng.uniform(0, 1, (nt, 3))
 
 
+@pytest.mark.parametrize("m2l", ["fp64", "auto"])
 @pytest.mark.parametrize("eps,tag,same_tol", [(1e-3, "e3", 1e-10), (1e-6, "e6", 3e-9),
                                               (1e-9, "e9", 1e-11)])
-def test_fmm_matches_reference_fmm_and_direct(cuda, eps, tag, same_tol):
+def test_fmm_matches_reference_fmm_and_direct(cuda, eps, tag, same_tol, m2l):
     """Same tree, lists and (bit-identical) unit operators as the reference, so
-    the two FMMs differ only by fp64 summation order, amplified by the
-    Tikhonov-damped check-to-equivalent solves in the surface representation
-    (measured 2.9e-10 at eps 1e-6) and not at all by the approximation."""
+    with the fp64 M2L the two FMMs differ only by fp64 summation order,
+    amplified by the Tikhonov-damped check-to-equivalent solves in the surface
+    representation (measured 2.9e-10 at eps 1e-6) and not at all by the
+    approximation.  The tensor-core M2L (int8 slices sized from eps) may add
+    up to eps / 100 against the reference FMM and stays within eps of the
+    direct sum."""
     b = _b()
     g = golden("fmm_apply.npz")
     src = b.FmmSources(g["src"], g["ch"], g["dip"])
-    res = b.evaluate_fmm(src, g["tgt"], eps, ("pot", "grad", "hess"))
+    res = b.evaluate_fmm(src, g["tgt"], eps, ("pot", "grad", "hess"), m2l=m2l)
     ref = b.evaluate_direct(src, g["tgt"], ("pot", "grad", "hess"))
+    tol = same_tol if m2l == "fp64" else same_tol + eps / 100
     for name in ("pot", "grad", "hess"):
         got = getattr(res, name)
-        assert rel_errs(got, g[f"{tag}_{name}"], 2) < same_tol, name   # vs reference FMM
+        assert rel_errs(got, g[f"{tag}_{name}"], 2) < tol, name        # vs reference FMM
         assert rel_errs(got, getattr(ref, name), 2) <= eps, name       # vs direct
+
+
+@pytest.mark.parametrize("eps,tol", [(1e-6, 1e-9), (1e-9, 1e-12)])
+def test_tensor_core_m2l_full_slices_equals_fp64(cuda, eps, tol):
+    """8 int8 slices carry the full fp64 mantissa: the tcgen05 M2L reproduces
+    the DGEMM M2L to roundoff (surface: Tikhonov-amplified roundoff)."""
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((20000, 3))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    q = rng.standard_normal((2, 20000))
+    plan = FmmPlan(x, x, eps, m2l="fp64")
+    a = plan.apply(q, None, ("pot", "grad"))
+    plan.set_m2l(8)
+    c = plan.apply(q, None, ("pot", "grad"))
+    assert rel_errs(c.pot, a.pot, 2) < tol
+    assert rel_errs(c.grad, a.grad, 2) < tol
+    plan.set_m2l(3)                      # coarsest: still a sane approximation
+    d = plan.apply(q, None, ("pot",))
+    assert 0 < rel_errs(d.pot, a.pot, 2) < 1e-5
+
+
+def test_tensor_core_m2l_rejects_bad_slices(cuda):
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(1)
+    x = rng.uniform(0, 1, (500, 3))
+    plan = FmmPlan(x, x, 1e-6)
+    for bad in (1, 2, 9):
+        with pytest.raises(ValueError):
+            plan.set_m2l(bad)
 
 
 def test_fmm_nonuniform_cloud_matches_reference(cuda):
@@ -44,12 +79,14 @@ def test_fmm_nonuniform_cloud_matches_reference(cuda):
     b = _b()
     g = golden("fmm_apply.npz")
     src = b.FmmSources(g["cl_src"], g["cl_ch"])
-    res = b.evaluate_fmm(src, g["cl_tgt"], 1e-6, ("pot", "grad"), ncrit=40)
+    res = b.evaluate_fmm(src, g["cl_tgt"], 1e-6, ("pot", "grad"), ncrit=40, m2l="fp64")
     assert rel_errs(res.pot, g["cl_pot"], 1) < 3e-9    # surface m=8: see above
     assert rel_errs(res.grad, g["cl_grad"], 1) < 3e-9
     ref = b.evaluate_direct(src, g["cl_tgt"], ("pot", "grad"))
-    assert rel_errs(res.pot, ref.pot, 1) <= 1e-6
-    assert rel_errs(res.grad, ref.grad, 1) <= 1e-6
+    fast = b.evaluate_fmm(src, g["cl_tgt"], 1e-6, ("pot", "grad"), ncrit=40)
+    for r in (res, fast):
+        assert rel_errs(r.pot, ref.pot, 1) <= 1e-6
+        assert rel_errs(r.grad, ref.grad, 1) <= 1e-6
 
 
 def test_device_sort_tree_equals_host_tree(cuda):
