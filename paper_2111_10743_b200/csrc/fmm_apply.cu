@@ -875,7 +875,7 @@ int ensure_oz(lb_fmm_plan* P, int nd, cudaStream_t st) {
     D.oz_b = nullptr;
     D.oz_cs = nullptr;
     D.oz_cols = 0;
-    LB_CUDA(cudaMalloc((void**)&D.oz_b, oz::pack_cols_bytes(nrep, 8, need)));
+    LB_CUDA(cudaMalloc((void**)&D.oz_b, oz::pack_cols_bytes_max(nrep, need)));
     LB_CUDA(cudaMalloc((void**)&D.oz_cs, sizeof(double) * need));
     D.oz_cols = need;
   }

@@ -11,41 +11,52 @@
 // bound the error by about S 2^{-7S} max|A[r,:]| max|X[:,c]| K, so S = 8
 // reaches fp64 roundoff and smaller S trade accuracy for speed.
 //
-// Layout (both operands K-major, SWIZZLE_NONE canonical core matrices: an
-// 8-row x 16-byte core matrix is 128 contiguous bytes; the two 16-byte K
-// halves of one 32-wide K chunk are LBO = 128 B apart, 8-row groups SBO =
-// 256 B apart):
+// Layout:
 //   A pack: [m tile (128 rows)][k chunk (32)][slice][4096 B]
-//   B pack: [n tile (64 cols)] [k chunk (32)][slice][2048 B]
-// so every pipeline stage is two contiguous bulk copies (cp.async.bulk).
+//   B pack: [n tile (NT cols)][k chunk (32)][slice][NT * 32 B]
+// both K-major SWIZZLE_NONE canonical core matrices (8 rows x 16 B = 128
+// contiguous bytes; the two 16-B K halves LBO = 128 B apart, 8-row groups
+// SBO = 256 B apart), so one pipeline stage is two bulk copies.
 //
-// Kernel: one CTA per (n tile, m tile), 6 warps: warp 0 streams the stages
-// (bulk copies completing on an mbarrier), warp 1 allocates TMEM and one lane
-// issues the S(S+1)/2 MMAs (128 x 64 x 32) per k chunk, warps 2-5 drain TMEM
-// (tcgen05.ld 32x32b) and write fp64.
+// Kernel: one CTA per (m tile, n tile), 6 warps: warp 0 streams the stages
+// into shared memory (cp.async.bulk completing on an mbarrier); warp 1
+// allocates TMEM and one lane issues, per k chunk, S tcgen05.cp (A slices
+// shared -> TMEM) and the S(S+1)/2 MMAs (128 x NT x 32, A from TMEM, B from
+// shared memory); warps 2-5 drain the accumulators (tcgen05.ld 32x32b) into
+// fp64.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 namespace lb {
 namespace oz {
 
 constexpr int kBM = 128;             // rows per tile (MMA M)
-constexpr int kNT = 64;              // default columns per tile (MMA N)
 constexpr int kBK = 32;              // K per MMA (kind::i8)
 constexpr int kABytes = kBM * kBK;   // one slice of one A stage
 
+// Tiling per slice count.  The accumulators of one pass (G diagonals of NT
+// TMEM columns) plus two A stages of 8 S columns must fit the 512 TMEM
+// columns; every tcgen05.mma carries a fixed issue cost (~25 cycles measured)
+// on top of 0.5 cycle per N column, so wide N with several passes over K
+// (each pass accumulates a range of diagonals, the epilogue warps carry the
+// fp64 partial sums across passes in registers) beats one narrow pass.
+// pass_end(S, p): first diagonal after pass p.
+__host__ __device__ constexpr int nt_for(int S) { return S <= 6 ? 128 : 96; }
+__host__ __device__ constexpr int npass_for(int S) { return S <= 3 ? 1 : 2; }
+__host__ __device__ constexpr int pass_end(int S, int p) {
+  return npass_for(S) == 1 || p > 0 ? S : (S == 4 ? 2 : S <= 6 ? 3 : 4);
+}
+__host__ __device__ constexpr int stage_bytes(int S, int NT) { return S * (kABytes + NT * kBK); }
 __host__ __device__ constexpr int stages_for(int S, int NT) {
-  return (S * (kABytes + NT * kBK)) * 4 <= 200 * 1024 ? 4 : (S * (kABytes + NT * kBK)) * 3 <= 200 * 1024 ? 3 : 2;
+  return stage_bytes(S, NT) * 6 <= 200 * 1024 ? 6
+         : stage_bytes(S, NT) * 5 <= 200 * 1024 ? 5
+         : stage_bytes(S, NT) * 4 <= 200 * 1024 ? 4 : 3;
 }
-__host__ __device__ constexpr int tmem_cols(int S, int NT) {
-  return S * NT <= 32 ? 32 : S * NT <= 64 ? 64 : S * NT <= 128 ? 128 : S * NT <= 256 ? 256 : 512;
-}
-__host__ __device__ constexpr size_t smem_bytes(int S, int NT) {
-  return (size_t)stages_for(S, NT) * S * (kABytes + NT * kBK);
-}
+__host__ __device__ constexpr size_t smem_bytes(int S, int NT) { return (size_t)stages_for(S, NT) * stage_bytes(S, NT); }
 
 // byte offset of element (row r within its 128/64 tile, k within its 32 chunk)
 // inside one slice block of the canonical layout
@@ -77,8 +88,7 @@ void pack_rows_host(const double* A, int nrep, uint8_t* pack, double* rs) {
       double v = ldexp(A[(size_t)r * nrep + k], 6 - e);
       for (int s = 0; s < S; ++s) {
         const double a = nearbyint(v);
-        pack[((size_t)(mt * KC + k / kBK) * S + s) * kABytes + core_offset(rl, k % kBK)] =
-            (uint8_t)(int8_t)(int)a;
+        pack[((size_t)(mt * KC + k / kBK) * S + s) * kABytes + core_offset(rl, k % kBK)] = (uint8_t)(int8_t)(int)a;
         v = (v - a) * 128.0;
       }
     }
@@ -124,9 +134,17 @@ inline size_t pack_rows_bytes(int nrep, int S) {
   const int KC = (nrep + kBK - 1) / kBK, MT = (nrep + kBM - 1) / kBM;
   return (size_t)MT * KC * S * kABytes;
 }
-inline size_t pack_cols_bytes(int nrep, int S, int64_t ncol, int NT = kNT) {
+inline size_t pack_cols_bytes(int nrep, int S, int64_t ncol, int NT) {
   const int KC = (nrep + kBK - 1) / kBK;
   return (size_t)((ncol + NT - 1) / NT) * KC * S * NT * kBK;
+}
+inline size_t pack_cols_bytes_max(int nrep, int64_t ncol) {
+  size_t m = 0;
+  for (int S = 3; S <= 8; ++S) {
+    const size_t b = pack_cols_bytes(nrep, S, ncol, nt_for(S));
+    m = b > m ? b : m;
+  }
+  return m;
 }
 
 // optional column gather of the M2L: column c = pair (p0 + c / nd), density l
@@ -259,20 +277,68 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// MODE 0: normal; 1 (harness only): load stage data once and re-issue the
-// MMAs on it, to measure the tensor-core + operand-fetch ceiling
-template <int S, int NT, int MODE = 0>
-__global__ void __launch_bounds__(192, 1)
+// COLL: 0 plain, 1 fill the A collector, 2 reuse it, 3 reuse it a last time
+// (consecutive MMAs on the same A slice keep it in the tensor core's
+// operand collector instead of re-reading TMEM)
+template <int COLL>
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                          uint32_t acc) {
+#define LB_MMA_TS(Q)                                                                          \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                            \
+               "tcgen05.mma.cta_group::1.kind::i8" Q " [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d), \
+               "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc))
+  if (COLL == 1) LB_MMA_TS(".collector::a::fill");
+  else if (COLL == 2) LB_MMA_TS(".collector::a::use");
+  else if (COLL == 3) LB_MMA_TS(".collector::a::lastuse");
+  else LB_MMA_TS("");
+#undef LB_MMA_TS
+}
+template <int D>
+__host__ __device__ constexpr double ldexp_const() {  // 2^{-7 D}
+  double r = 1.0;
+  for (int i = 0; i < D; ++i) r *= 0.0078125;
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+
+__device__ __forceinline__ void cp_s2t_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+// A operand from TMEM (lane = row, 4 int8 per 32-bit column): each k chunk's
+// A slices are bulk-copied to shared memory with the B slices and moved to
+// TMEM by tcgen05.cp, which the tensor pipe executes in order with the MMAs;
+// consecutive MMAs on one A slice reuse it from the operand collector.
+// Passes: pass p accumulates diagonals [pass_end(p-1), pass_end(p)) and needs
+// the slice prefixes A_0.., B_0.. up to its last diagonal (one bulk copy
+// each per chunk).  TMEM: G = max diagonals per pass accumulators of NT
+// columns, then 2 A stages of S slices x 8 columns.
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, each half of the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+__host__ __device__ constexpr int gmax_for(int S) {
+  return npass_for(S) == 1 ? S : (pass_end(S, 0) > S - pass_end(S, 0) ? pass_end(S, 0) : S - pass_end(S, 0));
+}
+
+template <int S, int NT, int FAKE = 0>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const uint8_t* __restrict__ Ap, const uint8_t* __restrict__ Bp, const double* __restrict__ rs,
                 const double* __restrict__ cs, int nrep, int KC, int64_t ncol, int64_t ldy,
                 double* __restrict__ Y) {
   constexpr int ST = stages_for(S, NT);
+  constexpr int NP = npass_for(S);
+  constexpr int G = gmax_for(S);
   constexpr int kBBytes = NT * kBK;
-  constexpr int kA = S * kABytes, kB = S * kBBytes;
-  constexpr int kCols = tmem_cols(S, NT);
+  constexpr int kA = S * kABytes, kB = S * kBBytes;  // full-prefix sizes in the packs
+  constexpr int kStage = stage_bytes(S, NT);
   constexpr uint32_t kIdesc = idesc_i8(NT);
+  constexpr uint32_t kAcol = G * NT;  // first A column
+  static_assert(G * NT + 2 * S * 8 <= 512, "TMEM budget");
+  static_assert(G <= 4, "int64 diagonal combine holds at most 4 diagonals");
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[ST], empty[ST], accf;
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], accf, tfree;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // m tiles of one n tile are adjacent in launch order: the n tile's B pack is
@@ -282,11 +348,12 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
+    mbar_init(&tfree, 32 * kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
-                 "r"(kCols));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -297,62 +364,145 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       const uint8_t* A = Ap + (int64_t)mt * KC * kA;
       const uint8_t* B = Bp + nt * KC * kB;
-      for (int kc = 0; kc < (MODE == 1 ? 1 : KC); ++kc) {
-        const int s = kc % ST;
-        if (kc >= ST) mbar_wait(&empty[s], ((kc / ST) - 1) & 1);
-        uint8_t* sa = smem + (size_t)s * (kA + kB);
-        mbar_expect_tx(&full[s], kA + kB);
-        bulk_g2s(sa, A + (int64_t)kc * kA, kA, &full[s]);
-        bulk_g2s(sa + kA, B + (int64_t)kc * kB, kB, &full[s]);
+      int g = 0;
+#pragma unroll 1
+      for (int p = 0; p < NP; ++p) {
+        const int d1 = p == 0 ? pass_end(S, 0) : pass_end(S, 1);
+#pragma unroll 1
+        for (int kc = 0; kc < KC; ++kc, ++g) {
+          const int s = g % ST;
+          if (g >= ST) mbar_wait(&empty[s], ((g / ST) - 1) & 1);
+          uint8_t* sa = smem + (size_t)s * kStage;
+          const uint32_t ab = d1 * kABytes, bb = d1 * kBBytes;
+          mbar_expect_tx(&full[s], (FAKE == 1 ? 0 : ab) + (FAKE == 2 ? 0 : bb));
+          if (FAKE != 1) bulk_g2s(sa, A + (int64_t)kc * kA, ab, &full[s]);
+          if (FAKE != 2) bulk_g2s(sa + S * kABytes, B + (int64_t)kc * kB, bb, &full[s]);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kc = 0; kc < (MODE == 1 ? 16 * KC : KC); ++kc) {
-        const int s = MODE == 1 ? 0 : kc % ST;
-        if (MODE == 0 || kc == 0) mbar_wait(&full[s], (kc / ST) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* sa = smem + (size_t)s * (kA + kB);
-        const uint8_t* sb = sa + kA;
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-          const uint64_t da = smem_desc(sa + i * kABytes);
-#pragma unroll
-          for (int j = 0; j < S - i; ++j)
-            mma_i8(tmem + (uint32_t)((i + j) * NT), da, smem_desc(sb + j * kBBytes), kIdesc,
-                   (kc > 0 || i > 0) ? 1u : 0u);
+      int g = 0;
+#pragma unroll 1
+      for (int p = 0; p < NP; ++p) {
+        if (p > 0) {  // the epilogue has drained the previous pass's accumulators
+          mbar_wait(&tfree, (p - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
-        if (MODE == 0) mma_commit(&empty[s]);
+#pragma unroll 1
+        for (int kc = 0; kc < KC; ++kc, ++g) {
+          const int s = g % ST;
+          const uint32_t ta0 = tmem + kAcol + (uint32_t)((g & 1) * S * 8);
+          mbar_wait(&full[s], (g / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + (size_t)s * kStage;
+          const uint8_t* sb = sa + S * kABytes;
+          if (FAKE != 4) {
+            // the two passes are separate unrolled bodies: the (i, j) pair
+            // lists are compile-time
+            auto body = [&](auto P0, auto P1) {
+              constexpr int d0 = decltype(P0)::value, d1 = decltype(P1)::value;
+#pragma unroll
+              for (int i = 0; i < d1; ++i) cp_s2t_128x256b(ta0 + (uint32_t)(i * 8), smem_desc(sa + i * kABytes));
+#pragma unroll
+              for (int i = 0; i < d1; ++i) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int jlo = d0 - i > 0 ? d0 - i : 0, jhi = d1 - i;  // j in [jlo, jhi)
+                const uint32_t ta = ta0 + (uint32_t)(i * 8);
+                const uint32_t acc = (kc > 0 || i > 0) ? 1u : 0u;
+                const uint64_t db = smem_desc(sb);
+                if (jhi - jlo == 1) {
+                  mma_i8_ts<0>(tmem + (uint32_t)((i + jlo - d0) * NT), ta, db + (uint64_t)((jlo * kBBytes) >> 4),
+                               kIdesc, acc);
+                } else {
+                  mma_i8_ts<1>(tmem + (uint32_t)((i + jlo - d0) * NT), ta, db + (uint64_t)((jlo * kBBytes) >> 4),
+                               kIdesc, acc);
+#pragma unroll
+                  for (int j = jlo + 1; j < jhi - 1; ++j)
+                    mma_i8_ts<2>(tmem + (uint32_t)((i + j - d0) * NT), ta, db + (uint64_t)((j * kBBytes) >> 4),
+                                 kIdesc, acc);
+                  mma_i8_ts<3>(tmem + (uint32_t)((i + jhi - 1 - d0) * NT), ta,
+                               db + (uint64_t)(((jhi - 1) * kBBytes) >> 4), kIdesc, acc);
+                }
+              }
+            };
+            if constexpr (NP == 1) {
+              body(std::integral_constant<int, 0>{}, std::integral_constant<int, S>{});
+            } else {
+              if (p == 0)
+                body(std::integral_constant<int, 0>{}, std::integral_constant<int, pass_end(S, 0)>{});
+              else
+                body(std::integral_constant<int, pass_end(S, 0)>{}, std::integral_constant<int, pass_end(S, 1)>{});
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf);
       }
-      mma_commit(&accf);
     }
     __syncwarp();
   } else {
-    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +32
-    mbar_wait(&accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +32 for column half
+    // (w - 2) / 4; fp64 partial sums stay in registers across passes
     const int q = warp & 3;
-    const int row = mt * kBM + q * 32 + lane;
-    const double rsc = row < nrep ? rs[row] : 0.0;
+    const int h = (warp - 2) >> 2;
+    constexpr int kHalf = ((NT / 8 + 1) / 2) * 8;
+    const int c0 = h * kHalf;
+    const int nc = h ? NT - kHalf : kHalf;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    double y[kHalf];
+#pragma unroll
+    for (int c = 0; c < kHalf; ++c) y[c] = 0.0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < NT; c0 += 8) {
-      uint32_t v[S][8];
+    for (int p = 0; p < NP; ++p) {
+      mbar_wait(&accf, p & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      auto drain = [&](auto P0, auto P1) {
+        constexpr int d0 = decltype(P0)::value, d1 = decltype(P1)::value;
 #pragma unroll
-      for (int d = 0; d < S; ++d)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[d][0]), "=r"(v[d][1]), "=r"(v[d][2]), "=r"(v[d][3]), "=r"(v[d][4]),
-                       "=r"(v[d][5]), "=r"(v[d][6]), "=r"(v[d][7])
-                     : "r"(tl + (uint32_t)(d * NT + c0)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int cg = 0; cg < kHalf; cg += 8) {
+          if (FAKE == 3 || cg >= nc) break;
+          uint32_t v[d1 - d0][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int64_t col = nt * NT + c0 + j;
-        double y = (double)(int32_t)v[S - 1][j];
+          for (int d = 0; d < d1 - d0; ++d)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[d][0]), "=r"(v[d][1]), "=r"(v[d][2]), "=r"(v[d][3]), "=r"(v[d][4]),
+                           "=r"(v[d][5]), "=r"(v[d][6]), "=r"(v[d][7])
+                         : "r"(tl + (uint32_t)(d * NT + c0 + cg)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int d = S - 2; d >= 0; --d) y = fma(y, 0.0078125, (double)(int32_t)v[d][j]);
-        if (row < nrep && col < ncol) Y[col * ldy + row] = y * rsc * cs[col];
+          for (int j = 0; j < 8; ++j) {
+            // combine the pass's diagonals exactly in int64 (|acc| < 2^27, at
+            // most 4 diagonals: |t| < 2^49), convert once by the 2^52 + 2^51
+            // magic add (no I2F), weight 2^{-7 (d1 - 1)}
+            long long t = (long long)(int32_t)v[0][j];
+#pragma unroll
+            for (int d = 1; d < d1 - d0; ++d) t = t * 128 + (long long)(int32_t)v[d][j];
+            const double td = __longlong_as_double(t + 0x4338000000000000LL) - 6755399441055744.0;
+            y[cg + j] = fma(td, ldexp_const<d1 - 1>(), y[cg + j]);
+          }
+        }
+      };
+      if constexpr (NP == 1) {
+        drain(std::integral_constant<int, 0>{}, std::integral_constant<int, S>{});
+      } else {
+        if (p == 0)
+          drain(std::integral_constant<int, 0>{}, std::integral_constant<int, pass_end(S, 0)>{});
+        else
+          drain(std::integral_constant<int, pass_end(S, 0)>{}, std::integral_constant<int, pass_end(S, 1)>{});
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tfree);
+    }
+    const int row = mt * kBM + q * 32 + lane;
+    if (row < nrep && FAKE != 3) {
+      const double rsc = rs[row];
+#pragma unroll
+      for (int c = 0; c < kHalf; ++c) {
+        const int64_t col = nt * NT + c0 + c;
+        if (c < nc && col < ncol) Y[col * ldy + row] = y[c] * rsc * cs[col];
       }
     }
   }
@@ -360,11 +510,11 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
-template <int S, int NT = kNT>
+template <int S, int NT = nt_for(S)>
 cudaError_t slice_cols(const double* X, int64_t ldx, int nrep, int64_t ncol, const ColGather* g,
                        uint8_t* pack, double* cs, cudaStream_t st) {
   if (ncol <= 0) return cudaSuccess;
@@ -376,27 +526,24 @@ cudaError_t slice_cols(const double* X, int64_t ldx, int nrep, int64_t ncol, con
   return cudaGetLastError();
 }
 
-template <int S, int NT = kNT, int MODE = 0>
+template <int S, int NT = nt_for(S), int FAKE = 0>
 cudaError_t gemm(const uint8_t* Ap, const uint8_t* Bp, const double* rs, const double* cs, int nrep,
                  int64_t ncol, double* Y, int64_t ldy, cudaStream_t st) {
   if (ncol <= 0) return cudaSuccess;
-  // co-resident CTAs must fit the 512 TMEM columns of an SM (tcgen05.alloc
-  // would otherwise stall a CTA until another one exits): reserve enough
-  // shared memory that at most 512 / tmem_cols CTAs fit
-  constexpr int kPerSm = 512 / tmem_cols(S, NT);
-  constexpr size_t kSmem = smem_bytes(S, NT) > 232448 / (kPerSm + 1) + 1024 ? smem_bytes(S, NT)
-                                                                            : 232448 / (kPerSm + 1) + 1024;
+  // every CTA allocates all 512 TMEM columns: reserve enough shared memory
+  // that a second CTA never lands on the SM (its tcgen05.alloc would stall)
+  constexpr size_t kSmem = smem_bytes(S, NT) > 232448 / 2 + 1024 ? smem_bytes(S, NT) : 232448 / 2 + 1024;
   static bool attr = false;
   if (!attr) {
     const cudaError_t e =
-        cudaFuncSetAttribute(gemm_kernel<S, NT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+        cudaFuncSetAttribute(gemm_kernel<S, NT, FAKE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int KC = (nrep + kBK - 1) / kBK, MT = (nrep + kBM - 1) / kBM;
   const int64_t ntile = (ncol + NT - 1) / NT;
-  gemm_kernel<S, NT, MODE><<<dim3((unsigned)MT, (unsigned)ntile), 192, kSmem, st>>>(
-      Ap, Bp, rs, cs, nrep, KC, ncol, ldy, Y);
+  gemm_kernel<S, NT, FAKE><<<dim3((unsigned)MT, (unsigned)ntile), kThreads, kSmem, st>>>(Ap, Bp, rs, cs, nrep, KC, ncol,
+                                                                              ldy, Y);
   return cudaGetLastError();
 }
 

@@ -40,9 +40,10 @@ def pattern_from_near(g, dev="cuda"):
     return indptr, cols.to(torch.int32)
 
 
-def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120):
+def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120, m2l="auto"):
     geom = Geometry.from_arrays(g)
-    op = LayerOperatorSet(geom, "a3", eps, corrections=cset, far=far, fmm_ncrit=ncrit)
+    op = LayerOperatorSet(geom, "a3", eps, corrections=cset, far=far, fmm_ncrit=ncrit,
+                          fmm_m2l=m2l)
     n = geom.nnodes
     tau = torch.from_numpy(np.random.default_rng(2).standard_normal(n)).cuda()
     out = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -62,7 +63,9 @@ def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120):
     nnz = int(cset.indices.shape[0])
     b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
     b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
-    print(json.dumps({"case": name, "far": op.far, "eps": eps, "fmm_ncrit": ncrit, "N": n,
+    slices = op._plan.m2l_slices if op.far == "fmm" else None
+    print(json.dumps({"case": name, "far": op.far, "eps": eps, "fmm_ncrit": ncrit,
+                      "m2l_slices": slices, "N": n,
                       "N_over": geom.noversampled, "nnz_per_kind": nnz,
                       "synthetic_corrections": synthetic, "apply_ms": best,
                       "stages_ms": {"far1": st[0], "spmv1": st[1], "far2": st[2],
@@ -93,7 +96,9 @@ if __name__ == "__main__":
                 for k in ("s", "sprime", "spp_plus_dprime")}
         cset = CorrectionSet(indptr, idx, vals)
         run("config3", g, cset, 5e-8, "fmm", synthetic=True)
+        run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300, m2l="fp64")
         run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300)
+        run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300, m2l="fp64")
         run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300)
         run("config3", g, cset, 5e-8, "direct", reps=2, synthetic=True)
     c4 = os.path.join(ROOT, "data", "config4_geom.npz")
@@ -108,4 +113,5 @@ if __name__ == "__main__":
         del indptr
         torch.cuda.empty_cache()
         run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=300)
+        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=300, m2l="fp64")
         run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=120)

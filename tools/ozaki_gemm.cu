@@ -13,7 +13,7 @@
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
 
-template <int S, int NT = 64>
+template <int S, int NT = lb::oz::nt_for(S)>
 int run(int nrep, int64_t ncol, int reps) {
   using namespace lb::oz;
   const int KC = (nrep + kBK - 1) / kBK, MT = (nrep + kBM - 1) / kBM;
@@ -92,13 +92,17 @@ int run(int nrep, int64_t ncol, int reps) {
   const float t_d = timeit(dgemm);
   const float t_s = timeit([&] { emu(true, false); });
   const float t_g = timeit([&] { emu(false, true); });
-  const float t_m = timeit([&] { CK((gemm<S, NT, 1>(dAp, dBp, drs, dcs, nrep, ncol, dY, nrep, 0))); });
+  const float t_f1 = timeit([&] { CK((gemm<S, NT, 1>(dAp, dBp, drs, dcs, nrep, ncol, dY, nrep, 0))); });
+  const float t_f2 = timeit([&] { CK((gemm<S, NT, 2>(dAp, dBp, drs, dcs, nrep, ncol, dY, nrep, 0))); });
+  const float t_f3 = timeit([&] { CK((gemm<S, NT, 3>(dAp, dBp, drs, dcs, nrep, ncol, dY, nrep, 0))); });
+  const float t_f4 = timeit([&] { CK((gemm<S, NT, 4>(dAp, dBp, drs, dcs, nrep, ncol, dY, nrep, 0))); });
+  printf("   no-A-copy %.3f ms  no-B-copy %.3f ms  no-epilogue %.3f ms  no-mma %.3f ms\n", t_f1, t_f2, t_f3, t_f4);
   const double fl = 2.0 * nrep * (double)nrep * ncol;
   const double mma = (double)S * (S + 1) / 2 * 2.0 * MT * kBM * (double)KC * kBK * NTL * NT;
   printf("S=%d NT=%d nrep=%d ncol=%ld | err max %.2e (of %.2e) col-rel %.2e | dgemm %.3f ms (%.1f TF) | "
-         "slice %.3f ms | i8gemm %.3f ms (%.1f TF-eq, %.0f TOPS) | mma-only %.0f TOPS\n",
+         "slice %.3f ms | i8gemm %.3f ms (%.1f TF-eq, %.0f TOPS)\n",
          S, NT, nrep, (long)ncol, emax, ymax, erel, t_d, fl / t_d * 1e-9, t_s, t_g, fl / t_g * 1e-9,
-         mma / t_g * 1e-9, 16 * mma / t_m * 1e-9);
+         mma / t_g * 1e-9);
   cudaFree(dA); cudaFree(dX); cudaFree(dY); cudaFree(dYr); cudaFree(drs); cudaFree(dcs);
   cudaFree(dAp); cudaFree(dBp);
   cublasDestroy(h);
@@ -107,15 +111,28 @@ int run(int nrep, int64_t ncol, int reps) {
 
 int main(int argc, char** argv) {
   const int64_t ncol = argc > 1 ? atol(argv[1]) : 65536;
+  const char* only = argc > 2 ? argv[2] : nullptr;  // e.g. "6" runs only S=6 at nrep 729
   const int reps = 10;
-  run<2, 256>(729, ncol, reps);
-  run<4, 128>(729, ncol, reps);
-  run<4, 64>(729, ncol, reps);
-  run<4, 32>(729, ncol, reps);
-  run<6, 64>(729, ncol, reps);
-  run<8, 64>(729, ncol, reps);
-  run<8, 32>(729, ncol, reps);
-  run<5, 64>(296, ncol, reps);
-  run<8, 64>(1331, ncol / 2, reps);
+  if (only) {
+    switch (atoi(only)) {
+      case 4: run<4>(729, ncol, reps); break;
+      case 5: run<5>(729, ncol, reps); break;
+      case 7: run<7>(729, ncol, reps); break;
+      case 6: run<6>(729, ncol, reps); break;
+      case 8: run<8>(729, ncol, reps); break;
+      default: break;
+    }
+    return 0;
+  }
+  run<3>(729, ncol, reps);
+  run<4>(729, ncol, reps);
+  run<5>(729, ncol, reps);
+  run<6>(729, ncol, reps);
+  run<7>(729, ncol, reps);
+  run<8>(729, ncol, reps);
+  run<4>(296, ncol, reps);
+  run<5>(296, ncol, reps);
+  run<6>(488, ncol, reps);
+  run<8>(1331, ncol / 2, reps);
   return 0;
 }

@@ -1,4 +1,4 @@
-// Feasibility spike (not part of the library): one CTA computes
+// Feasibility spike (not part of the library; A_TMEM variant: A read from TMEM): one CTA computes
 // C[128 x N] (int32) = A[128 x K] . B[N x K]^T with tcgen05.mma kind::i8,
 // operands K-major in the SWIZZLE_NONE (interleaved core-matrix) layout,
 // accumulator in TMEM, read back with tcgen05.ld.  Checked against the host.
@@ -33,7 +33,7 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int N>
+template <int N, int ATM>
 __global__ void __launch_bounds__(128) spike_kernel(const int8_t* A, const int8_t* B, int K, int32_t* C) {
   constexpr int M = 128;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(128) spike_kernel(const int8_t* A, const int8_
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
   }
-  if (tid < 32) {  // warp 0 allocates TMEM (N columns, power of 2 >= 32)
+  if (tid < 32) {  // warp 0 allocates TMEM: 512 columns (acc at 0, A at 256)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(N < 32 ? 32 : N));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;");  // smem writes -> async (tensor) proxy
@@ -65,16 +65,49 @@ __global__ void __launch_bounds__(128) spike_kernel(const int8_t* A, const int8_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  const uint32_t tmA = tmem + 256;
+  if (ATM == 2) {
+    // tcgen05.cp smem (canonical K-major core matrices) -> TMEM, issued in order with the MMAs
+    if (tid == 0)
+      for (int ks = 0; ks < KS && ks < 32; ++ks)
+        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmA + 8 * ks),
+                     "l"(make_desc(smem_u32(sA + ks * (M / 8) * 256), 128, 256)));
+  }
+  if (ATM == 1) {
+    // row tid of A, K chunk ks -> TMEM lane tid, columns 8 ks .. 8 ks + 7 (4 int8 per column)
+    const int w = tid / 32;
+    for (int ks = 0; ks < KS && ks < 32; ++ks) {
+      uint32_t r[8];
+      for (int c = 0; c < 8; ++c) {
+        uint32_t v = 0;
+        for (int b = 0; b < 4; ++b) v |= (uint32_t)(uint8_t)A[tid * K + ks * 32 + 4 * c + b] << (8 * b);
+        r[c] = v;
+      }
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                       tmA + ((uint32_t)(w * 32) << 16) + (uint32_t)(8 * ks)),
+                   "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
   if (tid == 0) {
     const uint32_t idesc = make_idesc_i8(M, N);
     for (int ks = 0; ks < KS; ++ks) {
       const uint64_t da = make_desc(smem_u32(sA + ks * (M / 8) * 256), 128, 256);
       const uint64_t db = make_desc(smem_u32(sB + ks * (N / 8) * 256), 128, 256);
       const uint32_t acc = ks > 0 ? 1u : 0u;
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-          "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      if (ATM)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "r"(tmA + 8 * ks), "l"(db), "r"(idesc), "r"(acc));
+      else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
         smem_u32(&mbar)));
@@ -107,10 +140,10 @@ __global__ void __launch_bounds__(128) spike_kernel(const int8_t* A, const int8_
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (tid < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N < 32 ? 32 : N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int N>
+template <int N, int ATM = 0>
 int run(int K) {
   const int M = 128;
   std::vector<int8_t> A(M * K), B(N * K);
@@ -125,8 +158,8 @@ int run(int K) {
   CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
   const size_t sm = (size_t)(M + N) * K;
-  CK(cudaFuncSetAttribute(spike_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  spike_kernel<N><<<1, 128, sm>>>(dA, dB, K, dC);
+  CK(cudaFuncSetAttribute(spike_kernel<N, ATM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  spike_kernel<N, ATM><<<1, 128, sm>>>(dA, dB, K, dC);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<int32_t> C(M * N);
@@ -141,7 +174,7 @@ int run(int K) {
         ++bad;
       }
     }
-  printf("N=%d K=%d mismatches=%ld\n", N, K, bad);
+  printf("N=%d K=%d A_in_tmem=%d mismatches=%ld\n", N, K, (int)ATM, bad);
   cudaFree(dA); cudaFree(dB); cudaFree(dC);
   return bad != 0;
 }
@@ -152,6 +185,10 @@ int main() {
   rc |= run<64>(128);
   rc |= run<128>(320);
   rc |= run<256>(96);
+  rc |= run<64, 1>(64);
+  rc |= run<128, 1>(320);
+  rc |= run<64, 2>(64);
+  rc |= run<128, 2>(320);
   printf("%s\n", rc ? "FAIL" : "PASS");
   return rc;
 }
