@@ -42,7 +42,9 @@ typedef enum {
   LB_ERR_NCCL = 5,
   LB_ERR_ARG = 6,
   LB_ERR_KEY = 7,
-  LB_ERR_BREAKDOWN = 8
+  LB_ERR_BREAKDOWN = 8,
+  LB_ERR_DEPTH = 9,
+  LB_ERR_NEARCAP = 10
 } lb_status;
 
 int lb_abi_version(void);
@@ -274,6 +276,61 @@ int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
  * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */
 int lb_fmm_plan_set_timing(lb_fmm_plan* plan, int on);
 int lb_fmm_stage_times(const lb_fmm_plan* plan, double* ms);
+
+/* ------------------------------------------------------------------------
+ * Near-correction build (quadrature.py, no device
+ * counterpart in the reference).
+ *
+ * Near map (build_near_map, quadrature.py:76-104): target t is near patch p
+ * when |x_t - center_p|^2 <= radii_eta_p^2 with radii_eta = (1 + eta) *
+ * patch radius (DEVICE arrays).  lb_near_map_count writes the per-target
+ * list length (own patch included); the caller scans it into offsets
+ * (n + 1) and checks the cap (NearMapCapError, quadrature.py:94-97);
+ * lb_near_map_fill writes the lists: own patch first, then ascending. */
+int lb_near_map_count(const double* nodes, int64_t n, const double* centers,
+                      const double* radii_eta, int64_t npatches,
+                      const int64_t* node_patch, int32_t* counts, void* stream);
+int lb_near_map_fill(const double* nodes, int64_t n, const double* centers,
+                     const double* radii_eta, int64_t npatches,
+                     const int64_t* node_patch, const int64_t* offsets,
+                     int32_t* patches, void* stream);
+
+/* compute_corrections (quadrature.py:663-701) for kinds S, D, S', S''+D'
+ * (gradient kinds need the principal-value constants: LB_ERR_ARG).  One
+ * entry per near (target, patch) pair; the adaptive subdivision, leaf rules,
+ * tolerance (0.1 eps max(sqrt(area fraction), 1e-3)) and geometric forcing are
+ * _adaptive_pairs' (quadrature.py:277-420).  values[k][pair_pos[i] + b] =
+ * (acc @ vinv - oversampled smooth rule @ over_interp)[b] for pair i.  All
+ * pointers DEVICE; rules (u or a, v or b, w) as the reference builds them
+ * (triangle_rule(order + 2); Duffy Gauss (order + 2) x (order + 1)); knorm =
+ * Koornwinder normalisation sqrt(2(2k+1)(k+l+1)) in k-major order;
+ * coeffs_km (npatches, nb, 9) = [x | dx/du | dx/dv] rows in k-major basis
+ * order; kmajor_perm as _kmajor_permutation (quadrature.py:147-156).
+ * Depth cap 30 -> LB_ERR_DEPTH (AdaptiveDepthError). */
+typedef struct {
+  int order, nk;
+  int kinds[7];
+  double eps;
+  const double* coeffs_km;
+  const double *nodes, *normals, *node_uv;
+  const int64_t* node_patch;
+  const int64_t* pair_tgt;
+  const int32_t* pair_pat;
+  const int64_t* pair_pos;
+  int64_t npairs;
+  const double* srule;
+  int nqs;
+  const double* drule;
+  int nqd;
+  const double* knorm;
+  const int32_t* kmajor_perm;
+  const double* vinv;
+  const double* over_interp;
+  int nbo;
+  const double *over_nodes, *over_normals, *over_weights;
+  double* values[7];
+} lb_corr_build_desc;
+int lb_corrections_build(const lb_corr_build_desc* desc, void* stream);
 
 /* ------------------------------------------------------------------------
  * Hardware probes (no reference counterpart): FP64 FMA-pipe peak

@@ -3,8 +3,10 @@ the reference Laplace-Beltrami package `lapbel` (arXiv:2111.10743).
 
 The public names mirror `lapbel/__init__.py:37-50` for the hot path: the point
 sums (FmmSources, FmmResult, evaluate_direct, evaluate_fmm, FmmPlan), the
-operator set (LayerOperatorSet, DensityVector) and the solver (gmres,
-solve_laplace_beltrami, SolveConfig, SolveReport).  All arithmetic runs in
+operator set (LayerOperatorSet, DensityVector), the solver (gmres,
+solve_laplace_beltrami, SolveConfig, SolveReport) and, widening into
+SURVEY §8(f) #1, the near-correction build (build_near_map,
+compute_corrections).  All arithmetic runs in
 libb200lb.so; there is no CPU fallback.
 """
 
@@ -17,6 +19,8 @@ from .operators import (FORMULATIONS, CorrectionSet, DensityVector, Geometry,
                         KernelKind, LayerOperatorSet, apply_layer)
 from .solver import (GmresBreakdown, SolveConfig, SolveReport, gmres,
                      solve_laplace_beltrami)
+from .quadrature import (AdaptiveDepthError, NearMap, NearMapCapError,
+                         build_near_map, compute_corrections)
 
 __all__ = [
     "FmmSources", "FmmResult", "FmmCapacityError", "FmmPlan",
@@ -24,4 +28,6 @@ __all__ = [
     "KernelKind", "FORMULATIONS", "DensityVector", "Geometry", "CorrectionSet",
     "LayerOperatorSet", "apply_layer", "SolveConfig", "SolveReport",
     "GmresBreakdown", "gmres", "solve_laplace_beltrami",
+    "NearMap", "NearMapCapError", "AdaptiveDepthError", "build_near_map",
+    "compute_corrections",
 ]

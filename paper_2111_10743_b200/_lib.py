@@ -25,6 +25,8 @@ LB_ERR_NCCL = 5
 LB_ERR_ARG = 6
 LB_ERR_KEY = 7
 LB_ERR_BREAKDOWN = 8
+LB_ERR_DEPTH = 9
+LB_ERR_NEARCAP = 10
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -68,6 +70,9 @@ SIGNATURES = {
     "lb_fmm_apply": [_P, _P, _P, _I32, _U32, _U32, _I32, _P, _P, _P, _P],
     "lb_fmm_plan_set_timing": [_P, _I32],
     "lb_fmm_plan_set_m2l": [_P, _I32],
+    "lb_near_map_count": [_P, _I64, _P, _P, _I64, _P, _P, _P],
+    "lb_near_map_fill": [_P, _I64, _P, _P, _I64, _P, _P, _P, _P],
+    "lb_corrections_build": [_P, _P],
     "lb_fmm_stage_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],
@@ -111,6 +116,14 @@ class FmmCapacityError(RuntimeError):
     (fmm.py:39-40)."""
 
 
+class AdaptiveDepthError(RuntimeError):
+    """Adaptive subdivision hit the depth cap (quadrature.py:62-63)."""
+
+
+class NearMapCapError(RuntimeError):
+    """A target's near set exceeded the patch cap (quadrature.py:58-59)."""
+
+
 class GmresBreakdown(RuntimeError):
     """Arnoldi norm underflow that is not a happy breakdown (solver.py:18)."""
 
@@ -128,6 +141,10 @@ def check(status: int, what: str = ""):
         raise KeyError(text)
     if status == LB_ERR_BREAKDOWN:
         raise GmresBreakdown(text)
+    if status == LB_ERR_DEPTH:
+        raise AdaptiveDepthError(text)
+    if status == LB_ERR_NEARCAP:
+        raise NearMapCapError(text)
     raise RuntimeError(f"libb200lb error {status}: {text}")
 
 

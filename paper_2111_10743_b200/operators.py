@@ -121,6 +121,13 @@ class Geometry:
     tangents_v: np.ndarray | None = None
     inv_metric: np.ndarray | None = None
     node_patch: np.ndarray | None = None
+    # chart coefficients (npat, nb, 3), node preimages (N, 2) and the
+    # Vandermonde inverse: the near-correction build's inputs (quadrature.py)
+    coeffs_x: np.ndarray | None = None
+    coeffs_dxdu: np.ndarray | None = None
+    coeffs_dxdv: np.ndarray | None = None
+    node_uv: np.ndarray | None = None
+    vinv: np.ndarray | None = None
     metadata: dict = field(default_factory=dict)
 
     @property
@@ -154,7 +161,9 @@ class Geometry:
                    over_weights=g("over_weights"),
                    over_interp=g("over_interp"), tangents_u=g("tangents_u"),
                    tangents_v=g("tangents_v"), inv_metric=g("inv_metric"),
-                   node_patch=g("node_patch"))
+                   node_patch=g("node_patch"), coeffs_x=g("coeffs_x"),
+                   coeffs_dxdu=g("coeffs_dxdu"), coeffs_dxdv=g("coeffs_dxdv"),
+                   node_uv=g("node_uv"), vinv=g("vinv"))
 
 
 def _over_interp(disc):
@@ -422,8 +431,12 @@ class LayerOperatorSet:
 
     Extra keyword arguments beyond the reference's:
       corrections : dict kind -> NearCorrections/CSR, or a CorrectionSet;
-                    when None the reference's compute_corrections builds
-                    them (requires lapbel to be importable).
+                    when None they are built ON THE DEVICE
+                    (quadrature.build_correction_set: near map + adaptive
+                    singular quadrature, csrc/quad.cu) if disc carries the
+                    chart coefficients and the kinds are S/D/S'/S''+D';
+                    otherwise by the reference's compute_corrections
+                    (requires lapbel to be importable).
       far         : "auto" (default), "direct" or "fmm".  use_fmm=False
                     always means exact all-pairs sweeps (the reference's
                     evaluate_direct path).  With use_fmm=True, "auto" keeps
@@ -456,9 +469,20 @@ class LayerOperatorSet:
             + [as_kind(k) for k in extra_kinds]))
         self.kinds = kinds
         self.t_q = 0.0
+        self.corrections_built_on = "given"
         if corrections is None:
-            corrections, self.near, self.t_q = _reference_corrections(
-                disc, kinds, self.eps, eta, near)
+            if _device_buildable(disc, kinds):
+                from .quadrature import build_correction_set, build_near_map
+                if near is None:
+                    near = build_near_map(disc, eta)
+                near = _as_near_map(near, eta)
+                corrections, self.t_q = build_correction_set(disc, near, kinds, self.eps)
+                self.near = near
+                self.corrections_built_on = "device"
+            else:
+                corrections, self.near, self.t_q = _reference_corrections(
+                    disc, kinds, self.eps, eta, near)
+                self.corrections_built_on = "reference"
         else:
             self.near = near
         if not isinstance(corrections, CorrectionSet):
@@ -710,6 +734,25 @@ class _CorrView:
     @property
     def matrix(self):
         return self._cset.matrix(self.kind)
+
+
+def _device_buildable(disc, kinds):
+    grad = (KernelKind.GRAD_S1, KernelKind.GRAD_S2, KernelKind.GRAD_S3)
+    return (all(getattr(disc, f, None) is not None
+                for f in ("coeffs_x", "coeffs_dxdu", "coeffs_dxdv", "node_uv", "node_patch"))
+            and not any(k in grad for k in kinds))
+
+
+def _as_near_map(near, eta):
+    """Accept this package's NearMap or the reference's (lists per target)."""
+    from .quadrature import NearMap
+    if isinstance(near, NearMap):
+        return near
+    lists = [np.asarray(x, dtype=np.int64) for x in near.near]
+    lens = np.array([len(x) for x in lists], dtype=np.int64)
+    return NearMap(float(getattr(near, "eta", eta)), int(getattr(near, "cap", 128)),
+                   np.concatenate([[0], np.cumsum(lens)]).astype(np.int64),
+                   np.concatenate(lists).astype(np.int32))
 
 
 def _reference_corrections(disc, kinds, eps, eta, near):

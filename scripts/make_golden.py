@@ -125,6 +125,13 @@ def geometry_arrays(disc, prefix=""):
         prefix + "over_normals": disc.over_normals,
         prefix + "over_weights": disc.over_weights,
         prefix + "over_interp": ref.over_interp,
+        # chart coefficients + node preimages + Vandermonde inverse: what the
+        # correction build (quadrature.py:159-220, 527-559) consumes
+        prefix + "coeffs_x": disc.coeffs_x,
+        prefix + "coeffs_dxdu": disc.coeffs_dxdu,
+        prefix + "coeffs_dxdv": disc.coeffs_dxdv,
+        prefix + "node_uv": disc.node_uv,
+        prefix + "vinv": ref.vinv,
     }
 
 
@@ -551,6 +558,47 @@ def config4():
     out.update(near_arrays(near))
     savez(os.path.join(DATA, "config4_geom.npz"), **out)
     print("config4", time.time() - t0)
+
+
+def augment():
+    """Add the correction-build inputs (chart coefficients, node preimages,
+    vinv) to fixtures generated before geometry_arrays carried them, by
+    rebuilding the same deterministic geometry (no correction rebuild)."""
+    cases = [
+        (os.path.join(GOLD, "opset_sphere_o3.npz"), lambda: shapes.build_sphere(3, 1)),
+        (os.path.join(GOLD, "opset_torus_o3.npz"), lambda: shapes.build_torus(3, 8, 4, 2.0, 1.0)),
+        (os.path.join(DATA, "config2.npz"), lambda: icosphere(7)),
+        (os.path.join(DATA, "config3_geom.npz"), lambda: shapes.build_torus(7, 64, 32, 2.0, 1.0)),
+    ]
+    for path, make in cases:
+        if not os.path.exists(path):
+            continue
+        old = dict(np.load(path))
+        disc = make()
+        assert np.array_equal(old["nodes"], disc.nodes), path
+        new = geometry_arrays(disc)
+        for k in ("coeffs_x", "coeffs_dxdu", "coeffs_dxdv", "node_uv", "vinv"):
+            old[k] = new[k]
+        savez(path, **old)
+
+
+def gold_quad():
+    """Correction-build goldens (quadrature.py:663-701): the reference's
+    near map and corrections for the non-PV kinds (S, D, S', S''+D') on an
+    order-7 cube sphere (N = 336) at eps 1e-10 (the order-3 sphere/torus
+    opset fixtures and data/config2.npz cover the other cases)."""
+    kinds = [KernelKind.SINGLE_LAYER, KernelKind.DOUBLE_LAYER,
+             KernelKind.SPRIME, KernelKind.SPP_PLUS_DPRIME]
+    for name, disc, eps in (("quad_sphere_o7", shapes.build_sphere(7, 0), 1e-10),):
+        near = build_near_map(disc, 2.0)
+        corrs, t_q = compute_corrections(disc, near, kinds, eps)
+        out = dict(geometry_arrays(disc))
+        out.update(corrections_arrays(corrs))
+        out.update(near_arrays(near))
+        out["eps"] = np.float64(eps)
+        out["t_q"] = np.float64(t_q)
+        print(name, disc.nnodes, "t_q", t_q)
+        savez(os.path.join(GOLD, f"{name}.npz"), **out)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,117 @@
+"""Device near-correction build (csrc/quad.cu) against the
+reference's own near maps and corrections (tests/golden/*.npz and
+data/config2.npz, written by scripts/make_golden.py from lapbel).
+
+Near maps and CSR patterns are integer work: bit-exact.  Correction values:
+the device runs the reference's adaptive subdivision, rules, tolerance and
+forcing, but sums in a different order (the reference runs numba fastmath),
+so an accept decision whose error sits at the leaf tolerance can flip and
+move that pair's integral by about the tolerance (0.1 eps per leaf, times
+|vinv| in node-weight units).  Measured worst cases: 7.5e-11 of max|value|
+and 1.9e-9 of the row's max at eps 1e-10 (config 2); the bars below are
+5 eps and 50 eps."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KINDS = ("s", "d", "sprime", "spp_plus_dprime")
+
+
+def _kind(name):
+    from paper_2111_10743_b200.operators import as_kind
+    return as_kind(name)
+
+
+def _case(name):
+    if name == "config2":
+        p = os.path.join(ROOT, "data", "config2.npz")
+        if not os.path.exists(p):
+            pytest.skip("data/config2.npz not present")
+        return dict(np.load(p))
+    return golden(name + ".npz")
+
+
+@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7"])
+def test_near_map_bit_exact(cuda, name):
+    from paper_2111_10743_b200 import Geometry
+    from paper_2111_10743_b200.quadrature import build_near_map
+    g = _case(name)
+    near = build_near_map(Geometry.from_arrays(g), float(g["near_eta"]))
+    assert np.array_equal(near.offsets, g["near_offsets"])
+    assert np.array_equal(near.patches, g["near_patches"])
+    # the reference's list-of-arrays view: self patch first
+    lists = near.near
+    assert all(lists[t][0] == g["node_patch"][t] for t in range(len(lists)))
+
+
+def test_near_map_cap_error(cuda):
+    from paper_2111_10743_b200 import Geometry
+    from paper_2111_10743_b200.quadrature import NearMapCapError, build_near_map
+    g = _case("opset_torus_o3")
+    with pytest.raises(NearMapCapError):
+        build_near_map(Geometry.from_arrays(g), 2.0, cap=4)
+    with pytest.raises(ValueError):
+        build_near_map(Geometry.from_arrays(g), 0.0)
+
+
+@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7", "config2"])
+def test_corrections_match_reference(cuda, name):
+    from paper_2111_10743_b200 import Geometry
+    from paper_2111_10743_b200.quadrature import NearMap, build_correction_set
+    g = _case(name)
+    geom = Geometry.from_arrays(g)
+    near = NearMap(float(g["near_eta"]), 128, g["near_offsets"], g["near_patches"])
+    kinds = [k for k in KINDS if "corr_" + k in g]
+    eps = float(g["eps"])
+    cset, t_q = build_correction_set(geom, near, [_kind(k) for k in kinds], eps)
+    ip = cset.indptr.cpu().numpy()
+    assert np.array_equal(ip, g["corr_indptr"])
+    assert np.array_equal(cset.indices.cpu().numpy(), g["corr_indices"])
+    rows = np.repeat(np.arange(len(ip) - 1), np.diff(ip))
+    for k in kinds:
+        v = cset.values[_kind(k)].cpu().numpy()
+        ref = g["corr_" + k]
+        diff = np.abs(v - ref)
+        assert diff.max() <= 5 * eps * np.abs(ref).max(), k
+        rowmax = np.maximum.reduceat(np.abs(ref), ip[:-1])
+        assert (diff / rowmax[rows]).max() <= 50 * eps, k
+
+
+def test_gradient_kinds_rejected(cuda):
+    from paper_2111_10743_b200 import Geometry
+    from paper_2111_10743_b200.quadrature import NearMap, build_correction_set
+    g = _case("opset_sphere_o3")
+    near = NearMap(2.0, 128, g["near_offsets"], g["near_patches"])
+    with pytest.raises(ValueError):
+        build_correction_set(Geometry.from_arrays(g), near, [_kind("grads1")], 1e-6)
+    with pytest.raises(ValueError):
+        build_correction_set(Geometry.from_arrays(g), near, [_kind("s")], 1e-2)
+
+
+def test_config2_solve_with_device_corrections(cuda):
+    """BASELINE config 2 end to end on the device: near map + corrections
+    (reference: 385 s of CPU) + A3 GMRES solve, against the reference's
+    solve with its own corrections."""
+    import paper_2111_10743_b200 as b
+    from paper_2111_10743_b200.quadrature import build_near_map
+    g = _case("config2")
+    geom = b.Geometry.from_arrays(g)
+    near = build_near_map(geom, 2.0)
+    op = b.LayerOperatorSet(geom, "a3", float(g["eps"]), near=near, far="direct")
+    assert op.t_q > 0 and op.corrections_built_on == "device"
+    rep = b.solve_laplace_beltrami(op, g["f"], b.SolveConfig(formulation="a3", eps=1e-10,
+                                                             eps_gmres=1e-10))
+    u = np.asarray(rep.u.values)
+    ref = g["a3_u"]
+    assert np.linalg.norm(u - ref) / np.linalg.norm(ref) < 1e-7
+    exact = g["u_exact"]
+    err = np.linalg.norm(u - exact) / np.linalg.norm(exact)
+    ref_err = np.linalg.norm(ref - exact) / np.linalg.norm(exact)
+    assert err < 1.01 * ref_err + 1e-9
