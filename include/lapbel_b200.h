@@ -295,8 +295,10 @@ int lb_near_map_fill(const double* nodes, int64_t n, const double* centers,
                      const int64_t* node_patch, const int64_t* offsets,
                      int32_t* patches, void* stream);
 
-/* compute_corrections (quadrature.py:663-701) for kinds S, D, S', S''+D'
- * (gradient kinds need the principal-value constants: LB_ERR_ARG).  One
+/* compute_corrections (quadrature.py:663-701) for all seven kinds (the
+ * gradient kinds add the principal-value constants of grad S over the own
+ * patch: adaptive curvature/double-layer terms + boundary line integral,
+ * quadrature.py:424-498, 562-590).  One
  * entry per near (target, patch) pair; the adaptive subdivision, leaf rules,
  * tolerance (0.1 eps max(sqrt(area fraction), 1e-3)) and geometric forcing are
  * _adaptive_pairs' (quadrature.py:277-420).  values[k][pair_pos[i] + b] =
@@ -329,6 +331,14 @@ typedef struct {
   int nbo;
   const double *over_nodes, *over_normals, *over_weights;
   double* values[7];
+  int64_t* stats;  /* optional DEVICE int64[2], accumulated: refinement steps, leaves evaluated */
+  /* gradient kinds only (principal-value constants, quadrature.py:562-590):
+   * n targets, mean-curvature coefficients (npatches, nb) k-major
+   * (curvature @ vinv.T), Gauss-Legendre panel rule on [0, 1] (ng, 2) */
+  int64_t n;
+  const double* hcoeff_km;
+  const double* gauss;
+  int ng;
 } lb_corr_build_desc;
 int lb_corrections_build(const lb_corr_build_desc* desc, void* stream);
 

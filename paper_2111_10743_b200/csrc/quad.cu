@@ -31,7 +31,7 @@ namespace lb {
 namespace {
 
 constexpr double kFourPi = 4.0 * 3.141592653589793;  // kernels.py:16
-constexpr int kQuadThreads = 128;
+constexpr int kQuadThreads = 256;
 constexpr int kMaxDepth = 30;                          // quadrature.py:43
 constexpr int kStackItems = 128;                       // >= 3 + 3 * kMaxDepth
 constexpr int kMaxKinds = 7;
@@ -112,7 +112,21 @@ struct QuadArgs {
   unsigned long long* next;  // work counter
   int* status;               // [0]: 0 ok / 1 depth cap
   long long* bad_pair;
+  unsigned long long* stats; // [0] refinement steps, [1] leaves evaluated (optional)
+  int mode;                  // 0: basis-weight rows (_row_integrand), 1: PV integrals (_pv_integrand)
+  const double* hcoeff;      // mode 1: (npat, nb) mean-curvature coefficients, k-major
 };
+
+__host__ __device__ __forceinline__ bool is_grad(int code) { return code >= LB_KIND_GRAD_S1 && code <= LB_KIND_GRAD_S3; }
+
+__global__ void self_pairs_kernel(const int64_t* __restrict__ node_patch, int64_t n, int64_t* __restrict__ tgt,
+                                  int32_t* __restrict__ pat) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    tgt[i] = i;
+    pat[i] = (int32_t)node_patch[i];
+  }
+}
 
 // Koornwinder basis at (u, v), k-major (_leafeval.py:25-61)
 template <int ORDER>
@@ -176,6 +190,8 @@ struct QuadSmem {
   double rr[Sh::LB * Sh::NQ];
   double vals[4 * kMaxKinds * Sh::NB];  // children values (all 4)
   double acc[kMaxKinds * Sh::NB];
+  double psi0[Sh::NB];   // basis at the node's preimage (shifted gradient rows)
+  double hco[Sh::NB];    // mode 1: the patch's curvature coefficients
   double item[Sh::ITEM];
   double cverts[4 * 6];
   double cmind[4], cdiam[4];
@@ -185,8 +201,8 @@ struct QuadSmem {
 
 // evaluate leaves [c0, c0 + L) of sm.cverts into sm.vals[c], cmind, cdiam
 template <int ORDER>
-__device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int L, bool duffy, const double x[3],
-                            const double nx[3]) {
+__device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int L, bool duffy, bool self,
+                            const double x[3], const double nx[3]) {
   using Sh = QuadShape<ORDER>;
   constexpr int NB = Sh::NB;
   const int nq = duffy ? A.nqd : A.nqs;
@@ -207,15 +223,19 @@ __device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int 
       uu = v[0] + aq * e1u + bq * e2u;
       vv = v[1] + aq * e1v + bq * e2v;
     }
-    double psi[NB];
+    const int base = l * Sh::NQ + q;
+    // basis straight into shared memory (the dot products below read it
+    // there anyway): keeps the register footprint low enough for 2 CTAs/SM
+    double* psi = sm.psi + base * NB;
     koornwinder_km<ORDER>(uu, vv, sm.norm, psi);
     double g[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) g[c] = 0.0;
-#pragma unroll
+#pragma unroll 4
     for (int b = 0; b < NB; ++b) {
+      const double pb = psi[b];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) g[c] += psi[b] * sm.coeffs[9 * b + c];
+      for (int c = 0; c < 9; ++c) g[c] += pb * sm.coeffs[9 * b + c];
     }
     const double cr0 = g[4] * g[8] - g[5] * g[7];
     const double cr1 = g[5] * g[6] - g[3] * g[8];
@@ -228,7 +248,21 @@ __device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int 
     const double invr = 1.0 / sqrt(rr);
     const double invr3 = invr / rr;
     const double w = wq * area2 * jac;
-    const int base = l * Sh::NQ + q;
+    if (A.mode == 1) {
+      // _pv_integrand (quadrature.py:252-274): 2H G n_y and (D kernel) n_y
+      double hc = 0.0;
+      for (int b = 0; b < NB; ++b) hc += psi[b] * sm.hco[b];
+      const double gk = invr / kFourPi;
+      const double dker = (r0 * ny0 + r1 * ny1 + r2 * ny2) / (rr * sqrt(rr)) / kFourPi;
+      const double c = 2.0 * hc * gk * w, dw = dker * w;
+      double* kwp = sm.kw + base * kMaxKinds;
+      kwp[0] = c * ny0;
+      kwp[1] = c * ny1;
+      kwp[2] = c * ny2;
+      kwp[3] = dw * ny0;
+      kwp[4] = dw * ny1;
+      kwp[5] = dw * ny2;
+    } else
     for (int k = 0; k < nk; ++k) {
       double ker;
       switch (A.codes[k]) {
@@ -248,21 +282,31 @@ __device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int 
       }
       sm.kw[base * kMaxKinds + k] = ker * w;
     }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) sm.psi[base * NB + b] = psi[b];
     sm.y[3 * base] = g[0];
     sm.y[3 * base + 1] = g[1];
     sm.y[3 * base + 2] = g[2];
     sm.rr[base] = rr;
   }
   __syncthreads();
-  // basis-weighted sums: vals[c][k][b] = sum_q kw[q][k] psi[q][b]
-  for (int o = threadIdx.x; o < L * nk * NB; o += blockDim.x) {
-    const int l = o / (nk * NB), kb = o - l * nk * NB, k = kb / NB, b = kb - k * NB;
+  // basis-weighted sums: vals[c][k][b] = sum_q kw[q][k] psi[q][b] (gradient
+  // kinds on the self patch use the shifted basis psi - psi0,
+  // _leafeval.py:172-174); mode 1: plain sums of the 6 PV components
+  const int nbv = A.mode == 1 ? 1 : NB;
+  for (int o = threadIdx.x; o < L * nk * nbv; o += blockDim.x) {
+    const int l = o / (nk * nbv), kb = o - l * nk * nbv, k = kb / nbv, b = kb - k * nbv;
     const double* kwp = sm.kw + l * Sh::NQ * kMaxKinds + k;
-    const double* pp = sm.psi + l * Sh::NQ * NB + b;
     double s = 0.0;
-    for (int q = 0; q < nq; ++q) s += kwp[q * kMaxKinds] * pp[q * NB];
+    if (A.mode == 1) {
+      for (int q = 0; q < nq; ++q) s += kwp[q * kMaxKinds];
+    } else {
+      const double* pp = sm.psi + l * Sh::NQ * NB + b;
+      if (self && is_grad(A.codes[k])) {
+        const double p0 = sm.psi0[b];
+        for (int q = 0; q < nq; ++q) s += kwp[q * kMaxKinds] * (pp[q * NB] - p0);
+      } else {
+        for (int q = 0; q < nq; ++q) s += kwp[q * kMaxKinds] * pp[q * NB];
+      }
+    }
     sm.vals[((c0 + l) * kMaxKinds + k) * NB + b] = s;
   }
   // distance to the target and leaf diameter (_leafeval.py:137-190): one warp per leaf
@@ -306,14 +350,17 @@ __device__ void eval_leaves(const QuadArgs& A, QuadSmem<ORDER>& sm, int c0, int 
 }
 
 template <int ORDER>
-__global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
+__global__ void __launch_bounds__(kQuadThreads, 2) quad_pairs_kernel(QuadArgs A) {
   using Sh = QuadShape<ORDER>;
   constexpr int NB = Sh::NB;
   constexpr int ITEM = Sh::ITEM;
   extern __shared__ __align__(16) unsigned char smraw[];
   QuadSmem<ORDER>& sm = *reinterpret_cast<QuadSmem<ORDER>*>(smraw);
   const int nk = A.nk;
-  const int nkb = nk * NB;
+  const int nbv = A.mode == 1 ? 1 : NB;
+  const int nkb = nk * nbv;
+  bool any_grad = false;
+  for (int k = 0; k < nk; ++k) any_grad |= A.mode == 0 && is_grad(A.codes[k]);
   double* stack = A.stack + (int64_t)blockIdx.x * kStackItems * ITEM;
   for (int i = threadIdx.x; i < NB; i += blockDim.x) sm.norm[i] = A.norm[i];
   for (;;) {
@@ -327,7 +374,9 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
     const double x[3] = {A.nodes[3 * t], A.nodes[3 * t + 1], A.nodes[3 * t + 2]};
     const double nx[3] = {A.normals[3 * t], A.normals[3 * t + 1], A.normals[3 * t + 2]};
     for (int i = threadIdx.x; i < NB * 9; i += blockDim.x) sm.coeffs[i] = A.coeffs[p * NB * 9 + i];
-    for (int i = threadIdx.x; i < nkb; i += blockDim.x) sm.acc[(i / NB) * NB + i % NB] = 0.0;
+    for (int i = threadIdx.x; i < nkb; i += blockDim.x) sm.acc[i] = 0.0;
+    if (A.mode == 1)
+      for (int i = threadIdx.x; i < NB; i += blockDim.x) sm.hco[i] = A.hcoeff[p * NB + i];
     // roots (quadrature.py:548-556): self -> 3 Duffy triangles at the node's
     // preimage, else the whole reference triangle
     const int nroot = self ? 3 : 1;
@@ -347,9 +396,10 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
       } else {
         for (int c = 0; c < 6; ++c) sm.cverts[c] = corners[c];
       }
+      if (self && any_grad) koornwinder_km<ORDER>(A.node_uv[2 * t], A.node_uv[2 * t + 1], sm.norm, sm.psi0);
     }
     __syncthreads();
-    eval_leaves<ORDER>(A, sm, 0, nroot, self, x, nx);
+    eval_leaves<ORDER>(A, sm, 0, nroot, self, self, x, nx);
     // push the roots (reverse order: the first root is refined first)
     int sp = 0;
     for (int r = nroot - 1; r >= 0; --r) {
@@ -361,7 +411,7 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
         else if (i == 7) val = 0.0;
         else if (i == 8) val = sm.cmind[r];
         else if (i == 9) val = sm.cdiam[r];
-        else val = sm.vals[(r * kMaxKinds + (i - 10) / NB) * NB + (i - 10) % NB];
+        else val = sm.vals[(r * kMaxKinds + (i - 10) / nbv) * NB + (i - 10) % nbv];
         it[i] = val;
       }
       ++sp;
@@ -405,12 +455,16 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
       }
       __syncthreads();
       for (int c0 = 0; c0 < nch; c0 += Sh::LB) {
-        eval_leaves<ORDER>(A, sm, c0, min(Sh::LB, nch - c0), duffy, x, nx);
+        eval_leaves<ORDER>(A, sm, c0, min(Sh::LB, nch - c0), duffy, self, x, nx);
+      }
+      if (A.stats && threadIdx.x == 0) {
+        atomicAdd(A.stats, 1ull);
+        atomicAdd(A.stats + 1, (unsigned long long)nch);
       }
       // fine = sum of the children; err = max |fine - vals|
       double e = 0.0;
       for (int i = threadIdx.x; i < nkb; i += blockDim.x) {
-        const int k = i / NB, b = i - k * NB;
+        const int k = i / nbv, b = i - k * nbv;
         double f = 0.0;
         for (int c = 0; c < nch; ++c) f += sm.vals[(c * kMaxKinds + k) * NB + b];
         e = fmax(e, fabs(f - sm.item[10 + i]));
@@ -427,7 +481,7 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
       const bool ok = (err <= tol) && !force;
       if (ok) {
         for (int i = threadIdx.x; i < nkb; i += blockDim.x) {
-          const int k = i / NB, b = i - k * NB;
+          const int k = i / nbv, b = i - k * nbv;
           double f = 0.0;
           for (int c = 0; c < nch; ++c) f += sm.vals[(c * kMaxKinds + k) * NB + b];
           sm.acc[i] += f;
@@ -443,7 +497,7 @@ __global__ void __launch_bounds__(kQuadThreads) quad_pairs_kernel(QuadArgs A) {
             else if (i == 7) val = (double)(depth + 1);
             else if (i == 8) val = sm.cmind[c];
             else if (i == 9) val = sm.cdiam[c];
-            else val = sm.vals[(c * kMaxKinds + (i - 10) / NB) * NB + (i - 10) % NB];
+            else val = sm.vals[(c * kMaxKinds + (i - 10) / nbv) * NB + (i - 10) % nbv];
             it[i] = val;
           }
           ++sp;
@@ -483,6 +537,9 @@ struct AsmArgs {
   const int64_t* pair_pos;    // CSR value offset of the pair's nb columns
   int64_t npairs;
   double* vals[kMaxKinds];    // CSR value arrays, one per kind
+  const int64_t* node_patch;  // self-pair test for the PV term
+  const double* pv;           // (N, 3) PV constants of grad S over the own patch, or null
+  const double* pvrow;        // (N, nb) interpolation row at the node's preimage
 };
 
 __global__ void __launch_bounds__(128) corr_assemble_kernel(AsmArgs A) {
@@ -537,9 +594,210 @@ __global__ void __launch_bounds__(128) corr_assemble_kernel(AsmArgs A) {
       for (int j = 0; j < nb; ++j) rows += accd[k * nb + j] * A.vinv[j * nb + b];
       double over = 0.0;
       for (int q = 0; q < nbo; ++q) over += kwo[q * nk + k] * A.over_interp[q * nb + b];
+      const int code = A.codes[k];
+      if (A.pv && is_grad(code) && A.node_patch[t] == p)  // quadrature.py:685-688
+        rows += A.pv[3 * t + (code - LB_KIND_GRAD_S1)] * A.pvrow[t * nb + b];
       A.vals[k][pos + b] = rows - over;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// principal-value constants (quadrature.py:424-498, 562-590)
+
+constexpr int kBndStack = 64;
+
+// line integral of G(x, y) nu around the own patch (_boundary_g_integral):
+// one warp per (target, edge), adaptive bisection of Gauss panels
+template <int ORDER>
+__global__ void __launch_bounds__(128) pv_boundary_kernel(const double* __restrict__ coeffs,
+                                                          const double* __restrict__ nodes,
+                                                          const int64_t* __restrict__ node_patch,
+                                                          const double* __restrict__ norm,
+                                                          const double* __restrict__ gauss, int ng, int64_t n,
+                                                          double eps, double* __restrict__ bnd, int* status) {
+  constexpr int NB = ORDER * (ORDER + 1) / 2;
+  __shared__ double sh[4][32][5];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * 4 + wib;
+  if (item >= 3 * n) return;
+  const int64_t t = item / 3;
+  const int e = (int)(item % 3);
+  const int64_t p = node_patch[t];
+  const double* cf = coeffs + p * NB * 9;
+  const double x0 = nodes[3 * t], x1 = nodes[3 * t + 1], x2 = nodes[3 * t + 2];
+  const double cu[3] = {0.0, 1.0, 0.0}, cv[3] = {0.0, 0.0, 1.0};
+  const double e0u = cu[e], e0v = cv[e], e1u = cu[(e + 1) % 3], e1v = cv[(e + 1) % 3];
+  const double du = e1u - e0u, dv = e1v - e0v;
+  double (*S)[5] = sh[wib];
+  // evaluate panel [a, b] on lanes [h * ng, h * ng + ng): returns (vals, dist, plen) on all lanes
+  auto panel = [&](double a, double b, int h, double out[5]) {
+    if (lane >= h * ng && lane < (h + 1) * ng) {
+      const int q = lane - h * ng;
+      const double tl = a + (b - a) * gauss[2 * q];
+      const double uu = e0u + tl * du, vv = e0v + tl * dv;
+      double psi[NB];
+      {
+        double buf[NB];
+        koornwinder_km<ORDER>(uu, vv, norm, buf);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) psi[i] = buf[i];
+      }
+      double g[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) g[c] = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) g[c] += psi[bb] * cf[9 * bb + c];
+      }
+      const double tv0 = g[3] * du + g[6] * dv, tv1 = g[4] * du + g[7] * dv, tv2 = g[5] * du + g[8] * dv;
+      const double tlen = sqrt(tv0 * tv0 + tv1 * tv1 + tv2 * tv2);
+      const double th0 = tv0 / tlen, th1 = tv1 / tlen, th2 = tv2 / tlen;
+      const double c0 = g[4] * g[8] - g[5] * g[7], c1 = g[5] * g[6] - g[3] * g[8], c2 = g[3] * g[7] - g[4] * g[6];
+      const double cn = sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+      const double n0 = c0 / cn, n1 = c1 / cn, n2 = c2 / cn;
+      const double nu0 = th1 * n2 - th2 * n1, nu1 = th2 * n0 - th0 * n2, nu2 = th0 * n1 - th1 * n0;
+      const double r0 = x0 - g[0], r1 = x1 - g[1], r2 = x2 - g[2];
+      const double gk = 1.0 / (kFourPi * sqrt(r0 * r0 + r1 * r1 + r2 * r2));
+      const double sc = gk * ((b - a) * gauss[2 * q + 1]) * tlen;
+      S[lane][0] = sc * nu0;
+      S[lane][1] = sc * nu1;
+      S[lane][2] = sc * nu2;
+      S[lane][3] = tlen;
+      S[lane][4] = sqrt(r0 * r0 + r1 * r1 + r2 * r2);  // |x - y_q|
+    }
+    __syncwarp();
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, tsum = 0.0;
+    for (int q = 0; q < ng; ++q) {  // ordered sums: deterministic
+      v0 += S[h * ng + q][0];
+      v1 += S[h * ng + q][1];
+      v2 += S[h * ng + q][2];
+      tsum += S[h * ng + q][3];
+    }
+    out[0] = v0;
+    out[1] = v1;
+    out[2] = v2;
+    out[3] = S[h * ng + ng / 2][4];          // distance to the middle node
+    out[4] = tsum / ng * (b - a);             // panel length
+    __syncwarp();
+  };
+  double st[kBndStack][6];  // a, b, v0, v1, v2 (dist/plen kept separately)
+  double sdist[kBndStack], splen[kBndStack];
+  int sdep[kBndStack];
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  double r[5];
+  panel(0.0, 1.0, 0, r);
+  int sp = 0;
+  st[0][0] = 0.0;
+  st[0][1] = 1.0;
+  st[0][2] = r[0];
+  st[0][3] = r[1];
+  st[0][4] = r[2];
+  sdist[0] = r[3];
+  splen[0] = r[4];
+  sdep[0] = 0;
+  sp = 1;
+  while (sp > 0) {
+    --sp;
+    const double a = st[sp][0], b = st[sp][1];
+    const double pv0 = st[sp][2], pv1 = st[sp][3], pv2 = st[sp][4], plen = splen[sp];
+    const int dep = sdep[sp];
+    if (dep >= kMaxDepth || sp >= kBndStack - 2) {
+      if (lane == 0) atomicExch(status, 3);
+      return;
+    }
+    const double mid = 0.5 * (a + b);
+    double r1[5], r2[5];
+    // both halves at once: lanes [0, ng) and [ng, 2 ng)
+    {
+      double o1[5], o2[5];
+      panel(a, mid, 0, o1);
+      panel(mid, b, 1, o2);
+      for (int i = 0; i < 5; ++i) { r1[i] = o1[i]; r2[i] = o2[i]; }
+    }
+    const double f0 = r1[0] + r2[0], f1 = r1[1] + r2[1], f2 = r1[2] + r2[2];
+    const double err = fmax(fabs(f0 - pv0), fmax(fabs(f1 - pv1), fabs(f2 - pv2)));
+    const bool force = plen > 0.8 * fmin(r1[3], r2[3]);
+    const bool ok = err <= 0.1 * eps * fmax(sqrt(b - a), 1e-3) && !force;
+    if (ok) {
+      acc0 += f0;
+      acc1 += f1;
+      acc2 += f2;
+    } else {
+      st[sp][0] = mid; st[sp][1] = b; st[sp][2] = r2[0]; st[sp][3] = r2[1]; st[sp][4] = r2[2];
+      sdist[sp] = r2[3]; splen[sp] = r2[4]; sdep[sp] = dep + 1; ++sp;
+      st[sp][0] = a; st[sp][1] = mid; st[sp][2] = r1[0]; st[sp][3] = r1[1]; st[sp][4] = r1[2];
+      sdist[sp] = r1[3]; splen[sp] = r1[4]; sdep[sp] = dep + 1; ++sp;
+    }
+  }
+  if (lane == 0) {
+    bnd[t * 9 + e * 3] = acc0;
+    bnd[t * 9 + e * 3 + 1] = acc1;
+    bnd[t * 9 + e * 3 + 2] = acc2;
+  }
+}
+
+// pv = -(boundary + curvature term + double-layer term) (quadrature.py:590)
+// and the interpolation row psi(uv0) @ vinv (quadrature.py:684)
+template <int ORDER>
+__global__ void pv_combine_kernel(const double* __restrict__ bnd, const double* __restrict__ pvacc,
+                                  const double* __restrict__ node_uv, const double* __restrict__ norm,
+                                  const int32_t* __restrict__ perm, const double* __restrict__ vinv, int64_t n,
+                                  double* __restrict__ pv, double* __restrict__ pvrow) {
+  constexpr int NB = ORDER * (ORDER + 1) / 2;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  for (int c = 0; c < 3; ++c) {
+    const double boundary = (bnd[t * 9 + c] + bnd[t * 9 + 3 + c]) + bnd[t * 9 + 6 + c];
+    pv[3 * t + c] = -((boundary + pvacc[6 * t + c]) + pvacc[6 * t + 3 + c]);
+  }
+  double psi[NB];
+  koornwinder_km<ORDER>(node_uv[2 * t], node_uv[2 * t + 1], norm, psi);
+  for (int b = 0; b < NB; ++b) {
+    double s = 0.0;
+    for (int j = 0; j < NB; ++j) s += psi[perm[j]] * vinv[j * NB + b];
+    pvrow[t * NB + b] = s;
+  }
+}
+
+template <int ORDER>
+int launch_quad(const QuadArgs& A, int grid, cudaStream_t st);
+
+template <int ORDER>
+int launch_pv(const lb_corr_build_desc* d, QuadArgs A, int grid, Scratch& s_pv, Scratch& s_row,
+              cudaStream_t st) {
+  constexpr int NB = ORDER * (ORDER + 1) / 2;
+  const int64_t n = d->n;
+  Scratch s_tgt, s_pat, s_acc, s_bnd;
+  LB_TRY(s_tgt.alloc(sizeof(int64_t) * n, st));
+  LB_TRY(s_pat.alloc(sizeof(int32_t) * n, st));
+  LB_TRY(s_acc.alloc(sizeof(double) * 6 * n, st));
+  LB_TRY(s_bnd.alloc(sizeof(double) * 9 * n, st));
+  LB_TRY(s_pv.alloc(sizeof(double) * 3 * n, st));
+  LB_TRY(s_row.alloc(sizeof(double) * NB * n, st));
+  self_pairs_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d->node_patch, n, static_cast<int64_t*>(s_tgt.ptr),
+                                                                static_cast<int32_t*>(s_pat.ptr));
+  LB_CHECK_LAUNCH();
+  // _pv_constants' adaptive part: 3 Duffy roots per target, 6 components
+  A.mode = 1;
+  A.nk = 6;
+  A.hcoeff = d->hcoeff_km;
+  A.pair_tgt = static_cast<int64_t*>(s_tgt.ptr);
+  A.pair_pat = static_cast<int32_t*>(s_pat.ptr);
+  A.npairs = n;
+  A.acc = static_cast<double*>(s_acc.ptr);
+  LB_CUDA(cudaMemsetAsync(A.next, 0, 8, st));
+  LB_TRY(launch_quad<ORDER>(A, grid, st));
+  pv_boundary_kernel<ORDER><<<(unsigned)ceil_div(3 * n, 4), 128, 0, st>>>(
+      d->coeffs_km, d->nodes, d->node_patch, d->knorm, d->gauss, d->ng, n, d->eps,
+      static_cast<double*>(s_bnd.ptr), A.status);
+  LB_CHECK_LAUNCH();
+  pv_combine_kernel<ORDER><<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(
+      static_cast<double*>(s_bnd.ptr), static_cast<double*>(s_acc.ptr), d->node_uv, d->knorm, d->kmajor_perm,
+      d->vinv, n, static_cast<double*>(s_pv.ptr), static_cast<double*>(s_row.ptr));
+  LB_CHECK_LAUNCH();
+  return LB_OK;
 }
 
 template <int ORDER>
@@ -594,10 +852,10 @@ int lb_corrections_build(const lb_corr_build_desc* d, void* stream) {
   for (int k = 0; k < d->nk; ++k) {
     const int c = d->kinds[k];
     if (c < 0 || c > 6) return fail(LB_ERR_KEY, "lb_corrections_build: unknown kind code");
-    if (c >= LB_KIND_GRAD_S1 && c <= LB_KIND_GRAD_S3)
-      return fail(LB_ERR_ARG,
-                  "lb_corrections_build: gradient kinds need the principal-value constants "
-                  "(quadrature.py:562-590), not built on the device yet");
+    if (is_grad(c)) {
+      if (!d->hcoeff_km || !d->gauss || d->ng < 1 || d->ng > 16 || d->n <= 0)
+        return fail(LB_ERR_ARG, "lb_corrections_build: gradient kinds need hcoeff_km, gauss, ng and n");
+    }
   }
   if (d->order < 2 || d->order > 9) return fail(LB_ERR_ARG, "lb_corrections_build: order must be in [2, 9]");
   const int nb = d->order * (d->order + 1) / 2;
@@ -621,6 +879,7 @@ int lb_corrections_build(const lb_corr_build_desc* d, void* stream) {
   A.srule = d->srule;
   A.drule = d->drule;
   A.norm = d->knorm;
+  A.stats = reinterpret_cast<unsigned long long*>(d->stats);
   if (d->nqs > (d->order + 2) * (d->order + 2) || d->nqd > (d->order + 2) * (d->order + 2))
     return fail(LB_ERR_ARG, "lb_corrections_build: leaf rules larger than (order + 2)^2 points");
   // scratch: basis integrals, per-CTA item stacks, counters
@@ -647,9 +906,26 @@ int lb_corrections_build(const lb_corr_build_desc* d, void* stream) {
     case 8: LB_TRY(launch_quad<8>(A, grid, st)); break;
     default: LB_TRY(launch_quad<9>(A, grid, st)); break;
   }
+  // principal-value constants for the gradient kinds (quadrature.py:679-688)
+  bool any_grad = false;
+  for (int k = 0; k < d->nk; ++k) any_grad |= is_grad(d->kinds[k]);
+  Scratch s_pv, s_row;
+  if (any_grad) {
+    switch (d->order) {
+      case 2: LB_TRY(launch_pv<2>(d, A, grid, s_pv, s_row, st)); break;
+      case 3: LB_TRY(launch_pv<3>(d, A, grid, s_pv, s_row, st)); break;
+      case 4: LB_TRY(launch_pv<4>(d, A, grid, s_pv, s_row, st)); break;
+      case 5: LB_TRY(launch_pv<5>(d, A, grid, s_pv, s_row, st)); break;
+      case 6: LB_TRY(launch_pv<6>(d, A, grid, s_pv, s_row, st)); break;
+      case 7: LB_TRY(launch_pv<7>(d, A, grid, s_pv, s_row, st)); break;
+      case 8: LB_TRY(launch_pv<8>(d, A, grid, s_pv, s_row, st)); break;
+      default: LB_TRY(launch_pv<9>(d, A, grid, s_pv, s_row, st)); break;
+    }
+  }
   int flags[6] = {0, 0, 0, 0, 0, 0};
   LB_CUDA(cudaMemcpyAsync(flags, static_cast<char*>(s_cnt.ptr) + 8, 16, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaStreamSynchronize(st));
+  if (flags[0] == 3) return fail(LB_ERR_DEPTH, "boundary integral depth cap");  // quadrature.py:478-479
   if (flags[0] != 0) {
     long long bp = 0;
     std::memcpy(&bp, &flags[2], 8);
@@ -678,6 +954,9 @@ int lb_corrections_build(const lb_corr_build_desc* d, void* stream) {
   B.pair_pat = d->pair_pat;
   B.pair_pos = d->pair_pos;
   B.npairs = d->npairs;
+  B.node_patch = d->node_patch;
+  B.pv = any_grad ? static_cast<const double*>(s_pv.ptr) : nullptr;
+  B.pvrow = any_grad ? static_cast<const double*>(s_row.ptr) : nullptr;
   const size_t smem = sizeof(double) * ((size_t)d->nbo * d->nk + (size_t)d->nk * nb);
   if (smem > 200 * 1024) return fail(LB_ERR_ARG, "lb_corrections_build: oversampled rule too large");
   LB_CUDA(cudaFuncSetAttribute(corr_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

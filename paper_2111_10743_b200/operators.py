@@ -434,7 +434,7 @@ class LayerOperatorSet:
                     when None they are built ON THE DEVICE
                     (quadrature.build_correction_set: near map + adaptive
                     singular quadrature, csrc/quad.cu) if disc carries the
-                    chart coefficients and the kinds are S/D/S'/S''+D';
+                    chart coefficients;
                     otherwise by the reference's compute_corrections
                     (requires lapbel to be importable).
       far         : "auto" (default), "direct" or "fmm".  use_fmm=False
@@ -737,10 +737,11 @@ class _CorrView:
 
 
 def _device_buildable(disc, kinds):
+    need = ["coeffs_x", "coeffs_dxdu", "coeffs_dxdv", "node_uv", "node_patch"]
     grad = (KernelKind.GRAD_S1, KernelKind.GRAD_S2, KernelKind.GRAD_S3)
-    return (all(getattr(disc, f, None) is not None
-                for f in ("coeffs_x", "coeffs_dxdu", "coeffs_dxdv", "node_uv", "node_patch"))
-            and not any(k in grad for k in kinds))
+    if any(k in grad for k in kinds):
+        need.append("curvature")
+    return all(getattr(disc, f, None) is not None for f in need)
 
 
 def _as_near_map(near, eta):

@@ -2,13 +2,14 @@
 
 Mirror of lapbel.quadrature's public operations for the kinds the A2/A3
 formulations use: ``build_near_map`` (quadrature.py:76-104) and
-``compute_corrections`` (quadrature.py:663-701) for S, D, S' and S''+D'.
+``compute_corrections`` (quadrature.py:663-701) for all seven kinds.
 The reference runs them once per geometry on the CPU (t_q: 438 s at BASELINE
 config 2, hours at config 3); here the near map is one device pass over the
 patch bounding spheres and the adaptive singular quadrature runs one CTA per
-(target, patch) pair (``csrc/quad.cu``).  The gradient kinds (A1) need the
-principal-value constants (quadrature.py:562-590) and are not built on the
-device yet: asking for them raises ValueError.
+(target, patch) pair (``csrc/quad.cu``); the gradient kinds (A1) add the
+principal-value constants (quadrature.py:562-590): the adaptive curvature and
+double-layer compensation integrals on the same kernel and the boundary line
+integral as one warp per (target, edge).
 
 Host work here is the reference's own small precomputations restated (leaf
 rules, k-major permutation, patch bounding spheres), so the device receives
@@ -31,6 +32,9 @@ __all__ = ["NearMap", "NearMapCapError", "AdaptiveDepthError", "build_near_map",
            "leaf_rules", "kmajor_permutation"]
 
 GRAD_KINDS = (KernelKind.GRAD_S1, KernelKind.GRAD_S2, KernelKind.GRAD_S3)
+
+# host / device split of the last build_correction_set call (seconds)
+LAST_BUILD: dict = {}
 
 
 NearMapCapError = _lib.NearMapCapError        # quadrature.py:58-59
@@ -191,7 +195,10 @@ class _Desc(ctypes.Structure):
                 ("kmajor_perm", ctypes.c_void_p), ("vinv", ctypes.c_void_p),
                 ("over_interp", ctypes.c_void_p), ("nbo", ctypes.c_int),
                 ("over_nodes", ctypes.c_void_p), ("over_normals", ctypes.c_void_p),
-                ("over_weights", ctypes.c_void_p), ("values", ctypes.c_void_p * 7)]
+                ("over_weights", ctypes.c_void_p), ("values", ctypes.c_void_p * 7),
+                ("stats", ctypes.c_void_p), ("n", ctypes.c_int64),
+                ("hcoeff_km", ctypes.c_void_p), ("gauss", ctypes.c_void_p),
+                ("ng", ctypes.c_int)]
 
 
 def _require(disc, name):
@@ -220,10 +227,7 @@ def build_correction_set(disc, near: NearMap, kinds, eps: float):
     if not (1e-12 <= eps <= 1e-3):
         raise ValueError("eps must lie in [1e-12, 1e-3]")
     kinds = [as_kind(k) for k in kinds]
-    if any(k in GRAD_KINDS for k in kinds):
-        raise ValueError("gradient kinds need the principal-value constants "
-                         "(quadrature.py:562-590); the device build covers "
-                         "S, D, S', S''+D'")
+    want_pv = any(k in GRAD_KINDS for k in kinds)
     t = _lib.torch()
     _lib.require_cuda()
     L = _bind()
@@ -231,25 +235,28 @@ def build_correction_set(disc, near: NearMap, kinds, eps: float):
     order = int(disc.order)
     nb = order * (order + 1) // 2
     n = disc.nnodes
-    offsets = np.asarray(near.offsets, dtype=np.int64)
-    patches = np.asarray(near.patches, dtype=np.int32)
-    counts = np.diff(offsets)
-    npairs = int(offsets[-1])
-    tgt = np.repeat(np.arange(n, dtype=np.int64), counts)
-    node_patch = np.asarray(disc.node_patch, dtype=np.int64)
-    # CSR pattern: per row the near patches sorted (the reference's
-    # csr_matrix canonical order), nb consecutive columns per patch
-    key = tgt * (int(patches.max()) + 1 if npairs else 1) + patches
-    order_sorted = np.argsort(key, kind="stable")
-    rank = np.empty(npairs, dtype=np.int64)
-    rank[order_sorted] = np.arange(npairs) - np.repeat(offsets[:-1], counts)
-    pair_pos = (offsets[:-1][tgt] + rank) * nb
-    sp = patches[order_sorted].astype(np.int64)
-    indices = (sp[:, None] * nb + np.arange(nb)[None, :]).reshape(-1).astype(np.int32)
-    indptr = offsets * nb
+    # CSR pattern on the device: per row the near patches sorted (the
+    # reference's csr_matrix canonical order), nb consecutive columns each
+    cuda = "cuda"
+    offs = _dev(np.asarray(near.offsets, dtype=np.int64))
+    pats = _dev(np.asarray(near.patches, dtype=np.int32))
+    npairs = int(offs[-1])
+    counts = offs[1:] - offs[:-1]
+    tgt = t.repeat_interleave(t.arange(n, device=cuda), counts)
+    node_patch = _dev(np.asarray(disc.node_patch, dtype=np.int64))
+    key = tgt * int(disc.npatches) + pats.to(t.int64)
+    _, order_sorted = t.sort(key, stable=True)
+    start = offs[:-1][tgt]
+    rank = t.empty_like(order_sorted)
+    rank[order_sorted] = t.arange(npairs, device=cuda) - start[order_sorted]
+    pair_pos = (start + rank) * nb
+    sp = pats[order_sorted].to(t.int64)
+    indices = (sp[:, None] * nb + t.arange(nb, device=cuda)[None, :]).reshape(-1).to(t.int32)
+    del sp, key, rank
+    indptr = offs * nb
     # work order: self pairs (Duffy, ~50x the leaves) first
-    is_self = node_patch[tgt] == patches
-    work = np.concatenate([np.nonzero(is_self)[0], np.nonzero(~is_self)[0]])
+    is_self = node_patch[tgt] == pats.to(t.int64)
+    work = t.cat([t.nonzero(is_self).flatten(), t.nonzero(~is_self).flatten()])
     # geometry in the leaf kernel's layout
     perm = kmajor_permutation(order)
     stacked = np.concatenate([_require(disc, "coeffs_x"), _require(disc, "coeffs_dxdu"),
@@ -265,10 +272,10 @@ def build_correction_set(disc, near: NearMap, kinds, eps: float):
         "nodes": dev(np.ascontiguousarray(disc.nodes, dtype=float)),
         "normals": dev(np.ascontiguousarray(disc.normals, dtype=float)),
         "node_uv": dev(np.ascontiguousarray(_require(disc, "node_uv"), dtype=float)),
-        "node_patch": dev(node_patch),
-        "pair_tgt": dev(np.ascontiguousarray(tgt[work])),
-        "pair_pat": dev(np.ascontiguousarray(patches[work])),
-        "pair_pos": dev(np.ascontiguousarray(pair_pos[work])),
+        "node_patch": node_patch,
+        "pair_tgt": tgt[work].contiguous(),
+        "pair_pat": pats[work].contiguous(),
+        "pair_pos": pair_pos[work].contiguous(),
         "srule": dev(np.ascontiguousarray(srule)),
         "drule": dev(np.ascontiguousarray(drule)),
         "knorm": dev(koornwinder_norms_kmajor(order).astype(float)),
@@ -308,10 +315,36 @@ def build_correction_set(disc, near: NearMap, kinds, eps: float):
     d.over_nodes = _lib.ptr(keep["over_nodes"])
     d.over_normals = _lib.ptr(keep["over_normals"])
     d.over_weights = _lib.ptr(keep["over_weights"])
+    stats = t.zeros(2, dtype=t.int64, device="cuda")
+    d.stats = _lib.ptr(stats)
+    d.n = n
+    if want_pv:
+        # principal-value inputs (quadrature.py:436-438, 564-565): mean
+        # curvature coefficients per patch (k-major) and the Gauss panel rule
+        from scipy.special import roots_legendre
+        vinv = np.asarray(_vinv(disc), dtype=float)
+        hn = np.asarray(_require(disc, "curvature"), dtype=float).reshape(disc.npatches, nb)
+        hco = hn @ vinv.T
+        hco_km = np.empty_like(hco)
+        hco_km[:, perm] = hco
+        gs, gw = roots_legendre(order + 2)
+        gauss = np.column_stack([0.5 * (gs + 1.0), 0.5 * gw])
+        keep["hcoeff"] = dev(np.ascontiguousarray(hco_km))
+        keep["gauss"] = dev(np.ascontiguousarray(gauss))
+        d.hcoeff_km = _lib.ptr(keep["hcoeff"])
+        d.gauss = _lib.ptr(keep["gauss"])
+        d.ng = gauss.shape[0]
+    t.cuda.synchronize()
+    t1 = time.perf_counter()
     _lib.check(L.lb_corrections_build(ctypes.byref(d), _lib.stream_handle(None)),
                "lb_corrections_build")
     t.cuda.synchronize()
-    cset = CorrectionSet(dev(indptr), dev(indices), values, shape=(n, n))
+    t2 = time.perf_counter()
+    st = stats.cpu().tolist()
+    LAST_BUILD.update({"prep_s": t1 - t0, "device_s": t2 - t1, "pairs": npairs,
+                       "self_pairs": int(is_self.sum()), "refinements": st[0],
+                       "leaves": st[1] + npairs + 2 * int(is_self.sum())})
+    cset = CorrectionSet(indptr, indices, values, shape=(n, n))
     return cset, time.perf_counter() - t0
 
 

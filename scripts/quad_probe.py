@@ -16,7 +16,9 @@ from paper_2111_10743_b200.operators import KernelKind  # noqa: E402
 from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map  # noqa: E402
 
 KINDS = {"s": KernelKind.SINGLE_LAYER, "d": KernelKind.DOUBLE_LAYER,
-         "sprime": KernelKind.SPRIME, "spp_plus_dprime": KernelKind.SPP_PLUS_DPRIME}
+         "sprime": KernelKind.SPRIME, "grads1": KernelKind.GRAD_S1,
+         "grads2": KernelKind.GRAD_S2, "grads3": KernelKind.GRAD_S3,
+         "spp_plus_dprime": KernelKind.SPP_PLUS_DPRIME}
 
 
 def load(name):
@@ -48,7 +50,8 @@ for name in sys.argv[1:] or ["quad_sphere_o7"]:
         t0 = time.perf_counter()
         cset, t_q = build_correction_set(geom, near, [KINDS[k] for k in kinds], eps)
         torch.cuda.synchronize()
-        out.update({"eps": eps, "t_q_s": time.perf_counter() - t0,
+        from paper_2111_10743_b200.quadrature import LAST_BUILD
+        out.update({"eps": eps, "t_q_s": time.perf_counter() - t0, "split": dict(LAST_BUILD),
                     "t_q_ref_s": float(g["t_q"]) if "t_q" in g else None,
                     "nnz": cset.nnz})
         if "corr_indptr" in g:

@@ -21,7 +21,7 @@ from conftest import golden
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KINDS = ("s", "d", "sprime", "spp_plus_dprime")
+KINDS = ("s", "d", "sprime", "grads1", "grads2", "grads3", "spp_plus_dprime")
 
 
 def _kind(name):
@@ -84,15 +84,30 @@ def test_corrections_match_reference(cuda, name):
         assert (diff / rowmax[rows]).max() <= 50 * eps, k
 
 
-def test_gradient_kinds_rejected(cuda):
+def test_bad_eps_rejected(cuda):
     from paper_2111_10743_b200 import Geometry
     from paper_2111_10743_b200.quadrature import NearMap, build_correction_set
     g = _case("opset_sphere_o3")
     near = NearMap(2.0, 128, g["near_offsets"], g["near_patches"])
     with pytest.raises(ValueError):
-        build_correction_set(Geometry.from_arrays(g), near, [_kind("grads1")], 1e-6)
-    with pytest.raises(ValueError):
         build_correction_set(Geometry.from_arrays(g), near, [_kind("s")], 1e-2)
+
+
+def test_a1_solve_with_device_corrections(cuda):
+    """A1 (S + grad S kinds, principal-value constants on the device) on the
+    order-3 cube sphere against the reference's A1 solve and apply."""
+    import paper_2111_10743_b200 as b
+    g = _case("opset_sphere_o3")
+    geom = b.Geometry.from_arrays(g)
+    near = b.build_near_map(geom, 2.0)
+    op = b.LayerOperatorSet(geom, "a1", float(g["eps"]), near=near, far="direct")
+    assert op.corrections_built_on == "device"
+    np.testing.assert_allclose(op.apply(g["tau"]), g["a1_apply"],
+                               atol=1e-6 * np.abs(g["a1_apply"]).max())
+    rep = b.solve_laplace_beltrami(op, g["f"], b.SolveConfig(formulation="a1", eps=1e-6,
+                                                             eps_gmres=1e-10, max_iter=60))
+    u = np.asarray(rep.u.values)
+    assert np.linalg.norm(u - g["a1_u"]) / np.linalg.norm(g["a1_u"]) < 1e-5
 
 
 def test_config2_solve_with_device_corrections(cuda):
