@@ -158,3 +158,25 @@ def test_shape_errors(cuda):
     with pytest.raises(ValueError):
         b.evaluate_direct(b.FmmSources(np.zeros((3, 3)), np.zeros((1, 3))),
                           np.zeros((3, 3)), ("pot", "laplacian"))
+
+
+def test_inv_sqrt_domain(cuda):
+    """The pairwise 1/r (lb_common.cuh inv_sqrt_skip: MUFU.RSQ64H seed + one
+    2nd-order fp64 step) over 2^-63 <= r < 2^64, and the coincident-pair skip
+    (r2 == 0 -> exactly 0)."""
+    import torch
+    from paper_2111_10743_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(0)
+    x = np.exp2(rng.uniform(-126.0, 127.9, 1 << 18))
+    x[:3] = [0.0, 1.0, 4.0]
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.check(L.lb_probe_rsqrt(_lib.ptr(xd), _lib.ptr(yd), len(x), 1,
+                                _lib.stream_handle()))
+    y = yd.cpu().numpy()
+    ref = 1.0 / np.sqrt(x[1:].astype(np.longdouble))
+    rel = np.abs((y[1:] - ref) / ref).astype(float)
+    assert rel.max() < 1e-15, rel.max()
+    assert y[0] == 0.0
+    assert abs(y[1] - 1.0) < 1e-15 and abs(y[2] - 0.5) < 1e-15

@@ -74,6 +74,9 @@ int main(int argc, char** argv) {
   // A3 call 2 uses the 8-double record; A3 call 1 reads the first 4 doubles
   // of a 4-double record: reuse the buffer (layout-only timing)
   for (int w : {1}) {
+    run<FarA1a, 4, 64, 64, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA1a, 2, 64, 128, true, 4, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA1a, 3, 64, 128, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 4, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 1, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
