@@ -11,9 +11,12 @@ Arnoldi update against K_ARNOLDI=4 basis vectors (the reference converges in
 (densities x N x N_over): 1 + 3 = 4 density-sweeps.
 
 Geometry + corrections come from data/config2.npz (built by running the
-reference, scripts/make_golden.py config2); without it the committed geometry
-subset is not enough, so the bench refuses (the round driver's box receives
-data/ with the repo snapshot).
+reference, scripts/make_golden.py config2; git-ignored, travels with the
+snapshot).  Without it the committed geometry bundle
+tests/golden/config2_geom.npz (the reference's geometry arrays, near map, the
+seeded tau and the reference's own A3 apply of it) is used and the
+corrections are built on the device (csrc/quad.cu, eps 1e-10, the same
+adaptive quadrature), which the JSON line then says.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -34,6 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 CONFIG2 = os.path.join(ROOT, "data", "config2.npz")
+CONFIG2_GEOM = os.path.join(ROOT, "tests", "golden", "config2_geom.npz")
 K_ARNOLDI = 4
 METRIC = "fp64 Laplace pot+grad interactions/s; GMRES operator-apply time vs N"
 UNIT = "interactions/s"
@@ -48,13 +52,34 @@ def _dist():
 
 
 def load_bundle():
-    if not os.path.exists(CONFIG2):
-        raise SystemExit(f"{CONFIG2} missing: run `python scripts/make_golden.py "
-                         "config2` where the reference is importable")
-    z = np.load(CONFIG2)
+    """Config-2 bundle: the reference-built one when present, else the
+    committed geometry bundle (corrections then come from the device build,
+    see with_corrections)."""
+    path = CONFIG2 if os.path.exists(CONFIG2) else CONFIG2_GEOM
+    z = np.load(path)
     keys = [k for k in z.files if not k.startswith(("a2_", "a3_"))]
-    return {k: z[k] for k in keys} | {k: z[k] for k in z.files
-                                      if k in ("a3_apply",)}
+    b = {k: z[k] for k in keys} | {k: z[k] for k in z.files if k in ("a3_apply",)}
+    b["_corrections"] = "reference" if "corr_indptr" in b else "device"
+    return b
+
+
+def with_corrections(b):
+    """Fill corr_* from the device correction build (quadrature.py mirror,
+    csrc/quad.cu) when the bundle carries none; returns the operator built on
+    the way (None when the bundle had the reference's corrections)."""
+    if "corr_indptr" in b:
+        return None
+    from paper_2111_10743_b200 import Geometry, LayerOperatorSet
+    op = LayerOperatorSet(Geometry.from_arrays(b), "a3", float(b["eps"]))
+    cs = op._cset
+
+    def host(a):
+        return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    b["corr_indptr"] = host(cs.indptr)
+    b["corr_indices"] = host(cs.indices)
+    for k, v in cs.values.items():
+        b["corr_" + k.value] = host(v)
+    return op
 
 
 class ClockSampler:
@@ -157,6 +182,10 @@ def run_reference(args):
     if rank != 0:
         return
     b = load_bundle()
+    if b["_corrections"] == "device":
+        import torch
+        torch.cuda.set_device(0)
+        with_corrections(b)
     n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
     inter = 4 * n * nover
     nthreads = os.cpu_count() or 1
@@ -183,7 +212,8 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads,
                          "kind": "port",
                          "sample": "full A3 apply of config 2 per step (oracle/"
-                                   "apply.py: C direct sums + numpy glue)"},
+                                   "apply.py: C direct sums + numpy glue; corrections "
+                                   f"built by the {b['_corrections']})"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -213,6 +243,7 @@ def main():
     from paper_2111_10743_b200.solver import _bind
 
     b = load_bundle()
+    op1 = with_corrections(b)
     n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
     inter = 4 * n * nover  # density-sweeps x targets x sources per step
     if world > 1:
@@ -223,7 +254,7 @@ def main():
         op = ShardedOperatorSet(Geometry.from_arrays(b), "a3", float(b["eps"]),
                                 CorrectionSet.from_arrays(b))
     else:
-        op = LayerOperatorSet.from_bundle(b, "a3")
+        op = op1 if op1 is not None else LayerOperatorSet.from_bundle(b, "a3")
     L = _bind()
     st = _lib.stream_handle()
 
@@ -331,7 +362,8 @@ def main():
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (config 2 geometry + reference-built corrections)",
+            "data": "synthetic (config 2 geometry + corrections built by the "
+                    f"{'reference' if b['_corrections'] == 'reference' else 'device (csrc/quad.cu)'})",
             "config": {"workload": "config2-A3-operator-apply+MGS(k=4)",
                        "N": n, "N_over": nover, "formulation": "a3",
                        "interactions_per_step": inter,

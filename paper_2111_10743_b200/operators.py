@@ -450,6 +450,10 @@ class LayerOperatorSet:
       fmm_m2l     : M2L arithmetic of that plan (FmmPlan.set_m2l): "auto"
                     (tcgen05 int8 slices sized from eps), "fp64" (DGEMM) or
                     a slice count in [3, 8].
+      correction_cache : path of an on-disk correction cache entry
+                    (corrcache.py, keyed by mesh hash, kinds, eps, eta): a
+                    device build is loaded from it on a key match and
+                    written to it otherwise.
     """
 
     FMM_CROSSOVER = 2.0e10  # target-source pairs per sweep
@@ -457,7 +461,7 @@ class LayerOperatorSet:
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
                  corrections=None, far: str = "auto", fmm_ncrit: int = 120,
-                 fmm_m2l="auto"):
+                 fmm_m2l="auto", correction_cache=None):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -476,9 +480,16 @@ class LayerOperatorSet:
                 if near is None:
                     near = build_near_map(disc, eta)
                 near = _as_near_map(near, eta)
-                corrections, self.t_q = build_correction_set(disc, near, kinds, self.eps)
+                if correction_cache is not None:  # corrcache.py: keyed file
+                    from .corrcache import cached_correction_set
+                    corrections, self.t_q, hit = cached_correction_set(
+                        correction_cache, disc, near, kinds, self.eps, eta)
+                    self.corrections_built_on = "cache" if hit else "device"
+                else:
+                    corrections, self.t_q = build_correction_set(disc, near, kinds,
+                                                                 self.eps)
+                    self.corrections_built_on = "device"
                 self.near = near
-                self.corrections_built_on = "device"
             else:
                 corrections, self.near, self.t_q = _reference_corrections(
                     disc, kinds, self.eps, eta, near)

@@ -130,3 +130,24 @@ def test_config2_solve_with_device_corrections(cuda):
     err = np.linalg.norm(u - exact) / np.linalg.norm(exact)
     ref_err = np.linalg.norm(ref - exact) / np.linalg.norm(exact)
     assert err < 1.01 * ref_err + 1e-9
+
+
+def test_correction_cache_roundtrip(cuda, tmp_path):
+    """corrcache.py through LayerOperatorSet(correction_cache=...): the first
+    construction builds on the device and writes the entry, the second loads
+    it (no rebuild) and applies identically."""
+    import paper_2111_10743_b200 as b
+    g = _case("opset_sphere_o3")
+    geom = b.Geometry.from_arrays(g)
+    path = str(tmp_path / "sphere.lbcorr")
+    op1 = b.LayerOperatorSet(geom, "a3", float(g["eps"]), far="direct",
+                             correction_cache=path)
+    assert op1.corrections_built_on == "device"
+    op2 = b.LayerOperatorSet(geom, "a3", float(g["eps"]), far="direct",
+                             correction_cache=path)
+    assert op2.corrections_built_on == "cache" and op2.t_q == 0.0
+    tau = np.asarray(g["tau"])
+    assert np.array_equal(op1.apply(tau), op2.apply(tau))
+    # another eps is a key miss: rebuilt, entry overwritten
+    op3 = b.LayerOperatorSet(geom, "a3", 1e-8, far="direct", correction_cache=path)
+    assert op3.corrections_built_on == "device"
