@@ -271,7 +271,9 @@ def main():
         _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
                                     _lib.ptr(hdev), st))
 
-    launches_per_step = 7 + 1  # apply: 7 kernels; MGS: one single-CTA kernel (n <= 12288)
+    # apply: 2 x (oversample, far sweep, CSR+epilogue) [+ add_scalar unless the
+    # second sweep is fused]; MGS: one single-CTA kernel (n <= 12288)
+    launches_per_step = (6 if op.dev.keep.get("phi_eta") is not None else 7) + 1
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
 
     # parity spot check against the reference's own A3 apply
@@ -310,7 +312,7 @@ def main():
         t_step = float(tt.item())
     value = inter / t_step  # one apply per step, shared by all ranks (strong scaling)
 
-    # dominant kernel: far sweep 2 (opfar_kernel<FarA3b>), timed alone
+    # dominant kernel: far sweep 2, timed alone
     from paper_2111_10743_b200.operators import _bind_opset  # noqa: F401
     far_t = far2_time(torch, op, tau, lib, _lib)
     nloc = op.dev.nrows if world > 1 else n
@@ -334,19 +336,25 @@ def main():
         e2e_t = float(tt.item())
 
     peak = fp64_peak_tflops(torch, lib, _lib)
-    traffic = None  # dram read+write bytes per launch of the dominant kernel (ncu --set full)
+    # dominant kernel: the second far sweep.  Fused A3 (exact sweeps + Phi):
+    # opfar_kernel<FarA3c>, 39 algorithmic flop per pair; otherwise
+    # opfar_kernel<FarA3b>, 44 (DESIGN.md §3 tables)
+    fused = op.dev.keep.get("phi_eta") is not None
+    kname = "FarA3c" if fused else "FarA3b"
+    flops_pair = 39.0 if fused else 44.0
+    traffic = None  # dram read+write bytes per launch of that kernel (ncu --set full)
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "round1",
                                            "ncu_full_config2_far_csr.json")))
         for k in prof:
-            if "FarA3b" in k["kernel"]:
+            if kname in k["kernel"]:
                 tb = [float(k[m].split()[0]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
                                                 "Gbyte": 1e9}[k[m].split()[1]]
                       for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")]
                 traffic = sum(tb)
     except (OSError, KeyError, ValueError):
         pass
-    far_flops = 44.0 * nloc * nover  # algorithmic flops of FarA3b per launch
+    far_flops = flops_pair * nloc * nover  # algorithmic flops per launch
     achieved = far_flops / far_t / 1e12
 
     cpu = None
@@ -370,12 +378,12 @@ def main():
                        "parallelism": f"target-shard{world}" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MB write)",
                        "apply_parity_vs_reference": parity},
-            "roofline": {"bound": "fp64", "kernel": "opfar_kernel<FarA3b>",
+            "roofline": {"bound": "fp64", "kernel": f"opfar_kernel<{kname}>",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak,
                          "peak_source": "measured in-run (lb_probe_dfma); nominal "
                                         f"{NOMINAL_FP64_TFLOPS}",
-                         "far2_ms": far_t * 1e3, "flops_per_pair": 44,
+                         "far2_ms": far_t * 1e3, "flops_per_pair": flops_pair,
                          "traffic": traffic,
                          "traffic_note": "bytes/launch from profiles/round1 ncu --set full: "
                                          "the kernel is FP64-bound, DRAM traffic is the "
@@ -393,7 +401,7 @@ def main():
 
 def far2_time(torch, op, tau, lib, _lib, which=2, reps=20):
     """Average device duration of one far sweep (default: A3 call 2,
-    opfar_kernel<FarA3b>) timed with CUDA events on its launching stream
+    FarA3c when fused, else FarA3b) timed with CUDA events on its launching stream
     (lb_opset_time_far); the packed sources are the last apply's."""
     import ctypes
     op.apply_device(tau)

@@ -132,6 +132,15 @@ typedef struct lb_opset lb_opset;
 int lb_opset_create(const lb_opset_desc* desc, lb_opset** out);
 int lb_opset_destroy(lb_opset* h);
 int lb_opset_set_phi0(lb_opset* h, const double* phi0);
+/* Phi = S^T w (device, n doubles, global rows; NULL detaches): the exact S
+ * operator's transpose applied to the node weights, so that the A3 W-average
+ * <w, S mu2> / sum(w) (operators.py:261) equals <Phi, mu2> / sum(w) with
+ * mu2 = S tau known after the first pass.  With it attached (and no FMM plan)
+ * apply_a3's second far sweep accumulates sp_mu1 - sppdp_mu2 - 2H sp_mu2 as
+ * ONE sum (no S[mu2] far sum, no S-kind read in the second SpMV pass) and the
+ * scalar all-reduce of a sharded apply moves from phase 1 to phase 0
+ * (lb_opset_phase_exchange reports it).  The pointer must outlive its use. */
+int lb_opset_set_eta_weights(lb_opset* h, const double* phi);
 /* Route every far-field call of the handle through an FMM plan built on
  * (over_nodes, nodes) (the reference's use_fmm=True path, operators.py:104-112)
  * instead of the exact all-pairs sweeps; NULL restores the sweeps.  The plan

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "lb_common.cuh"
 
@@ -12,6 +13,23 @@ constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
 
 struct Tgt {
   double x, y, z, nx, ny, nz;
+  double n3x, n3y, n3z, h;  // n/3 and -2H/3 (FarA3c only; dead elsewhere)
+};
+
+// Functors accumulate NACC values per target (default NOUT) and may project
+// them onto the NOUT written outputs once per tile (finish(), reading the
+// target normal from global memory then instead of holding it in registers).
+template <class F, class = void>
+struct FarTraits {
+  static constexpr int NACC = F::NOUT;
+  static constexpr bool PROJ = false;
+  static constexpr bool TC = false;
+};
+template <class F>
+struct FarTraits<F, std::void_t<decltype(F::NACC)>> {
+  static constexpr int NACC = F::NACC;
+  static constexpr bool PROJ = true;
+  static constexpr bool TC = F::TC;
 };
 
 // ---------------------------------------------------------------------------
@@ -34,17 +52,25 @@ struct FarS {
 };
 
 // A3 call 1 (operators.py:237): charge c, pot + n_t.grad.
-//   a0 += c/r ; a1 += c (n_t.r)/r^3   (n_t.grad = -a1)        record [x y z c]
+//   a0 += c/r ; a1..3 += c r/r^3, projected once per tile: out1 = n_t.a1..3
+//   (n_t.grad = -out1).  Accumulating the vector (3 FMA) instead of n_t.r per
+//   pair (3 ops + 1 FMA) saves one FP64 op per pair and keeps the normal out
+//   of the registers.                                          record [x y z c]
 struct FarA3a {
-  static constexpr int S = 4, NOUT = 2;
-  static constexpr bool TN = true;
+  static constexpr int S = 4, NOUT = 2, NACC = 4;
+  static constexpr bool TN = false, TC = false;
   __device__ static void pair(const Tgt& t, const double* s, double* a) {
     LB_GEOM
     const double ci = s[3] * invr;
     const double ci3 = ci * (invr * invr);
     a[0] += ci;
-    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
-    a[1] = fma(ci3, rnt, a[1]);
+    a[1] = fma(ci3, r0, a[1]);
+    a[2] = fma(ci3, r1, a[2]);
+    a[3] = fma(ci3, r2, a[3]);
+  }
+  __device__ static void finish(const double* nrm, const double* a, double* o) {
+    o[0] = a[0];
+    o[1] = fma(nrm[2], a[3], fma(nrm[1], a[2], nrm[0] * a[1]));
   }
 };
 
@@ -81,6 +107,34 @@ struct FarA3b {
     a[2] = fma(s[7], g, a[2]);
     a[3] = fma(s[7] * invr3, kspp, a[3]);
   }
+};
+
+// A3 call 2 fused with its glue (operators.py:247-263, eta aside): the far
+// part of  sp_mu1 - sppdp_mu2 - 2H sp_mu2  as ONE accumulator
+//   a0 += r^-3 [ (n_t.r)(c0 - 2H c1) + c1 Kspp ],  result_far = -a0 / 4pi
+// with Kspp = 3 (n_t.r)(dn.r)/r^2 - n_t.dn.  The factor 3 is folded into the
+// record (slot 7 holds 3 c1, written by the oversample) and the target
+// (n_t/3, -2H/3), so  Kspp/3 = (n_t.r)(dn.r)/r^2 - (n_t/3).dn:
+// 31 FP64 ops per pair (FarA3b: 34) and one output instead of four; S[mu2]
+// for the W-average comes from eta = <Phi, mu2> (Phi = S^T w, precomputed).
+//   record [x y z nx ny nz c0 3c1]
+struct FarA3c {
+  static constexpr int S = 8, NOUT = 1, NACC = 1;
+  static constexpr bool TN = true, TC = true;
+  __device__ static void pair(const Tgt& t, const double* s, double* a) {
+    LB_GEOM
+    const double invr2 = invr * invr;
+    const double invr3 = invr * invr2;
+    const double dn0 = t.nx - s[3], dn1 = t.ny - s[4], dn2 = t.nz - s[5];
+    const double rnt = fma(t.nz, r2, fma(t.ny, r1, t.nx * r0));
+    const double rdn = fma(dn2, r2, fma(dn1, r1, dn0 * r0));
+    const double ndn3 = fma(t.n3z, dn2, fma(t.n3y, dn1, t.n3x * dn0));
+    const double c0p = fma(t.h, s[7], s[6]);              // c0 - 2H c1
+    const double k3 = fma(rnt * rdn, invr2, -ndn3);       // Kspp / 3
+    const double inner = fma(rnt, c0p, s[7] * k3);
+    a[0] = fma(invr3, inner, a[0]);
+  }
+  __device__ static void finish(const double*, const double* a, double* o) { o[0] = a[0]; }
 };
 
 // A2 call 1 (operators.py:200-212): charge c and dipole c n_s (c = w tau).
@@ -206,9 +260,12 @@ template <class F, int TPT, int BT, int TS, bool PF = true, int UR = 4, int MINB
 __global__ void __launch_bounds__(BT, MINB) opfar_kernel(const double* __restrict__ nodes,
                                                    const double* __restrict__ normals, int64_t n,
                                                    const double* __restrict__ pack, SkLayout L,
-                                                   double* __restrict__ part) {
+                                                   double* __restrict__ part,
+                                                   const double* __restrict__ curv = nullptr) {
+  using Tr = FarTraits<F>;
   constexpr int S = F::S;
   constexpr int NO = F::NOUT;
+  constexpr int NA = Tr::NACC;
   __shared__ __align__(16) double sh[TS * S];
   const int64_t b = blockIdx.x;
   int64_t u = b * L.U / L.G;
@@ -218,7 +275,7 @@ __global__ void __launch_bounds__(BT, MINB) opfar_kernel(const double* __restric
     const int64_t c0 = u - t * L.C;
     const int64_t c1 = min(L.C, c0 + (u_end - u));
     Tgt tg[TPT];
-    double acc[TPT][NO];
+    double acc[TPT][NA];
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
       const int64_t i = t * (BT * TPT) + (int64_t)j * BT + threadIdx.x;
@@ -233,8 +290,14 @@ __global__ void __launch_bounds__(BT, MINB) opfar_kernel(const double* __restric
       } else {
         tg[j].nx = tg[j].ny = tg[j].nz = 0.0;
       }
+      if (Tr::TC) {
+        tg[j].n3x = tg[j].nx * (1.0 / 3.0);
+        tg[j].n3y = tg[j].ny * (1.0 / 3.0);
+        tg[j].n3z = tg[j].nz * (1.0 / 3.0);
+        tg[j].h = in ? curv[i] * (-2.0 / 3.0) : 0.0;
+      }
 #pragma unroll
-      for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
+      for (int o = 0; o < NA; ++o) acc[j][o] = 0.0;
     }
     // the next source tile is prefetched into registers while the current
     // one is consumed from shared memory (hides the L2 latency behind fp64
@@ -281,8 +344,16 @@ __global__ void __launch_bounds__(BT, MINB) opfar_kernel(const double* __restric
     const int64_t k = b - L.bfirst(t);
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
+      double out[NO];
+      if constexpr (Tr::PROJ) {
+        const int64_t i = min(n - 1, t * (BT * TPT) + (int64_t)j * BT + threadIdx.x);
+        F::finish(normals + 3 * i, acc[j], out);
+      } else {
 #pragma unroll
-      for (int o = 0; o < NO; ++o) part[L.idx(t, k, o, NO, j * BT + threadIdx.x)] = acc[j][o];
+        for (int o = 0; o < NO; ++o) out[o] = acc[j][o];
+      }
+#pragma unroll
+      for (int o = 0; o < NO; ++o) part[L.idx(t, k, o, NO, j * BT + threadIdx.x)] = out[o];
     }
     u += c1 - c0;
   }

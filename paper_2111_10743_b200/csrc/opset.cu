@@ -36,6 +36,7 @@ namespace lb {
 struct OvsArgs {
   const double* in[3];
   int slot[3];
+  double scale[3];  // per-input factor folded into the record (FarA3c: 3 c1)
   int nv;
   double* in0_add_target;  // == in[0] when the scalar must be added, else null
   const double* add_scalar;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(128) oversample_kernel(OvsArgs a) {
     for (int v = 0; v < a.nv; ++v) {
       double s = 0.0;
       for (int b = 0; b < nb; ++b) s = fma(__ldg(row + b), sv[v * nb + b], s);
-      a.pack[gi * a.S + a.slot[v]] = w * s;
+      a.pack[gi * a.S + a.slot[v]] = (w * a.scale[v]) * s;
     }
   }
 }
@@ -120,6 +121,11 @@ struct MixA3p2 {  // [S' mu1, S mu2, S' mu2, (S''+D') mu2]; vals {S', S, S''+D'}
   __host__ __device__ static constexpr int vi(int j) { return j == 0 ? 0 : (j == 1 ? 1 : (j == 2 ? 0 : 2)); }
   __host__ __device__ static constexpr int xi(int j) { return j == 0 ? 0 : 1; }
 };
+struct MixA3p2F {  // [S' mu1, S' mu2, (S''+D') mu2]; vals {S', S''+D'}, xs {mu1, mu2}
+  static constexpr int K = 2, X = 2;
+  __host__ __device__ static constexpr int vi(int j) { return j == 2 ? 1 : 0; }
+  __host__ __device__ static constexpr int xi(int j) { return j == 0 ? 0 : 1; }
+};
 
 constexpr int kCsrBT = 256;
 constexpr int kCsrRows = 8;  // rows per block: one warp per row (power of 2)
@@ -168,6 +174,33 @@ struct EpiA3p1 : EpiBase {
   __device__ double operator()(int64_t i, const double* acc) const {
     s_tau[i] = fma(f(0, i), kInv4Pi, acc[0]);
     sp_tau[i] = fma(-f(1, i), kInv4Pi, acc[1]);
+    return 0.0;
+  }
+};
+
+// A3 pass 1 with the W-average folded in: eta = <Phi, s_tau> / sum(w), where
+// Phi = S^T w (lb_opset_set_eta_weights) so that <w, S mu2> = <Phi, mu2> and
+// mu2 = s_tau is known here, one pass before the reference forms s_mu2
+struct EpiA3p1R : EpiA3p1 {
+  static constexpr bool kReduce = true;
+  const double* phi;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double s = fma(f(0, i), kInv4Pi, acc[0]);
+    s_tau[i] = s;
+    sp_tau[i] = fma(-f(1, i), kInv4Pi, acc[1]);
+    return phi[i] * s;
+  }
+};
+
+// A3 pass 2 after the fused sweep (FarA3c): one far output, eta already
+// reduced by pass 1 (scal[0]); corrections [S' mu1, S' mu2, (S''+D') mu2]
+struct EpiA3p2F : EpiBase {
+  static constexpr bool kReduce = false;
+  const double *tau, *curv, *eta;
+  double* result;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double corr = fma(-2.0 * curv[i], acc[1], acc[0] - acc[2]);
+    result[i] = fma(-f(0, i), kInv4Pi, fma(tau[i], -0.25, corr)) + eta[0];
     return 0.0;
   }
 };
@@ -395,6 +428,7 @@ struct lb_opset {
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   double* scal = nullptr;  // [0] W-average / eta
+  const double* phi_eta = nullptr;  // Phi = S^T w (global rows): fused A3 pass 2
   int csr_blocks = 0;
   int csr_wpr = 1;
   // optional FMM far field (lb_opset_set_fmm) and its scratch
@@ -452,18 +486,20 @@ int run_far(const lb_opset* h, const double* pack, SkLayout* out, cudaStream_t s
   if (L.tiles * L.kmax * F::NOUT * L.tt > h->part_cap)
     return fail(LB_ERR_ARG, "opset: partial buffer too small");
   opfar_kernel<F, TPT, kFarBT, far_ts<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(
-      h->d.nodes + 3 * h->r0, h->d.normals + 3 * h->r0, h->nr, pack, L, h->part);
+      h->d.nodes + 3 * h->r0, h->d.normals + 3 * h->r0, h->nr, pack, L, h->part,
+      h->d.curvature ? h->d.curvature + h->r0 : nullptr);
   LB_CHECK_LAUNCH();
   *out = L;
   return LB_OK;
 }
 
 int oversample(const lb_opset* h, int nv, const double* const* in, const int* slot, double* pack,
-               int S, bool add_ws, cudaStream_t st) {
+               int S, bool add_ws, cudaStream_t st, const double* scale = nullptr) {
   OvsArgs a{};
   for (int v = 0; v < nv; ++v) {
     a.in[v] = in[v];
     a.slot[v] = slot[v];
+    a.scale[v] = scale ? scale[v] : 1.0;
   }
   a.nv = nv;
   a.in0_add_target = add_ws ? const_cast<double*>(in[0]) : nullptr;
@@ -515,18 +551,20 @@ double* V(const lb_opset* h, int k) { return h->vec + (int64_t)k * h->d.n; }
 // projection to the same per-target outputs), returning the partial layout
 // the CSR epilogue reads.
 
-enum FarKind { FK_S, FK_A3A, FK_A3B, FK_A2A, FK_A2B, FK_A1A, FK_A1B, FK_D };
+enum FarKind { FK_S, FK_A3A, FK_A3B, FK_A2A, FK_A2B, FK_A1A, FK_A1B, FK_D, FK_A3C };
 
 struct FarSpec {
   double* pack;
   int S;
   int slot[3];
+  double scale[3] = {1.0, 1.0, 1.0};
 };
 
 FarSpec far_spec(lb_opset* h, FarKind k) {
   switch (k) {
     case FK_S: case FK_A3A: case FK_A1A: return {h->pack4, 4, {3, 0, 0}};
     case FK_A3B: return {h->pack8, 8, {6, 7, 0}};
+    case FK_A3C: return {h->pack8, 8, {6, 7, 0}, {1.0, 3.0, 1.0}};
     case FK_A2A: case FK_D: return {h->pack8, 8, {6, 0, 0}};
     case FK_A2B: return {h->pack8, 8, {7, 6, 0}};
     default: return {h->pack6, 6, {3, 4, 5}};  // FK_A1B
@@ -535,7 +573,7 @@ FarSpec far_spec(lb_opset* h, FarKind k) {
 
 int far_nout(FarKind k) {
   switch (k) {
-    case FK_S: case FK_A1B: case FK_D: return 1;
+    case FK_S: case FK_A1B: case FK_D: case FK_A3C: return 1;
     case FK_A3A: case FK_A2B: return 2;
     default: return 4;
   }
@@ -590,11 +628,12 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
               cudaStream_t st) {
   if (!h->fmm) {
     const FarSpec sp = far_spec(h, kind);
-    LB_TRY(oversample(h, nv, in, sp.slot, sp.pack, sp.S, add_ws, st));
+    LB_TRY(oversample(h, nv, in, sp.slot, sp.pack, sp.S, add_ws, st, sp.scale));
     switch (kind) {
       case FK_S: return run_far<FarS>(h, sp.pack, L, st);
       case FK_A3A: return run_far<FarA3a>(h, sp.pack, L, st);
       case FK_A3B: return run_far<FarA3b>(h, sp.pack, L, st);
+      case FK_A3C: return run_far<FarA3c>(h, sp.pack, L, st);
       case FK_A2A: return run_far<FarA2a>(h, sp.pack, L, st);
       case FK_A2B: return run_far<FarA2b>(h, sp.pack, L, st);
       case FK_A1A: return run_far<FarA1a>(h, sp.pack, L, st);
@@ -667,6 +706,13 @@ void tmark(lb_opset* h, cudaStream_t st) {
   if (h->timing && h->nev < 16) cudaEventRecord(h->ev[h->nev++], st);
 }
 
+// A3 with the fused second sweep (FarA3c + EpiA3p2F, eta from Phi in pass 1):
+// exact sweeps only (the FMM path projects its pot/grad/hess outputs onto the
+// reference's four quantities) and only once Phi = S^T w has been attached.
+bool a3_fused(const lb_opset* h) {
+  return h->phi_eta && !h->fmm && h->d.corr[LB_KIND_SPRIME] && h->d.corr[LB_KIND_SPP_PLUS_DPRIME];
+}
+
 int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out, cudaStream_t st) {
   const auto* C = h->d.corr;
   SkLayout L{};
@@ -675,17 +721,39 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
   if (form == 3) {
     double* s_tau = V(h, 0);
     double* sp_tau = V(h, 1);
+    const bool fused = a3_fused(h);
     if (phase == 0) {
       const double* in1[1] = {tau};
       LB_TRY(far_stage(h, FK_A3A, 1, in1, false, &L, st));
       tmark(h, st);
+      const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
+      const double* xs[2] = {tau, tau};
+      if (fused) {
+        auto e = base_epi<EpiA3p1R>(h, L, 2);
+        e.s_tau = s_tau;
+        e.sp_tau = sp_tau;
+        e.phi = h->phi_eta + h->r0;
+        return run_csr<2, EpiA3p1R>(h, vals, xs, e, st, h->wsum);
+      }
       auto e = base_epi<EpiA3p1>(h, L, 2);
       e.s_tau = s_tau;
       e.sp_tau = sp_tau;
-      const double* vals[2] = {C[LB_KIND_S], C[LB_KIND_SPRIME]};
-      const double* xs[2] = {tau, tau};
       return run_csr<2, EpiA3p1>(h, vals, xs, e, st);  // MixOneX<2> measured slower (1.39 vs 1.19 ms, config 3)
     }
+    if (phase == 1 && fused) {
+      const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
+      LB_TRY(far_stage(h, FK_A3C, 2, in2, false, &L, st));
+      tmark(h, st);
+      auto e = base_epi<EpiA3p2F>(h, L, 1);
+      e.tau = tau;
+      e.curv = h->d.curvature;
+      e.eta = h->scal;
+      e.result = out;
+      const double* vals[3] = {C[LB_KIND_SPRIME], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+      const double* xs[3] = {sp_tau, s_tau, s_tau};
+      return run_csr<3, EpiA3p2F, MixA3p2F>(h, vals, xs, e, st);
+    }
+    if (phase == 2 && fused) return LB_OK;  // eta added by the pass-2 epilogue
     if (phase == 1) {
       const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
       LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L, st));
@@ -821,6 +889,7 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   cap = std::max(cap, far_part_size<FarS>(h));
   cap = std::max(cap, far_part_size<FarA3a>(h));
   cap = std::max(cap, far_part_size<FarA3b>(h));
+  cap = std::max(cap, far_part_size<FarA3c>(h));
   cap = std::max(cap, far_part_size<FarA2a>(h));
   cap = std::max(cap, far_part_size<FarA2b>(h));
   cap = std::max(cap, far_part_size<FarD>(h));
@@ -924,6 +993,12 @@ int lb_opset_set_phi0(lb_opset* h, const double* phi0) {
   return LB_OK;
 }
 
+int lb_opset_set_eta_weights(lb_opset* h, const double* phi) {
+  if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_eta_weights: null handle");
+  h->phi_eta = phi;
+  return LB_OK;
+}
+
 int lb_opset_set_timing(lb_opset* h, int on) {
   if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_timing: null handle");
   if (on && !h->ev[0])
@@ -979,8 +1054,9 @@ int lb_opset_phase_exchange(const lb_opset* h, int formulation, int phase, int* 
   *nvec = 0;
   *reduce_scalar = 0;
   if (formulation == 3) {
-    if (phase == 0) { *nvec = 2; vecs[0] = 0; vecs[1] = 1; }
-    else if (phase == 1) *reduce_scalar = 1;
+    // fused A3: eta is reduced by pass 1 (phase 0) and consumed by pass 2
+    if (phase == 0) { *nvec = 2; vecs[0] = 0; vecs[1] = 1; *reduce_scalar = a3_fused(h) ? 1 : 0; }
+    else if (phase == 1) *reduce_scalar = a3_fused(h) ? 0 : 1;
   } else if (phase == 0) {
     *nvec = formulation == 2 ? 2 : 3;
     for (int k = 0; k < *nvec; ++k) vecs[k] = k;
@@ -1026,7 +1102,11 @@ int lb_opset_time_far(lb_opset* h, int which, int reps, double* seconds_host, vo
     switch (which) {
       case 0: rc = run_far<FarS>(h, h->pack4, &ns, st); break;
       case 1: rc = run_far<FarA3a>(h, h->pack4, &ns, st); break;
-      case 2: rc = run_far<FarA3b>(h, h->pack8, &ns, st); break;
+      case 2:
+        rc = a3_fused(h) ? run_far<FarA3c>(h, h->pack8, &ns, st) : run_far<FarA3b>(h, h->pack8, &ns, st);
+        break;
+      case 8: rc = run_far<FarA3b>(h, h->pack8, &ns, st); break;
+      case 9: rc = run_far<FarA3c>(h, h->pack8, &ns, st); break;
       case 3: rc = run_far<FarA2a>(h, h->pack8, &ns, st); break;
       case 4: rc = run_far<FarA2b>(h, h->pack8, &ns, st); break;
       case 5: rc = run_far<FarA1a>(h, h->pack4, &ns, st); break;

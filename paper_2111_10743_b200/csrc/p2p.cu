@@ -208,7 +208,7 @@ int run_direct_chunk(const double* tgt, int64_t nt, const double* src, int64_t n
   const SkLayout L = make_sk_layout(nt, ns_pad, BT * TPT, TS, (int64_t)sm_count() * per_sm);
   Scratch part;
   LB_TRY(part.alloc(sizeof(double) * L.tiles * L.kmax * NA * L.tt, st));
-  kern<<<(unsigned)L.G, BT, 0, st>>>(tgt, nullptr, nt, pack.as<double>(), L, part.as<double>());
+  kern<<<(unsigned)L.G, BT, 0, st>>>(tgt, nullptr, nt, pack.as<double>(), L, part.as<double>(), nullptr);
   LB_CHECK_LAUNCH();
   const int64_t nfin = (int64_t)NDC * nt;
   p2p_sk_finalize_kernel<<<(unsigned)ceil_div(nfin, 256), 256, 0, st>>>(

@@ -277,6 +277,7 @@ def _bind_opset():
         L.lb_opset_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(P)]
         L.lb_opset_destroy.argtypes = [P]
         L.lb_opset_set_phi0.argtypes = [P, P]
+        L.lb_opset_set_eta_weights.argtypes = [P, P]
         L.lb_opset_set_fmm.argtypes = [P, P]
         L.lb_opset_apply_phase.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
         L.lb_opset_phase_exchange.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
@@ -350,6 +351,13 @@ class DeviceOperator:
         _lib.check(self._L.lb_opset_set_fmm(
             self.handle, plan._h if plan is not None else ctypes.c_void_p(0)),
             "lb_opset_set_fmm")
+
+    def set_eta_weights(self, phi_dev):
+        """Attach Phi = S^T w (lb_opset_set_eta_weights; None detaches)."""
+        self.keep["phi_eta"] = phi_dev
+        _lib.check(self._L.lb_opset_set_eta_weights(
+            self.handle, ctypes.c_void_p(phi_dev.data_ptr() if phi_dev is not None else 0)),
+            "lb_opset_set_eta_weights")
 
     def set_phi0(self, phi0_dev):
         self.keep["phi0"] = phi0_dev
@@ -425,6 +433,31 @@ def _device_view(addr, shape, t):
     return t.as_tensor(_Cai(), device="cuda").view(*shape)
 
 
+def eta_weights(disc, corrections: CorrectionSet):
+    """Phi = S^T w: the transpose of the exact S operator (far sweep over the
+    oversampled rule + the S corrections) applied to the node weights, so the
+    A3 W-average <w, S mu2> / sum(w) (operators.py:261) is <Phi, mu2> / sum(w)
+    (lb_opset_set_eta_weights).  Far part: phi_s = sum_t w_t / |x_t - y_s|
+    (coincident pairs skipped, like the sweep) on the device P2P, pulled back
+    through w_over and the oversampling; correction part: C_S^T w (scipy CSC
+    matvec: fixed order, deterministic)."""
+    import scipy.sparse as sp
+    from .fmm import FmmSources, evaluate_direct
+    w = np.asarray(disc.weights, dtype=float)
+    n = w.shape[0]
+    oi = np.asarray(_over_interp(disc), dtype=float)  # (nbo, nb)
+    phi_over = evaluate_direct(FmmSources(np.asarray(disc.nodes), w[None]),
+                               np.asarray(disc.over_nodes), ("pot",)).pot[0]
+    pulled = ((np.asarray(disc.over_weights) * phi_over).reshape(-1, oi.shape[0]) @ oi).ravel()
+    vals = corrections.values[KernelKind.SINGLE_LAYER]
+
+    def host(a):
+        return a.cpu().numpy() if _lib.is_torch(a) else np.asarray(a)
+    C = sp.csr_matrix((host(vals), host(corrections.indices), host(corrections.indptr)),
+                      shape=(n, n))
+    return pulled / FOUR_PI + C.T @ w
+
+
 class LayerOperatorSet:
     """Corrections + geometry + far-field machinery for one formulation
     (operators.py:70-273), resident on the B200.
@@ -450,6 +483,10 @@ class LayerOperatorSet:
       fmm_m2l     : M2L arithmetic of that plan (FmmPlan.set_m2l): "auto"
                     (tcgen05 int8 slices sized from eps), "fp64" (DGEMM) or
                     a slice count in [3, 8].
+      fuse_a3     : A3 with exact sweeps runs its second sweep fused with the
+                    glue (one accumulator, eta from Phi = S^T w: eta_weights,
+                    lb_opset_set_eta_weights); False keeps the four-output
+                    sweep of the reference's quantities.
       correction_cache : path of an on-disk correction cache entry
                     (corrcache.py, keyed by mesh hash, kinds, eps, eta): a
                     device build is loaded from it on a key match and
@@ -461,7 +498,7 @@ class LayerOperatorSet:
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
                  corrections=None, far: str = "auto", fmm_ncrit: int = 120,
-                 fmm_m2l="auto", correction_cache=None):
+                 fmm_m2l="auto", correction_cache=None, fuse_a3: bool = True):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -518,6 +555,9 @@ class LayerOperatorSet:
             self.far = "fmm"
         else:
             self._plan = None
+        if self.formulation == "a3" and self.far == "direct" and fuse_a3:
+            # fused second A3 sweep (FarA3c): needs Phi = S^T w once
+            self.dev.set_eta_weights(_lib.to_device(eta_weights(disc, corrections)))
         self._n = n
         self._out = _lib.empty((n,))
         # S[1], stored once for the SWS term of A1 (operators.py:99-100)

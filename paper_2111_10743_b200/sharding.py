@@ -137,6 +137,10 @@ class ShardedOperatorSet:
             from .fmm_plan import FmmPlan
             self._plan = FmmPlan(disc.over_nodes, disc.nodes[r0:r0 + nr], self.eps)
             self.dev.set_fmm(self._plan)
+        elif self.formulation == "a3":
+            # fused second sweep; Phi is global (every rank computes it whole)
+            from .operators import eta_weights
+            self.dev.set_eta_weights(_lib.to_device(eta_weights(disc, corrections)))
         self.driver = ShardedApply(_DeviceBackend(self.dev), self.parts, rank,
                                    group)
         self.rank, self.world, self.n = rank, world, n

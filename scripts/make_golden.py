@@ -499,6 +499,17 @@ def config2(eps=1e-10):
     print("total", time.time() - t0)
 
 
+def config2_geom():
+    """tests/golden/config2_geom.npz (committed): data/config2.npz without the
+    corrections (the bench's fallback builds them on the device) but with the
+    reference's A3 apply of the seeded tau and its A3 solve, so the parity
+    spot checks stay reference-anchored."""
+    z = np.load(os.path.join(DATA, "config2.npz"))
+    keep = {k: z[k] for k in z.files if not k.startswith("corr_")
+            and not k.startswith("a2_")}
+    savez(os.path.join(GOLD, "config2_geom.npz"), **keep)
+
+
 def config3():
     """BASELINE config 3 geometry (build_torus(7, 64, 32, 2, 1): N = 114,688)
     and its near map (eta 2, cap raised to 256: the default 128 raises

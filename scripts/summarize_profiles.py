@@ -52,6 +52,26 @@ def step_summary():
     return L
 
 
+def bench_summary():
+    """The launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`
+    (the bench command itself), aggregated by kernel."""
+    L = launches(os.path.join(G, "launches_bench.csv"))
+    agg = defaultdict(lambda: [0, 0.0])
+    for nm, m in L:
+        agg[nm.replace("void ", "").strip()][0] += 1
+        agg[nm.replace("void ", "").strip()][1] += m["gpu__time_duration.sum"]
+    tot = sum(v[1] for v in agg.values())
+    lines = ["# `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`: ncu launch list",
+             "", "Every launch of the bench command (setup, parity apply, warm-up, timed "
+             "steps, the far-sweep timing reps, e2e steps, the DFMA peak probe), "
+             "aggregated by kernel; cold-cache and serialised (shares, not absolutes).", "",
+             "| kernel | launches | us | share |", "|---|---|---|---|"]
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| `{k}` | {c} | {t:.1f} | {100 * t / tot:.1f}% |")
+    lines.append(f"| total | {sum(v[0] for v in agg.values())} | {tot:.1f} | |")
+    open(os.path.join(OUT, "bench_launches.md"), "w").write("\n".join(lines) + "\n")
+
+
 def fmm_summary():
     L = launches(os.path.join(G, "launches_fmm.csv"))
     agg = defaultdict(lambda: [0, 0.0])
@@ -99,6 +119,8 @@ if __name__ == "__main__":
     what = sys.argv[1:] or ["step", "fmm", "full"]
     if "step" in what:
         step_summary()
+    if "bench" in what:
+        bench_summary()
     if "fmm" in what:
         fmm_summary()
     if "full" in what:

@@ -209,3 +209,28 @@ def test_two_far_calls_with_four_densities_through_the_seam(cuda):
             assert len(calls) == 2 and sum(calls) == 4, (form, far, calls)
             tol = 1e-10 if far == "direct" else 1e-7
             assert np.abs(got - fused).max() <= tol * np.abs(fused).max() + 2e-7 * (form != "a1"), (form, far)
+
+
+@pytest.mark.parametrize("fixture", ["opset_sphere_o3.npz", "opset_torus_o3.npz"])
+def test_a3_fused_matches_unfused(cuda, fixture):
+    """The fused second A3 sweep (FarA3c: one accumulator for
+    sp_mu1 - sppdp_mu2 - 2H sp_mu2, eta = <Phi, mu2> with Phi = S^T w) against
+    the four-output sweep of the reference's quantities (fuse_a3=False): the
+    same operator up to summation order."""
+    from paper_2111_10743_b200 import LayerOperatorSet
+    from paper_2111_10743_b200.operators import eta_weights
+    g = golden(fixture)
+    fused = LayerOperatorSet.from_bundle(g, "a3")
+    plain = LayerOperatorSet.from_bundle(g, "a3", fuse_a3=False)
+    assert fused.dev.keep.get("phi_eta") is not None
+    assert plain.dev.keep.get("phi_eta") is None
+    for seed in (0, 1):
+        tau = np.random.default_rng(seed).standard_normal(len(g["tau"]))
+        assert _rel(fused.apply(tau), plain.apply(tau)) < 1e-12
+    # Phi really is S^T w: <Phi, x> == <w, S x> for a random x
+    x = np.random.default_rng(5).standard_normal(len(g["tau"]))
+    from paper_2111_10743_b200 import KernelKind
+    phi = eta_weights(fused.disc, fused._cset)
+    sx = plain.apply_layer(KernelKind.SINGLE_LAYER, x)
+    lhs, rhs = np.dot(phi, x), np.dot(g["weights"], sx)
+    assert abs(lhs - rhs) <= 1e-12 * np.abs(phi).sum() * np.abs(x).max()

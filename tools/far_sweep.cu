@@ -27,10 +27,10 @@ void run(const char* name, const double* nodes, const double* normals, int64_t n
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int w = 0; w < 3; ++w) kern<<<(unsigned)L.G, BT>>>(nodes, normals, n, pack, L, part);
+  for (int w = 0; w < 3; ++w) kern<<<(unsigned)L.G, BT>>>(nodes, normals, n, pack, L, part, nodes);
   const int reps = 20;
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) kern<<<(unsigned)L.G, BT>>>(nodes, normals, n, pack, L, part);
+  for (int r = 0; r < reps; ++r) kern<<<(unsigned)L.G, BT>>>(nodes, normals, n, pack, L, part, nodes);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -79,6 +79,11 @@ int main(int argc, char** argv) {
     run<FarA1a, 3, 64, 128, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 4, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, true, 2, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 3, 64, 128, true, 2, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 4, 64, 128, true, 2, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 64, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, true, 1, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, false, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, false, 2, 12>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
@@ -87,6 +92,9 @@ int main(int argc, char** argv) {
     run<FarA3b, 1, 128, 128, false, 4, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 1, 256, 128, false, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3a, 4, 64, 64, true, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 4, 64, 128, true, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 2, 64, 128, true, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3a, 3, 64, 128, true, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3a, 4, 64, 64, true, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3a, 4, 64, 64, true, 1, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3a, 4, 64, 64, false, 2, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
