@@ -141,6 +141,11 @@ int lb_opset_set_phi0(lb_opset* h, const double* phi0);
  * scalar all-reduce of a sharded apply moves from phase 1 to phase 0
  * (lb_opset_phase_exchange reports it).  The pointer must outlive its use. */
 int lb_opset_set_eta_weights(lb_opset* h, const double* phi);
+/* FMM far field only: run apply_a3's second far call on two FMM densities
+ * (charge c0 with dipole -c1 n, and charge c1; default, 1) or on the
+ * reference's three (0: charges c0, c1 and dipole c1 n, operators.py:247-250).
+ * Both give the same operator; two densities cut M2L and leaf work by 1/3. */
+int lb_opset_set_fmm_a3(lb_opset* h, int two_densities);
 /* Route every far-field call of the handle through an FMM plan built on
  * (over_nodes, nodes) (the reference's use_fmm=True path, operators.py:104-112)
  * instead of the exact all-pairs sweeps; NULL restores the sweeps.  The plan

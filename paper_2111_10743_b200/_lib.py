@@ -47,6 +47,7 @@ SIGNATURES = {
     "lb_opset_destroy": [_P],
     "lb_opset_set_phi0": [_P, _P],
     "lb_opset_set_eta_weights": [_P, _P],
+    "lb_opset_set_fmm_a3": [_P, _I32],
     "lb_opset_set_fmm": [_P, _P],
     "lb_opset_apply_phase": [_P, _I32, _I32, _P, _P, _P],
     "lb_opset_phase_exchange": [_P, _I32, _I32, _P, _P, _P],

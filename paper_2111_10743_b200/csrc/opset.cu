@@ -205,6 +205,21 @@ struct EpiA3p2F : EpiBase {
   }
 };
 
+// A3 pass 2 after the two-density FMM call (FK_A3M): far outputs
+// [sp_mu1 - sppdp_mu2 - 2H sp_mu2 (x -4pi), S[mu2] far]; corrections as EpiA3p2
+// (MixA3p2); reduces w * s_mu2 (eta is added by phase 2)
+struct EpiA3p2M : EpiBase {
+  static constexpr bool kReduce = true;
+  const double *tau, *curv, *w;
+  double* result;
+  __device__ double operator()(int64_t i, const double* acc) const {
+    const double s_mu2 = fma(f(1, i), kInv4Pi, acc[1]);
+    const double corr = fma(-2.0 * curv[i], acc[2], acc[0] - acc[3]);
+    result[i] = fma(-f(0, i), kInv4Pi, fma(tau[i], -0.25, corr));
+    return w[i] * s_mu2;
+  }
+};
+
 // A3 pass 2 (operators.py:252-263) minus the eta term; reduces w * s_mu2
 struct EpiA3p2 : EpiBase {
   static constexpr bool kReduce = true;
@@ -429,6 +444,7 @@ struct lb_opset {
   unsigned* ticket = nullptr;
   double* scal = nullptr;  // [0] W-average / eta
   const double* phi_eta = nullptr;  // Phi = S^T w (global rows): fused A3 pass 2
+  bool fmm_a3_two = true;  // FMM path: A3's second call on 2 densities (lb_opset_set_fmm_a3)
   int csr_blocks = 0;
   int csr_wpr = 1;
   // optional FMM far field (lb_opset_set_fmm) and its scratch
@@ -551,7 +567,7 @@ double* V(const lb_opset* h, int k) { return h->vec + (int64_t)k * h->d.n; }
 // projection to the same per-target outputs), returning the partial layout
 // the CSR epilogue reads.
 
-enum FarKind { FK_S, FK_A3A, FK_A3B, FK_A2A, FK_A2B, FK_A1A, FK_A1B, FK_D, FK_A3C };
+enum FarKind { FK_S, FK_A3A, FK_A3B, FK_A2A, FK_A2B, FK_A1A, FK_A1B, FK_D, FK_A3C, FK_A3M };
 
 struct FarSpec {
   double* pack;
@@ -575,23 +591,25 @@ int far_nout(FarKind k) {
   switch (k) {
     case FK_S: case FK_A1B: case FK_D: case FK_A3C: return 1;
     case FK_A3A: case FK_A2B: return 2;
+    case FK_A3M: return 2;
     default: return 4;
   }
 }
 
-// c * n_over dipoles for FMM densities
+// sign * c * n_over dipoles for FMM densities
 __global__ void dipole_kernel(const double* __restrict__ c, const double* __restrict__ nrm, int64_t ns,
-                              double* __restrict__ out) {
+                              double* __restrict__ out, double sign = 1.0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
-  for (int k = 0; k < 3; ++k) out[3 * i + k] = c[i] * nrm[3 * i + k];
+  const double ci = sign * c[i];
+  for (int k = 0; k < 3; ++k) out[3 * i + k] = ci * nrm[3 * i + k];
 }
 
 // FMM outputs -> the functor outputs, written as a one-segment stream-K layout
 __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t n,
                                const double* __restrict__ pot, const double* __restrict__ grad,
                                const double* __restrict__ hess, SkLayout L, int nout,
-                               double* __restrict__ part) {
+                               double* __restrict__ part, const double* __restrict__ curv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double nx = nrm[3 * i], ny = nrm[3 * i + 1], nz = nrm[3 * i + 2];
@@ -609,6 +627,9 @@ __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t
     case FK_S: case FK_D: a[0] = pot[i]; break;
     case FK_A3A: a[0] = pot[i]; a[1] = -ng(0); break;
     case FK_A3B: a[0] = -ng(0); a[1] = pot[n + i]; a[2] = -ng(1); a[3] = nhn(1) + ng(2); break;
+    // fused A3 call 2 on two FMM densities: X = (charge c0, dipole -c1 n) and
+    // B = (charge c1): a0 = FarA3b's a0 + a3 - 2H a2 = -n.grad X + n.H_B.n + 2H n.grad B
+    case FK_A3M: a[0] = fma(2.0 * curv[i], ng(1), nhn(1) - ng(0)); a[1] = pot[n + i]; break;
     case FK_A2A: a[0] = pot[i]; a[1] = pot[n + i]; a[2] = -ng(0); a[3] = nhn(0) + ng(1); break;
     case FK_A2B: a[0] = pot[i]; a[1] = pot[n + i]; break;
     case FK_A1A:
@@ -665,6 +686,9 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
       LB_CUDA(cudaMemcpyAsync(ch + no, c1, sizeof(double) * no, cudaMemcpyDeviceToDevice, st));
       dipole_kernel<<<g, 256, 0, st>>>(c1, h->d.over_normals, no, dp + 2 * no * 3);
       nd = 3; cm = 3; dm = 4; level = 2; chp = ch; dpp = dp; break;
+    case FK_A3M:  // charges [c0, c1] (f_ch already holds them), dipoles [-c1 n, 0]
+      dipole_kernel<<<g, 256, 0, st>>>(c1, h->d.over_normals, no, dp, -1.0);
+      nd = 2; cm = 3; dm = 1; level = 2; chp = c0; dpp = dp; break;
     case FK_A2A:  // charge c0 on density 0, dipole c0 n on density 1
       dipole_kernel<<<g, 256, 0, st>>>(c0, h->d.over_normals, no, dp + no * 3);
       nd = 2; cm = 1; dm = 2; level = 2; chp = c0; dpp = dp; break;
@@ -690,7 +714,8 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
   l1.kmax = 1;
   const int nout = far_nout(kind);
   project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals + 3 * h->r0, n, h->f_pot,
-                                                             h->f_grad, h->f_hess, l1, nout, h->part);
+                                                             h->f_grad, h->f_hess, l1, nout, h->part,
+                                                             h->d.curvature + h->r0);
   LB_CHECK_LAUNCH();
   *L = l1;
   return LB_OK;
@@ -754,6 +779,21 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
       return run_csr<3, EpiA3p2F, MixA3p2F>(h, vals, xs, e, st);
     }
     if (phase == 2 && fused) return LB_OK;  // eta added by the pass-2 epilogue
+    if (phase == 1 && h->fmm && h->fmm_a3_two) {
+      // FMM far field: the second call on two densities (X = c0 - dipole c1 n,
+      // B = c1) instead of three, projected straight onto the fused sum
+      const double* in2[2] = {sp_tau, s_tau};
+      LB_TRY(far_stage(h, FK_A3M, 2, in2, false, &L, st));
+      tmark(h, st);
+      auto e = base_epi<EpiA3p2M>(h, L, 2);
+      e.tau = tau;
+      e.curv = h->d.curvature;
+      e.w = h->d.weights;
+      e.result = out;
+      const double* vals[4] = {C[LB_KIND_SPRIME], C[LB_KIND_S], C[LB_KIND_SPRIME], C[LB_KIND_SPP_PLUS_DPRIME]};
+      const double* xs[4] = {sp_tau, s_tau, s_tau, s_tau};
+      return run_csr<4, EpiA3p2M, MixA3p2>(h, vals, xs, e, st, h->wsum);
+    }
     if (phase == 1) {
       const double* in2[2] = {sp_tau, s_tau};  // mu1 = S' tau, mu2 = S tau
       LB_TRY(far_stage(h, FK_A3B, 2, in2, false, &L, st));
@@ -990,6 +1030,12 @@ int lb_opset_set_fmm(lb_opset* h, lb_fmm_plan* plan) {
 int lb_opset_set_phi0(lb_opset* h, const double* phi0) {
   if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_phi0: null handle");
   h->d.phi0 = phi0;
+  return LB_OK;
+}
+
+int lb_opset_set_fmm_a3(lb_opset* h, int two_densities) {
+  if (!h) return lb::fail(LB_ERR_ARG, "lb_opset_set_fmm_a3: null handle");
+  h->fmm_a3_two = two_densities != 0;
   return LB_OK;
 }
 

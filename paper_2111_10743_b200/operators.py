@@ -278,6 +278,7 @@ def _bind_opset():
         L.lb_opset_destroy.argtypes = [P]
         L.lb_opset_set_phi0.argtypes = [P, P]
         L.lb_opset_set_eta_weights.argtypes = [P, P]
+        L.lb_opset_set_fmm_a3.argtypes = [P, ctypes.c_int]
         L.lb_opset_set_fmm.argtypes = [P, P]
         L.lb_opset_apply_phase.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
         L.lb_opset_phase_exchange.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
@@ -358,6 +359,12 @@ class DeviceOperator:
         _lib.check(self._L.lb_opset_set_eta_weights(
             self.handle, ctypes.c_void_p(phi_dev.data_ptr() if phi_dev is not None else 0)),
             "lb_opset_set_eta_weights")
+
+    def set_fmm_a3(self, two_densities: bool):
+        """FMM path: A3's second call on 2 densities (default) or the
+        reference's 3 (lb_opset_set_fmm_a3)."""
+        _lib.check(self._L.lb_opset_set_fmm_a3(self.handle, int(bool(two_densities))),
+                   "lb_opset_set_fmm_a3")
 
     def set_phi0(self, phi0_dev):
         self.keep["phi0"] = phi0_dev

@@ -234,3 +234,22 @@ def test_a3_fused_matches_unfused(cuda, fixture):
     sx = plain.apply_layer(KernelKind.SINGLE_LAYER, x)
     lhs, rhs = np.dot(phi, x), np.dot(g["weights"], sx)
     assert abs(lhs - rhs) <= 1e-12 * np.abs(phi).sum() * np.abs(x).max()
+
+
+@pytest.mark.parametrize("fixture", ["opset_sphere_o3.npz", "opset_torus_o3.npz"])
+def test_a3_fmm_two_densities(cuda, fixture):
+    """FMM far field: A3's second call on two densities (X = charge c0 with
+    dipole -c1 n, B = charge c1; lb_opset_set_fmm_a3(1), the default) against
+    the reference's three (lb_opset_set_fmm_a3(0)) and against the exact
+    sweeps: the same operator within the FMM's requested precision."""
+    from paper_2111_10743_b200 import LayerOperatorSet
+    g = golden(fixture)
+    tau = np.asarray(g["tau"])
+    exact = LayerOperatorSet.from_bundle(g, "a3", far="direct").apply(tau)
+    op = LayerOperatorSet.from_bundle(g, "a3", eps=1e-10, far="fmm")
+    two = op.apply(tau)
+    op.dev.set_fmm_a3(False)
+    three = op.apply(tau)
+    assert _rel(two, three) < 1e-8
+    assert _rel(two, exact) < 1e-8
+    assert _rel(three, exact) < 1e-8
