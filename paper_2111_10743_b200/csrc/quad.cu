@@ -399,7 +399,11 @@ __global__ void __launch_bounds__(kQuadThreads, 2) quad_pairs_kernel(QuadArgs A)
       if (self && any_grad) koornwinder_km<ORDER>(A.node_uv[2 * t], A.node_uv[2 * t + 1], sm.norm, sm.psi0);
     }
     __syncthreads();
-    eval_leaves<ORDER>(A, sm, 0, nroot, self, self, x, nx);
+    // in batches of LB leaves (orders 8-9 hold 2 leaves' basis tables, a
+    // self pair has 3 Duffy roots)
+    for (int c0 = 0; c0 < nroot; c0 += Sh::LB) {
+      eval_leaves<ORDER>(A, sm, c0, min(Sh::LB, nroot - c0), self, self, x, nx);
+    }
     // push the roots (reverse order: the first root is refined first)
     int sp = 0;
     for (int r = nroot - 1; r >= 0; --r) {

@@ -1,10 +1,12 @@
 """GMRES operator-apply time vs N (the second half of the BASELINE metric).
 
   config 2: icosphere order 7, N = 8,960 (reference-built corrections);
-  config 3: torus build_torus(7, 64, 32, 2, 1), N = 114,688, the reference's
-            near map (eta 2, cap 256) as the CSR pattern with SYNTHETIC values
-            (the reference's correction build takes hours at this size), so
-            this case times the apply only (no solve, no parity).
+  config 3: torus build_torus(7, 64, 32, 2, 1), N = 114,688: corrections
+            built on the device (quadrature.build_correction_set, eps 5e-8;
+            the reference's own build takes hours at this size), or with
+            --synthetic SYNTHETIC values on the reference's near-map pattern
+            (eta 2, cap 256): apply timing only;
+  config 4: wavy torus, N = 1,202,940 (same two options; eps 1e-9).
 Far field exact (all-pairs) and through the device FMM.  A3 formulation.
 Prints JSON lines with the stage split (far 1, SpMV 1, far 2, SpMV 2 + glue)
 and the SpMV passes' achieved HBM bandwidth.
@@ -61,13 +63,16 @@ def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120, m2l="auto")
     op.apply_device(tau, out)
     st = op.dev.stage_times()
     nnz = int(cset.indices.shape[0])
+    fused = op.dev.keep.get("phi_eta") is not None  # pass 2 reads 2 kinds, else 3
     b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
-    b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
+    b2 = nnz * ((2 if fused else 3) * 8 + 4) + 8 * (n + 1)
     slices = op._plan.m2l_slices if op.far == "fmm" else None
-    print(json.dumps({"case": name, "far": op.far, "eps": eps, "fmm_ncrit": ncrit,
+    print(json.dumps({"case": name, "far": op.far, "fused_a3": fused, "eps": eps,
+                      "fmm_ncrit": ncrit,
                       "m2l_slices": slices, "N": n,
                       "N_over": geom.noversampled, "nnz_per_kind": nnz,
-                      "synthetic_corrections": synthetic, "apply_ms": best,
+                      "synthetic_corrections": synthetic, "build": BUILD.get(name),
+                      "apply_ms": best,
                       "stages_ms": {"far1": st[0], "spmv1": st[1], "far2": st[2],
                                     "spmv2+glue": st[3], "eta": st[4]},
                       "spmv1_GBps": b1 / (st[1] * 1e-3) / 1e9,
@@ -78,8 +83,39 @@ def run(name, g, cset, eps, far, reps=5, synthetic=False, ncrit=120, m2l="auto")
     torch.cuda.empty_cache()
 
 
+BUILD = {}
+
+
+def corrections(name, g, eps, synthetic, seed):
+    if synthetic:
+        indptr, idx = pattern_from_near(g)
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        vals = {k: 1e-4 * torch.randn(idx.numel(), dtype=torch.float64, device="cuda",
+                                      generator=gen)
+                for k in ("s", "sprime", "spp_plus_dprime")}
+        return CorrectionSet(indptr, idx, vals)
+    import time
+    from paper_2111_10743_b200 import FORMULATIONS
+    from paper_2111_10743_b200.quadrature import LAST_BUILD, build_correction_set, build_near_map
+    geom = Geometry.from_arrays(g)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    near = build_near_map(geom, 2.0, cap=256)
+    torch.cuda.synchronize()
+    t_near = time.perf_counter() - t0
+    same = bool(np.array_equal(near.offsets, g["near_offsets"])
+                and np.array_equal(near.patches, g["near_patches"]))
+    cset, t_q = build_correction_set(geom, near, list(FORMULATIONS["a3"]), eps)
+    BUILD[name] = {"eps": eps, "t_near_s": t_near, "near_equal_reference": same,
+                   "t_q_s": t_q, "split": dict(LAST_BUILD)}
+    print(json.dumps({"case": name, "build": BUILD[name]}), flush=True)
+    return cset
+
+
 if __name__ == "__main__":
-    only = sys.argv[1:]
+    args = sys.argv[1:]
+    synthetic = "--synthetic" in args
+    only = [a for a in args if not a.startswith("--")]
     c2 = os.path.join(ROOT, "data", "config2.npz")
     if os.path.exists(c2) and (not only or "config2" in only):
         g = dict(np.load(c2))
@@ -89,29 +125,16 @@ if __name__ == "__main__":
     c3 = os.path.join(ROOT, "data", "config3_geom.npz")
     if os.path.exists(c3) and (not only or "config3" in only):
         g = dict(np.load(c3))
-        indptr, idx = pattern_from_near(g)
-        gen = torch.Generator(device="cuda").manual_seed(3)
-        vals = {k: 1e-4 * torch.randn(idx.numel(), dtype=torch.float64, device="cuda",
-                                      generator=gen)
-                for k in ("s", "sprime", "spp_plus_dprime")}
-        cset = CorrectionSet(indptr, idx, vals)
-        run("config3", g, cset, 5e-8, "fmm", synthetic=True)
-        run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300, m2l="fp64")
-        run("config3", g, cset, 5e-8, "fmm", synthetic=True, ncrit=300)
-        run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300, m2l="fp64")
-        run("config3", g, cset, 1e-9, "fmm", synthetic=True, ncrit=300)
-        run("config3", g, cset, 5e-8, "direct", reps=2, synthetic=True)
+        cset = corrections("config3", g, 5e-8, synthetic, 3)
+        run("config3", g, cset, 5e-8, "fmm", synthetic=synthetic, ncrit=300)
+        run("config3", g, cset, 5e-8, "fmm", synthetic=synthetic, ncrit=120)
+        run("config3", g, cset, 1e-9, "fmm", synthetic=synthetic, ncrit=300)
+        run("config3", g, cset, 5e-8, "direct", reps=2, synthetic=synthetic)
     c4 = os.path.join(ROOT, "data", "config4_geom.npz")
     if os.path.exists(c4) and (not only or "config4" in only):
         g = dict(np.load(c4))
-        indptr, idx = pattern_from_near(g)
-        gen = torch.Generator(device="cuda").manual_seed(4)
-        vals = {k: 1e-4 * torch.randn(idx.numel(), dtype=torch.float64, device="cuda",
-                                      generator=gen)
-                for k in ("s", "sprime", "spp_plus_dprime")}
-        cset = CorrectionSet(indptr, idx, vals)
-        del indptr
+        cset = corrections("config4", g, 1e-9, synthetic, 4)
         torch.cuda.empty_cache()
-        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=300)
-        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=300, m2l="fp64")
-        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=True, ncrit=120)
+        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=synthetic, ncrit=300)
+        run("config4", g, cset, 1e-9, "fmm", reps=2, synthetic=synthetic, ncrit=300,
+            m2l="fp64")

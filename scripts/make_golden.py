@@ -600,7 +600,10 @@ def gold_quad():
     opset fixtures and data/config2.npz cover the other cases)."""
     kinds = [KernelKind.SINGLE_LAYER, KernelKind.DOUBLE_LAYER,
              KernelKind.SPRIME, KernelKind.SPP_PLUS_DPRIME]
-    for name, disc, eps in (("quad_sphere_o7", shapes.build_sphere(7, 0), 1e-10),):
+    cases = (("quad_sphere_o7", shapes.build_sphere(7, 0), 1e-10),)
+    if len(sys.argv) > 2:  # e.g. `gold_quad o9`: the order-9 cube sphere (config 4's order)
+        cases = (("quad_sphere_o9", shapes.build_sphere(9, 0), 1e-9),)
+    for name, disc, eps in cases:
         near = build_near_map(disc, 2.0)
         corrs, t_q = compute_corrections(disc, near, kinds, eps)
         out = dict(geometry_arrays(disc))

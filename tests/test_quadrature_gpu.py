@@ -38,7 +38,8 @@ def _case(name):
     return golden(name + ".npz")
 
 
-@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7"])
+@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7",
+                                  "quad_sphere_o9"])
 def test_near_map_bit_exact(cuda, name):
     from paper_2111_10743_b200 import Geometry
     from paper_2111_10743_b200.quadrature import build_near_map
@@ -61,8 +62,12 @@ def test_near_map_cap_error(cuda):
         build_near_map(Geometry.from_arrays(g), 0.0)
 
 
-@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7", "config2"])
+@pytest.mark.parametrize("name", ["opset_sphere_o3", "opset_torus_o3", "quad_sphere_o7",
+                                  "quad_sphere_o9", "config2"])
 def test_corrections_match_reference(cuda, name):
+    """quad_sphere_o9: reference order 9 (config 4's order), where a CTA holds
+    only two leaves' basis tables and a self pair's three Duffy roots are
+    evaluated in two batches."""
     from paper_2111_10743_b200 import Geometry
     from paper_2111_10743_b200.quadrature import NearMap, build_correction_set
     g = _case(name)
