@@ -458,7 +458,36 @@ constexpr int kLeafBT = 128;
 constexpr int kLeafTS = 128;
 constexpr int kLeafMaxSets = 512;
 
-template <int ND, bool HD, int LEVEL>
+// Projected pair of the two-density A3 call (fmm_apply_a3proj), where density
+// X = charge c0 with dipole -c1 n_s and density B = charge c1.  Record
+// [x y z | cX  n_s | cB  0]: real sources carry their normal n_s in X's
+// dipole slots (their X dipole is -cB n_s by construction), equivalent
+// sources zeros.  Outputs per target:
+//   a[0] += -n.grad X + n.H_B.n = r^-3 [cX (n.r) + cB Kspp],
+//           Kspp = 3 (n.r)(dn.r)/r^2 - n.dn, dn = n - n_s  (formed first: the
+//           accurate form of FarA3c; n_s = 0 gives the equivalent sources'
+//           charge-only terms exactly)
+//   a[1] += cB / r          a[2] += n.grad B = -cB (n.r) / r^3
+// ~40 flop instead of the ~130 of two densities' gradients and Hessians.
+__device__ __forceinline__ void pair_a3(double tx, double ty, double tz, double nx, double ny,
+                                        double nz, const double* __restrict__ rec, double* a) {
+  const double r0 = tx - rec[0], r1 = ty - rec[1], r2 = tz - rec[2];
+  const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+  const double invr = inv_sqrt_skip(rr);
+  const double invr2 = invr * invr;
+  const double invr3 = invr * invr2;
+  const double rnt = fma(nz, r2, fma(ny, r1, nx * r0));
+  const double dn0 = nx - rec[4], dn1 = ny - rec[5], dn2 = nz - rec[6];
+  const double rdn = fma(dn2, r2, fma(dn1, r1, dn0 * r0));
+  const double ndn = fma(nz, dn2, fma(ny, dn1, nx * dn0));
+  const double cX = rec[3], cB = rec[7];
+  const double kspp = fma(3.0 * rnt * rdn, invr2, -ndn);
+  a[0] = fma(invr3, fma(cX, rnt, cB * kspp), a[0]);
+  a[1] = fma(cB, invr, a[1]);
+  a[2] = fma(-cB * invr3, rnt, a[2]);
+}
+
+template <int ND, bool HD, int LEVEL, bool A3P = false>
 __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     const int64_t* __restrict__ leaves, const int64_t* __restrict__ u_off,
     const int64_t* __restrict__ u_list, const int64_t* __restrict__ w_off,
@@ -468,11 +497,13 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     const double* __restrict__ tpos, const double* __restrict__ cs, const double* __restrict__ vs,
     int64_t ns, int64_t nt, const double* __restrict__ pts, int nrep, int surface, double de_scale,
     double ue_scale, const double* __restrict__ loc, const double* __restrict__ up,
-    double* __restrict__ tout) {
+    double* __restrict__ tout, const double* __restrict__ tnrm = nullptr,
+    const double* __restrict__ snrm = nullptr) {
   using Lay = SrcLayout<ND, true, HD>;
   constexpr int S = Lay::stride;
   constexpr int NC = ncomp(LEVEL);
-  constexpr int NA = ND * NC;
+  constexpr int NA = A3P ? 3 : ND * NC;
+  static_assert(!A3P || (ND == 2 && HD), "projected leaf: the two-density A3 call only");
   constexpr int kTS = S > 8 ? kLeafTS / 2 : kLeafTS;
   __shared__ __align__(16) double sh[kTS * S];
   __shared__ int64_t set_end[kLeafMaxSets + 1];
@@ -495,6 +526,12 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     const bool in = t < t1;
     const double tx = in ? tpos[3 * t] : 0.0, ty = in ? tpos[3 * t + 1] : 0.0,
                  tz = in ? tpos[3 * t + 2] : 0.0;
+    double nx = 0.0, ny = 0.0, nz = 0.0;
+    if (A3P && in) {
+      nx = tnrm[3 * t];
+      ny = tnrm[3 * t + 1];
+      nz = tnrm[3 * t + 2];
+    }
     double acc[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) acc[a] = 0.0;
@@ -546,6 +583,11 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
               if (HD)
                 for (int kk = 0; kk < 3; ++kk) r[o++] = vs[((int64_t)l * ns + j) * 3 + kk];
             }
+            if (A3P) {  // X's dipole slots carry the source normal (see pair_a3)
+              r[4] = snrm[3 * j];
+              r[5] = snrm[3 * j + 1];
+              r[6] = snrm[3 * j + 2];
+            }
           } else {  // equivalent charges: own DE set (loc) or a W box (up)
             const int64_t eb = -1 - box;
             const bool de = eb == b && surface && (lo + sb0) == nu;
@@ -564,7 +606,11 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
           }
         }
         __syncthreads();
-        for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+        if constexpr (A3P) {
+          for (int k = ph; k < n; k += kSplit) pair_a3(tx, ty, tz, nx, ny, nz, sh + k * S, acc);
+        } else {
+          for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+        }
       }
     }
     // combine the source phases (fixed order), one component at a time
@@ -579,11 +625,16 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
       }
     }
     if (in && ph == 0) {
+      if constexpr (A3P) {
 #pragma unroll
-      for (int l = 0; l < ND; ++l) {
-        double* o = tout + ((int64_t)l * nt + t) * 10;
+        for (int c = 0; c < 3; ++c) tout[t * 3 + c] = acc[c];
+      } else {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) o[c] += acc[l * NC + c];
+        for (int l = 0; l < ND; ++l) {
+          double* o = tout + ((int64_t)l * nt + t) * 10;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) o[c] += acc[l * NC + c];
+        }
       }
     }
   }
@@ -606,6 +657,22 @@ __global__ void fmm_scatter_kernel(const double* __restrict__ tout, const int64_
     const double hv[9] = {v[4], v[7], v[8], v[7], v[5], v[9], v[8], v[9], v[6]};
     for (int k = 0; k < 9; ++k) hess[row * 9 + k] = hv[k];
   }
+}
+
+// reference-order rows -> sorted rows (target normals) and back (projections)
+__global__ void gather_rows3_kernel(const double* __restrict__ in, const int64_t* __restrict__ sorted,
+                                    int64_t n, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t r = sorted[t];
+  for (int k = 0; k < 3; ++k) out[3 * t + k] = in[3 * r + k];
+}
+__global__ void scatter_proj_kernel(const double* __restrict__ tproj, const int64_t* __restrict__ sorted,
+                                    int64_t n, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t r = sorted[t];
+  for (int c = 0; c < 3; ++c) out[(int64_t)c * n + r] = tproj[3 * t + c];
 }
 
 // ---------------------------------------------------------------------------
@@ -904,7 +971,8 @@ int gemm_rm(cublasHandle_t h, const double* A, const double* X, double* Y, int n
 template <int ND>
 int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const double* charges,
                 const double* dipoles, int level, double* pot, double* grad, double* hess,
-                cudaStream_t st, std::vector<cudaEvent_t>& ev) {
+                cudaStream_t st, std::vector<cudaEvent_t>& ev, const double* proj_nrm = nullptr,
+                double* proj_out = nullptr, const double* proj_snrm = nullptr) {
   FmmTree& t = P->tree;
   FmmDevice& D = P->dev;
   const int nrep = P->nrep;
@@ -1037,6 +1105,17 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   mark(5);
   // ---- leaf stage (fmm.py:937-988)
   LB_CUDA(cudaMemsetAsync(D.tout, 0, sizeof(double) * ND * t.nt * 10, st));
+  if (proj_out) {
+    if (t.nt > 0) {
+      gather_rows3_kernel<<<(unsigned)ceil_div(t.nt, 256), 256, 0, st>>>(proj_nrm, D.tgt_sorted, t.nt, D.tnrm);
+      LB_CHECK_LAUNCH();
+    }
+    if (t.ns > 0) {
+      gather_rows3_kernel<<<(unsigned)ceil_div(t.ns, 256), 256, 0, st>>>(proj_snrm, D.src_sorted, t.ns, D.snrm);
+      LB_CHECK_LAUNCH();
+    }
+    LB_CUDA(cudaMemsetAsync(D.tproj, 0, sizeof(double) * 3 * t.nt, st));
+  }
   if (D.n_tleaf > 0) {
     if (!surface) {
       const size_t sm = l2t_smem(n, level);
@@ -1053,7 +1132,17 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,       \
       D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,      \
       surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout)
-    if (hd) {
+    if constexpr (ND == 2) {
+      if (proj_out) {  // projected leaf (fmm_apply_a3proj): writes tproj, not tout
+        leaf_kernel<2, true, 2, true><<<(unsigned)D.n_tleaf, kLeafBT, 0, st>>>(
+            D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,
+            D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,
+            surface ? P->ue_scale : 1.0, D.loc, D.up, D.tproj, D.tnrm, D.snrm);
+        LB_CHECK_LAUNCH();
+      }
+    }
+    if (proj_out) {
+    } else if (hd) {
       if (level == 0) LB_LEAF(true, 0); else if (level == 1) LB_LEAF(true, 1); else LB_LEAF(true, 2);
     } else {
       if (level == 0) LB_LEAF(false, 0); else if (level == 1) LB_LEAF(false, 1); else LB_LEAF(false, 2);
@@ -1066,6 +1155,10 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   fmm_scatter_kernel<<<(unsigned)ceil_div((int64_t)ND * t.nt, 256), 256, 0, st>>>(
       D.tout, D.tgt_sorted, t.nt, ND, d0, level, pot, grad, hess);
   LB_CHECK_LAUNCH();
+  if (proj_out && t.nt > 0) {
+    scatter_proj_kernel<<<(unsigned)ceil_div(t.nt, 256), 256, 0, st>>>(D.tproj, D.tgt_sorted, t.nt, proj_out);
+    LB_CHECK_LAUNCH();
+  }
   mark(8);
   return LB_OK;
 }
@@ -1079,7 +1172,7 @@ void fmm_release_device(lb_fmm_plan* P) {
                   D.p2m_leaves, D.up_child, D.up_parent, D.dn_child, D.dn_parent, D.v_src,
                   D.v_tgt_pair_off, D.v_tgts, D.v_off_idx, D.v_scale, D.x_boxes, D.x_off,
                   D.x_leaves, D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.cs, D.vs, D.up,
-                  D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct};
+                  D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct, D.tnrm, D.tproj, D.snrm};
   for (void* p : ptrs) cudaFree(p);
   if (P->rep == 0) cudaFree(D.loc);
   cudaFree(D.oz_a);
@@ -1147,9 +1240,13 @@ int lb_fmm_stage_times(const lb_fmm_plan* P, double* ms) {
   return LB_OK;
 }
 
-int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, int nd,
-                 uint32_t cmask, uint32_t dmask, int level, double* pot, double* grad,
-                 double* hess, void* stream) {
+}  // extern "C"
+
+namespace lb {
+int fmm_apply_impl(lb_fmm_plan* P, const double* charges, const double* dipoles, int nd,
+                   uint32_t cmask, uint32_t dmask, int level, double* pot, double* grad,
+                   double* hess, cudaStream_t st, const double* proj_nrm, double* proj_out,
+                   const double* proj_snrm) {
   if (!P) return fail(LB_ERR_ARG, "lb_fmm_apply: null plan");
   if (P->rep < 0) return fail(LB_ERR_ARG, "lb_fmm_apply: operators not set");
   if (nd <= 0 || nd > 32) return fail(LB_ERR_SHAPE, "lb_fmm_apply: nd must be in [1, 32]");
@@ -1161,7 +1258,8 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
   dmask &= valid;
   if ((cmask && !charges) || (dmask && !dipoles))
     return fail(LB_ERR_ARG, "lb_fmm_apply: active mask without a density array");
-  cudaStream_t st = as_stream(stream);
+  if (proj_out && (nd != 2 || level != 2 || !proj_nrm || !proj_snrm))
+    return fail(LB_ERR_ARG, "fmm_apply_a3proj: two densities at level 2 with target and source normals");
   {
     const cudaError_t stale = cudaGetLastError();
     if (stale != cudaSuccess)
@@ -1169,6 +1267,12 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
                                    cudaGetErrorString(stale));
   }
   if (!P->dev.ready) LB_TRY(build_device(P));
+  if (proj_out && !P->dev.tproj) {
+    const int64_t nt = std::max<int64_t>(P->tree.nt, 1);
+    LB_CUDA(cudaMalloc((void**)&P->dev.tnrm, sizeof(double) * 3 * nt));
+    LB_CUDA(cudaMalloc((void**)&P->dev.tproj, sizeof(double) * 3 * nt));
+    LB_CUDA(cudaMalloc((void**)&P->dev.snrm, sizeof(double) * 3 * std::max<int64_t>(P->tree.ns, 1)));
+  }
   LB_BLAS(cublasSetStream(P->dev.blas, st));
   std::vector<cudaEvent_t> ev;
   if (P->timing) {
@@ -1182,7 +1286,10 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
     int rc;
     switch (ndc) {
       case 1: rc = apply_chunk<1>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
-      case 2: rc = apply_chunk<2>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
+      case 2:
+        rc = apply_chunk<2>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev,
+                            proj_nrm, proj_out, proj_snrm);
+        break;
       case 3: rc = apply_chunk<3>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
       default: rc = apply_chunk<4>(P, d0, cmask, dmask, charges, dipoles, level, pot, grad, hess, st, ev); break;
     }
@@ -1203,6 +1310,23 @@ int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, i
     for (auto& e : ev) cudaEventDestroy(e);
   }
   return LB_OK;
+}
+
+int fmm_apply_a3proj(lb_fmm_plan* P, const double* charges, const double* dipoles,
+                     const double* tnrm, const double* snrm, double* pot, double* grad, double* hess,
+                     double* proj, cudaStream_t st) {
+  if (!proj) return fail(LB_ERR_ARG, "fmm_apply_a3proj: null projection output");
+  return fmm_apply_impl(P, charges, dipoles, 2, 3u, 1u, 2, pot, grad, hess, st, tnrm, proj, snrm);
+}
+}  // namespace lb
+
+extern "C" {
+
+int lb_fmm_apply(lb_fmm_plan* P, const double* charges, const double* dipoles, int nd,
+                 uint32_t cmask, uint32_t dmask, int level, double* pot, double* grad,
+                 double* hess, void* stream) {
+  return lb::fmm_apply_impl(P, charges, dipoles, nd, cmask, dmask, level, pot, grad, hess,
+                            as_stream(stream), nullptr, nullptr, nullptr);
 }
 
 }  // extern "C"

@@ -58,6 +58,9 @@ struct FmmDevice {
   int64_t tmp_cols = 0;
   // outputs in sorted target order (nd, nt, 10) before the scatter
   double* tout = nullptr;
+  // projected leaf stage (fmm_apply_a3proj): target normals in sorted order
+  // (nt, 3) and the four projections per target (nt, 4)
+  double *tnrm = nullptr, *tproj = nullptr, *snrm = nullptr;
   int64_t* btgt_oct = nullptr;               // octant (x | y<<1 | z<<2) of every slot
   std::vector<int64_t> level_slot_off;       // slot range of every level
   std::vector<int64_t> v_tpoff_host;         // host copy of v_tgt_pair_off
@@ -93,4 +96,14 @@ struct lb_fmm_plan {
 
 namespace lb {
 void fmm_release_device(lb_fmm_plan* p);
+// The two-density A3 call (charges (2, ns): X = c0, B = c1; dipoles (2, ns, 3):
+// X only, = -c1 n_s) at level 2 with a PROJECTED leaf stage: besides
+// pot/grad/hess of the grid L2T part (zero in surface mode), proj (3, nt)
+// receives, in reference target order, the leaf stage's -n.grad X + n.H_B.n
+// (in the accurate Kspp form, source normals snrm (ns, 3)), pot B and
+// n.grad B, with n the target normals tnrm (nt, 3).  The caller adds the same
+// projections of pot/grad/hess.
+int fmm_apply_a3proj(lb_fmm_plan* P, const double* charges, const double* dipoles,
+                     const double* tnrm, const double* snrm, double* pot, double* grad, double* hess,
+                     double* proj, cudaStream_t st);
 }

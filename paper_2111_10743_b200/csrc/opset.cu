@@ -25,6 +25,13 @@
 #include "opfar.cuh"
 #include "reduce.cuh"
 
+struct lb_fmm_plan;
+namespace lb {  // fmm_plan.h (fmm_apply.cu): the two-density A3 call with a projected leaf stage
+int fmm_apply_a3proj(lb_fmm_plan* P, const double* charges, const double* dipoles, const double* tnrm,
+                     const double* snrm, double* pot, double* grad, double* hess, double* proj,
+                     cudaStream_t st);
+}
+
 namespace lb {
 
 // ---------------------------------------------------------------------------
@@ -455,6 +462,7 @@ struct lb_opset {
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double *f_ch = nullptr, *f_ch3 = nullptr, *f_dp = nullptr;
   double *f_pot = nullptr, *f_grad = nullptr, *f_hess = nullptr;
+  double* f_proj = nullptr;  // (4, nr): projected leaf outputs of the 2-density A3 call
 };
 
 namespace lb {
@@ -609,7 +617,8 @@ __global__ void dipole_kernel(const double* __restrict__ c, const double* __rest
 __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t n,
                                const double* __restrict__ pot, const double* __restrict__ grad,
                                const double* __restrict__ hess, SkLayout L, int nout,
-                               double* __restrict__ part, const double* __restrict__ curv) {
+                               double* __restrict__ part, const double* __restrict__ curv,
+                               const double* __restrict__ proj) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double nx = nrm[3 * i], ny = nrm[3 * i + 1], nz = nrm[3 * i + 2];
@@ -629,7 +638,11 @@ __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t
     case FK_A3B: a[0] = -ng(0); a[1] = pot[n + i]; a[2] = -ng(1); a[3] = nhn(1) + ng(2); break;
     // fused A3 call 2 on two FMM densities: X = (charge c0, dipole -c1 n) and
     // B = (charge c1): a0 = FarA3b's a0 + a3 - 2H a2 = -n.grad X + n.H_B.n + 2H n.grad B
-    case FK_A3M: a[0] = fma(2.0 * curv[i], ng(1), nhn(1) - ng(0)); a[1] = pot[n + i]; break;
+    case FK_A3M: {  // + the projected leaf stage [-n.grad X + n.H_B.n, pot B, n.grad B]
+      a[0] = fma(2.0 * curv[i], ng(1) + proj[2 * n + i], (nhn(1) - ng(0)) + proj[i]);
+      a[1] = pot[n + i] + proj[n + i];
+      break;
+    }
     case FK_A2A: a[0] = pot[i]; a[1] = pot[n + i]; a[2] = -ng(0); a[3] = nhn(0) + ng(1); break;
     case FK_A2B: a[0] = pot[i]; a[1] = pot[n + i]; break;
     case FK_A1A:
@@ -700,7 +713,12 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
     case FK_A1B: nd = 3; cm = 7; level = 1; chp = c0; break;
   }
   LB_CHECK_LAUNCH();
-  {
+  if (kind == FK_A3M) {  // projected leaf stage (fmm_plan.h: fmm_apply_a3proj)
+    if (!h->f_proj) LB_CUDA(cudaMalloc((void**)&h->f_proj, sizeof(double) * 3 * std::max<int64_t>(n, 1)));
+    const int rc = fmm_apply_a3proj(h->fmm, chp, dpp, h->d.normals + 3 * h->r0, h->d.over_normals,
+                                    h->f_pot, h->f_grad, h->f_hess, h->f_proj, st);
+    if (rc != LB_OK) return fail(rc, std::string("far_stage(A3 two densities): ") + lb_last_error_string());
+  } else {
     int rc = lb_fmm_apply(h->fmm, chp, dpp, nd, cm, dm, level, h->f_pot, h->f_grad, h->f_hess, st);
     if (rc != LB_OK) return fail(rc, std::string("far_stage(kind ") + std::to_string((int)kind) +
                                          "): " + lb_last_error_string());
@@ -715,7 +733,7 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
   const int nout = far_nout(kind);
   project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals + 3 * h->r0, n, h->f_pot,
                                                              h->f_grad, h->f_hess, l1, nout, h->part,
-                                                             h->d.curvature + h->r0);
+                                                             h->d.curvature + h->r0, h->f_proj);
   LB_CHECK_LAUNCH();
   *L = l1;
   return LB_OK;
@@ -986,6 +1004,8 @@ int lb_opset_destroy(lb_opset* h) {
   cudaFree(h->f_pot);
   cudaFree(h->f_grad);
   cudaFree(h->f_hess);
+  cudaFree(h->f_proj);
+  h->f_proj = nullptr;
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   delete h;
