@@ -72,6 +72,53 @@ def bench_summary():
     open(os.path.join(OUT, "bench_launches.md"), "w").write("\n".join(lines) + "\n")
 
 
+def avn_summary():
+    """profiles/round1/apply_vs_n.jsonl (scripts/apply_vs_n.py output) -> .md"""
+    rows = [json.loads(l) for l in open(os.path.join(OUT, "apply_vs_n.jsonl"))]
+    try:
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        hbm = 6552.6
+    L = ["# GMRES operator-apply time vs N (A3, B200, round 1)", "",
+         "Second half of the BASELINE metric.  Corrections: config 2 built by the reference "
+         "(eps 1e-10); configs 3 and 4 built ON THE DEVICE (`quadrature.build_correction_set`, "
+         "csrc/quad.cu: the reference's adaptive quadrature; near map bit-exact against the "
+         "reference's) because the reference's own build takes hours (config 3) to more than a "
+         "day (config 4).  Stage times from `lb_opset_stage_times` (CUDA events).  Exact-sweep "
+         "A3 runs the fused second sweep (FarA3c); the FMM path runs A3's second call on two FMM "
+         "densities with a projected leaf stage.  `scripts/apply_vs_n.py`.", "",
+         "| case | N | N_over | nnz/kind | far field | apply ms | far 1 ms | SpMV 1 ms (HBM frac) "
+         "| far 2 ms | SpMV 2 + glue ms (HBM frac) |", "|---|---|---|---|---|---|---|---|---|---|"]
+    builds = []
+    for r in rows:
+        if "apply_ms" not in r:
+            builds.append(r)
+            continue
+        if r["far"] == "direct":
+            far = "direct (exact fp64 sweeps, fused)"
+        else:
+            m2l = "fp64 DGEMM" if r["m2l_slices"] == 0 else f"tcgen05 int8 S={r['m2l_slices']}"
+            far = f"fmm eps={r['eps']:g} ncrit={r['fmm_ncrit']} M2L {m2l}"
+        st = r["stages_ms"]
+        L.append(f"| {r['case']} | {r['N']} | {r['N_over']} | {r['nnz_per_kind']:.3g} | {far} | "
+                 f"{r['apply_ms']:.2f} | {st['far1']:.2f} | {st['spmv1']:.3f} "
+                 f"({r['spmv1_GBps'] / hbm:.2f}) | {st['far2']:.2f} | {st['spmv2+glue']:.3f} "
+                 f"({r['spmv2_GBps'] / hbm:.2f}) |")
+    L += ["", "Device correction builds:", "",
+          "| case | eps | pairs | near map s | t_q s | leaves evaluated |", "|---|---|---|---|---|---|"]
+    for b in builds:
+        bb = b["build"]
+        L.append(f"| {b['case']} | {bb['eps']:g} | {bb['split']['pairs']} | {bb['t_near_s']:.2f} "
+                 f"(bit-exact: {bb['near_equal_reference']}) | {bb['t_q_s']:.1f} | "
+                 f"{bb['split']['leaves']:.3g} |")
+    L += ["", "SpMV algorithmic bytes: pass 1 = nnz (2*8 + 4) + 8(N+1); pass 2 = nnz (k*8 + 4) + "
+          "8(N+1) with k = 2 value arrays (fused: S', S''+D') or 3 (FMM path: S', S, S''+D'); x "
+          f"gathers hit L2.  HBM peak = {hbm} GB/s (MEASURED_PEAKS.json).  Config 2's CSR "
+          "(66 MB/kind) is L2-sized, so its passes are latency-bound.  Earlier rows of this round "
+          "(3-density FMM, synthetic values): apply_vs_n_pre_fusion.jsonl."]
+    open(os.path.join(OUT, "apply_vs_n.md"), "w").write("\n".join(L) + "\n")
+
+
 def fmm_summary():
     L = launches(os.path.join(G, "launches_fmm.csv"))
     agg = defaultdict(lambda: [0, 0.0])
@@ -121,6 +168,8 @@ if __name__ == "__main__":
         step_summary()
     if "bench" in what:
         bench_summary()
+    if "avn" in what:
+        avn_summary()
     if "fmm" in what:
         fmm_summary()
     if "full" in what:
