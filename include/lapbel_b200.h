@@ -285,6 +285,14 @@ int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
  * about 1e3 * 2^(-7S) of max|K| max|x| (S = 8: fp64 roundoff).  Needs
  * nrep <= 2048. */
 int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
+/* Low-rank M2L (slices = -1 above): per canonical key k the factors of the
+ * truncated SVD  canon_k ~= A_k B_k, A_k (nrep, r_k), B_k (r_k, nrep), both
+ * row-major and concatenated over k in key order.  The product then costs
+ * 2 nrep r_k instead of nrep^2 per column (fp64 cuBLAS).  A B200 design
+ * option with no reference counterpart: the truncation tolerance is the
+ * caller's (fmm_plan.py ties it to eps / 100). */
+int lb_fmm_plan_set_m2l_factors(lb_fmm_plan* plan, const int32_t* ranks, const double* a,
+                                const double* b);
 /* device time of each stage of the last apply, ms (HOST double[9]):
  * gather+P2M, M2M, M2L, X, L2L, L2T (grid), leaf (U+DE+W), scatter, total.  Recorded
  * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */

@@ -968,6 +968,38 @@ int gemm_rm(cublasHandle_t h, const double* A, const double* X, double* Y, int n
   return LB_OK;
 }
 
+// Y (m, ncols) = A (m, k) row-major  X (k, ncols) column-major
+int gemm_rm2(cublasHandle_t h, const double* A, const double* X, double* Y, int m, int k, int64_t ncols,
+             double alpha, double beta) {
+  if (ncols <= 0) return LB_OK;
+  LB_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, m, (int)ncols, k, &alpha, A, k, X, k, &beta, Y, m));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(LB_ERR_CUDA, std::string("after cublasDgemm: ") + cudaGetErrorString(e));
+  return LB_OK;
+}
+
+// low-rank M2L: device copies of the factors and the rank-sized staging
+int ensure_lowrank(lb_fmm_plan* P, int nd) {
+  FmmDevice& D = P->dev;
+  if (!D.lr_a) {
+    LB_CUDA(cudaMalloc((void**)&D.lr_a, sizeof(double) * std::max<size_t>(P->lr_a_host.size(), 1)));
+    LB_CUDA(cudaMalloc((void**)&D.lr_b, sizeof(double) * std::max<size_t>(P->lr_b_host.size(), 1)));
+    LB_CUDA(cudaMemcpy(D.lr_a, P->lr_a_host.data(), sizeof(double) * P->lr_a_host.size(), cudaMemcpyHostToDevice));
+    LB_CUDA(cudaMemcpy(D.lr_b, P->lr_b_host.data(), sizeof(double) * P->lr_b_host.size(), cudaMemcpyHostToDevice));
+  }
+  int rmax = 1;
+  for (int r : P->lr_rank) rmax = std::max(rmax, r);
+  const int64_t need = (int64_t)rmax * D.tmp_cols * nd;
+  if (D.lr_t_cap < need) {
+    cudaFree(D.lr_t);
+    D.lr_t = nullptr;
+    LB_CUDA(cudaMalloc((void**)&D.lr_t, sizeof(double) * need));
+    D.lr_t_cap = need;
+  }
+  return LB_OK;
+}
+
 template <int ND>
 int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const double* charges,
                 const double* dipoles, int level, double* pot, double* grad, double* hess,
@@ -1032,7 +1064,8 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   }
   mark(2);
   // ---- M2L (fmm.py:873-886), by canonical key, chunked at target boundaries
-  LB_TRY(ensure_oz(P, ND, st));
+  if (P->m2l_slices < 0) LB_TRY(ensure_lowrank(P, ND));
+  else LB_TRY(ensure_oz(P, ND, st));
   for (int k = 0; k < P->ncanon; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
     if (pe == pb) continue;
@@ -1056,7 +1089,14 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
         m2l_gather_kernel<<<(unsigned)(np * ND), 128, 0, st>>>(D.up, D.v_src, D.v_off_idx, D.v_scale,
                                                                D.perm_inv, p0, np, ND, nrep, D.tmpA);
         LB_CHECK_LAUNCH();
-        LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+        if (P->m2l_slices < 0) {  // K_k ~= A_k B_k: two thin DGEMMs through the rank-r_k staging
+          const int r = P->lr_rank[k];
+          const int64_t o = P->lr_off[k] * nrep;
+          LB_TRY(gemm_rm2(D.blas, D.lr_b + o, D.tmpA, D.lr_t, r, nrep, np * ND, 1.0, 0.0));
+          LB_TRY(gemm_rm2(D.blas, D.lr_a + o, D.lr_t, D.tmpB, nrep, r, np * ND, 1.0, 0.0));
+        } else {
+          LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+        }
       }
       m2l_accum_kernel<<<(unsigned)(tj - ti), 128, 0, st>>>(D.tmpB, D.v_tgts, D.v_tgt_pair_off,
                                                             D.v_off_idx, D.perm,
@@ -1177,6 +1217,9 @@ void fmm_release_device(lb_fmm_plan* P) {
   if (P->rep == 0) cudaFree(D.loc);
   cudaFree(D.oz_a);
   cudaFree(D.oz_rs);
+  cudaFree(D.lr_a);
+  cudaFree(D.lr_b);
+  cudaFree(D.lr_t);
   cudaFree(D.oz_b);
   cudaFree(D.oz_cs);
   if (D.blas) cublasDestroy(D.blas);
@@ -1218,10 +1261,36 @@ int lb_fmm_plan_set_operators(lb_fmm_plan* P, const lb_fmm_ops* o) {
   return LB_OK;
 }
 
+int lb_fmm_plan_set_m2l_factors(lb_fmm_plan* P, const int32_t* ranks, const double* a, const double* b) {
+  if (!P || !ranks || !a || !b) return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l_factors: null argument");
+  if (P->ncanon <= 0 || P->nrep <= 0) return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l_factors: operators not set");
+  std::vector<int64_t> off(P->ncanon + 1, 0);
+  for (int k = 0; k < P->ncanon; ++k) {
+    if (ranks[k] < 1 || ranks[k] > P->nrep)
+      return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l_factors: rank outside [1, nrep]");
+    off[k + 1] = off[k] + ranks[k];
+  }
+  P->lr_rank.assign(ranks, ranks + P->ncanon);
+  P->lr_off = off;
+  const size_t total = (size_t)off.back() * P->nrep;
+  P->lr_a_host.assign(a, a + total);
+  P->lr_b_host.assign(b, b + total);
+  FmmDevice& D = P->dev;  // device copies are rebuilt on the next apply
+  cudaFree(D.lr_a);
+  cudaFree(D.lr_b);
+  D.lr_a = D.lr_b = nullptr;
+  return LB_OK;
+}
+
 int lb_fmm_plan_set_m2l(lb_fmm_plan* P, int slices) {
   if (!P) return fail(LB_ERR_ARG, "null plan");
+  if (slices == -1) {
+    if (P->lr_rank.empty()) return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: low-rank M2L needs factors");
+    P->m2l_slices = -1;
+    return LB_OK;
+  }
   if (slices != 0 && (slices < 3 || slices > 8))
-    return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: slices must be 0 (fp64) or in [3, 8]");
+    return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: slices must be -1 (low rank), 0 (fp64) or in [3, 8]");
   if (slices != 0 && P->nrep > 2048)
     return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: tensor-core M2L needs nrep <= 2048");
   P->m2l_slices = slices;

@@ -71,6 +71,10 @@ struct FmmDevice {
   uint8_t* oz_b = nullptr;                   // column slices of one M2L chunk
   double* oz_cs = nullptr;                   // column scales of one M2L chunk
   int64_t oz_cols = 0;                       // column capacity of oz_b / oz_cs
+  // low-rank M2L (lb_fmm_plan_set_m2l_factors): per canonical key K = A B,
+  // A (nrep, r_k) and B (r_k, nrep) row-major, packed; staging (r_max, cols)
+  double *lr_a = nullptr, *lr_b = nullptr, *lr_t = nullptr;
+  int64_t lr_t_cap = 0;
 };
 
 }  // namespace lb
@@ -91,7 +95,11 @@ struct lb_fmm_plan {
   std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
   std::vector<double> stage_ms;             // last apply's per-stage device times
   bool timing = false;
-  int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices
+  int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices;
+                                            // -1: low-rank factors (fp64 DGEMM pair)
+  std::vector<int32_t> lr_rank;             // per canonical key
+  std::vector<int64_t> lr_off;              // packed offsets (ncanon + 1), in doubles per factor / nrep
+  std::vector<double> lr_a_host, lr_b_host;
 };
 
 namespace lb {

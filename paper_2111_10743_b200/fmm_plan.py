@@ -62,6 +62,37 @@ def m2l_slices_for(eps: float, nrep: int) -> int:
     return int(min(8, max(3, s)))
 
 
+_LOWRANK_CACHE: dict = {}
+
+
+def m2l_factors(canon: np.ndarray, tol: float):
+    """Truncated SVD of every canonical M2L matrix (B200 design option, no
+    reference counterpart): canon_k ~= A_k B_k keeping the singular values
+    above tol * sigma_max(canon_k), so the M2L of one column costs
+    2 nrep r_k instead of nrep^2 (the grid operators at n = 9 have r_k <= 63,
+    mean 36, at tol 1e-11).  Returns (ranks int32, A packed, B packed)."""
+    key = (id(canon), canon.shape, float(tol))
+    if key in _LOWRANK_CACHE:
+        return _LOWRANK_CACHE[key]
+    ranks, As, Bs = [], [], []
+    for K in canon:
+        u, sv, vt = np.linalg.svd(K)
+        r = max(1, int((sv > tol * sv[0]).sum()))
+        ranks.append(r)
+        As.append(np.ascontiguousarray(u[:, :r] * sv[:r]))
+        Bs.append(np.ascontiguousarray(vt[:r]))
+    out = (np.asarray(ranks, dtype=np.int32), np.concatenate([a.ravel() for a in As]),
+           np.concatenate([b.ravel() for b in Bs]))
+    _LOWRANK_CACHE[key] = out
+    return out
+
+
+def m2l_lowrank_tol(eps: float) -> float:
+    """SVD truncation of the low-rank M2L: eps / 100 (the M2L then moves the
+    FMM result by far less than its requested precision), in [1e-13, 1e-8]."""
+    return float(min(1e-8, max(1e-13, eps / 100.0)))
+
+
 # ---------------------------------------------------------------------------
 # unit-box operators (host precompute, cached like the reference's lru_cache)
 
@@ -243,6 +274,7 @@ def _bind():
         L.lb_fmm_apply.argtypes = [P, P, P, I32, ctypes.c_uint32,
                                    ctypes.c_uint32, I32, P, P, P, P]
         L.lb_fmm_plan_set_timing.argtypes = [P, I32]
+        L.lb_fmm_plan_set_m2l_factors.argtypes = [P, P, P, P]
         L.lb_fmm_stage_times.argtypes = [P, P]
         _bound = True
     return L
@@ -341,13 +373,21 @@ class FmmPlan:
         self.set_m2l(m2l)
 
     def set_m2l(self, m2l="auto"):
-        """M2L arithmetic: "fp64" (DGEMM, the reference's arithmetic), "auto"
-        (tcgen05 int8 slices sized from eps, m2l_slices_for) or an explicit
-        slice count in [3, 8] (8 = fp64 roundoff)."""
+        """M2L arithmetic: "fp64" (DGEMM on the dense canonical matrices, the
+        reference's arithmetic), "auto" = "lowrank" (truncated-SVD factors at
+        m2l_lowrank_tol(eps), two thin fp64 DGEMMs: the canonical M2L
+        matrices have rank <= 63 of 729 at 1e-11, so this beats the dense
+        tensor-core product), or an explicit tcgen05 int8 slice count in
+        [3, 8] (m2l_slices_for(eps) sizes it; 8 = fp64 roundoff)."""
         if m2l == "fp64":
             s = 0
-        elif m2l == "auto":
-            s = m2l_slices_for(self.eps, self.nrep)
+        elif m2l in ("auto", "lowrank"):
+            ranks, a, b = m2l_factors(self.ops["canon"], m2l_lowrank_tol(self.eps))
+            _lib.check(self._L.lb_fmm_plan_set_m2l_factors(
+                self._h, ranks.ctypes.data_as(ctypes.c_void_p), a.ctypes.data_as(ctypes.c_void_p),
+                b.ctypes.data_as(ctypes.c_void_p)), "lb_fmm_plan_set_m2l_factors")
+            self.m2l_ranks = ranks
+            s = -1
         else:
             s = int(m2l)
         _lib.check(self._L.lb_fmm_plan_set_m2l(self._h, s), "lb_fmm_plan_set_m2l")

@@ -28,7 +28,9 @@ for n, eps in zip(args[::2], args[1::2]):
     idx = rng.choice(n, 400, replace=False)
     ref = b.evaluate_direct(b.FmmSources(x, q), x[idx], ("pot", "grad"))
     base = None
-    modes = ["fp64", "auto"] + [s for s in (5, 6, 7, 8) if s != b.fmm_plan.m2l_slices_for(eps, plan.nrep)]
+    modes = ["fp64", b.fmm_plan.m2l_slices_for(eps, plan.nrep), "lowrank"] + ([] if os.environ.get("QUICK") else
+                                           [s for s in (5, 6, 7, 8)
+                                            if s != b.fmm_plan.m2l_slices_for(eps, plan.nrep)])
     for mode in modes:
         plan.set_m2l(mode)
         pot = torch.empty((nd, n), dtype=torch.float64, device="cuda")
@@ -59,4 +61,6 @@ for n, eps in zip(args[::2], args[1::2]):
         print(json.dumps({"N": n, "eps": eps, "nd": nd, "rep": plan.rep, "nrep": plan.nrep,
                           "m2l": mode, "slices": plan.m2l_slices, "apply_ms": min(ts),
                           "m2l_ms": st["m2l"], "err_vs_direct_400": err,
-                          "dev_vs_fp64_fmm": dev}), flush=True)
+                          "dev_vs_fp64_fmm": dev,
+                          "ranks": None if mode != "lowrank" else
+                          [int(plan.m2l_ranks.max()), float(plan.m2l_ranks.mean())]}), flush=True)

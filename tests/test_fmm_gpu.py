@@ -21,7 +21,7 @@ def _cloud(m, nt, seed=0):
     return rng, rng.uniform(0, 1, (m, 3)), rng.uniform(0, 1, (nt, 3))
 
 
-@pytest.mark.parametrize("m2l", ["fp64", "auto"])
+@pytest.mark.parametrize("m2l", ["fp64", "auto", 6])
 @pytest.mark.parametrize("eps,tag,same_tol", [(1e-3, "e3", 1e-10), (1e-6, "e6", 3e-9),
                                               (1e-9, "e9", 1e-11)])
 def test_fmm_matches_reference_fmm_and_direct(cuda, eps, tag, same_tol, m2l):
@@ -29,9 +29,9 @@ def test_fmm_matches_reference_fmm_and_direct(cuda, eps, tag, same_tol, m2l):
     with the fp64 M2L the two FMMs differ only by fp64 summation order,
     amplified by the Tikhonov-damped check-to-equivalent solves in the surface
     representation (measured 2.9e-10 at eps 1e-6) and not at all by the
-    approximation.  The tensor-core M2L (int8 slices sized from eps) may add
-    up to eps / 100 against the reference FMM and stays within eps of the
-    direct sum."""
+    approximation.  The default low-rank M2L ("auto": truncated SVD at
+    eps / 100) and the tensor-core M2L (6 int8 slices) may add up to eps / 100
+    against the reference FMM and stay within eps of the direct sum."""
     b = _b()
     g = golden("fmm_apply.npz")
     src = b.FmmSources(g["src"], g["ch"], g["dip"])

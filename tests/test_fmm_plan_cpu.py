@@ -106,3 +106,26 @@ def test_order_for_eps_thresholds():
     assert order_for_eps(5e-8) == ("surface", 10, 1)
     assert order_for_eps(1e-9) == ("grid", 9, 2)
     assert order_for_eps(1e-10) == ("grid", 11, 2)
+
+
+def test_lowrank_m2l_factors():
+    """fmm_plan.m2l_factors: canon_k ~= A_k B_k within tol * sigma_max per key,
+    ranks far below nrep (the reason the low-rank M2L beats the dense
+    product), and the packing the C ABI expects (row-major, key order)."""
+    from paper_2111_10743_b200.fmm_plan import m2l_factors, m2l_lowrank_tol, unit_operators_grid
+    ops = unit_operators_grid(9, 2)
+    canon = ops["canon"]
+    tol = m2l_lowrank_tol(1e-9)
+    assert abs(tol - 1e-11) < 1e-24
+    ranks, a, b = m2l_factors(canon, tol)
+    nrep = canon.shape[1]
+    assert ranks.shape == (canon.shape[0],) and ranks.max() <= 80 and ranks.min() >= 1
+    assert a.size == b.size == int(ranks.sum()) * nrep
+    off = 0
+    for k, r in enumerate(ranks):
+        A = a[off * nrep:(off + r) * nrep].reshape(nrep, r)
+        B = b[off * nrep:(off + r) * nrep].reshape(r, nrep)
+        K = canon[k]
+        s0 = np.linalg.norm(K, 2)
+        assert np.linalg.norm(K - A @ B, 2) <= 1.01 * tol * s0
+        off += r
