@@ -119,6 +119,40 @@ def avn_summary():
     open(os.path.join(OUT, "apply_vs_n.md"), "w").write("\n".join(L) + "\n")
 
 
+def c5_summary():
+    """profiles/round1/config5_sweep.jsonl (scripts/config5_sweep.py) -> .md"""
+    rows = [json.loads(l) for l in open(os.path.join(OUT, "config5_sweep.jsonl"))]
+    pk = rows[0]["fp64_peak_tflops_measured"]
+    L = ["# BASELINE config 5 sweep (B200, round 1)", "",
+         f"Measured FP64 FMA-pipe peak in the same run: {pk:.1f} TFLOP/s (lb_probe_dfma).", "",
+         "## Direct P2P (charge, pot+grad, sources == targets, self skipped)", "",
+         "| N | GPU time | interactions/s | TFLOP/s (20 flop) | frac of measured FP64 | "
+         "CPU oracle, 16 threads (scaled sample) | speed-up |", "|---|---|---|---|---|---|---|"]
+    for r in rows:
+        if r.get("case", "").startswith("p2p"):
+            L.append(f"| {r['case'].split('=')[1]} | {r['gpu_s'] * 1e3:.2f} ms | "
+                     f"{r['interactions_per_s']:.3e} | {r['tflops_20flop']:.1f} | "
+                     f"{r['frac_of_measured_fp64']:.2f} | {r['cpu_oracle_s_scaled']:.2f} s "
+                     f"({r['cpu_sample']}) | {r['speedup_vs_cpu_oracle']:.0f}x |")
+    L += ["", "## FMM (FmmPlan on the device; the reference's tree, lists and unit operators; "
+          "M2L by the default low-rank factors)", "",
+          "| case | rep | plan s | apply ms | N^2/t | err vs direct (200 targets) | M2L ms | "
+          "X ms | leaf ms | reference apply (survey container, 8 vCPU) |",
+          "|---|---|---|---|---|---|---|---|---|---|"]
+    refs = {"N=1000000 eps=1e-06": "67.1 s", "N=1000000 eps=1e-09": "581.0 s"}
+    for r in rows:
+        if r.get("case", "").startswith("fmm"):
+            c = r["case"][4:]
+            st = r["stages_ms"]
+            L.append(f"| {c} | {r['rep']} m={r['m']} | {r['plan_s']:.2f} | {r['apply_s'] * 1e3:.1f} | "
+                     f"{r['effective_interactions_per_s']:.2e} | {r['err_vs_direct_200_targets']:.1e} | "
+                     f"{st['m2l']:.1f} | {st['x']:.1f} | {st['leaf']:.1f} | "
+                     f"{refs.get(c, 'not run (hours)')} |")
+    L += ["", "Earlier rows of this round with the tcgen05 int8 M2L: config5_sweep_tc_m2l.jsonl "
+          "(1e6 at 1e-9: 197 ms; 1e7 at 1e-9: 1.28 s)."]
+    open(os.path.join(OUT, "config5_sweep.md"), "w").write("\n".join(L) + "\n")
+
+
 def fmm_summary():
     L = launches(os.path.join(G, "launches_fmm.csv"))
     agg = defaultdict(lambda: [0, 0.0])
@@ -170,6 +204,8 @@ if __name__ == "__main__":
         bench_summary()
     if "avn" in what:
         avn_summary()
+    if "c5" in what:
+        c5_summary()
     if "fmm" in what:
         fmm_summary()
     if "full" in what:
