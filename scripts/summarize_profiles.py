@@ -97,7 +97,7 @@ def avn_summary():
         if r["far"] == "direct":
             far = "direct (exact fp64 sweeps, fused)"
         else:
-            m2l = "fp64 DGEMM" if r["m2l_slices"] == 0 else f"tcgen05 int8 S={r['m2l_slices']}"
+            m2l = {0: "fp64 dense DGEMM", -1: "low-rank fp64"}.get(r["m2l_slices"], f"tcgen05 int8 S={r['m2l_slices']}")
             far = f"fmm eps={r['eps']:g} ncrit={r['fmm_ncrit']} M2L {m2l}"
         st = r["stages_ms"]
         L.append(f"| {r['case']} | {r['N']} | {r['N_over']} | {r['nnz_per_kind']:.3g} | {far} | "
