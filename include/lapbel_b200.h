@@ -285,6 +285,13 @@ int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
  * about 1e3 * 2^(-7S) of max|K| max|x| (S = 8: fp64 roundoff).  Needs
  * nrep <= 2048. */
 int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
+/* Owned targets [t0, t1) in the caller's target order (t1 < 0: all, the
+ * default).  The tree and lists stay the reference's; M2L, X list, L2L and the
+ * leaf stage then run only for boxes with owned targets below them, and only
+ * the owned targets' outputs are defined.  A sharded apply gives every rank
+ * the same plan with its own row range; the outputs at owned
+ * targets equal the unsharded plan's. */
+int lb_fmm_plan_set_target_range(lb_fmm_plan* plan, int64_t t0, int64_t t1);
 /* Low-rank M2L (slices = -1 above): per canonical key k the factors of the
  * truncated SVD  canon_k ~= A_k B_k, A_k (nrep, r_k), B_k (r_k, nrep), both
  * row-major and concatenated over k in key order.  The product then costs

@@ -73,6 +73,7 @@ SIGNATURES = {
     "lb_fmm_plan_set_timing": [_P, _I32],
     "lb_fmm_plan_set_m2l": [_P, _I32],
     "lb_fmm_plan_set_m2l_factors": [_P, _P, _P, _P],
+    "lb_fmm_plan_set_target_range": [_P, _I64, _I64],
     "lb_near_map_count": [_P, _I64, _P, _P, _I64, _P, _P, _P],
     "lb_near_map_fill": [_P, _I64, _P, _P, _I64, _P, _P, _P, _P],
     "lb_corrections_build": [_P, _P],

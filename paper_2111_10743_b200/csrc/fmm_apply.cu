@@ -489,6 +489,7 @@ __device__ __forceinline__ void pair_a3(double tx, double ty, double tz, double 
 
 template <int ND, bool HD, int LEVEL, bool A3P = false>
 __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
+    const int64_t* __restrict__ items, double* __restrict__ part,
     const int64_t* __restrict__ leaves, const int64_t* __restrict__ u_off,
     const int64_t* __restrict__ u_list, const int64_t* __restrict__ w_off,
     const int64_t* __restrict__ w_list, const double* __restrict__ bctr,
@@ -509,15 +510,18 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
   __shared__ int64_t set_end[kLeafMaxSets + 1];
   __shared__ int64_t set_box[kLeafMaxSets];
   __shared__ double red[kLeafBT];
-  const int64_t b = leaves[blockIdx.x];
+  // work item: target leaf li, virtual sources [vb, ve), partial slot (or -1)
+  const int64_t li = items[4 * blockIdx.x], vb = items[4 * blockIdx.x + 1];
+  const int64_t ve = items[4 * blockIdx.x + 2], poff = items[4 * blockIdx.x + 3];
+  const int64_t b = leaves[li];
   const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
   // leaves hold few targets (~17 on average at ncrit 120): size the target
   // pass to the leaf and give the remaining threads other source phases
   int kTgt = 16;
   while (kTgt < t1 - t0 && kTgt < kLeafBT) kTgt <<= 1;
   const int kSplit = kLeafBT / kTgt;
-  const int64_t ub = u_off[blockIdx.x], nu = u_off[blockIdx.x + 1] - ub;
-  const int64_t wb = w_off[blockIdx.x], nw = w_off[blockIdx.x + 1] - wb;
+  const int64_t ub = u_off[li], nu = u_off[li + 1] - ub;
+  const int64_t wb = w_off[li], nw = w_off[li + 1] - wb;
   const int64_t nde = surface ? 1 : 0;
   const int64_t nsets_all = nu + nde + nw;
   const int ti = threadIdx.x % kTgt, ph = threadIdx.x / kTgt;
@@ -535,7 +539,8 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     double acc[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) acc[a] = 0.0;
-    for (int64_t sb0 = 0; sb0 < nsets_all; sb0 += kLeafMaxSets) {
+    int64_t vbase = 0;  // virtual index of this batch's first source
+    for (int64_t sb0 = 0; sb0 < nsets_all && vbase < ve; sb0 += kLeafMaxSets) {
       const int nsets = (int)min((int64_t)kLeafMaxSets, nsets_all - sb0);
       __syncthreads();
       if (threadIdx.x == 0) {  // prefix sizes of this batch of source sets
@@ -560,8 +565,9 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
       }
       __syncthreads();
       const int64_t total = set_end[nsets - 1];
-      for (int64_t v0 = 0; v0 < total; v0 += kTS) {
-        const int n = (int)min((int64_t)kTS, total - v0);
+      const int64_t vlo = max((int64_t)0, vb - vbase), vhi = min(total, ve - vbase);
+      for (int64_t v0 = vlo; v0 < vhi; v0 += kTS) {
+        const int n = (int)min((int64_t)kTS, vhi - v0);
         __syncthreads();
         for (int k = threadIdx.x; k < n; k += kLeafBT) {
           const int64_t v = v0 + k;
@@ -606,12 +612,17 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
           }
         }
         __syncthreads();
+        // unrolled over sources: independent pair chains give the FP64 pipe
+        // ILP (one pair at a time is a serial DADD-DFMA-MUFU-DFMA chain)
         if constexpr (A3P) {
+#pragma unroll 4
           for (int k = ph; k < n; k += kSplit) pair_a3(tx, ty, tz, nx, ny, nz, sh + k * S, acc);
         } else {
+#pragma unroll 4
           for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
         }
       }
+      vbase += total;
     }
     // combine the source phases (fixed order), one component at a time
     if (kSplit > 1) {
@@ -624,7 +635,10 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
           for (int q = 1; q < kSplit; ++q) acc[a] += red[q * kTgt + ti];
       }
     }
-    if (in && ph == 0) {
+    if (in && ph == 0 && poff >= 0) {  // split leaf: this item's partial (reduced in order later)
+#pragma unroll
+      for (int a = 0; a < NA; ++a) part[poff + (t - t0) * NA + a] = acc[a];
+    } else if (in && ph == 0) {
       if constexpr (A3P) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) tout[t * 3 + c] = acc[c];
@@ -636,6 +650,42 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
           for (int c = 0; c < NC; ++c) o[c] += acc[l * NC + c];
         }
       }
+    }
+  }
+}
+
+// items[4i+3] = slot[i] * width (doubles) for split items, -1 otherwise
+__global__ void scale_item_offsets_kernel(int64_t* __restrict__ items, const int64_t* __restrict__ slot,
+                                          int64_t n, int64_t width) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) items[4 * i + 3] = slot[i] < 0 ? -1 : slot[i] * width;
+}
+
+// partials of split leaves, summed in item order (deterministic) into the
+// leaf's outputs: generic acc[l * NC + c] -> tout[(l * nt + t) * 10 + c] (+=,
+// the grid L2T is already there); projected acc[a] -> tproj[t * 3 + a]
+template <int ND, int NC, bool A3P>
+__global__ void leaf_reduce_kernel(const int64_t* __restrict__ split_leaf, const int64_t* __restrict__ item_off,
+                                   const int64_t* __restrict__ items, const int64_t* __restrict__ leaves,
+                                   const int64_t* __restrict__ btgt, const double* __restrict__ part,
+                                   int64_t nt, double* __restrict__ tout) {
+  constexpr int NA = A3P ? 3 : ND * NC;
+  const int64_t si = blockIdx.x;
+  const int64_t li = split_leaf[si];
+  const int64_t b = leaves[li];
+  const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
+  const int64_t i0 = item_off[2 * si], i1 = item_off[2 * si + 1];
+  for (int64_t x = threadIdx.x; x < (t1 - t0) * NA; x += blockDim.x) {
+    const int64_t lt = x / NA;
+    const int a = (int)(x - lt * NA);
+    double v = 0.0;
+    for (int64_t it = i0; it < i1; ++it) v += part[items[4 * it + 3] + x];
+    const int64_t t = t0 + lt;
+    if (A3P) {
+      tout[t * 3 + a] = v;
+    } else {
+      const int l = a / NC, c = a - l * NC;
+      tout[((int64_t)l * nt + t) * 10 + c] += v;
     }
   }
 }
@@ -705,6 +755,16 @@ int build_device(lb_fmm_plan* P) {
     level_slot_off.push_back((int64_t)P->id_of.size());
   }
   const auto& S = P->slot_of;
+  // owned targets (lb_fmm_plan_set_target_range): a sharded apply replicates
+  // the reference's tree on every rank and runs the downward pass and the
+  // leaf stage only where its own targets are; owned(b) counts them below b
+  std::vector<int64_t> own_pref(t.nt + 1, 0);
+  for (int64_t q = 0; q < t.nt; ++q) {
+    const int64_t o = t.tgt_sorted[q];
+    const bool mine = P->own_t1 < 0 || (o >= P->own_t0 && o < P->own_t1);
+    own_pref[q + 1] = own_pref[q] + (mine ? 1 : 0);
+  }
+  auto owned = [&](int64_t b) { return own_pref[t.tgt_hi[b]] - own_pref[t.tgt_lo[b]]; };
   std::vector<double> ctr(3 * nb), hf(nb), spos_s(3 * t.ns), tpos_s(3 * t.nt);
   std::vector<int64_t> bsrc(2 * nb), btgt(2 * nb), octant(nb, 0);
   for (int64_t b = 0; b < nb; ++b) {
@@ -773,8 +833,14 @@ int build_device(lb_fmm_plan* P) {
           uc.push_back(s);
           upar.push_back(S[p]);
         }
-        dch.push_back(s);  // fmm.py:923-935: every child
-        dpar.push_back(S[p]);
+        // fmm.py:923-935 passes down to every child; children without targets
+        // in their subtree never reach an L2T or a leaf, so they are skipped
+        // (the results at the targets are unchanged; a plan whose targets are
+        // one rank's rows skips most of the downward pass)
+        if (owned(b) > 0) {
+          dch.push_back(s);
+          dpar.push_back(S[p]);
+        }
       }
       D.up_off.push_back((int64_t)uc.size());
       D.dn_off.push_back((int64_t)dch.size());
@@ -793,6 +859,7 @@ int build_device(lb_fmm_plan* P) {
   for (int l = 0; l < t.nlev; ++l) {
     const double hl = t.half / std::ldexp(1.0, l);  // fmm.py:879
     for (int64_t b : t.levels[l]) {
+      if (owned(b) == 0) continue;  // no (owned) targets below b: its local expansion is unused
       for (int64_t q = 0; q < t.vlist.size(b); ++q) {
         const int64_t s = t.vlist.row(b)[q];
         const int dx = (int)(t.ijk[3 * s] - t.ijk[3 * b]);
@@ -837,6 +904,7 @@ int build_device(lb_fmm_plan* P) {
   // X list (fmm.py:891-911): boxes with sourceful X entries
   std::vector<int64_t> xb, xo{0}, xl;
   for (int64_t b = 0; b < nb; ++b) {
+    if (owned(b) == 0) continue;  // as for M2L
     bool any = false;
     for (int64_t q = 0; q < t.xlist.size(b); ++q) {
       const int64_t x = t.xlist.row(b)[q];
@@ -851,7 +919,7 @@ int build_device(lb_fmm_plan* P) {
   // leaf stage (fmm.py:940-988): target leaves, their U (with sources) and W lists
   std::vector<int64_t> tl, uo{0}, ul, wo{0}, wl;
   for (int64_t b = 0; b < nb; ++b) {
-    if (!t.is_leaf[b] || t.tgt_hi[b] == t.tgt_lo[b]) continue;
+    if (!t.is_leaf[b] || owned(b) == 0) continue;
     tl.push_back(S[b]);
     for (int64_t q = 0; q < t.ulist.size(b); ++q) {
       const int64_t u = t.ulist.row(b)[q];
@@ -862,6 +930,46 @@ int build_device(lb_fmm_plan* P) {
     wo.push_back((int64_t)wl.size());
   }
   D.n_tleaf = (int64_t)tl.size();
+  // work items: a leaf's virtual source list [U sources | own DE set | W sets]
+  // is cut into segments of at most ~2^20 (target, source) pairs, so no block
+  // is the kernel's critical path (measured: SMs idle half of the leaf stage
+  // on config 3 without this); split leaves reduce their partials in order
+  {
+    std::vector<int64_t> items, islot, sleaf, srange;
+    int64_t slots = 0;
+    for (int64_t li = 0; li < D.n_tleaf; ++li) {
+      const int64_t b = P->id_of[tl[li]];
+      const int64_t ntl = t.tgt_hi[b] - t.tgt_lo[b];
+      int64_t vtot = (P->rep == 0 ? nrep : 0) + (wo[li + 1] - wo[li]) * (int64_t)nrep;
+      for (int64_t q = uo[li]; q < uo[li + 1]; ++q) {
+        const int64_t u = P->id_of[ul[q]];
+        vtot += t.src_hi[u] - t.src_lo[u];
+      }
+      const int64_t seg = std::max<int64_t>(1024, ((int64_t)1 << 20) / std::max<int64_t>(ntl, 1));
+      const int64_t nseg = std::max<int64_t>(1, ceil_div(vtot, seg));
+      if (nseg > 1) {
+        sleaf.push_back(li);
+        srange.push_back((int64_t)(items.size() / 4));
+        srange.push_back((int64_t)(items.size() / 4) + nseg);
+      }
+      for (int64_t k = 0; k < nseg; ++k) {
+        items.push_back(li);
+        items.push_back(k * seg);
+        items.push_back(k + 1 == nseg ? vtot : (k + 1) * seg);
+        items.push_back(-1);
+        islot.push_back(nseg == 1 ? -1 : slots);
+        if (nseg > 1) slots += ntl;
+      }
+    }
+    D.n_items = (int64_t)(items.size() / 4);
+    D.n_split = (int64_t)sleaf.size();
+    D.part_doubles = slots;
+    D.part_width = -1;
+    LB_TRY(upload(&D.leaf_items, items));
+    LB_TRY(upload(&D.leaf_item_slot, islot));
+    LB_TRY(upload(&D.split_leaf, sleaf));
+    LB_TRY(upload(&D.split_item_off, srange));  // [first item, end) per split leaf
+  }
   LB_TRY(upload(&D.t_leaves, tl));
   LB_TRY(upload(&D.u_off, uo));
   LB_TRY(upload(&D.u_list, ul));
@@ -1167,25 +1275,54 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       LB_CHECK_LAUNCH();
     }
     mark(6);
+    // partial slots of split leaves for this chunk's accumulator width
+    {
+      const int64_t na = proj_out ? 3 : (int64_t)ND * ncomp(level);
+      const int64_t need = D.part_doubles * na;
+      if (need > D.leaf_part_cap) {
+        cudaFree(D.leaf_part);
+        D.leaf_part = nullptr;
+        LB_CUDA(cudaMalloc((void**)&D.leaf_part, sizeof(double) * std::max<int64_t>(need, 1)));
+        D.leaf_part_cap = need;
+      }
+      // items[4i+3] holds the partial offset in units of (target slots); scale
+      // it to doubles for this width once per width change
+      if (D.part_width != na) {
+        scale_item_offsets_kernel<<<(unsigned)ceil_div(std::max<int64_t>(D.n_items, 1), 256), 256, 0, st>>>(
+            D.leaf_items, D.leaf_item_slot, D.n_items, na);
+        LB_CHECK_LAUNCH();
+        D.part_width = na;
+      }
+    }
 #define LB_LEAF(HD, LV)                                                                        \
-  leaf_kernel<ND, HD, LV><<<(unsigned)D.n_tleaf, kLeafBT, 0, st>>>(                                 \
+  leaf_kernel<ND, HD, LV><<<(unsigned)D.n_items, kLeafBT, 0, st>>>(                                 \
+      D.leaf_items, D.leaf_part,                                                                \
       D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,       \
       D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,      \
-      surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout)
+      surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout);                                      \
+  LB_CHECK_LAUNCH();                                                                           \
+  if (D.n_split > 0)                                                                           \
+    leaf_reduce_kernel<ND, ncomp(LV), false><<<(unsigned)D.n_split, 128, 0, st>>>(             \
+        D.split_leaf, D.split_item_off, D.leaf_items, D.t_leaves, D.btgt, D.leaf_part, t.nt, D.tout)
     if constexpr (ND == 2) {
       if (proj_out) {  // projected leaf (fmm_apply_a3proj): writes tproj, not tout
-        leaf_kernel<2, true, 2, true><<<(unsigned)D.n_tleaf, kLeafBT, 0, st>>>(
+        leaf_kernel<2, true, 2, true><<<(unsigned)D.n_items, kLeafBT, 0, st>>>(
+            D.leaf_items, D.leaf_part,
             D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,
             D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,
             surface ? P->ue_scale : 1.0, D.loc, D.up, D.tproj, D.tnrm, D.snrm);
+        LB_CHECK_LAUNCH();
+        if (D.n_split > 0)
+          leaf_reduce_kernel<2, 1, true><<<(unsigned)D.n_split, 128, 0, st>>>(
+              D.split_leaf, D.split_item_off, D.leaf_items, D.t_leaves, D.btgt, D.leaf_part, t.nt, D.tproj);
         LB_CHECK_LAUNCH();
       }
     }
     if (proj_out) {
     } else if (hd) {
-      if (level == 0) LB_LEAF(true, 0); else if (level == 1) LB_LEAF(true, 1); else LB_LEAF(true, 2);
+      if (level == 0) { LB_LEAF(true, 0); } else if (level == 1) { LB_LEAF(true, 1); } else { LB_LEAF(true, 2); }
     } else {
-      if (level == 0) LB_LEAF(false, 0); else if (level == 1) LB_LEAF(false, 1); else LB_LEAF(false, 2);
+      if (level == 0) { LB_LEAF(false, 0); } else if (level == 1) { LB_LEAF(false, 1); } else { LB_LEAF(false, 2); }
     }
 #undef LB_LEAF
     LB_CHECK_LAUNCH();
@@ -1212,7 +1349,8 @@ void fmm_release_device(lb_fmm_plan* P) {
                   D.p2m_leaves, D.up_child, D.up_parent, D.dn_child, D.dn_parent, D.v_src,
                   D.v_tgt_pair_off, D.v_tgts, D.v_off_idx, D.v_scale, D.x_boxes, D.x_off,
                   D.x_leaves, D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.cs, D.vs, D.up,
-                  D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct, D.tnrm, D.tproj, D.snrm};
+                  D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct, D.tnrm, D.tproj, D.snrm,
+                  D.leaf_items, D.leaf_item_slot, D.split_leaf, D.split_item_off, D.leaf_part};
   for (void* p : ptrs) cudaFree(p);
   if (P->rep == 0) cudaFree(D.loc);
   cudaFree(D.oz_a);
@@ -1294,6 +1432,17 @@ int lb_fmm_plan_set_m2l(lb_fmm_plan* P, int slices) {
   if (slices != 0 && P->nrep > 2048)
     return fail(LB_ERR_ARG, "lb_fmm_plan_set_m2l: tensor-core M2L needs nrep <= 2048");
   P->m2l_slices = slices;
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_target_range(lb_fmm_plan* P, int64_t t0, int64_t t1) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  if (t1 >= 0 && (t0 < 0 || t0 > t1 || t1 > P->tree.nt))
+    return fail(LB_ERR_SHAPE, "lb_fmm_plan_set_target_range: range outside [0, nt]");
+  if (t0 == P->own_t0 && t1 == P->own_t1) return LB_OK;
+  P->own_t0 = t0;
+  P->own_t1 = t1;
+  fmm_release_device(P);  // lists are rebuilt on the next apply
   return LB_OK;
 }
 

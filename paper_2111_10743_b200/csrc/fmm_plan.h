@@ -51,6 +51,16 @@ struct FmmDevice {
   // leaf stage
   int64_t *t_leaves = nullptr, *u_off = nullptr, *u_list = nullptr, *w_off = nullptr, *w_list = nullptr;
   int64_t n_tleaf = 0;
+  // leaf work items: (target-leaf index, virtual source range [vb, ve),
+  // partial offset or -1 for a leaf done by one item); heavy leaves are split
+  // so no block carries more than ~2^20 pairs (load balance, not arithmetic)
+  int64_t* leaf_items = nullptr;             // (n_items, 4)
+  int64_t n_items = 0;
+  int64_t *split_leaf = nullptr, *split_item_off = nullptr;  // split leaves, their item ranges
+  int64_t n_split = 0, part_doubles = 0;     // partial slots (targets x items) of split leaves
+  int64_t* leaf_item_slot = nullptr;        // per item: first partial target slot, or -1
+  double* leaf_part = nullptr;
+  int64_t leaf_part_cap = 0, part_width = -1;
   // work arrays (per nd)
   double *cs = nullptr, *vs = nullptr;       // sorted charges (nd,ns), dipoles (nd,ns,3)
   double *up = nullptr, *dc = nullptr, *loc = nullptr;  // (nbox, nd, nrep) slot order
@@ -95,6 +105,7 @@ struct lb_fmm_plan {
   std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
   std::vector<double> stage_ms;             // last apply's per-stage device times
   bool timing = false;
+  int64_t own_t0 = 0, own_t1 = -1;          // owned targets [t0, t1) (original order); t1 < 0: all
   int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices;
                                             // -1: low-rank factors (fp64 DGEMM pair)
   std::vector<int32_t> lr_rank;             // per canonical key

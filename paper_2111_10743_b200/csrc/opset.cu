@@ -462,7 +462,8 @@ struct lb_opset {
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double *f_ch = nullptr, *f_ch3 = nullptr, *f_dp = nullptr;
   double *f_pot = nullptr, *f_grad = nullptr, *f_hess = nullptr;
-  double* f_proj = nullptr;  // (4, nr): projected leaf outputs of the 2-density A3 call
+  double* f_proj = nullptr;  // (3, nt): projected leaf outputs of the 2-density A3 call
+  int64_t fmm_nt = 0;        // the plan's targets: nr, or all n (replicated plan, owned range)
 };
 
 namespace lb {
@@ -614,7 +615,10 @@ __global__ void dipole_kernel(const double* __restrict__ c, const double* __rest
 }
 
 // FMM outputs -> the functor outputs, written as a one-segment stream-K layout
-__global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t n,
+// pot/grad/hess/proj point at this handle's first row inside the plan's target
+// arrays, whose per-density stride is ntp (= n for a plan on the handle's rows,
+// = all nodes for a replicated plan with an owned-target range)
+__global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t n, int64_t ntp,
                                const double* __restrict__ pot, const double* __restrict__ grad,
                                const double* __restrict__ hess, SkLayout L, int nout,
                                double* __restrict__ part, const double* __restrict__ curv,
@@ -623,11 +627,11 @@ __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t
   if (i >= n) return;
   const double nx = nrm[3 * i], ny = nrm[3 * i + 1], nz = nrm[3 * i + 2];
   auto ng = [&](int l) {  // n . grad_l
-    const double* g = grad + ((int64_t)l * n + i) * 3;
+    const double* g = grad + ((int64_t)l * ntp + i) * 3;
     return nx * g[0] + ny * g[1] + nz * g[2];
   };
   auto nhn = [&](int l) {  // n . hess_l . n
-    const double* H = hess + ((int64_t)l * n + i) * 9;
+    const double* H = hess + ((int64_t)l * ntp + i) * 9;
     return nx * (H[0] * nx + H[1] * ny + H[2] * nz) + ny * (H[3] * nx + H[4] * ny + H[5] * nz) +
            nz * (H[6] * nx + H[7] * ny + H[8] * nz);
   };
@@ -635,22 +639,22 @@ __global__ void project_kernel(int kind, const double* __restrict__ nrm, int64_t
   switch (kind) {
     case FK_S: case FK_D: a[0] = pot[i]; break;
     case FK_A3A: a[0] = pot[i]; a[1] = -ng(0); break;
-    case FK_A3B: a[0] = -ng(0); a[1] = pot[n + i]; a[2] = -ng(1); a[3] = nhn(1) + ng(2); break;
+    case FK_A3B: a[0] = -ng(0); a[1] = pot[ntp + i]; a[2] = -ng(1); a[3] = nhn(1) + ng(2); break;
     // fused A3 call 2 on two FMM densities: X = (charge c0, dipole -c1 n) and
     // B = (charge c1): a0 = FarA3b's a0 + a3 - 2H a2 = -n.grad X + n.H_B.n + 2H n.grad B
     case FK_A3M: {  // + the projected leaf stage [-n.grad X + n.H_B.n, pot B, n.grad B]
-      a[0] = fma(2.0 * curv[i], ng(1) + proj[2 * n + i], (nhn(1) - ng(0)) + proj[i]);
-      a[1] = pot[n + i] + proj[n + i];
+      a[0] = fma(2.0 * curv[i], ng(1) + proj[2 * ntp + i], (nhn(1) - ng(0)) + proj[i]);
+      a[1] = pot[ntp + i] + proj[ntp + i];
       break;
     }
-    case FK_A2A: a[0] = pot[i]; a[1] = pot[n + i]; a[2] = -ng(0); a[3] = nhn(0) + ng(1); break;
-    case FK_A2B: a[0] = pot[i]; a[1] = pot[n + i]; break;
+    case FK_A2A: a[0] = pot[i]; a[1] = pot[ntp + i]; a[2] = -ng(0); a[3] = nhn(0) + ng(1); break;
+    case FK_A2B: a[0] = pot[i]; a[1] = pot[ntp + i]; break;
     case FK_A1A:
       a[0] = pot[i];
       for (int k = 0; k < 3; ++k) a[1 + k] = -grad[i * 3 + k];
       break;
     case FK_A1B:
-      a[0] = -(grad[(0 * n + i) * 3 + 0] + grad[(1 * n + i) * 3 + 1] + grad[(2 * n + i) * 3 + 2]);
+      a[0] = -(grad[(0 * ntp + i) * 3 + 0] + grad[(1 * ntp + i) * 3 + 1] + grad[(2 * ntp + i) * 3 + 2]);
       break;
   }
   const int64_t t = i / L.tt;
@@ -714,9 +718,10 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
   }
   LB_CHECK_LAUNCH();
   if (kind == FK_A3M) {  // projected leaf stage (fmm_plan.h: fmm_apply_a3proj)
-    if (!h->f_proj) LB_CUDA(cudaMalloc((void**)&h->f_proj, sizeof(double) * 3 * std::max<int64_t>(n, 1)));
-    const int rc = fmm_apply_a3proj(h->fmm, chp, dpp, h->d.normals + 3 * h->r0, h->d.over_normals,
-                                    h->f_pot, h->f_grad, h->f_hess, h->f_proj, st);
+    if (!h->f_proj) LB_CUDA(cudaMalloc((void**)&h->f_proj, sizeof(double) * 3 * std::max<int64_t>(h->fmm_nt, 1)));
+    const double* tn = h->fmm_nt == h->nr ? h->d.normals + 3 * h->r0 : h->d.normals;
+    const int rc = fmm_apply_a3proj(h->fmm, chp, dpp, tn, h->d.over_normals, h->f_pot, h->f_grad,
+                                    h->f_hess, h->f_proj, st);
     if (rc != LB_OK) return fail(rc, std::string("far_stage(A3 two densities): ") + lb_last_error_string());
   } else {
     int rc = lb_fmm_apply(h->fmm, chp, dpp, nd, cm, dm, level, h->f_pot, h->f_grad, h->f_hess, st);
@@ -731,9 +736,10 @@ int far_stage(lb_opset* h, FarKind kind, int nv, const double* const* in, bool a
   l1.G = l1.tiles;
   l1.kmax = 1;
   const int nout = far_nout(kind);
-  project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>((int)kind, h->d.normals + 3 * h->r0, n, h->f_pot,
-                                                             h->f_grad, h->f_hess, l1, nout, h->part,
-                                                             h->d.curvature + h->r0, h->f_proj);
+  const int64_t ntp = h->fmm_nt, toff = ntp == h->nr ? 0 : h->r0;
+  project_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+      (int)kind, h->d.normals + 3 * h->r0, n, ntp, h->f_pot + toff, h->f_grad + 3 * toff,
+      h->f_hess + 9 * toff, l1, nout, h->part, h->d.curvature + h->r0, h->f_proj ? h->f_proj + toff : nullptr);
   LB_CHECK_LAUNCH();
   *L = l1;
   return LB_OK;
@@ -1015,35 +1021,43 @@ int lb_opset_destroy(lb_opset* h) {
 int lb_opset_set_fmm(lb_opset* h, lb_fmm_plan* plan) {
   using namespace lb;
   if (!h) return fail(LB_ERR_ARG, "lb_opset_set_fmm: null handle");
-  h->fmm = plan;
-  if (!plan || h->f_ch) return LB_OK;
+  h->fmm = nullptr;
+  if (!plan) return LB_OK;
   int64_t sizes[10];
   LB_TRY(lb_fmm_plan_info(plan, sizes, nullptr));
-  if (sizes[2] != h->d.n_over || sizes[3] != h->nr) {
-    h->fmm = nullptr;
+  // targets: this handle's rows, or every node (a replicated plan whose owned
+  // target range is this handle's rows, lb_fmm_plan_set_target_range)
+  if (sizes[2] != h->d.n_over || (sizes[3] != h->nr && sizes[3] != h->d.n))
     return fail(LB_ERR_SHAPE, "lb_opset_set_fmm: plan sources/targets must be over_nodes/nodes");
+  const int64_t no = h->d.n_over, nt = sizes[3];
+  if (!h->f_ch || nt > h->fmm_nt) {
+    for (double** p : {&h->f_ch, &h->f_ch3, &h->f_dp, &h->f_pot, &h->f_grad, &h->f_hess, &h->f_proj}) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+    cudaError_t e = cudaSuccess;
+    auto A = [&](double** p, int64_t k) { if (e == cudaSuccess) e = cudaMalloc((void**)p, sizeof(double) * k); };
+    A(&h->f_ch, 3 * no);
+    A(&h->f_ch3, 3 * no);
+    A(&h->f_dp, 9 * no);
+    A(&h->f_pot, 3 * nt);
+    A(&h->f_grad, 9 * nt);
+    A(&h->f_hess, 27 * nt);
+    if (e == cudaSuccess) e = cudaMemset(h->f_ch3, 0, sizeof(double) * 3 * no);
+    if (e == cudaSuccess) e = cudaMemset(h->f_dp, 0, sizeof(double) * 9 * no);
+    if (e == cudaSuccess) e = cudaMemset(h->f_ch, 0, sizeof(double) * 3 * no);
+    if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("lb_opset_set_fmm: ") + cudaGetErrorString(e));
   }
-  const int64_t no = h->d.n_over, n = h->nr;
-  cudaError_t e = cudaSuccess;
-  auto A = [&](double** p, int64_t k) { if (e == cudaSuccess) e = cudaMalloc((void**)p, sizeof(double) * k); };
-  A(&h->f_ch, 3 * no);
-  A(&h->f_ch3, 3 * no);
-  A(&h->f_dp, 9 * no);
-  A(&h->f_pot, 3 * n);
-  A(&h->f_grad, 9 * n);
-  A(&h->f_hess, 27 * n);
-  if (e == cudaSuccess) e = cudaMemset(h->f_ch3, 0, sizeof(double) * 3 * no);
-  if (e == cudaSuccess) e = cudaMemset(h->f_dp, 0, sizeof(double) * 9 * no);
-  if (e == cudaSuccess) e = cudaMemset(h->f_ch, 0, sizeof(double) * 3 * no);
-  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("lb_opset_set_fmm: ") + cudaGetErrorString(e));
+  h->fmm_nt = nt;
   // the one-segment projection layout must fit the partial buffer
-  const int64_t need = ceil_div(n, 64) * 64 * 4;
+  const int64_t need = ceil_div(h->nr, 64) * 64 * 4;
   if (need > h->part_cap) {
     cudaFree(h->part);
     h->part = nullptr;
     LB_CUDA(cudaMalloc(&h->part, sizeof(double) * need));
     h->part_cap = need;
   }
+  h->fmm = plan;
   return LB_OK;
 }
 

@@ -275,6 +275,7 @@ def _bind():
                                    ctypes.c_uint32, I32, P, P, P, P]
         L.lb_fmm_plan_set_timing.argtypes = [P, I32]
         L.lb_fmm_plan_set_m2l_factors.argtypes = [P, P, P, P]
+        L.lb_fmm_plan_set_target_range.argtypes = [P, I64, I64]
         L.lb_fmm_stage_times.argtypes = [P, P]
         _bound = True
     return L
@@ -451,6 +452,13 @@ class FmmPlan:
 
     def set_timing(self, on=True):
         _lib.check(self._L.lb_fmm_plan_set_timing(self._h, 1 if on else 0))
+
+    def set_target_range(self, t0: int = 0, t1: int = -1):
+        """Owned targets [t0, t1) (lb_fmm_plan_set_target_range; t1 < 0: all).
+        The tree and lists stay the reference's; only the owned targets'
+        outputs are computed (a sharded apply's rows)."""
+        _lib.check(self._L.lb_fmm_plan_set_target_range(self._h, int(t0), int(t1)),
+                   "lb_fmm_plan_set_target_range")
 
     def stage_times(self):
         """Device ms of gather+P2M, M2M, M2L, X, L2L, L2T, leaf, scatter, total."""

@@ -134,8 +134,12 @@ class ShardedOperatorSet:
         kinds = list(FORMULATIONS[self.formulation])
         self.dev = DeviceOperator(disc, corrections, kinds, row0=r0, nrows=nr)
         if far == "fmm":
+            # the reference's tree over ALL sources and targets on every rank
+            # (deterministic, identical), downward pass + leaf stage only for
+            # this rank's target rows: its outputs equal the unsharded FMM's
             from .fmm_plan import FmmPlan
-            self._plan = FmmPlan(disc.over_nodes, disc.nodes[r0:r0 + nr], self.eps)
+            self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps)
+            self._plan.set_target_range(r0, r0 + nr)
             self.dev.set_fmm(self._plan)
         elif self.formulation == "a3":
             # fused second sweep; Phi is global (every rank computes it whole)

@@ -59,8 +59,9 @@ def test_emulated_shards_match_unsharded(cuda, fixture, form, far):
         devs, plans = [], []
         for r0, nr in parts:
             d = DeviceOperator(geom, cset, list(FORMULATIONS[form]), row0=r0, nrows=nr)
-            if far == "fmm":
-                pl = FmmPlan(geom.over_nodes, geom.nodes[r0:r0 + nr], 1e-10)
+            if far == "fmm":  # replicated tree, owned target rows (sharding.py)
+                pl = FmmPlan(geom.over_nodes, geom.nodes, 1e-10)
+                pl.set_target_range(r0, r0 + nr)
                 d.set_fmm(pl)
                 plans.append(pl)
             devs.append(d)
@@ -74,6 +75,5 @@ def test_emulated_shards_match_unsharded(cuda, fixture, form, far):
             d.set_phi0(phi0)
         got = _emulate(devs, parts, code, tau, torch)
         err = (got - ref).abs().max().item() / ref.abs().max().item()
-        # FMM shards build their own trees over their targets: a different,
-        # equally valid eps = 1e-10 approximation (100 x eps after S''+D' noise)
-        assert err < (1e-12 if far == "direct" else 1e-8), (world, err)
+        # FMM shards share the unsharded tree: the same approximation
+        assert err < 1e-12, (world, err)
