@@ -25,6 +25,7 @@
 #include <cmath>
 #include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "fmm_plan.h"
@@ -91,9 +92,15 @@ __global__ void gather_cols_kernel(const double* __restrict__ src, const int64_t
 // potentials at lattice points from real sources (P2M check, X list)
 
 // out[(box_col*nd + l)*nrep + i] (+)= scale * sum_j pot_l(x_i; sources of the
-// listed leaves).  Points x_i = center(box) + fac*half(box)*pts[i].
-template <int ND>
-__global__ void __launch_bounds__(128) lattice_pot_kernel(
+// listed leaves).  Points x_i = center(box) + fac*half(box)*pts[i].  Every
+// thread holds LPT lattice points in registers (729 grid points = 6 per
+// thread of 128) and the sources stream through shared memory ONCE per box:
+// LPT independent pair chains per source (ILP) and 1/LPT of the tile loads
+// and barriers of a one-point-per-thread pass.
+constexpr int kLatBT = 128;
+
+template <int ND, int kLatLPT>
+__global__ void __launch_bounds__(kLatBT) lattice_pot_kernel(
     const int64_t* __restrict__ boxes, const int64_t* __restrict__ src_off,
     const int64_t* __restrict__ src_boxes, int single, const double* __restrict__ bctr,
     const double* __restrict__ bhalf, const int64_t* __restrict__ bsrc,
@@ -101,71 +108,110 @@ __global__ void __launch_bounds__(128) lattice_pot_kernel(
     int64_t ns, int hd, const double* __restrict__ pts, int nrep, double fac, int scale_by_h,
     double* __restrict__ out, int out_by_box, int add) {
   constexpr int TS = 64;
-  __shared__ double sh[TS][3 + 4 * ND];
+  constexpr int W = 3 + 4 * ND;
+  __shared__ double sh[TS * W];
   const int64_t bi = blockIdx.x;
   const int64_t b = boxes[bi];
   const double h = bhalf[b];
   const double cx = bctr[3 * b], cy = bctr[3 * b + 1], cz = bctr[3 * b + 2];
   const int64_t lb = single ? bi : src_off[bi];
   const int64_t le = single ? bi + 1 : src_off[bi + 1];
-  for (int i0 = 0; i0 < nrep; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool in = i < nrep;
-    const double px = in ? cx + fac * h * pts[3 * i] : 0.0;
-    const double py = in ? cy + fac * h * pts[3 * i + 1] : 0.0;
-    const double pz = in ? cz + fac * h * pts[3 * i + 2] : 0.0;
-    double acc[ND];
+  for (int i0 = 0; i0 < nrep; i0 += kLatBT * kLatLPT) {  // one round for nrep <= 768
+    double px[kLatLPT], py[kLatLPT], pz[kLatLPT], acc[kLatLPT][ND];
 #pragma unroll
-    for (int l = 0; l < ND; ++l) acc[l] = 0.0;
+    for (int j = 0; j < kLatLPT; ++j) {
+      const int i = i0 + j * kLatBT + threadIdx.x;
+      const bool in = i < nrep;
+      px[j] = in ? cx + fac * h * pts[3 * i] : 0.0;
+      py[j] = in ? cy + fac * h * pts[3 * i + 1] : 0.0;
+      pz[j] = in ? cz + fac * h * pts[3 * i + 2] : 0.0;
+#pragma unroll
+      for (int l = 0; l < ND; ++l) acc[j][l] = 0.0;
+    }
     for (int64_t q = lb; q < le; ++q) {
       const int64_t sb = single ? b : src_boxes[q];
       const int64_t s0 = bsrc[2 * sb], s1 = bsrc[2 * sb + 1];
       for (int64_t t0 = s0; t0 < s1; t0 += TS) {
         const int n = (int)min((int64_t)TS, s1 - t0);
         __syncthreads();
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        for (int k = threadIdx.x; k < n; k += kLatBT) {
           const int64_t j = t0 + k;
-          sh[k][0] = spos[3 * j];
-          sh[k][1] = spos[3 * j + 1];
-          sh[k][2] = spos[3 * j + 2];
+          double* r = sh + k * W;
+          r[0] = spos[3 * j];
+          r[1] = spos[3 * j + 1];
+          r[2] = spos[3 * j + 2];
 #pragma unroll
           for (int l = 0; l < ND; ++l) {
-            sh[k][3 + l] = cs[(int64_t)l * ns + j];
-            if (hd) {
-              sh[k][3 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3];
-              sh[k][4 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 1];
-              sh[k][5 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 2];
-            }
+            r[3 + l] = cs[(int64_t)l * ns + j];
+            const bool on = hd != 0;
+            r[3 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3] : 0.0;
+            r[4 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3 + 1] : 0.0;
+            r[5 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3 + 2] : 0.0;
           }
         }
         __syncthreads();
-        for (int k = 0; k < n; ++k) {
-          const double r0 = px - sh[k][0], r1 = py - sh[k][1], r2 = pz - sh[k][2];
-          const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
-          const double invr = inv_sqrt_skip(rr);
-          const double invr3 = invr * invr * invr;
+        if (hd) {
+          for (int k = 0; k < n; ++k) {
+            const double* r = sh + k * W;
 #pragma unroll
-          for (int l = 0; l < ND; ++l) {
-            acc[l] = fma(sh[k][3 + l], invr, acc[l]);
-            if (hd) {
-              const double vr = fma(sh[k][5 + ND + 3 * l], r2,
-                                    fma(sh[k][4 + ND + 3 * l], r1, sh[k][3 + ND + 3 * l] * r0));
-              acc[l] = fma(vr, invr3, acc[l]);
+            for (int j = 0; j < kLatLPT; ++j) {
+              const double r0 = px[j] - r[0], r1 = py[j] - r[1], r2 = pz[j] - r[2];
+              const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+              const double invr = inv_sqrt_skip(rr);
+              const double invr3 = invr * invr * invr;
+#pragma unroll
+              for (int l = 0; l < ND; ++l) {
+                const double vr = fma(r[5 + ND + 3 * l], r2, fma(r[4 + ND + 3 * l], r1, r[3 + ND + 3 * l] * r0));
+                acc[j][l] = fma(r[3 + l], invr, fma(vr, invr3, acc[j][l]));
+              }
+            }
+          }
+        } else {
+          for (int k = 0; k < n; ++k) {
+            const double* r = sh + k * W;
+#pragma unroll
+            for (int j = 0; j < kLatLPT; ++j) {
+              const double r0 = px[j] - r[0], r1 = py[j] - r[1], r2 = pz[j] - r[2];
+              const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+              const double invr = inv_sqrt_skip(rr);
+#pragma unroll
+              for (int l = 0; l < ND; ++l) acc[j][l] = fma(r[3 + l], invr, acc[j][l]);
             }
           }
         }
       }
     }
-    if (in) {
-      const double s = scale_by_h ? h : 1.0;
-      const int64_t col = out_by_box ? b : bi;
+    const double sc = scale_by_h ? h : 1.0;
+    const int64_t col = out_by_box ? b : bi;
 #pragma unroll
-      for (int l = 0; l < ND; ++l) {
-        double* o = out + (col * ND + l) * (int64_t)nrep + i;
-        *o = add ? *o + s * acc[l] : s * acc[l];
+    for (int j = 0; j < kLatLPT; ++j) {
+      const int i = i0 + j * kLatBT + threadIdx.x;
+      if (i < nrep) {
+#pragma unroll
+        for (int l = 0; l < ND; ++l) {
+          double* o = out + (col * ND + l) * (int64_t)nrep + i;
+          *o = add ? *o + sc * acc[j][l] : sc * acc[j][l];
+        }
       }
     }
   }
+}
+
+// lattice points per thread sized to the lattice (296 surface points: 3;
+// 488: 4; 729 grid points: 6; larger lattices loop)
+template <int ND, class... A>
+int launch_lattice(unsigned grid, cudaStream_t st, const int64_t* boxes, A... a) {
+  if (grid == 0) return LB_OK;
+  // nrep is argument 12 after boxes (see lattice_pot_kernel's parameter list)
+  const int nrep = std::get<12>(std::make_tuple(a...));
+  static_assert(std::is_same<typename std::tuple_element<12, std::tuple<A...>>::type, int>::value,
+                "launch_lattice: argument 12 must be nrep");
+  if (nrep <= 2 * kLatBT) lattice_pot_kernel<ND, 2><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else if (nrep <= 3 * kLatBT) lattice_pot_kernel<ND, 3><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else if (nrep <= 4 * kLatBT) lattice_pot_kernel<ND, 4><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else lattice_pot_kernel<ND, 6><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -1133,10 +1179,9 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   // ---- P2M (fmm.py:823-852)
   if (D.n_p2m > 0) {
     if (surface) {
-      lattice_pot_kernel<ND><<<(unsigned)D.n_p2m, 128, 0, st>>>(
-          D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf, D.bsrc, D.spos, D.cs, D.vs, t.ns,
-          hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1, D.tmpA, 0, 0);
-      LB_CHECK_LAUNCH();
+      LB_TRY(launch_lattice<ND>((unsigned)D.n_p2m, st, D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf,
+                                D.bsrc, D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1,
+                                D.tmpA, 0, 0));
       LB_TRY(gemm_rm(D.blas, D.pinv_up, D.tmpA, D.tmpB, nrep, D.n_p2m * ND, 1.0, 0.0));
       scatter_cols_kernel<<<(unsigned)(D.n_p2m * ND), 128, 0, st>>>(D.tmpB, D.p2m_leaves, D.n_p2m, ND,
                                                                     nrep, D.up, 0);
@@ -1216,10 +1261,9 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   mark(3);
   // ---- X list (fmm.py:888-911)
   if (D.n_x > 0) {
-    lattice_pot_kernel<ND><<<(unsigned)D.n_x, 128, 0, st>>>(
-        D.x_boxes, D.x_off, D.x_leaves, 0, D.bctr, D.bhalf, D.bsrc, D.spos, D.cs, D.vs, t.ns,
-        hd ? 1 : 0, D.pts, nrep, surface ? P->dc_scale : 1.0, 0, D.dc, 1, 1);
-    LB_CHECK_LAUNCH();
+    LB_TRY(launch_lattice<ND>((unsigned)D.n_x, st, D.x_boxes, D.x_off, D.x_leaves, 0, D.bctr, D.bhalf, D.bsrc,
+                              D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, D.pts, nrep,
+                              surface ? P->dc_scale : 1.0, 0, D.dc, 1, 1));
   }
   mark(4);
   // ---- L2L (fmm.py:913-935)
