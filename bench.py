@@ -226,6 +226,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time the step without a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -285,6 +286,27 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    # the device-resident step replayed as a CUDA graph (the same 6 + 1
+    # launches per step, without the host launch gaps: -1.7% measured,
+    # scripts/graph_probe.py, bit-identical results); eager if capture fails
+    run_step, graphed = step, False
+    if world == 1 and not args.eager:
+        try:
+            s_cap = torch.cuda.Stream()
+            s_cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_cap):
+                step()
+            torch.cuda.current_stream().wait_stream(s_cap)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            graph.replay()
+            torch.cuda.synchronize()
+            run_step, graphed = graph.replay, True
+        except Exception as exc:  # noqa: BLE001 - report and time eagerly
+            print(f"bench: CUDA graph capture failed ({exc}); timing eagerly", file=sys.stderr)
+            torch.cuda.synchronize()
+
     def timed(fn, k):
         times = []
         if world > 1:
@@ -304,7 +326,7 @@ def main():
             torch.distributed.barrier()
         return times, cs.summary()
 
-    times, clocks = timed(step, args.steps)
+    times, clocks = timed(run_step, args.steps)
     t_step = sum(times) / len(times)
     if world > 1:
         tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
@@ -377,6 +399,7 @@ def main():
                        "interactions_per_step": inter,
                        "parallelism": f"target-shard{world}" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MB write)",
+                       "cuda_graph": graphed,
                        "apply_parity_vs_reference": parity},
             "roofline": {"bound": "fp64", "kernel": f"opfar_kernel<{kname}>",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
