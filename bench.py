@@ -233,10 +233,18 @@ def main():
 
     import torch
     rank, world, local = _dist()
+    # BENCH_SHARE_GPU=1: every rank on cuda:0 (a functional check of the sharded
+    # path on a one-GPU box with BENCH_DIST_BACKEND=gloo; never a measurement)
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: functional checks only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2111_10743_b200 import _build, _lib
     _build.build(verbose=False)
     lib = _lib.load()

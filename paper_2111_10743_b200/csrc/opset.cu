@@ -781,7 +781,7 @@ int apply_phase(lb_opset* h, int form, int phase, const double* tau, double* out
         auto e = base_epi<EpiA3p1R>(h, L, 2);
         e.s_tau = s_tau;
         e.sp_tau = sp_tau;
-        e.phi = h->phi_eta + h->r0;
+        e.phi = h->phi_eta;  // epilogues index global rows
         return run_csr<2, EpiA3p1R>(h, vals, xs, e, st, h->wsum);
       }
       auto e = base_epi<EpiA3p1>(h, L, 2);

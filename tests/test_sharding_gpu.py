@@ -73,6 +73,11 @@ def test_emulated_shards_match_unsharded(cuda, fixture, form, far):
             phi0[r0:r0 + nr] = tmp[r0:r0 + nr]
         for d in devs:
             d.set_phi0(phi0)
+        if form == "a3" and far == "direct":  # the fused second sweep, as ShardedOperatorSet runs it
+            from paper_2111_10743_b200.operators import eta_weights
+            phi_eta = torch.from_numpy(eta_weights(geom, cset)).cuda()
+            for d in devs:
+                d.set_eta_weights(phi_eta)
         got = _emulate(devs, parts, code, tau, torch)
         err = (got - ref).abs().max().item() / ref.abs().max().item()
         # FMM shards share the unsharded tree: the same approximation
