@@ -84,6 +84,14 @@ int main(int argc, char** argv) {
     run<FarA3c, 3, 64, 128, true, 2, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3c, 4, 64, 128, true, 2, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3c, 2, 64, 64, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 128, 128, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 256, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 1, 128, 128, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, false, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, true, 4, 2>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 32, 128, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+    run<FarA3c, 2, 64, 128, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, 2);
     run<FarA3b, 2, 64, 128, true, 1, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, false, 2, 1>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA3b, 2, 64, 128, false, 2, 12>("A3b", dn, dnn, n, dp, ns_pad, dpart, w);
