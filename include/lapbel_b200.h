@@ -305,6 +305,10 @@ int lb_fmm_plan_set_m2l_factors(lb_fmm_plan* plan, const int32_t* ranks, const d
  * only when timing was enabled with lb_fmm_plan_set_timing(plan, 1). */
 int lb_fmm_plan_set_timing(lb_fmm_plan* plan, int on);
 int lb_fmm_stage_times(const lb_fmm_plan* plan, double* ms);
+/* host wall-clock ms of the plan's setup (HOST double[5]): Morton keys +
+ * sort, tree (box numbering, ranges), interaction lists, device state
+ * (built on the first apply; 0 before it), total. */
+int lb_fmm_setup_times(const lb_fmm_plan* plan, double* ms);
 
 /* ------------------------------------------------------------------------
  * Near-correction build (quadrature.py, no device

@@ -21,7 +21,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
     "--expt-relaxed-constexpr",
-    "-Xptxas", "-warn-spills",
+    "-Xptxas", "-warn-spills", "-Xcompiler", "-fopenmp",
 ]
 
 
@@ -50,11 +50,39 @@ def needs_build(out=LIB):
     return any(os.path.getmtime(d) > t for d in deps())
 
 
+def _obj(src):
+    return os.path.join(ROOT, "build", "obj", os.path.basename(src) + ".o")
+
+
 def build(force=False, verbose=True, extra=()):
+    """Compile every source to its own object in parallel (one nvcc per
+    translation unit, only the stale ones), then link the shared library."""
     if not force and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *sources(), "-lcudart", "-lcublas",
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(os.path.join(ROOT, "build", "obj"), exist_ok=True)
+    hdr = [d for d in deps() if d not in sources()]
+    t_hdr = max(os.path.getmtime(h) for h in hdr)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def stale(src):
+        o = _obj(src)
+        return force or not os.path.exists(o) or \
+            os.path.getmtime(o) < max(os.path.getmtime(src), t_hdr)
+
+    def compile_one(src):
+        cmd = [_nvcc(), *flags, *extra, "-I", os.path.join(ROOT, "include"),
+               "-c", src, "-o", _obj(src) + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(_obj(src) + ".tmp", _obj(src))
+
+    todo = [s for s in sources() if stale(s)]
+    with ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, todo))
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+           "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp", *[_obj(s) for s in sources()], "-lcudart", "-lcublas", "-lgomp",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -23,6 +23,7 @@
 // DGEMMs are plain cuBLAS calls; every other stage is a hand-written kernel.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <map>
 #include <string>
 #include <tuple>
@@ -829,8 +830,10 @@ int build_device(lb_fmm_plan* P) {
       octant[s] = ox | (oy << 1) | (oz << 2);  // bit k = offset along axis k
     }
   }
+#pragma omp parallel for schedule(static)
   for (int64_t p = 0; p < t.ns; ++p)
     for (int k = 0; k < 3; ++k) spos_s[3 * p + k] = P->spos[3 * t.src_sorted[p] + k];
+#pragma omp parallel for schedule(static)
   for (int64_t p = 0; p < t.nt; ++p)
     for (int k = 0; k < 3; ++k) tpos_s[3 * p + k] = P->tpos[3 * t.tgt_sorted[p] + k];
   LB_TRY(upload(&D.spos, spos_s));
@@ -896,50 +899,95 @@ int build_device(lb_fmm_plan* P) {
   LB_TRY(upload(&D.up_parent, upar));
   LB_TRY(upload(&D.dn_child, dch));
   LB_TRY(upload(&D.dn_parent, dpar));
-  // M2L pairs: offset index of each lattice offset
-  std::map<std::tuple<int, int, int>, int> off_index;
-  for (int d = 0; d < P->noff; ++d)
-    off_index[{P->off_vec[3 * d], P->off_vec[3 * d + 1], P->off_vec[3 * d + 2]}] = d;
-  struct Pair { int64_t tgt, src; int32_t off; double scale; };
-  std::vector<std::vector<Pair>> by_key(P->ncanon);
-  for (int l = 0; l < t.nlev; ++l) {
-    const double hl = t.half / std::ldexp(1.0, l);  // fmm.py:879
-    for (int64_t b : t.levels[l]) {
-      if (owned(b) == 0) continue;  // no (owned) targets below b: its local expansion is unused
+  // M2L pairs grouped by canonical key, each group in target-slot order (the
+  // walk below visits targets in slot order, so no sort is needed).  Lattice
+  // offsets are looked up in a dense table; boxes are split into contiguous
+  // chunks whose per-key counts place every pair deterministically.
+  constexpr int kOffR = 8, kOffW = 2 * kOffR + 1;
+  std::vector<int32_t> off_table(kOffW * kOffW * kOffW, -1);
+  for (int d = 0; d < P->noff; ++d) {
+    const int* v = &P->off_vec[3 * d];
+    if (std::abs(v[0]) > kOffR || std::abs(v[1]) > kOffR || std::abs(v[2]) > kOffR)
+      return fail(LB_ERR_ARG, "fmm: M2L lattice offset out of range");
+    off_table[((v[0] + kOffR) * kOffW + (v[1] + kOffR)) * kOffW + (v[2] + kOffR)] = d;
+  }
+  std::vector<int64_t> vt_boxes;  // target boxes in slot order
+  for (int64_t sl = 0; sl < nb; ++sl) {
+    const int64_t b = P->id_of[sl];
+    if (owned(b) > 0 && t.vlist.size(b) > 0) vt_boxes.push_back(b);
+  }
+  const int nk = P->ncanon;
+  const int64_t nvt = (int64_t)vt_boxes.size();
+  const int nchunk = (int)std::min<int64_t>(std::max<int64_t>(nvt, 1), 256);
+  std::vector<int64_t> kcnt((size_t)nchunk * nk, 0);
+  bool bad_off = false;
+  auto pair_off = [&](int64_t b, int64_t src) {
+    const int64_t dx = t.ijk[3 * src] - t.ijk[3 * b], dy = t.ijk[3 * src + 1] - t.ijk[3 * b + 1],
+                  dz = t.ijk[3 * src + 2] - t.ijk[3 * b + 2];
+    if (std::llabs(dx) > kOffR || std::llabs(dy) > kOffR || std::llabs(dz) > kOffR) return -1;
+    return (int)off_table[((dx + kOffR) * kOffW + (dy + kOffR)) * kOffW + (dz + kOffR)];
+  };
+#pragma omp parallel for schedule(static) reduction(|| : bad_off)
+  for (int c = 0; c < nchunk; ++c) {
+    for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
+      const int64_t b = vt_boxes[i];
       for (int64_t q = 0; q < t.vlist.size(b); ++q) {
-        const int64_t s = t.vlist.row(b)[q];
-        const int dx = (int)(t.ijk[3 * s] - t.ijk[3 * b]);
-        const int dy = (int)(t.ijk[3 * s + 1] - t.ijk[3 * b + 1]);
-        const int dz = (int)(t.ijk[3 * s + 2] - t.ijk[3 * b + 2]);
-        auto it = off_index.find({dx, dy, dz});
-        if (it == off_index.end()) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
-        const int d = it->second;
-        by_key[P->off_key[d]].push_back({S[b], S[s], d, 1.0 / hl});
+        const int d = pair_off(b, t.vlist.row(b)[q]);
+        if (d < 0) { bad_off = true; continue; }
+        ++kcnt[(size_t)c * nk + P->off_key[d]];
       }
     }
   }
-  std::vector<int64_t> vsrc, vtgts, tpoff{0};
-  std::vector<int32_t> voff;
-  std::vector<double> vscale;
-  D.v_key_pair_off.assign(1, 0);
+  if (bad_off) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
+  D.v_key_pair_off.assign(nk + 1, 0);
+  for (int k = 0; k < nk; ++k) {
+    int64_t tot = 0;
+    for (int c = 0; c < nchunk; ++c) tot += kcnt[(size_t)c * nk + k];
+    D.v_key_pair_off[k + 1] = D.v_key_pair_off[k] + tot;
+  }
+  const int64_t npairs = D.v_key_pair_off[nk];
+  std::vector<int64_t> kpos((size_t)nchunk * nk);  // chunk c's first slot in key k
+  for (int k = 0; k < nk; ++k) {
+    int64_t at = D.v_key_pair_off[k];
+    for (int c = 0; c < nchunk; ++c) {
+      kpos[(size_t)c * nk + k] = at;
+      at += kcnt[(size_t)c * nk + k];
+    }
+  }
+  std::vector<int64_t> vsrc(npairs), vtgt(npairs);
+  std::vector<int32_t> voff(npairs);
+  std::vector<double> vscale(npairs);
+#pragma omp parallel for schedule(static)
+  for (int c = 0; c < nchunk; ++c) {
+    int64_t* pos = &kpos[(size_t)c * nk];
+    for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
+      const int64_t b = vt_boxes[i];
+      const double inv_h = 1.0 / (t.half / std::ldexp(1.0, t.level[b]));  // fmm.py:879
+      for (int64_t q = 0; q < t.vlist.size(b); ++q) {
+        const int64_t src = t.vlist.row(b)[q];
+        const int d = pair_off(b, src);
+        const int64_t at = pos[P->off_key[d]]++;
+        vsrc[at] = S[src];
+        vtgt[at] = S[b];
+        voff[at] = d;
+        vscale[at] = inv_h;
+      }
+    }
+  }
+  std::vector<int64_t> vtgts, tpoff{0};
   D.v_key_tgt_off.assign(1, 0);
   D.max_key_pairs = 0;
-  for (int k = 0; k < P->ncanon; ++k) {
-    auto& v = by_key[k];
-    std::stable_sort(v.begin(), v.end(), [](const Pair& a, const Pair& b) { return a.tgt < b.tgt; });
-    for (size_t i = 0; i < v.size(); ++i) {
-      if (i == 0 || v[i].tgt != v[i - 1].tgt) {
-        if (i > 0) tpoff.push_back((int64_t)vsrc.size());
-        vtgts.push_back(v[i].tgt);
+  for (int k = 0; k < nk; ++k) {
+    const int64_t a = D.v_key_pair_off[k], e = D.v_key_pair_off[k + 1];
+    for (int64_t i = a; i < e; ++i) {
+      if (i == a || vtgt[i] != vtgt[i - 1]) {
+        if (i > a) tpoff.push_back(i);
+        vtgts.push_back(vtgt[i]);
       }
-      vsrc.push_back(v[i].src);
-      voff.push_back(v[i].off);
-      vscale.push_back(v[i].scale);
     }
-    if (!v.empty()) tpoff.push_back((int64_t)vsrc.size());
-    D.v_key_pair_off.push_back((int64_t)vsrc.size());
+    if (e > a) tpoff.push_back(e);
     D.v_key_tgt_off.push_back((int64_t)vtgts.size());
-    D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, (int64_t)v.size());
+    D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, e - a);
   }
   LB_TRY(upload(&D.v_src, vsrc));
   LB_TRY(upload(&D.v_tgts, vtgts));
@@ -1528,7 +1576,11 @@ int fmm_apply_impl(lb_fmm_plan* P, const double* charges, const double* dipoles,
       return fail(LB_ERR_CUDA, std::string("lb_fmm_apply: error pending before the call: ") +
                                    cudaGetErrorString(stale));
   }
-  if (!P->dev.ready) LB_TRY(build_device(P));
+  if (!P->dev.ready) {
+    const auto c0 = std::chrono::steady_clock::now();
+    LB_TRY(build_device(P));
+    P->setup_ms[3] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+  }
   if (proj_out && !P->dev.tproj) {
     const int64_t nt = std::max<int64_t>(P->tree.nt, 1);
     LB_CUDA(cudaMalloc((void**)&P->dev.tnrm, sizeof(double) * 3 * nt));

@@ -3,6 +3,7 @@
 // the device passes.  FmmPlan.__init__ equivalent (fmm.py:729-748).
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -97,11 +98,18 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
   t.nt = nt;
   t.ncrit = ncrit;
   int rc;
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto c0 = clk::now();
+  auto c1 = c0;
   if (flags & LB_FMM_DEVICE_SORT) {
     tree_bounds(spos, ns, tpos, nt, t.center, &t.half);
     std::vector<uint64_t> codes;
     std::vector<int64_t> order;
     rc = device_sorted_keys(t, spos, tpos, codes, order);
+    c1 = clk::now();
     if (rc == LB_OK) rc = tree_from_sorted(t, std::move(codes), std::move(order));
   } else {
     rc = tree_build_host(t, spos, ns, tpos, nt, ncrit);
@@ -110,7 +118,12 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
     delete p;
     return rc;
   }
+  const auto c2 = clk::now();
   tree_lists(t, buffer);
+  const auto c3 = clk::now();
+  p->setup_ms[0] = ms(c0, c1);
+  p->setup_ms[1] = ms(c1, c2);
+  p->setup_ms[2] = ms(c2, c3);
   p->spos.assign(spos, spos + 3 * ns);
   p->tpos.assign(tpos, tpos + 3 * nt);
   *out = p;
@@ -121,6 +134,14 @@ int lb_fmm_plan_destroy(lb_fmm_plan* p) {
   if (!p) return LB_OK;
   fmm_release_device(p);
   delete p;
+  return LB_OK;
+}
+
+int lb_fmm_setup_times(const lb_fmm_plan* p, double* out) {
+  if (!p || !out) return fail(LB_ERR_ARG, "lb_fmm_setup_times: null argument");
+  double tot = 0;
+  for (int i = 0; i < 4; ++i) tot += (out[i] = p->setup_ms[i]);
+  out[4] = tot;
   return LB_OK;
 }
 

@@ -104,6 +104,7 @@ struct lb_fmm_plan {
   lb::FmmDevice dev;
   std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
   std::vector<double> stage_ms;             // last apply's per-stage device times
+  double setup_ms[4] = {0, 0, 0, 0};        // keys+sort, tree, lists, device state (host ms)
   bool timing = false;
   int64_t own_t0 = 0, own_t1 = -1;          // owned targets [t0, t1) (original order); t1 < 0: all
   int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices;

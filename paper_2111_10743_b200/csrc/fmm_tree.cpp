@@ -7,7 +7,6 @@
 #include <cmath>
 #include <numeric>
 #include <string>
-#include <unordered_set>
 
 #include "../../include/lapbel_b200.h"
 
@@ -191,45 +190,84 @@ static bool near_boxes(const FmmTree& t, int64_t a, int64_t b, int buffer) {
   return true;
 }
 
+// Lists in flat arrays, every pass parallel over boxes (OpenMP) and every
+// list in the reference's order: the count and the fill of a box run the
+// same walk, so placement depends on the box alone.
 void tree_lists(FmmTree& t, int buffer) {
   t.buffer = buffer;
   const int64_t nbox = t.nbox();
-  std::vector<std::vector<int64_t>> cols(nbox), v(nbox), u(nbox), w(nbox), x(nbox);
-  cols[0] = {0};
-  for (int lev = 1; lev < t.nlev; ++lev) {  // fmm.py:669-679
-    for (int64_t b : t.levels[lev]) {
-      const int64_t* bi = &t.ijk[3 * b];
-      for (int64_t pc : cols[t.parent[b]]) {
-        const int64_t* ch = t.children.row(pc);
-        for (int64_t q = 0; q < t.children.size(pc); ++q) {
-          const int64_t c = ch[q];
-          const int64_t* ci = &t.ijk[3 * c];
-          const int64_t d = std::max({std::llabs(ci[0] - bi[0]), std::llabs(ci[1] - bi[1]),
-                                      std::llabs(ci[2] - bi[2])});
-          if (d <= buffer) cols[b].push_back(c);
-          else if (t.nsrc[c] > 0) v[b].push_back(c);
-        }
+  const int K = (2 * buffer + 1) * (2 * buffer + 1) * (2 * buffer + 1);  // colleagues per box, max
+  std::vector<int32_t> colf((size_t)nbox * K), ncol(nbox, 0);
+  std::vector<int64_t> nv(nbox, 0);
+  colf[0] = 0;
+  ncol[0] = 1;
+  const int64_t* ijk = t.ijk.data();
+  auto cheb = [&](int64_t a, int64_t b) {
+    return std::max({std::llabs(ijk[3 * a] - ijk[3 * b]), std::llabs(ijk[3 * a + 1] - ijk[3 * b + 1]),
+                     std::llabs(ijk[3 * a + 2] - ijk[3 * b + 2])});
+  };
+  // colleagues and V, level by level (fmm.py:669-679): children of the
+  // parent's colleagues, in the parent's colleague order then octant order
+  auto walk_cv = [&](int64_t b, auto&& on_col, auto&& on_v) {
+    const int64_t p = t.parent[b];
+    for (int q = 0; q < ncol[p]; ++q) {
+      const int64_t pc = colf[(size_t)p * K + q];
+      const int64_t* ch = t.children.row(pc);
+      for (int64_t r = 0; r < t.children.size(pc); ++r) {
+        const int64_t c = ch[r];
+        if (cheb(c, b) <= buffer) on_col(c);
+        else if (t.nsrc[c] > 0) on_v(c);
       }
+    }
+  };
+  for (int lev = 1; lev < t.nlev; ++lev) {
+    const std::vector<int64_t>& L = t.levels[lev];
+#pragma omp parallel for schedule(dynamic, 512)
+    for (int64_t i = 0; i < (int64_t)L.size(); ++i) {
+      const int64_t b = L[i];
+      int nc = 0;
+      int64_t cv = 0;
+      int32_t* dst = &colf[(size_t)b * K];
+      walk_cv(b, [&](int64_t c) { dst[nc++] = (int32_t)c; }, [&](int64_t) { ++cv; });
+      ncol[b] = nc;
+      nv[b] = cv;
     }
   }
-  for (int64_t b = 0; b < nbox; ++b) {  // fmm.py:684-714, leaves in ascending id
-    if (!t.is_leaf[b]) continue;
-    const bool has_tgt = t.tgt_hi[b] > t.tgt_lo[b];
+  auto scan = [&](const std::vector<int64_t>& cnt, Csr& out) {
+    out.off.assign(nbox + 1, 0);
+    for (int64_t b = 0; b < nbox; ++b) out.off[b + 1] = out.off[b] + cnt[b];
+    out.idx.assign(out.off[nbox], 0);
+  };
+  {
+    std::vector<int64_t> nc64(ncol.begin(), ncol.end());
+    scan(nc64, t.colleagues);
+  }
+  scan(nv, t.vlist);
+#pragma omp parallel for schedule(dynamic, 512)
+  for (int64_t b = 0; b < nbox; ++b) {
+    int64_t* c = &t.colleagues.idx[t.colleagues.off[b]];
+    for (int q = 0; q < ncol[b]; ++q) c[q] = colf[(size_t)b * K + q];
+    if (b == 0) continue;
+    int64_t* v = &t.vlist.idx[t.vlist.off[b]];
+    int64_t n = 0;
+    walk_cv(b, [](int64_t) {}, [&](int64_t k) { v[n++] = k; });
+  }
+  // U, W, X for non-empty leaves in ascending id (fmm.py:684-714).  The
+  // reference dedupes the ancestor walk with a set; colleagues of an
+  // ancestor a are boxes of a's level, so no box can repeat there.
+  auto walk_uwx = [&](int64_t b, std::vector<int64_t>& stack, auto&& on_u, auto&& on_w, auto&& on_x) {
     const bool has_src = t.src_hi[b] > t.src_lo[b];
-    if (!has_tgt && !has_src) continue;
-    std::unordered_set<int64_t> seen;
-    for (int64_t a = b; a != -1; a = t.parent[a]) {
-      for (int64_t c : cols[a]) {
-        if (t.is_leaf[c] && c != b && near_boxes(t, b, c, buffer) && !seen.count(c)) {
-          seen.insert(c);
-          u[b].push_back(c);
-        }
+    for (int64_t a = b; a != -1; a = t.parent[a])
+      for (int q = 0; q < ncol[a]; ++q) {
+        const int64_t c = colf[(size_t)a * K + q];
+        if (t.is_leaf[c] && c != b && near_boxes(t, b, c, buffer)) on_u(c);
       }
-    }
-    u[b].push_back(b);
-    std::vector<int64_t> stack;
-    for (int64_t c : cols[b])
+    on_u(b);
+    stack.clear();
+    for (int q = 0; q < ncol[b]; ++q) {
+      const int64_t c = colf[(size_t)b * K + q];
       if (!t.is_leaf[c]) stack.push_back(c);
+    }
     while (!stack.empty()) {
       const int64_t c = stack.back();
       stack.pop_back();
@@ -237,27 +275,60 @@ void tree_lists(FmmTree& t, int buffer) {
       for (int64_t q = 0; q < t.children.size(c); ++q) {
         const int64_t k = ch[q];
         if (near_boxes(t, b, k, buffer)) {
-          if (t.is_leaf[k]) u[b].push_back(k);
+          if (t.is_leaf[k]) on_u(k);
           else stack.push_back(k);
         } else {
-          if (t.nsrc[k] > 0) w[b].push_back(k);
-          if (has_src) x[k].push_back(b);
+          if (t.nsrc[k] > 0) on_w(k);
+          if (has_src) on_x(k);
         }
       }
     }
+  };
+  auto active = [&](int64_t b) {
+    return t.is_leaf[b] && (t.tgt_hi[b] > t.tgt_lo[b] || t.src_hi[b] > t.src_lo[b]);
+  };
+  std::vector<int64_t> nu(nbox, 0), nw(nbox, 0), nx(nbox, 0);
+#pragma omp parallel
+  {
+    std::vector<int64_t> stack;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t b = 0; b < nbox; ++b) {
+      if (!active(b)) continue;
+      int64_t cu = 0, cw = 0;
+      walk_uwx(b, stack, [&](int64_t) { ++cu; }, [&](int64_t) { ++cw; }, [&](int64_t k) {
+#pragma omp atomic
+        ++nx[k];
+      });
+      nu[b] = cu;
+      nw[b] = cw;
+    }
   }
-  t.colleagues = Csr();
-  t.vlist = Csr();
-  t.ulist = Csr();
-  t.wlist = Csr();
-  t.xlist = Csr();
-  for (int64_t b = 0; b < nbox; ++b) {
-    t.colleagues.push_row(cols[b]);
-    t.vlist.push_row(v[b]);
-    t.ulist.push_row(u[b]);
-    t.wlist.push_row(w[b]);
-    t.xlist.push_row(x[b]);
+  scan(nu, t.ulist);
+  scan(nw, t.wlist);
+  scan(nx, t.xlist);
+  std::vector<int64_t> xcur(t.xlist.off.begin(), t.xlist.off.end() - 1);
+#pragma omp parallel
+  {
+    std::vector<int64_t> stack;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t b = 0; b < nbox; ++b) {
+      if (!active(b)) continue;
+      int64_t* u = &t.ulist.idx[t.ulist.off[b]];
+      int64_t* w = &t.wlist.idx[t.wlist.off[b]];
+      int64_t cu = 0, cw = 0;
+      walk_uwx(b, stack, [&](int64_t k) { u[cu++] = k; }, [&](int64_t k) { w[cw++] = k; },
+               [&](int64_t k) {
+                 int64_t pos;
+#pragma omp atomic capture
+                 pos = xcur[k]++;
+                 t.xlist.idx[pos] = b;
+               });
+    }
   }
+  // X[k] lists its sources in ascending leaf id, as the reference's loop order
+#pragma omp parallel for schedule(dynamic, 512)
+  for (int64_t k = 0; k < nbox; ++k)
+    std::sort(t.xlist.idx.begin() + t.xlist.off[k], t.xlist.idx.begin() + t.xlist.off[k + 1]);
 }
 
 }  // namespace lb

@@ -295,6 +295,7 @@ def _bind():
         L.lb_fmm_plan_set_m2l_factors.argtypes = [P, P, P, P]
         L.lb_fmm_plan_set_target_range.argtypes = [P, I64, I64]
         L.lb_fmm_stage_times.argtypes = [P, P]
+        L.lb_fmm_setup_times.argtypes = [P, P]
         _bound = True
     return L
 
@@ -484,6 +485,13 @@ class FmmPlan:
         _lib.check(self._L.lb_fmm_stage_times(self._h, ms.ctypes.data_as(ctypes.c_void_p)))
         return dict(zip(("p2m", "m2m", "m2l", "x", "l2l", "l2t", "leaf",
                          "scatter", "total"), ms.tolist()))
+
+    def setup_times(self):
+        """Host ms of the plan setup: keys+sort, tree, lists, device state
+        (first apply), total."""
+        ms = np.zeros(5)
+        _lib.check(self._L.lb_fmm_setup_times(self._h, ms.ctypes.data_as(ctypes.c_void_p)))
+        return dict(zip(("sort", "tree", "lists", "device", "total"), ms.tolist()))
 
     def apply_device(self, charges, dipoles, nd, cmask, dmask, level, pot,
                      grad=None, hess=None, stream=None):
