@@ -306,8 +306,9 @@ int lb_fmm_plan_set_m2l_factors(lb_fmm_plan* plan, const int32_t* ranks, const d
 int lb_fmm_plan_set_timing(lb_fmm_plan* plan, int on);
 int lb_fmm_stage_times(const lb_fmm_plan* plan, double* ms);
 /* host wall-clock ms of the plan's setup (HOST double[5]): Morton keys +
- * sort, tree (box numbering, ranges), interaction lists, device state
- * (built on the first apply; 0 before it), total. */
+ * sort (with LB_FMM_DEVICE_SORT: the whole device tree build), tree (host
+ * build: box numbering and ranges; 0 on the device path), interaction lists,
+ * device state (built on the first apply; 0 before it), total. */
 int lb_fmm_setup_times(const lb_fmm_plan* plan, double* ms);
 
 /* ------------------------------------------------------------------------

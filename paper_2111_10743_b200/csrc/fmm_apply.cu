@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <cmath>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <tuple>
@@ -786,6 +788,15 @@ int upload(T** dst, const std::vector<T>& v) {
 }
 
 int build_device(lb_fmm_plan* P) {
+  const bool verbose = std::getenv("LB_FMM_VERBOSE") != nullptr;
+  auto tick = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    const auto now = std::chrono::steady_clock::now();
+    if (verbose)
+      std::fprintf(stderr, "build_device %-12s %8.1f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - tick).count());
+    tick = now;
+  };
   FmmTree& t = P->tree;
   FmmDevice& D = P->dev;
   const int64_t nb = t.nbox();
@@ -836,6 +847,7 @@ int build_device(lb_fmm_plan* P) {
 #pragma omp parallel for schedule(static)
   for (int64_t p = 0; p < t.nt; ++p)
     for (int k = 0; k < 3; ++k) tpos_s[3 * p + k] = P->tpos[3 * t.tgt_sorted[p] + k];
+  mark("geometry");
   LB_TRY(upload(&D.spos, spos_s));
   LB_TRY(upload(&D.tpos, tpos_s));
   LB_TRY(upload(&D.src_sorted, t.src_sorted));
@@ -863,6 +875,7 @@ int build_device(lb_fmm_plan* P) {
     for (int i = 0; i < nrep; ++i) pinv[(int64_t)d * nrep + P->off_perm[(int64_t)d * nrep + i]] = i;
   LB_TRY(upload(&D.perm, P->off_perm));
   LB_TRY(upload(&D.perm_inv, pinv));
+  mark("uploads");
   // P2M leaves (fmm.py:826) and M2M / L2L groups per (level, octant)
   std::vector<int64_t> p2m;
   for (int64_t b = 0; b < nb; ++b)
@@ -899,6 +912,7 @@ int build_device(lb_fmm_plan* P) {
   LB_TRY(upload(&D.up_parent, upar));
   LB_TRY(upload(&D.dn_child, dch));
   LB_TRY(upload(&D.dn_parent, dpar));
+  mark("m2m/l2l");
   // M2L pairs grouped by canonical key, each group in target-slot order (the
   // walk below visits targets in slot order, so no sort is needed).  Lattice
   // offsets are looked up in a dense table; boxes are split into contiguous
@@ -974,6 +988,7 @@ int build_device(lb_fmm_plan* P) {
       }
     }
   }
+  mark("m2l pairs");
   std::vector<int64_t> vtgts, tpoff{0};
   D.v_key_tgt_off.assign(1, 0);
   D.max_key_pairs = 0;
@@ -989,12 +1004,14 @@ int build_device(lb_fmm_plan* P) {
     D.v_key_tgt_off.push_back((int64_t)vtgts.size());
     D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, e - a);
   }
+  mark("m2l tgts");
   LB_TRY(upload(&D.v_src, vsrc));
   LB_TRY(upload(&D.v_tgts, vtgts));
   LB_TRY(upload(&D.v_tgt_pair_off, tpoff));
   D.v_tpoff_host = tpoff;
   LB_TRY(upload(&D.v_off_idx, voff));
   LB_TRY(upload(&D.v_scale, vscale));
+  mark("m2l upload");
   // X list (fmm.py:891-911): boxes with sourceful X entries
   std::vector<int64_t> xb, xo{0}, xl;
   for (int64_t b = 0; b < nb; ++b) {
@@ -1010,6 +1027,7 @@ int build_device(lb_fmm_plan* P) {
   LB_TRY(upload(&D.x_boxes, xb));
   LB_TRY(upload(&D.x_off, xo));
   LB_TRY(upload(&D.x_leaves, xl));
+  mark("x list");
   // leaf stage (fmm.py:940-988): target leaves, their U (with sources) and W lists
   std::vector<int64_t> tl, uo{0}, ul, wo{0}, wl;
   for (int64_t b = 0; b < nb; ++b) {
@@ -1024,6 +1042,7 @@ int build_device(lb_fmm_plan* P) {
     wo.push_back((int64_t)wl.size());
   }
   D.n_tleaf = (int64_t)tl.size();
+  mark("leaf lists");
   // work items: a leaf's virtual source list [U sources | own DE set | W sets]
   // is cut into segments of at most ~2^20 (target, source) pairs, so no block
   // is the kernel's critical path (measured: SMs idle half of the leaf stage
@@ -1064,6 +1083,7 @@ int build_device(lb_fmm_plan* P) {
     LB_TRY(upload(&D.split_leaf, sleaf));
     LB_TRY(upload(&D.split_item_off, srange));  // [first item, end) per split leaf
   }
+  mark("leaf items");
   LB_TRY(upload(&D.t_leaves, tl));
   LB_TRY(upload(&D.u_off, uo));
   LB_TRY(upload(&D.u_list, ul));
@@ -1073,7 +1093,9 @@ int build_device(lb_fmm_plan* P) {
   // companion buffer
   D.btgt_oct = doct;
   D.level_slot_off = level_slot_off;
+  mark("leaf upload");
   if (cublasCreate(&D.blas) != CUBLAS_STATUS_SUCCESS) return fail(LB_ERR_CUDA, "cublasCreate failed");
+  mark("cublas");
   D.ready = true;
   return LB_OK;
 }

@@ -36,49 +36,6 @@ __global__ void morton_keys_kernel(const double* __restrict__ spos, int64_t ns,
   idx[i] = i;
 }
 
-// device keys + stable LSD radix sort on the 60 key bits (ties keep input
-// order, fmm.py:577 kind="stable"); returns sorted keys and order on the host
-int device_sorted_keys(const FmmTree& t, const double* spos, const double* tpos,
-                       std::vector<uint64_t>& codes, std::vector<int64_t>& order) {
-  const int64_t m = t.ns + t.nt;
-  double *ds = nullptr, *dt = nullptr;
-  uint64_t *k0 = nullptr, *k1 = nullptr;
-  int64_t *v0 = nullptr, *v1 = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0;
-  auto cleanup = [&]() {
-    cudaFree(ds); cudaFree(dt); cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1);
-    cudaFree(tmp);
-  };
-  cudaError_t e = cudaSuccess;
-  auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 16)); };
-  A((void**)&ds, sizeof(double) * 3 * t.ns);
-  A((void**)&dt, sizeof(double) * 3 * t.nt);
-  A((void**)&k0, sizeof(uint64_t) * m);
-  A((void**)&k1, sizeof(uint64_t) * m);
-  A((void**)&v0, sizeof(int64_t) * m);
-  A((void**)&v1, sizeof(int64_t) * m);
-  if (e == cudaSuccess && t.ns) e = cudaMemcpy(ds, spos, sizeof(double) * 3 * t.ns, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && t.nt) e = cudaMemcpy(dt, tpos, sizeof(double) * 3 * t.nt, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) {
-    morton_keys_kernel<<<(unsigned)ceil_div(m, 256), 256>>>(ds, t.ns, dt, t.nt, t.center[0],
-                                                            t.center[1], t.center[2], t.half, k0, v0);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess)
-    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, v1, (int64_t)m, 0, 3 * kMaxDepth);
-  A(&tmp, tmp_bytes);
-  if (e == cudaSuccess)
-    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int64_t)m, 0, 3 * kMaxDepth);
-  codes.resize(m);
-  order.resize(m);
-  if (e == cudaSuccess) e = cudaMemcpy(codes.data(), k1, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess) e = cudaMemcpy(order.data(), v1, sizeof(int64_t) * m, cudaMemcpyDeviceToHost);
-  cleanup();
-  if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("fmm tree keys: ") + cudaGetErrorString(e));
-  return LB_OK;
-}
-
 }  // namespace lb
 
 using namespace lb;
@@ -104,13 +61,10 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
   };
   const auto c0 = clk::now();
   auto c1 = c0;
+  double dev_lists_ms = -1;
   if (flags & LB_FMM_DEVICE_SORT) {
-    tree_bounds(spos, ns, tpos, nt, t.center, &t.half);
-    std::vector<uint64_t> codes;
-    std::vector<int64_t> order;
-    rc = device_sorted_keys(t, spos, tpos, codes, order);
+    rc = tree_build_device(t, spos, tpos, buffer, &dev_lists_ms);  // fmm_tree_dev.cu
     c1 = clk::now();
-    if (rc == LB_OK) rc = tree_from_sorted(t, std::move(codes), std::move(order));
   } else {
     rc = tree_build_host(t, spos, ns, tpos, nt, ncrit);
   }
@@ -119,11 +73,15 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
     return rc;
   }
   const auto c2 = clk::now();
-  tree_lists(t, buffer);
+  if (dev_lists_ms < 0) tree_lists(t, buffer);
   const auto c3 = clk::now();
   p->setup_ms[0] = ms(c0, c1);
   p->setup_ms[1] = ms(c1, c2);
   p->setup_ms[2] = ms(c2, c3);
+  if (dev_lists_ms >= 0) {  // the device build timed its lists inside the first interval
+    p->setup_ms[0] -= dev_lists_ms;
+    p->setup_ms[2] = dev_lists_ms;
+  }
   p->spos.assign(spos, spos + 3 * ns);
   p->tpos.assign(tpos, tpos + 3 * nt);
   *out = p;

@@ -103,6 +103,58 @@ def test_device_sort_tree_equals_host_tree(cuda):
         assert np.array_equal(a.raw["u_off"], off) and np.array_equal(a.raw["u"], flat)
 
 
+def _raw_tree(spos, tpos, eps, ncrit, device):
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    p = FmmPlan(spos, tpos, eps, ncrit=ncrit, device_sort=device)
+    return p.tree.raw, p.setup_times()
+
+
+@pytest.mark.parametrize("case", ["uniform", "clustered", "sphere_b2", "tiny", "dups", "one_tgt",
+                                  "chains"])
+def test_device_tree_and_lists_equal_host(cuda, case):
+    """The device tree (fmm_tree_dev.cu: level-synchronous boxes, numbering
+    from preorder positions) against the host DFS build, every exported array
+    bit for bit (the host build is pinned to the reference's goldens)."""
+    rng = np.random.default_rng(7)
+    eps, ncrit = 1e-6, 120
+    if case == "uniform":
+        s, t = rng.random((150000, 3)), rng.random((90000, 3))
+    elif case == "clustered":
+        c = rng.standard_normal((12, 3))
+        s = c[rng.integers(0, 12, 200000)] + 1e-3 * rng.standard_normal((200000, 3))
+        t = c[rng.integers(0, 12, 50000)] + 1e-2 * rng.standard_normal((50000, 3))
+        ncrit = 60
+    elif case == "sphere_b2":
+        s = rng.standard_normal((200000, 3))
+        s /= np.linalg.norm(s, axis=1)[:, None]
+        t, eps = s[::3].copy(), 1e-9
+    elif case == "tiny":
+        s, t = rng.random((50, 3)), rng.random((20, 3))
+    elif case == "dups":
+        s = np.repeat(rng.random((3000, 3)), 40, axis=0)
+        t = s[::7].copy()
+    elif case == "chains":  # close pairs, ncrit 1: deep chains, many more boxes than m / 8
+        p = rng.random((6000, 3))
+        s = np.concatenate([p, p + 1e-6 * rng.standard_normal((6000, 3))])
+        t, ncrit = rng.random((100, 3)), 1
+    else:
+        s, t = rng.random((20000, 3)), rng.random((1, 3))
+    a, times = _raw_tree(s, t, eps, ncrit, True)
+    b, _ = _raw_tree(s, t, eps, ncrit, False)
+    assert times["tree"] < 1.0 and times["sort"] > 0.0  # the device path ran (no host tree)
+    for name in b:
+        assert np.array_equal(a[name], b[name]), name
+
+
+def test_device_tree_capacity_error(cuda):
+    from paper_2111_10743_b200 import FmmCapacityError
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    pos = np.zeros((200000, 3))
+    pos[-1] = [1.0, 0, 0]
+    with pytest.raises(FmmCapacityError):
+        FmmPlan(pos, np.array([[2.0, 0, 0]]), 1e-6, ncrit=100, device_sort=True)
+
+
 def test_fmm_all_zero_returns_zero(cuda):
     b = _b()
     _, pos, tgt = _cloud(500, 100)
