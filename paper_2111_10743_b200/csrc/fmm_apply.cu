@@ -21,6 +21,8 @@
 //   scatter  : sorted targets -> reference layout (pot, grad, full hess)
 //
 // DGEMMs are plain cuBLAS calls; every other stage is a hand-written kernel.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <chrono>
@@ -775,6 +777,102 @@ __global__ void scatter_proj_kernel(const double* __restrict__ tproj, const int6
 }
 
 // ---------------------------------------------------------------------------
+// M2L pair grouping on the device (from the device tree build's V list):
+// pairs laid out in (target slot, V order), stable radix sort by canonical
+// key, then per-(key, target) groups -- the same arrays build_device's host
+// path produces.
+
+__global__ void gather3_kernel(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                               double* __restrict__ dst) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t o = idx[p];
+  dst[3 * p] = src[3 * o];
+  dst[3 * p + 1] = src[3 * o + 1];
+  dst[3 * p + 2] = src[3 * o + 2];
+}
+
+__global__ void m2l_count_kernel(const int64_t* __restrict__ id_of, const uint8_t* __restrict__ owned_id,
+                                 const int64_t* __restrict__ voff, int64_t nslot, int64_t* __restrict__ cnt) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  const int64_t b = id_of[s];
+  cnt[s] = owned_id[b] ? voff[b + 1] - voff[b] : 0;
+}
+
+constexpr int kOffR = 8, kOffW = 2 * kOffR + 1;  // dense lattice-offset table
+
+__global__ void m2l_fill_kernel(const int64_t* __restrict__ id_of, const uint8_t* __restrict__ owned_id,
+                                const int64_t* __restrict__ voff, const int64_t* __restrict__ vidx,
+                                const int64_t* __restrict__ poff, const int64_t* __restrict__ ijk,
+                                const int32_t* __restrict__ level, const double* __restrict__ inv_h,
+                                const int32_t* __restrict__ off_table, const int32_t* __restrict__ off_key,
+                                const int64_t* __restrict__ slot_of, int64_t nslot, int32_t* __restrict__ keys,
+                                int64_t* __restrict__ ids, int64_t* __restrict__ tgt, int64_t* __restrict__ src,
+                                int32_t* __restrict__ off, double* __restrict__ scale, int* __restrict__ bad) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  const int64_t b = id_of[s];
+  if (!owned_id[b]) return;
+  int64_t at = poff[s];
+  const double sc = inv_h[level[b]];
+  for (int64_t q = voff[b]; q < voff[b + 1]; ++q, ++at) {
+    const int64_t c = vidx[q];
+    const int64_t dx = ijk[3 * c] - ijk[3 * b], dy = ijk[3 * c + 1] - ijk[3 * b + 1],
+                  dz = ijk[3 * c + 2] - ijk[3 * b + 2];
+    int d = -1;
+    if (llabs(dx) <= kOffR && llabs(dy) <= kOffR && llabs(dz) <= kOffR)
+      d = off_table[((dx + kOffR) * kOffW + (dy + kOffR)) * kOffW + (dz + kOffR)];
+    if (d < 0) {
+      atomicExch(bad, 1);
+      d = 0;
+    }
+    keys[at] = off_key[d];
+    ids[at] = at;
+    tgt[at] = s;
+    src[at] = slot_of[c];
+    off[at] = d;
+    scale[at] = sc;
+  }
+}
+
+__global__ void m2l_gather_pairs_kernel(const int64_t* __restrict__ perm, const int32_t* __restrict__ keys_s,
+                                        const int64_t* __restrict__ tgt, const int64_t* __restrict__ src,
+                                        const int32_t* __restrict__ off, const double* __restrict__ scale,
+                                        int64_t n, int64_t* __restrict__ tgt_s, int64_t* __restrict__ src_s,
+                                        int32_t* __restrict__ off_s, double* __restrict__ scale_s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+  tgt_s[i] = tgt[j];
+  src_s[i] = src[j];
+  off_s[i] = off[j];
+  scale_s[i] = scale[j];
+}
+
+__global__ void m2l_group_flags_kernel(const int32_t* __restrict__ keys_s, const int64_t* __restrict__ tgt_s,
+                                       int64_t n, int64_t* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = (i == 0 || keys_s[i] != keys_s[i - 1] || tgt_s[i] != tgt_s[i - 1]) ? 1 : 0;
+}
+
+__global__ void m2l_groups_kernel(const int32_t* __restrict__ keys_s, const int64_t* __restrict__ tgt_s,
+                                  const int64_t* __restrict__ flag, const int64_t* __restrict__ grp_incl,
+                                  int64_t n, int64_t* __restrict__ vtgts, int64_t* __restrict__ tpoff,
+                                  int64_t* __restrict__ kpair, int64_t* __restrict__ kgrp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  const int64_t g = grp_incl[i] - 1;
+  vtgts[g] = tgt_s[i];
+  tpoff[g] = i;
+  if (i == 0 || keys_s[i] != keys_s[i - 1]) {
+    kpair[keys_s[i]] = i;
+    kgrp[keys_s[i]] = g;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side: device state
 
 namespace {
@@ -784,6 +882,129 @@ int upload(T** dst, const std::vector<T>& v) {
   cudaError_t e = cudaMalloc((void**)dst, std::max<size_t>(v.size() * sizeof(T), 16));
   if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("fmm upload: ") + cudaGetErrorString(e));
+  return LB_OK;
+}
+
+// M2L pairs from the device V list (see the kernels above); fills the same
+// FmmDevice arrays as the host path in build_device
+int m2l_pairs_device(lb_fmm_plan* P, const std::vector<uint8_t>& own_id, const std::vector<int32_t>& off_table) {
+  FmmTree& t = P->tree;
+  FmmDevice& D = P->dev;
+  const int64_t nb = t.nbox();
+  const int nk = P->ncanon;
+  std::vector<void*> tmp;
+  auto grab = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) tmp.push_back(*p);
+    return e;
+  };
+  struct Free {
+    std::vector<void*>& v;
+    ~Free() { for (void* p : v) cudaFree(p); }
+  } free_tmp{tmp};
+  std::vector<double> inv_h(t.nlev);
+  for (int l = 0; l < t.nlev; ++l) inv_h[l] = 1.0 / (t.half / std::ldexp(1.0, l));  // fmm.py:879
+  int64_t *d_idof, *d_slot, *d_ijk, *cnt, *poff;
+  uint8_t* d_own;
+  int32_t *d_lev, *d_table, *d_key;
+  double* d_invh;
+  int* d_bad;
+  auto up = [&](void** p, const void* src, size_t bytes) -> cudaError_t {
+    cudaError_t e = grab(p, bytes);
+    if (e == cudaSuccess && bytes) e = cudaMemcpy(*p, src, bytes, cudaMemcpyHostToDevice);
+    return e;
+  };
+  LB_CUDA(up((void**)&d_idof, P->id_of.data(), 8 * nb));
+  LB_CUDA(up((void**)&d_slot, P->slot_of.data(), 8 * nb));
+  LB_CUDA(up((void**)&d_ijk, t.ijk.data(), 24 * nb));
+  LB_CUDA(up((void**)&d_own, own_id.data(), nb));
+  LB_CUDA(up((void**)&d_lev, t.level.data(), 4 * nb));
+  LB_CUDA(up((void**)&d_table, off_table.data(), 4 * off_table.size()));
+  LB_CUDA(up((void**)&d_key, P->off_key.data(), 4 * P->off_key.size()));
+  LB_CUDA(up((void**)&d_invh, inv_h.data(), 8 * inv_h.size()));
+  LB_CUDA(grab((void**)&d_bad, sizeof(int)));
+  LB_CUDA(cudaMemset(d_bad, 0, sizeof(int)));
+  LB_CUDA(grab((void**)&cnt, 8 * (nb + 1)));
+  LB_CUDA(grab((void**)&poff, 8 * (nb + 1)));
+  LB_CUDA(cudaMemset(cnt + nb, 0, 8));
+  const unsigned gb = (unsigned)std::max<int64_t>(1, ceil_div(nb, 256));
+  m2l_count_kernel<<<gb, 256>>>(d_idof, d_own, P->tdev.v_off, nb, cnt);
+  LB_CHECK_LAUNCH();
+  size_t sbytes = 0;
+  void* stmp = nullptr;
+  LB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sbytes, cnt, poff, nb + 1));
+  LB_CUDA(grab(&stmp, sbytes));
+  LB_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sbytes, cnt, poff, nb + 1));
+  int64_t np = 0;
+  LB_CUDA(cudaMemcpy(&np, poff + nb, 8, cudaMemcpyDeviceToHost));
+  int32_t *keys, *keys_s, *off;
+  int64_t *ids, *perm, *tgt, *src, *flag, *grp, *kpair, *kgrp;
+  double* scale;
+  LB_CUDA(grab((void**)&keys, 4 * np));
+  LB_CUDA(grab((void**)&keys_s, 4 * np));
+  LB_CUDA(grab((void**)&off, 4 * np));
+  LB_CUDA(grab((void**)&ids, 8 * np));
+  LB_CUDA(grab((void**)&perm, 8 * np));
+  LB_CUDA(grab((void**)&tgt, 8 * np));
+  LB_CUDA(grab((void**)&src, 8 * np));
+  LB_CUDA(grab((void**)&scale, 8 * np));
+  m2l_fill_kernel<<<gb, 256>>>(d_idof, d_own, P->tdev.v_off, P->tdev.v_idx, poff, d_ijk, d_lev, d_invh, d_table,
+                               d_key, d_slot, nb, keys, ids, tgt, src, off, scale, d_bad);
+  LB_CHECK_LAUNCH();
+  int bad = 0;
+  LB_CUDA(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
+  int kbits = 1;
+  while ((1 << kbits) < nk) ++kbits;
+  size_t rbytes = 0;
+  void* rtmp = nullptr;
+  LB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, rbytes, keys, keys_s, ids, perm, np, 0, kbits));
+  LB_CUDA(grab(&rtmp, rbytes));
+  LB_CUDA(cub::DeviceRadixSort::SortPairs(rtmp, rbytes, keys, keys_s, ids, perm, np, 0, kbits));  // stable
+  LB_CUDA(cudaMalloc((void**)&D.v_src, std::max<int64_t>(16, 8 * np)));
+  LB_CUDA(cudaMalloc((void**)&D.v_off_idx, std::max<int64_t>(16, 4 * np)));
+  LB_CUDA(cudaMalloc((void**)&D.v_scale, std::max<int64_t>(16, 8 * np)));
+  int64_t* tgt_s = ids;  // reuse
+  const unsigned gp = (unsigned)std::max<int64_t>(1, ceil_div(np, 256));
+  m2l_gather_pairs_kernel<<<gp, 256>>>(perm, keys_s, tgt, src, off, scale, np, tgt_s, D.v_src, D.v_off_idx,
+                                       D.v_scale);
+  LB_CHECK_LAUNCH();
+  flag = src;  // reuse (gathered already)
+  grp = tgt;
+  m2l_group_flags_kernel<<<gp, 256>>>(keys_s, tgt_s, np, flag);
+  LB_CHECK_LAUNCH();
+  size_t ibytes = 0;
+  void* itmp = nullptr;
+  LB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, ibytes, flag, grp, np));
+  LB_CUDA(grab(&itmp, ibytes));
+  if (np) LB_CUDA(cub::DeviceScan::InclusiveSum(itmp, ibytes, flag, grp, np));
+  int64_t ng = 0;
+  if (np) LB_CUDA(cudaMemcpy(&ng, grp + np - 1, 8, cudaMemcpyDeviceToHost));
+  LB_CUDA(cudaMalloc((void**)&D.v_tgts, std::max<int64_t>(16, 8 * ng)));
+  LB_CUDA(cudaMalloc((void**)&D.v_tgt_pair_off, 8 * (ng + 1)));
+  LB_CUDA(grab((void**)&kpair, 8 * std::max(nk, 1)));
+  LB_CUDA(grab((void**)&kgrp, 8 * std::max(nk, 1)));
+  LB_CUDA(cudaMemset(kpair, 0xff, 8 * std::max(nk, 1)));
+  LB_CUDA(cudaMemset(kgrp, 0xff, 8 * std::max(nk, 1)));
+  m2l_groups_kernel<<<gp, 256>>>(keys_s, tgt_s, flag, grp, np, D.v_tgts, D.v_tgt_pair_off, kpair, kgrp);
+  LB_CHECK_LAUNCH();
+  LB_CUDA(cudaMemcpy(D.v_tgt_pair_off + ng, &np, 8, cudaMemcpyHostToDevice));
+  D.v_tpoff_host.resize(ng + 1);
+  LB_CUDA(cudaMemcpy(D.v_tpoff_host.data(), D.v_tgt_pair_off, 8 * (ng + 1), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> kp(nk), kg(nk);
+  if (nk) {
+    LB_CUDA(cudaMemcpy(kp.data(), kpair, 8 * nk, cudaMemcpyDeviceToHost));
+    LB_CUDA(cudaMemcpy(kg.data(), kgrp, 8 * nk, cudaMemcpyDeviceToHost));
+  }
+  D.v_key_pair_off.assign(nk + 1, np);
+  D.v_key_tgt_off.assign(nk + 1, ng);
+  for (int k = nk - 1; k >= 0; --k) {  // empty keys start where the next key does
+    D.v_key_pair_off[k] = kp[k] >= 0 ? kp[k] : D.v_key_pair_off[k + 1];
+    D.v_key_tgt_off[k] = kg[k] >= 0 ? kg[k] : D.v_key_tgt_off[k + 1];
+  }
+  D.max_key_pairs = 0;
+  for (int k = 0; k < nk; ++k)
+    D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, D.v_key_pair_off[k + 1] - D.v_key_pair_off[k]);
   return LB_OK;
 }
 
@@ -823,7 +1044,10 @@ int build_device(lb_fmm_plan* P) {
     own_pref[q + 1] = own_pref[q] + (mine ? 1 : 0);
   }
   auto owned = [&](int64_t b) { return own_pref[t.tgt_hi[b]] - own_pref[t.tgt_lo[b]]; };
-  std::vector<double> ctr(3 * nb), hf(nb), spos_s(3 * t.ns), tpos_s(3 * t.nt);
+  std::vector<uint8_t> own_id(nb);
+  for (int64_t b = 0; b < nb; ++b) own_id[b] = owned(b) > 0 ? 1 : 0;
+  const bool dev_tree = P->tdev.spos != nullptr;
+  std::vector<double> ctr(3 * nb), hf(nb), spos_s(dev_tree ? 0 : 3 * t.ns), tpos_s(dev_tree ? 0 : 3 * t.nt);
   std::vector<int64_t> bsrc(2 * nb), btgt(2 * nb), octant(nb, 0);
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t s = S[b];
@@ -841,17 +1065,38 @@ int build_device(lb_fmm_plan* P) {
       octant[s] = ox | (oy << 1) | (oz << 2);  // bit k = offset along axis k
     }
   }
+  if (dev_tree) {  // positions and sorted index lists are on the device already
+    auto dev_copy = [&](int64_t** dst, const int64_t* src, int64_t n) -> cudaError_t {
+      cudaError_t e = cudaMalloc((void**)dst, std::max<size_t>(16, 8 * n));
+      if (e == cudaSuccess && n) e = cudaMemcpy(*dst, src, 8 * n, cudaMemcpyDeviceToDevice);
+      return e;
+    };
+    LB_CUDA(dev_copy(&D.src_sorted, P->tdev.src_sorted, t.ns));
+    LB_CUDA(dev_copy(&D.tgt_sorted, P->tdev.tgt_sorted, t.nt));
+    LB_CUDA(cudaMalloc((void**)&D.spos, std::max<size_t>(16, 24 * t.ns)));
+    LB_CUDA(cudaMalloc((void**)&D.tpos, std::max<size_t>(16, 24 * t.nt)));
+    if (t.ns) {
+      gather3_kernel<<<(unsigned)ceil_div(t.ns, 256), 256>>>(P->tdev.spos, D.src_sorted, t.ns, D.spos);
+      LB_CHECK_LAUNCH();
+    }
+    if (t.nt) {
+      gather3_kernel<<<(unsigned)ceil_div(t.nt, 256), 256>>>(P->tdev.tpos, D.tgt_sorted, t.nt, D.tpos);
+      LB_CHECK_LAUNCH();
+    }
+    mark("geometry");
+  } else {
 #pragma omp parallel for schedule(static)
-  for (int64_t p = 0; p < t.ns; ++p)
-    for (int k = 0; k < 3; ++k) spos_s[3 * p + k] = P->spos[3 * t.src_sorted[p] + k];
+    for (int64_t p = 0; p < t.ns; ++p)
+      for (int k = 0; k < 3; ++k) spos_s[3 * p + k] = P->spos[3 * t.src_sorted[p] + k];
 #pragma omp parallel for schedule(static)
-  for (int64_t p = 0; p < t.nt; ++p)
-    for (int k = 0; k < 3; ++k) tpos_s[3 * p + k] = P->tpos[3 * t.tgt_sorted[p] + k];
-  mark("geometry");
-  LB_TRY(upload(&D.spos, spos_s));
-  LB_TRY(upload(&D.tpos, tpos_s));
-  LB_TRY(upload(&D.src_sorted, t.src_sorted));
-  LB_TRY(upload(&D.tgt_sorted, t.tgt_sorted));
+    for (int64_t p = 0; p < t.nt; ++p)
+      for (int k = 0; k < 3; ++k) tpos_s[3 * p + k] = P->tpos[3 * t.tgt_sorted[p] + k];
+    mark("geometry");
+    LB_TRY(upload(&D.spos, spos_s));
+    LB_TRY(upload(&D.tpos, tpos_s));
+    LB_TRY(upload(&D.src_sorted, t.src_sorted));
+    LB_TRY(upload(&D.tgt_sorted, t.tgt_sorted));
+  }
   LB_TRY(upload(&D.bctr, ctr));
   LB_TRY(upload(&D.bhalf, hf));
   LB_TRY(upload(&D.bsrc, bsrc));
@@ -917,7 +1162,6 @@ int build_device(lb_fmm_plan* P) {
   // walk below visits targets in slot order, so no sort is needed).  Lattice
   // offsets are looked up in a dense table; boxes are split into contiguous
   // chunks whose per-key counts place every pair deterministically.
-  constexpr int kOffR = 8, kOffW = 2 * kOffR + 1;
   std::vector<int32_t> off_table(kOffW * kOffW * kOffW, -1);
   for (int d = 0; d < P->noff; ++d) {
     const int* v = &P->off_vec[3 * d];
@@ -925,92 +1169,96 @@ int build_device(lb_fmm_plan* P) {
       return fail(LB_ERR_ARG, "fmm: M2L lattice offset out of range");
     off_table[((v[0] + kOffR) * kOffW + (v[1] + kOffR)) * kOffW + (v[2] + kOffR)] = d;
   }
-  std::vector<int64_t> vt_boxes;  // target boxes in slot order
-  for (int64_t sl = 0; sl < nb; ++sl) {
-    const int64_t b = P->id_of[sl];
-    if (owned(b) > 0 && t.vlist.size(b) > 0) vt_boxes.push_back(b);
-  }
-  const int nk = P->ncanon;
-  const int64_t nvt = (int64_t)vt_boxes.size();
-  const int nchunk = (int)std::min<int64_t>(std::max<int64_t>(nvt, 1), 256);
-  std::vector<int64_t> kcnt((size_t)nchunk * nk, 0);
-  bool bad_off = false;
-  auto pair_off = [&](int64_t b, int64_t src) {
-    const int64_t dx = t.ijk[3 * src] - t.ijk[3 * b], dy = t.ijk[3 * src + 1] - t.ijk[3 * b + 1],
-                  dz = t.ijk[3 * src + 2] - t.ijk[3 * b + 2];
-    if (std::llabs(dx) > kOffR || std::llabs(dy) > kOffR || std::llabs(dz) > kOffR) return -1;
-    return (int)off_table[((dx + kOffR) * kOffW + (dy + kOffR)) * kOffW + (dz + kOffR)];
-  };
-#pragma omp parallel for schedule(static) reduction(|| : bad_off)
-  for (int c = 0; c < nchunk; ++c) {
-    for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
-      const int64_t b = vt_boxes[i];
-      for (int64_t q = 0; q < t.vlist.size(b); ++q) {
-        const int d = pair_off(b, t.vlist.row(b)[q]);
-        if (d < 0) { bad_off = true; continue; }
-        ++kcnt[(size_t)c * nk + P->off_key[d]];
-      }
+  if (P->tdev.v_idx) {
+    LB_TRY(m2l_pairs_device(P, own_id, off_table));
+  } else {
+    std::vector<int64_t> vt_boxes;  // target boxes in slot order
+    for (int64_t sl = 0; sl < nb; ++sl) {
+      const int64_t b = P->id_of[sl];
+      if (owned(b) > 0 && t.vlist.size(b) > 0) vt_boxes.push_back(b);
     }
-  }
-  if (bad_off) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
-  D.v_key_pair_off.assign(nk + 1, 0);
-  for (int k = 0; k < nk; ++k) {
-    int64_t tot = 0;
-    for (int c = 0; c < nchunk; ++c) tot += kcnt[(size_t)c * nk + k];
-    D.v_key_pair_off[k + 1] = D.v_key_pair_off[k] + tot;
-  }
-  const int64_t npairs = D.v_key_pair_off[nk];
-  std::vector<int64_t> kpos((size_t)nchunk * nk);  // chunk c's first slot in key k
-  for (int k = 0; k < nk; ++k) {
-    int64_t at = D.v_key_pair_off[k];
+    const int nk = P->ncanon;
+    const int64_t nvt = (int64_t)vt_boxes.size();
+    const int nchunk = (int)std::min<int64_t>(std::max<int64_t>(nvt, 1), 256);
+    std::vector<int64_t> kcnt((size_t)nchunk * nk, 0);
+    bool bad_off = false;
+    auto pair_off = [&](int64_t b, int64_t src) {
+      const int64_t dx = t.ijk[3 * src] - t.ijk[3 * b], dy = t.ijk[3 * src + 1] - t.ijk[3 * b + 1],
+                    dz = t.ijk[3 * src + 2] - t.ijk[3 * b + 2];
+      if (std::llabs(dx) > kOffR || std::llabs(dy) > kOffR || std::llabs(dz) > kOffR) return -1;
+      return (int)off_table[((dx + kOffR) * kOffW + (dy + kOffR)) * kOffW + (dz + kOffR)];
+    };
+  #pragma omp parallel for schedule(static) reduction(|| : bad_off)
     for (int c = 0; c < nchunk; ++c) {
-      kpos[(size_t)c * nk + k] = at;
-      at += kcnt[(size_t)c * nk + k];
-    }
-  }
-  std::vector<int64_t> vsrc(npairs), vtgt(npairs);
-  std::vector<int32_t> voff(npairs);
-  std::vector<double> vscale(npairs);
-#pragma omp parallel for schedule(static)
-  for (int c = 0; c < nchunk; ++c) {
-    int64_t* pos = &kpos[(size_t)c * nk];
-    for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
-      const int64_t b = vt_boxes[i];
-      const double inv_h = 1.0 / (t.half / std::ldexp(1.0, t.level[b]));  // fmm.py:879
-      for (int64_t q = 0; q < t.vlist.size(b); ++q) {
-        const int64_t src = t.vlist.row(b)[q];
-        const int d = pair_off(b, src);
-        const int64_t at = pos[P->off_key[d]]++;
-        vsrc[at] = S[src];
-        vtgt[at] = S[b];
-        voff[at] = d;
-        vscale[at] = inv_h;
+      for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
+        const int64_t b = vt_boxes[i];
+        for (int64_t q = 0; q < t.vlist.size(b); ++q) {
+          const int d = pair_off(b, t.vlist.row(b)[q]);
+          if (d < 0) { bad_off = true; continue; }
+          ++kcnt[(size_t)c * nk + P->off_key[d]];
+        }
       }
     }
-  }
-  mark("m2l pairs");
-  std::vector<int64_t> vtgts, tpoff{0};
-  D.v_key_tgt_off.assign(1, 0);
-  D.max_key_pairs = 0;
-  for (int k = 0; k < nk; ++k) {
-    const int64_t a = D.v_key_pair_off[k], e = D.v_key_pair_off[k + 1];
-    for (int64_t i = a; i < e; ++i) {
-      if (i == a || vtgt[i] != vtgt[i - 1]) {
-        if (i > a) tpoff.push_back(i);
-        vtgts.push_back(vtgt[i]);
+    if (bad_off) return fail(LB_ERR_ARG, "fmm: V-list offset without an M2L operator");
+    D.v_key_pair_off.assign(nk + 1, 0);
+    for (int k = 0; k < nk; ++k) {
+      int64_t tot = 0;
+      for (int c = 0; c < nchunk; ++c) tot += kcnt[(size_t)c * nk + k];
+      D.v_key_pair_off[k + 1] = D.v_key_pair_off[k] + tot;
+    }
+    const int64_t npairs = D.v_key_pair_off[nk];
+    std::vector<int64_t> kpos((size_t)nchunk * nk);  // chunk c's first slot in key k
+    for (int k = 0; k < nk; ++k) {
+      int64_t at = D.v_key_pair_off[k];
+      for (int c = 0; c < nchunk; ++c) {
+        kpos[(size_t)c * nk + k] = at;
+        at += kcnt[(size_t)c * nk + k];
       }
     }
-    if (e > a) tpoff.push_back(e);
-    D.v_key_tgt_off.push_back((int64_t)vtgts.size());
-    D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, e - a);
+    std::vector<int64_t> vsrc(npairs), vtgt(npairs);
+    std::vector<int32_t> voff(npairs);
+    std::vector<double> vscale(npairs);
+  #pragma omp parallel for schedule(static)
+    for (int c = 0; c < nchunk; ++c) {
+      int64_t* pos = &kpos[(size_t)c * nk];
+      for (int64_t i = nvt * c / nchunk; i < nvt * (c + 1) / nchunk; ++i) {
+        const int64_t b = vt_boxes[i];
+        const double inv_h = 1.0 / (t.half / std::ldexp(1.0, t.level[b]));  // fmm.py:879
+        for (int64_t q = 0; q < t.vlist.size(b); ++q) {
+          const int64_t src = t.vlist.row(b)[q];
+          const int d = pair_off(b, src);
+          const int64_t at = pos[P->off_key[d]]++;
+          vsrc[at] = S[src];
+          vtgt[at] = S[b];
+          voff[at] = d;
+          vscale[at] = inv_h;
+        }
+      }
+    }
+    mark("m2l pairs");
+    std::vector<int64_t> vtgts, tpoff{0};
+    D.v_key_tgt_off.assign(1, 0);
+    D.max_key_pairs = 0;
+    for (int k = 0; k < nk; ++k) {
+      const int64_t a = D.v_key_pair_off[k], e = D.v_key_pair_off[k + 1];
+      for (int64_t i = a; i < e; ++i) {
+        if (i == a || vtgt[i] != vtgt[i - 1]) {
+          if (i > a) tpoff.push_back(i);
+          vtgts.push_back(vtgt[i]);
+        }
+      }
+      if (e > a) tpoff.push_back(e);
+      D.v_key_tgt_off.push_back((int64_t)vtgts.size());
+      D.max_key_pairs = std::max<int64_t>(D.max_key_pairs, e - a);
+    }
+    mark("m2l tgts");
+    LB_TRY(upload(&D.v_src, vsrc));
+    LB_TRY(upload(&D.v_tgts, vtgts));
+    LB_TRY(upload(&D.v_tgt_pair_off, tpoff));
+    D.v_tpoff_host = tpoff;
+    LB_TRY(upload(&D.v_off_idx, voff));
+    LB_TRY(upload(&D.v_scale, vscale));
   }
-  mark("m2l tgts");
-  LB_TRY(upload(&D.v_src, vsrc));
-  LB_TRY(upload(&D.v_tgts, vtgts));
-  LB_TRY(upload(&D.v_tgt_pair_off, tpoff));
-  D.v_tpoff_host = tpoff;
-  LB_TRY(upload(&D.v_off_idx, voff));
-  LB_TRY(upload(&D.v_scale, vscale));
   mark("m2l upload");
   // X list (fmm.py:891-911): boxes with sourceful X entries
   std::vector<int64_t> xb, xo{0}, xl;
@@ -1096,6 +1344,7 @@ int build_device(lb_fmm_plan* P) {
   mark("leaf upload");
   if (cublasCreate(&D.blas) != CUBLAS_STATUS_SUCCESS) return fail(LB_ERR_CUDA, "cublasCreate failed");
   mark("cublas");
+  LB_CUDA(cudaStreamSynchronize(0));  // the setup kernels above ran on the legacy stream
   D.ready = true;
   return LB_OK;
 }

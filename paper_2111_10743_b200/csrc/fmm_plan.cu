@@ -63,12 +63,13 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
   auto c1 = c0;
   double dev_lists_ms = -1;
   if (flags & LB_FMM_DEVICE_SORT) {
-    rc = tree_build_device(t, spos, tpos, buffer, &dev_lists_ms);  // fmm_tree_dev.cu
+    rc = tree_build_device(t, spos, tpos, buffer, &dev_lists_ms, &p->tdev);  // fmm_tree_dev.cu
     c1 = clk::now();
   } else {
     rc = tree_build_host(t, spos, ns, tpos, nt, ncrit);
   }
   if (rc != LB_OK) {
+    p->tdev.release();
     delete p;
     return rc;
   }
@@ -91,6 +92,7 @@ int lb_fmm_plan_create(const double* spos, int64_t ns, const double* tpos, int64
 int lb_fmm_plan_destroy(lb_fmm_plan* p) {
   if (!p) return LB_OK;
   fmm_release_device(p);
+  p->tdev.release();
   delete p;
   return LB_OK;
 }

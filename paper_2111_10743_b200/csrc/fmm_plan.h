@@ -87,6 +87,19 @@ struct FmmDevice {
   int64_t lr_t_cap = 0;
 };
 
+// device arrays kept from the device tree build (fmm_tree_dev.cu): the
+// apply's device state is gathered from them instead of re-uploaded
+struct TreeDev {
+  double *spos = nullptr, *tpos = nullptr;         // original order
+  int64_t *src_sorted = nullptr, *tgt_sorted = nullptr;
+  int64_t *v_off = nullptr, *v_idx = nullptr;      // V list (by box id)
+  void release() {
+    cudaFree(spos); cudaFree(tpos); cudaFree(src_sorted); cudaFree(tgt_sorted);
+    cudaFree(v_off); cudaFree(v_idx);
+    *this = TreeDev();
+  }
+};
+
 }  // namespace lb
 
 struct lb_fmm_plan {
@@ -102,6 +115,7 @@ struct lb_fmm_plan {
   int ncanon = 0, noff = 0;
   double ue_scale = 1.05, uc_scale = 2.85, dc_scale = 1.05, de_scale = 2.85;
   lb::FmmDevice dev;
+  lb::TreeDev tdev;                         // device tree build leftovers (empty on the host path)
   std::vector<int64_t> slot_of, id_of;      // box id <-> level-major slot
   std::vector<double> stage_ms;             // last apply's per-stage device times
   double setup_ms[4] = {0, 0, 0, 0};        // keys+sort, tree, lists, device state (host ms)
@@ -116,6 +130,13 @@ struct lb_fmm_plan {
 
 namespace lb {
 void fmm_release_device(lb_fmm_plan* p);
+// Device path (fmm_tree_dev.cu): keys, radix sort, boxes, the reference
+// numbering and the interaction lists on the GPU; fills everything
+// tree_from_sorted + tree_lists do except the sorted codes / order.
+// lists_ms (optional) receives the lists' share; keep (optional) receives
+// device copies of the positions, sorted index lists and the V list.
+int tree_build_device(FmmTree& t, const double* spos, const double* tpos, int buffer, double* lists_ms,
+                      TreeDev* keep);
 // The two-density A3 call (charges (2, ns): X = c0, B = c1; dipoles (2, ns, 3):
 // X only, = -c1 n_s) at level 2 with a PROJECTED leaf stage: besides
 // pot/grad/hess of the grid L2T part (zero in surface mode), proj (3, nt)

@@ -64,12 +64,6 @@ int tree_from_sorted(FmmTree& t, std::vector<uint64_t>&& codes, std::vector<int6
 int tree_build_host(FmmTree& t, const double* spos, int64_t ns, const double* tpos, int64_t nt,
                     int ncrit);
 
-// Device path (fmm_tree_dev.cu): keys, radix sort, boxes, the reference
-// numbering and the interaction lists on the GPU; fills everything
-// tree_from_sorted + tree_lists do except the sorted codes / order (which
-// stay on the device).  lists_ms (optional) receives the lists' share.
-int tree_build_device(FmmTree& t, const double* spos, const double* tpos, int buffer, double* lists_ms);
-
 void tree_lists(FmmTree& t, int buffer);
 
 uint64_t morton_key(const double* p, const double center[3], double half);

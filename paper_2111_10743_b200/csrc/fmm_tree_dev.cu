@@ -385,6 +385,11 @@ struct TreeScratch {
     if (err == cudaSuccess) ptrs.push_back(p);
     return (T*)p;
   }
+  template <class T>
+  T* release(T* p) {  // hand ownership to the caller
+    ptrs.erase(std::remove(ptrs.begin(), ptrs.end(), (void*)p), ptrs.end());
+    return p;
+  }
   ~TreeScratch() {
     for (void* p : ptrs) cudaFree(p);
   }
@@ -427,7 +432,8 @@ cudaError_t d2h(std::vector<T>& dst, const T* src, int64_t n) {
                                                         ": " + cudaGetErrorString(_e));       \
   } while (0)
 
-int tree_build_device(FmmTree& t, const double* spos, const double* tpos, int buffer, double* lists_ms) {
+int tree_build_device(FmmTree& t, const double* spos, const double* tpos, int buffer, double* lists_ms,
+                      TreeDev* keep) {
   const int64_t m = t.ns + t.nt;
   if (m >= ((int64_t)1 << 31)) return fail(LB_ERR_SHAPE, "fmm device tree: more than 2^31 points");
   TreeScratch S;
@@ -703,6 +709,15 @@ int tree_build_device(FmmTree& t, const double* spos, const double* tpos, int bu
     t.tgt_hi[b] = tr[2 * b + 1];
     t.nsrc[b] = t.src_hi[b] - t.src_lo[b];  // a box's range holds exactly its subtree (fmm.py:636-639)
     t.levels[t.level[b]].push_back(b);
+  }
+  if (keep) {
+    keep->release();
+    keep->spos = S.release(ds);
+    keep->tpos = S.release(dt);
+    keep->src_sorted = S.release(src_sorted);
+    keep->tgt_sorted = S.release(tgt_sorted);
+    keep->v_off = S.release(voff);
+    keep->v_idx = S.release(vidx);
   }
   return LB_OK;
 }

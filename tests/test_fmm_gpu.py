@@ -146,6 +146,31 @@ def test_device_tree_and_lists_equal_host(cuda, case):
         assert np.array_equal(a[name], b[name]), name
 
 
+@pytest.mark.parametrize("eps,rng_t", [(1e-6, None), (1e-9, None), (1e-6, (1000, 25000))])
+def test_device_plan_apply_bit_identical_to_host_plan(cuda, eps, rng_t):
+    """Device tree + lists + device M2L grouping vs the host build: the same
+    arrays, so the applies agree bit for bit (also with an owned target range)."""
+    import torch
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(11)
+    s = rng.standard_normal((60000, 3))
+    s /= np.linalg.norm(s, axis=1)[:, None]
+    t = rng.random((40000, 3)) - 0.5
+    q = torch.from_numpy(rng.standard_normal((2, 60000))).cuda()
+    out = []
+    for dev in (True, False):
+        p = FmmPlan(s, t, eps, device_sort=dev)
+        if rng_t:
+            p.set_target_range(*rng_t)
+        pot = torch.zeros((2, 40000), dtype=torch.float64, device="cuda")
+        grad = torch.zeros((2, 40000, 3), dtype=torch.float64, device="cuda")
+        p.apply_device(q, None, 2, 3, 0, 1, pot, grad)
+        torch.cuda.synchronize()
+        sl = slice(*rng_t) if rng_t else slice(None)
+        out.append((pot[:, sl].cpu().numpy(), grad[:, sl].cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
 def test_device_tree_capacity_error(cuda):
     from paper_2111_10743_b200 import FmmCapacityError
     from paper_2111_10743_b200.fmm_plan import FmmPlan
