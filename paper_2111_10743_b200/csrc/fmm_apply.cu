@@ -566,19 +566,20 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
   const int64_t ve = items[4 * blockIdx.x + 2], poff = items[4 * blockIdx.x + 3];
   const int64_t b = leaves[li];
   const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
-  // leaves hold few targets (~17 on average at ncrit 120): size the target
-  // pass to the leaf and give the remaining threads other source phases
-  int kTgt = 16;
-  while (kTgt < t1 - t0 && kTgt < kLeafBT) kTgt <<= 1;
+  // leaves hold few targets (~17 on average at ncrit 120): the target pass
+  // is the leaf's own size (not a power of two: 17 targets would leave 15 of
+  // every 32 threads idle) and the remaining threads take other source phases
+  const int kTgt = (int)min((int64_t)kLeafBT, max((int64_t)1, t1 - t0));
   const int kSplit = kLeafBT / kTgt;
   const int64_t ub = u_off[li], nu = u_off[li + 1] - ub;
   const int64_t wb = w_off[li], nw = w_off[li + 1] - wb;
   const int64_t nde = surface ? 1 : 0;
   const int64_t nsets_all = nu + nde + nw;
   const int ti = threadIdx.x % kTgt, ph = threadIdx.x / kTgt;
+  const bool active = ph < kSplit;  // the last kLeafBT % kTgt threads only stage sources
   for (int64_t tb = t0; tb < t1; tb += kTgt) {
     const int64_t t = tb + ti;
-    const bool in = t < t1;
+    const bool in = active && t < t1;
     const double tx = in ? tpos[3 * t] : 0.0, ty = in ? tpos[3 * t + 1] : 0.0,
                  tz = in ? tpos[3 * t + 2] : 0.0;
     double nx = 0.0, ny = 0.0, nz = 0.0;
@@ -665,12 +666,14 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
         __syncthreads();
         // unrolled over sources: independent pair chains give the FP64 pipe
         // ILP (one pair at a time is a serial DADD-DFMA-MUFU-DFMA chain)
-        if constexpr (A3P) {
+        if (active) {
+          if constexpr (A3P) {
 #pragma unroll 4
-          for (int k = ph; k < n; k += kSplit) pair_a3(tx, ty, tz, nx, ny, nz, sh + k * S, acc);
-        } else {
+            for (int k = ph; k < n; k += kSplit) pair_a3(tx, ty, tz, nx, ny, nz, sh + k * S, acc);
+          } else {
 #pragma unroll 4
-          for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+            for (int k = ph; k < n; k += kSplit) pair_generic<ND, true, HD, LEVEL>(tx, ty, tz, sh + k * S, acc);
+          }
         }
       }
       vbase += total;
