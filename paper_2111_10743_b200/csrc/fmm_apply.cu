@@ -1133,27 +1133,35 @@ int build_device(lb_fmm_plan* P) {
   std::vector<int64_t> uc, upar, dch, dpar;
   D.up_off.assign(1, 0);
   D.dn_off.assign(1, 0);
-  for (int l = 0; l < t.nlev; ++l) {
-    for (int oct = 0; oct < 8; ++oct) {
-      for (int64_t b : (l > 0 ? t.levels[l] : std::vector<int64_t>{})) {
-        const int64_t s = S[b];
-        if (octant[s] != oct) continue;
-        const int64_t p = t.parent[b];
-        if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) {  // fmm.py:855-859
-          uc.push_back(s);
-          upar.push_back(S[p]);
+  {  // buckets per (level, octant), boxes in ascending id within a level
+    std::vector<std::vector<int64_t>> bu(8), bd(8);
+    for (int l = 0; l < t.nlev; ++l) {
+      for (auto& v : bu) v.clear();
+      for (auto& v : bd) v.clear();
+      if (l > 0)
+        for (int64_t b : t.levels[l]) {
+          const int64_t s = S[b];
+          const int oct = (int)octant[s];
+          const int64_t p = t.parent[b];
+          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) bu[oct].push_back(b);  // fmm.py:855-859
+          // fmm.py:923-935 passes down to every child; children without targets
+          // in their subtree never reach an L2T or a leaf, so they are skipped
+          // (the results at the targets are unchanged; a plan whose targets are
+          // one rank's rows skips most of the downward pass)
+          if (own_id[b]) bd[oct].push_back(b);
         }
-        // fmm.py:923-935 passes down to every child; children without targets
-        // in their subtree never reach an L2T or a leaf, so they are skipped
-        // (the results at the targets are unchanged; a plan whose targets are
-        // one rank's rows skips most of the downward pass)
-        if (owned(b) > 0) {
-          dch.push_back(s);
-          dpar.push_back(S[p]);
+      for (int oct = 0; oct < 8; ++oct) {
+        for (int64_t b : bu[oct]) {
+          uc.push_back(S[b]);
+          upar.push_back(S[t.parent[b]]);
         }
+        for (int64_t b : bd[oct]) {
+          dch.push_back(S[b]);
+          dpar.push_back(S[t.parent[b]]);
+        }
+        D.up_off.push_back((int64_t)uc.size());
+        D.dn_off.push_back((int64_t)dch.size());
       }
-      D.up_off.push_back((int64_t)uc.size());
-      D.dn_off.push_back((int64_t)dch.size());
     }
   }
   LB_TRY(upload(&D.up_child, uc));
@@ -1263,35 +1271,66 @@ int build_device(lb_fmm_plan* P) {
     LB_TRY(upload(&D.v_scale, vscale));
   }
   mark("m2l upload");
-  // X list (fmm.py:891-911): boxes with sourceful X entries
-  std::vector<int64_t> xb, xo{0}, xl;
+  // X list (fmm.py:891-911): boxes with sourceful X entries; leaf stage
+  // (fmm.py:940-988): target leaves, their U (with sources) and W lists.
+  // Count / scan / fill, parallel over boxes, same order as a serial walk.
+  std::vector<int64_t> xcnt(nb, 0), ucnt(nb, 0), wcnt(nb, 0);
+  std::vector<uint8_t> is_tl(nb, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t b = 0; b < nb; ++b) {
-    if (owned(b) == 0) continue;  // as for M2L
-    bool any = false;
+    if (!own_id[b]) continue;  // as for M2L
     for (int64_t q = 0; q < t.xlist.size(b); ++q) {
       const int64_t x = t.xlist.row(b)[q];
-      if (t.src_hi[x] > t.src_lo[x]) { any = true; xl.push_back(S[x]); }
+      xcnt[b] += t.src_hi[x] > t.src_lo[x] ? 1 : 0;
     }
-    if (any) { xb.push_back(S[b]); xo.push_back((int64_t)xl.size()); }
+    if (!t.is_leaf[b]) continue;
+    is_tl[b] = 1;
+    for (int64_t q = 0; q < t.ulist.size(b); ++q) {
+      const int64_t u = t.ulist.row(b)[q];
+      ucnt[b] += t.src_hi[u] > t.src_lo[u] ? 1 : 0;
+    }
+    wcnt[b] = t.wlist.size(b);
+  }
+  std::vector<int64_t> xb, xo{0}, tl, uo{0}, wo{0}, xpos(nb), upos(nb), wpos(nb);
+  for (int64_t b = 0; b < nb; ++b) {
+    xpos[b] = xo.back();
+    if (xcnt[b] > 0) {
+      xb.push_back(S[b]);
+      xo.push_back(xo.back() + xcnt[b]);
+    }
+    upos[b] = uo.back();
+    wpos[b] = wo.back();
+    if (is_tl[b]) {
+      tl.push_back(S[b]);
+      uo.push_back(uo.back() + ucnt[b]);
+      wo.push_back(wo.back() + wcnt[b]);
+    }
+  }
+  std::vector<int64_t> xl(xo.back()), ul(uo.back()), wl(wo.back());
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t b = 0; b < nb; ++b) {
+    if (xcnt[b] > 0) {
+      int64_t o = xpos[b];
+      for (int64_t q = 0; q < t.xlist.size(b); ++q) {
+        const int64_t x = t.xlist.row(b)[q];
+        if (t.src_hi[x] > t.src_lo[x]) xl[o++] = S[x];
+      }
+    }
+    if (is_tl[b]) {
+      int64_t o = upos[b];
+      for (int64_t q = 0; q < t.ulist.size(b); ++q) {
+        const int64_t u = t.ulist.row(b)[q];
+        if (t.src_hi[u] > t.src_lo[u]) ul[o++] = S[u];
+      }
+      o = wpos[b];
+      for (int64_t q = 0; q < t.wlist.size(b); ++q) wl[o++] = S[t.wlist.row(b)[q]];
+    }
   }
   D.n_x = (int64_t)xb.size();
   LB_TRY(upload(&D.x_boxes, xb));
   LB_TRY(upload(&D.x_off, xo));
   LB_TRY(upload(&D.x_leaves, xl));
   mark("x list");
-  // leaf stage (fmm.py:940-988): target leaves, their U (with sources) and W lists
-  std::vector<int64_t> tl, uo{0}, ul, wo{0}, wl;
-  for (int64_t b = 0; b < nb; ++b) {
-    if (!t.is_leaf[b] || owned(b) == 0) continue;
-    tl.push_back(S[b]);
-    for (int64_t q = 0; q < t.ulist.size(b); ++q) {
-      const int64_t u = t.ulist.row(b)[q];
-      if (t.src_hi[u] > t.src_lo[u]) ul.push_back(S[u]);
-    }
-    uo.push_back((int64_t)ul.size());
-    for (int64_t q = 0; q < t.wlist.size(b); ++q) wl.push_back(S[t.wlist.row(b)[q]]);
-    wo.push_back((int64_t)wl.size());
-  }
   D.n_tleaf = (int64_t)tl.size();
   mark("leaf lists");
   // work items: a leaf's virtual source list [U sources | own DE set | W sets]

@@ -148,7 +148,10 @@ def c5_summary():
                      f"{r['effective_interactions_per_s']:.2e} | {r['err_vs_direct_200_targets']:.1e} | "
                      f"{st['m2l']:.1f} | {st['x']:.1f} | {st['leaf']:.1f} | "
                      f"{refs.get(c, 'not run (hours)')} |")
-    L += ["", "Earlier rows of this round with the tcgen05 int8 M2L: config5_sweep_tc_m2l.jsonl "
+    L += ["", "`plan s` is FmmPlan construction including the unit operators' first "
+          "(cached) host precompute (grid n=9: ~2 s, paid by the first 1e-9 row); the setup "
+          "split without it is in plan_setup.md.",
+          "", "Earlier rows of this round with the tcgen05 int8 M2L: config5_sweep_tc_m2l.jsonl "
           "(1e6 at 1e-9: 197 ms; 1e7 at 1e-9: 1.28 s)."]
     open(os.path.join(OUT, "config5_sweep.md"), "w").write("\n".join(L) + "\n")
 
