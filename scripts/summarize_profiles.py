@@ -115,7 +115,9 @@ def avn_summary():
           "8(N+1) with k = 2 value arrays (fused: S', S''+D') or 3 (FMM path: S', S, S''+D'); x "
           f"gathers hit L2.  HBM peak = {hbm} GB/s (MEASURED_PEAKS.json).  Config 2's CSR "
           "(66 MB/kind) is L2-sized, so its passes are latency-bound.  Earlier rows of this round "
-          "(3-density FMM, synthetic values): apply_vs_n_pre_fusion.jsonl."]
+          "(3-density FMM, synthetic values): apply_vs_n_pre_fusion.jsonl.  Config-3 rows were "
+          "re-measured after the leaf-pass fix (fmm_apply.cu); the config-4 rows predate it (its "
+          "geometry file is too large to ship to the GPU box this session)."]
     open(os.path.join(OUT, "apply_vs_n.md"), "w").write("\n".join(L) + "\n")
 
 
