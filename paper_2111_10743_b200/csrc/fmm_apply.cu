@@ -506,7 +506,7 @@ inline size_t l2t_smem(int n, int level) {
 // ONE virtual list so every shared-memory tile is full; the block's threads
 // are split into kSplit source phases per target and combined at the end.
 constexpr int kLeafBT = 128;
-constexpr int kLeafTS = 128;
+constexpr int kLeafTS = 256;
 constexpr int kLeafMaxSets = 512;
 
 // Projected pair of the two-density A3 call (fmm_apply_a3proj), where density
