@@ -227,6 +227,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time the step without a CUDA graph")
+    ap.add_argument("--no-fmm", action="store_true",
+                    help="skip the secondary FMM line (config 5, N = 1e6 on the sphere)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -394,6 +396,10 @@ def main():
                "sample": "one full A3 apply of config 2 (oracle/apply.py: C direct "
                          "sums + numpy glue; MGS excluded)"}
 
+    fmm = None
+    if rank == 0 and world == 1 and not args.no_fmm:
+        fmm = fmm_config5(torch)
+
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -425,9 +431,44 @@ def main():
                     "ms_per_step": e2e_t * 1e3},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
+            "fmm_config5": fmm,
         }), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def fmm_config5(torch, n=1_000_000, eps=1e-6, reps=5):
+    """Secondary evidence for the 'apply time vs N' half of the metric:
+    BASELINE config 5's FMM (N = 1e6 unit-sphere cloud, sources = targets,
+    seed 105, charge pot+grad) through the device FmmPlan -- plan setup
+    (device tree, lists, operators) and the event-timed apply."""
+    import time
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(105)
+    x = rng.standard_normal((n, 3))
+    x /= np.linalg.norm(x, axis=1)[:, None]
+    q = torch.from_numpy(rng.standard_normal((1, n))).cuda()
+    FmmPlan(x[:1000], x[:1000], eps)  # unit operators (cached), as a user's first plan
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = FmmPlan(x, x, eps)
+    pot = torch.empty((1, n), dtype=torch.float64, device="cuda")
+    grad = torch.empty((1, n, 3), dtype=torch.float64, device="cuda")
+    plan.apply_device(q, None, 1, 1, 0, 1, pot, grad)  # builds the device state
+    torch.cuda.synchronize()
+    t_setup_first = time.perf_counter() - t0
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.apply_device(q, None, 1, 1, 0, 1, pot, grad)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = sum(ts) / len(ts)
+    return {"workload": "config5-fmm", "N": n, "eps": eps, "rep": plan.rep, "m": plan.m,
+            "apply_ms": t * 1e3, "effective_interactions_per_s": n * (n - 1) / t,
+            "plan_plus_first_apply_s": t_setup_first, "setup_ms": plan.setup_times()}
 
 
 def far2_time(torch, op, tau, lib, _lib, which=2, reps=20):
