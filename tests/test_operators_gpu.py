@@ -159,6 +159,23 @@ def test_config2_solve(cuda, form):
     assert e_ours < 3e-7 and abs(e_ours - e_ref) < 1e-8 + 0.01 * e_ref
 
 
+def test_config2_solve_device_corrections(cuda):
+    """BASELINE config 2 without the large reference bundle: the committed
+    geometry golden (tests/golden/config2_geom.npz: the reference's A3 apply of
+    the seeded tau, its GMRES history and solution) with the corrections
+    built on the device (csrc/quad.cu).  Same bar as test_config2_solve."""
+    from paper_2111_10743_b200 import (Geometry, LayerOperatorSet, SolveConfig,
+                                       solve_laplace_beltrami)
+    g = golden("config2_geom.npz")
+    op = LayerOperatorSet(Geometry.from_arrays(g), "a3", float(g["eps"]))
+    assert _rel(op.apply(g["tau"]), g["a3_apply"]) < 1e-10
+    rep = solve_laplace_beltrami(op, g["f"], SolveConfig(
+        formulation="a3", eps=float(g["eps"]), eps_gmres=1e-10))
+    w = g["weights"]
+    assert rep.converged and rep.n_iter == len(g["a3_hist"])
+    assert _wl2(rep.u.values, g["a3_u"], w) < 1e-8
+
+
 @pytest.mark.parametrize("fixture,forms", FIXTURES)
 def test_apply_with_fmm_far_field(cuda, fixture, forms):
     """use_fmm path (operators.py:104-112): every far call through the device
