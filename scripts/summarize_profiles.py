@@ -62,8 +62,8 @@ def bench_summary():
         agg[nm.replace("void ", "").strip()][1] += m["gpu__time_duration.sum"]
     tot = sum(v[1] for v in agg.values())
     lines = ["# `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`: ncu launch list",
-             "", "Every launch of the bench command (setup, parity apply, warm-up, timed "
-             "steps, the far-sweep timing reps, e2e steps, the DFMA peak probe), "
+             "", "Every launch of the bench command (setup incl. the device correction build, parity apply, warm-up, timed "
+             "steps, the far-sweep timing reps, e2e steps, the DFMA peak probe, the secondary config-5 FMM line), "
              "aggregated by kernel; cold-cache and serialised (shares, not absolutes).", "",
              "| kernel | launches | us | share |", "|---|---|---|---|"]
     for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
