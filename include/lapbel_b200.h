@@ -377,6 +377,37 @@ typedef struct {
 int lb_corrections_build(const lb_corr_build_desc* desc, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Surface geometry from chart expansions (the lbmesh reader
+ * `read_mesh`, meshio.py:35-50, ends in build_from_coefficients,
+ * surface.py:176-307).  One CTA per patch evaluates nodes, tangents, normals,
+ * metric and its inverse, |X_u x X_v|, mean curvature (spectral second
+ * derivatives of the stored tangents), the smooth node weights and the
+ * oversampled nodes / normals / weights.  Reference-element tables
+ * (simplex.py:359-397, row-major, DEVICE): vand, dmat_u, dmat_v (nb x nb),
+ * psi_rule and weight_interp (nq x nb), rule_wts (nq), psi_over (no x nb),
+ * psi_child (4 x nq x nb: the basis at the rule mapped into each child
+ * triangle) and w_interp_o (nq x no/4).  stats (DEVICE double[6]) receives
+ * max |D_u X - X_u| over D_v too, max |X_u|,|X_v|, min |X_u x X_v| at the
+ * nodes, the same at the oversampled nodes, and the squared norms of the
+ * top-degree and of all coefficients of coeffs_x: the caller raises the
+ * reference's consistency / DegeneratePatchError checks from them
+ * (surface.py:199-223, 265-267).  Outputs are (npatches * nb) or
+ * (npatches * no) rows, patch-major. */
+typedef struct lb_geom_desc {
+  int order, nb, nq, no;
+  int64_t npatches;
+  const double *coeffs_x, *coeffs_dxdu, *coeffs_dxdv; /* (npatches, nb, 3) */
+  const double *vand, *dmat_u, *dmat_v, *psi_rule, *rule_wts, *weight_interp;
+  const double *psi_over, *psi_child, *w_interp_o;
+  double *nodes, *tangents_u, *tangents_v, *normals; /* (N, 3) */
+  double *metric, *inv_metric;                       /* (N, 2, 2) */
+  double *sqrt_det_g, *curvature, *weights;          /* (N) */
+  double *over_nodes, *over_normals, *over_weights;  /* (N_over, 3/3/1) */
+  double* stats;
+} lb_geom_desc;
+int lb_geom_build(const lb_geom_desc* desc, void* stream);
+
+/* ------------------------------------------------------------------------
  * Hardware probes (no reference counterpart): FP64 FMA-pipe peak
  * (flops = blocks*256*iters*256) and the 1/sqrt seed/refinement, used to state
  * the measured fp64 roofline and the kernel's rsqrt accuracy. */

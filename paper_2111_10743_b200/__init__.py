@@ -6,7 +6,8 @@ sums (FmmSources, FmmResult, evaluate_direct, evaluate_fmm, FmmPlan), the
 operator set (LayerOperatorSet, DensityVector), the solver (gmres,
 solve_laplace_beltrami, SolveConfig, SolveReport) and, widening into
 SURVEY §8(f) #1, the near-correction build (build_near_map,
-compute_corrections).  All arithmetic runs in
+compute_corrections) and, §8(f) #4, the lbmesh reader/writer with the
+device geometry build (read_mesh, write_mesh, build_from_coefficients).  All arithmetic runs in
 libb200lb.so; there is no CPU fallback.
 """
 
@@ -21,6 +22,10 @@ from .solver import (GmresBreakdown, SolveConfig, SolveReport, gmres,
                      solve_laplace_beltrami)
 from .quadrature import (AdaptiveDepthError, NearMap, NearMapCapError,
                          build_near_map, compute_corrections)
+from .simplex import ReferenceElement, reference_element
+from .surface import (DegeneratePatchError, SurfaceDiscretization,
+                      build_from_coefficients)
+from .meshio import read_mesh, write_mesh
 
 __all__ = [
     "FmmSources", "FmmResult", "FmmCapacityError", "FmmPlan",
@@ -29,5 +34,7 @@ __all__ = [
     "LayerOperatorSet", "apply_layer", "SolveConfig", "SolveReport",
     "GmresBreakdown", "gmres", "solve_laplace_beltrami",
     "NearMap", "NearMapCapError", "AdaptiveDepthError", "build_near_map",
-    "compute_corrections",
+    "compute_corrections", "ReferenceElement", "reference_element",
+    "DegeneratePatchError", "SurfaceDiscretization", "build_from_coefficients",
+    "read_mesh", "write_mesh",
 ]

@@ -77,6 +77,7 @@ SIGNATURES = {
     "lb_near_map_count": [_P, _I64, _P, _P, _I64, _P, _P, _P],
     "lb_near_map_fill": [_P, _I64, _P, _P, _I64, _P, _P, _P, _P],
     "lb_corrections_build": [_P, _P],
+    "lb_geom_build": [_P, _P],
     "lb_fmm_stage_times": [_P, _P],
     "lb_fmm_setup_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],

@@ -170,11 +170,8 @@ def _over_interp(disc):
     oi = getattr(disc, "over_interp", None)
     if oi is not None:
         return np.asarray(oi, dtype=float)
-    try:  # the reference's own element (host precompute, simplex.py:383)
-        from lapbel.simplex import reference_element
-    except ImportError as exc:  # pragma: no cover
-        raise ValueError("disc has no over_interp and lapbel is not "
-                         "importable to build it") from exc
+    # the reference element's table (simplex.py:383), restated in simplex.py
+    from .simplex import reference_element
     return reference_element(disc.order).over_interp
 
 
@@ -474,9 +471,8 @@ class LayerOperatorSet:
                     when None they are built ON THE DEVICE
                     (quadrature.build_correction_set: near map + adaptive
                     singular quadrature, csrc/quad.cu) if disc carries the
-                    chart coefficients;
-                    otherwise by the reference's compute_corrections
-                    (requires lapbel to be importable).
+                    chart coefficients; otherwise ValueError (there is
+                    no CPU correction build).
       far         : "auto" (default), "direct" or "fmm".  use_fmm=False
                     always means exact all-pairs sweeps (the reference's
                     evaluate_direct path).  With use_fmm=True, "auto" keeps
@@ -535,9 +531,11 @@ class LayerOperatorSet:
                     self.corrections_built_on = "device"
                 self.near = near
             else:
-                corrections, self.near, self.t_q = _reference_corrections(
-                    disc, kinds, self.eps, eta, near)
-                self.corrections_built_on = "reference"
+                raise ValueError(
+                    "corrections must be passed in, or disc must carry the "
+                    "chart coefficients (coeffs_x/coeffs_dxdu/coeffs_dxdv, "
+                    "e.g. from meshio.read_mesh or "
+                    "surface.build_from_coefficients) for the device build")
         else:
             self.near = near
         if not isinstance(corrections, CorrectionSet):
@@ -812,22 +810,6 @@ def _as_near_map(near, eta):
     return NearMap(float(getattr(near, "eta", eta)), int(getattr(near, "cap", 128)),
                    np.concatenate([[0], np.cumsum(lens)]).astype(np.int64),
                    np.concatenate(lists).astype(np.int32))
-
-
-def _reference_corrections(disc, kinds, eps, eta, near):
-    try:
-        from lapbel.kernels import KernelKind as RefKind
-        from lapbel.quadrature import build_near_map, compute_corrections
-    except ImportError as exc:
-        raise ValueError(
-            "corrections must be passed in (building them is the reference's "
-            "CPU precompute, quadrature.py:663-701, and lapbel is not "
-            "importable here)") from exc
-    if near is None:
-        near = build_near_map(disc, eta)
-    ref_kinds = [RefKind(k.value) for k in kinds]
-    corrs, t_q = compute_corrections(disc, near, ref_kinds, eps)
-    return {as_kind(k): v for k, v in corrs.items()}, near, t_q
 
 
 def apply_layer(opset: LayerOperatorSet, kind, density) -> DensityVector:

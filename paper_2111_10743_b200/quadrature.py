@@ -213,10 +213,8 @@ def _vinv(disc):
     v = getattr(disc, "vinv", None)
     if v is not None:
         return np.asarray(v, dtype=float)
-    try:  # ReferenceElement.vinv (simplex.py:359-383), host precompute
-        from lapbel.simplex import reference_element
-    except ImportError as exc:  # pragma: no cover
-        raise ValueError("disc has no vinv and lapbel is not importable") from exc
+    # ReferenceElement.vinv (simplex.py:359-383), restated in simplex.py
+    from .simplex import reference_element
     return reference_element(disc.order).vinv
 
 

@@ -1,0 +1,108 @@
+"""Device geometry build (csrc/geom.cu, `build_from_coefficients`,
+surface.py:176-307) and the lbmesh reader (meshio.py:35-50) against the
+reference's own outputs: its read_mesh of a file its write_mesh produced
+(tests/golden/mesh_twisted_torus_o5.npz) and the geometry arrays stored with
+the order-3/7/9 fixtures.  Floating point: the device sums the same products
+in a different order than numpy/BLAS, so the bar is a relative max-norm of
+1e-13 per field (1e-12 for the inverse metric, whose det g cancels, and
+1e-11 for the mean curvature, a second spectral derivative),
+index fields bit-exact.  Also the reference's error behaviour: a
+mis-wired derivative expansion is a ValueError, a zero-area chart a
+DegeneratePatchError."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, golden
+
+pytestmark = pytest.mark.gpu
+
+FLOAT = ["nodes", "tangents_u", "tangents_v", "normals", "inv_metric",
+         "weights", "over_nodes", "over_normals", "over_weights"]
+
+
+# the inverse metric divides by det g = g11 g22 - g12^2 (cancellation on
+# sheared charts), the curvature is a second spectral derivative
+TOL = {"inv_metric": 1e-12, "curvature": 1e-11}
+
+
+def _rel(a, b):
+    scale = np.abs(b).max()
+    return np.abs(np.asarray(a) - b).max() / (scale if scale > 0 else 1.0)
+
+
+def _check(disc, g, fields):
+    for f in fields:
+        tol = TOL.get(f, 1e-13)
+        assert disc.__dict__[f].shape == g[f].shape, f
+        assert _rel(disc.__dict__[f], g[f]) < tol, (f, _rel(disc.__dict__[f], g[f]))
+
+
+def test_read_mesh_matches_reference(cuda):
+    from paper_2111_10743_b200 import read_mesh
+    disc = read_mesh(os.path.join(GOLD, "twisted_torus_o5.lbmesh"))
+    g = golden("mesh_twisted_torus_o5.npz")
+    _check(disc, g, FLOAT + ["curvature", "metric", "sqrt_det_g"])
+    for f in ("node_patch", "over_patch"):
+        np.testing.assert_array_equal(disc.__dict__[f], g[f])
+    for f in ("node_uv", "over_uv", "coeffs_x", "coeffs_dxdu", "coeffs_dxdv"):
+        np.testing.assert_array_equal(disc.__dict__[f], g[f])
+    assert disc.node_family == str(g["family"])
+    assert disc.npatches == 48 and disc.nnodes == 720
+
+
+@pytest.mark.parametrize("fixture", ["opset_torus_o3.npz", "config2_geom.npz",
+                                     "quad_sphere_o9.npz"])
+def test_build_from_coefficients_matches_fixture(cuda, fixture):
+    from paper_2111_10743_b200 import build_from_coefficients
+    g = golden(fixture)
+    disc = build_from_coefficients(int(g["order"]), g["coeffs_x"],
+                                   g["coeffs_dxdu"], g["coeffs_dxdv"])
+    _check(disc, g, FLOAT + ["curvature"])
+    np.testing.assert_array_equal(disc.node_patch, g["node_patch"])
+    np.testing.assert_array_equal(disc.over_interp, g["over_interp"])
+    if "vinv" in g:
+        np.testing.assert_array_equal(disc.vinv, g["vinv"])
+
+
+def test_read_mesh_feeds_the_operator_set(cuda, tmp_path):
+    # the reader's discretization drives the device correction build and the
+    # A3 apply exactly as the reference's arrays do
+    from paper_2111_10743_b200 import LayerOperatorSet, read_mesh
+    from paper_2111_10743_b200.operators import Geometry
+    disc = read_mesh(os.path.join(GOLD, "twisted_torus_o5.lbmesh"))
+    g = golden("mesh_twisted_torus_o5.npz")
+    arrs = dict(g)
+    arrs["over_interp"] = disc.over_interp
+    arrs["vinv"] = disc.vinv
+    ref_geo = Geometry.from_arrays(arrs)
+    tau = np.sin(disc.nodes[:, 0]) + disc.nodes[:, 2] ** 2
+    a = LayerOperatorSet(disc, "a3", 1e-8).apply(tau)
+    b = LayerOperatorSet(ref_geo, "a3", 1e-8).apply(tau)
+    a, b = np.asarray(a), np.asarray(b)
+    assert np.abs(a - b).max() / np.abs(b).max() < 1e-9
+
+
+def test_miswired_derivatives_raise(cuda):
+    from paper_2111_10743_b200 import build_from_coefficients
+    # swapped X_u / X_v blocks: the reference raises "relative mismatch
+    # 1.00e+00, allowed 2.00e-01" on these coefficients (the under-resolved
+    # order-3 torus passes its loose tail tolerance in both builds)
+    g = golden("config2_geom.npz")
+    with pytest.raises(ValueError, match=r"mismatch 1\.00e\+00, allowed 2\.00e-01"):
+        build_from_coefficients(7, g["coeffs_x"], g["coeffs_dxdv"],
+                                g["coeffs_dxdu"])
+    t = golden("opset_torus_o3.npz")
+    build_from_coefficients(3, t["coeffs_x"], t["coeffs_dxdv"], t["coeffs_dxdu"])
+
+
+def test_degenerate_patch_raises(cuda):
+    from paper_2111_10743_b200 import DegeneratePatchError, build_from_coefficients
+    g = golden("opset_torus_o3.npz")
+    cu = g["coeffs_dxdu"].copy()
+    cv = g["coeffs_dxdv"].copy()
+    cv[5] = cu[5]  # X_u = X_v on patch 5: zero area element
+    with pytest.raises(DegeneratePatchError):
+        build_from_coefficients(3, g["coeffs_x"], cu, cv, consistency_tol=1e9)
