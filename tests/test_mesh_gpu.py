@@ -106,3 +106,27 @@ def test_degenerate_patch_raises(cuda):
     cv[5] = cu[5]  # X_u = X_v on patch 5: zero area element
     with pytest.raises(DegeneratePatchError):
         build_from_coefficients(3, g["coeffs_x"], cu, cv, consistency_tol=1e9)
+
+
+def test_config2_solve_from_lbmesh(cuda, tmp_path):
+    """The whole drop-in pipeline from a mesh file: BASELINE config 2's charts
+    written in the lbmesh format, read back (device geometry), device near map
+    + corrections, A3 GMRES solve -- against the reference's apply and solve
+    stored in tests/golden/config2_geom.npz (same bars as
+    test_operators_gpu.test_config2_solve_device_corrections)."""
+    from paper_2111_10743_b200 import (LayerOperatorSet, SolveConfig, read_mesh,
+                                       solve_laplace_beltrami, write_mesh)
+    from paper_2111_10743_b200.operators import Geometry
+    g = golden("config2_geom.npz")
+    path = tmp_path / "config2.lbmesh"
+    write_mesh(path, Geometry.from_arrays(g))
+    disc = read_mesh(path)
+    assert _rel(disc.nodes, g["nodes"]) < 1e-13
+    op = LayerOperatorSet(disc, "a3", float(g["eps"]))
+    assert _rel(op.apply(g["tau"]), g["a3_apply"]) < 1e-10
+    rep = solve_laplace_beltrami(op, g["f"], SolveConfig(
+        formulation="a3", eps=float(g["eps"]), eps_gmres=1e-10))
+    w = g["weights"]
+    assert rep.converged and rep.n_iter == len(g["a3_hist"])
+    d = rep.u.values - g["a3_u"]
+    assert np.sqrt(np.dot(w, d * d) / np.dot(w, g["a3_u"] ** 2)) < 1e-8
