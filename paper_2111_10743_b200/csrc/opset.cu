@@ -477,7 +477,13 @@ constexpr int kFarBT = 64;
 
 template <class F>
 constexpr int far_tpt() {
-  return F::S <= 4 && F::NOUT <= 2 ? 4 : 2;
+  // FarA3a: 2 targets/thread with an 8-deep pair unroll (135 registers, 6
+  // CTAs/SM): 381 vs 394 us at config 2 (tools/far_sweep.cu a3a, B200)
+  return std::is_same<F, FarA3a>::value ? 2 : (F::S <= 4 && F::NOUT <= 2 ? 4 : 2);
+}
+template <class F>
+constexpr int far_ur() {
+  return std::is_same<F, FarA3a>::value ? 8 : 4;
 }
 template <class F>
 constexpr int far_ts() {
@@ -491,7 +497,7 @@ SkLayout far_layout(const lb_opset* h) {
   static int per_sm = -1;
   if (per_sm < 0) {
     int b = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, opfar_kernel<F, TPT, kFarBT, far_ts<F>()>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, opfar_kernel<F, TPT, kFarBT, far_ts<F>(), true, far_ur<F>()>,
                                                   kFarBT, 0);
     per_sm = std::max(b, 1);
   }
@@ -510,7 +516,7 @@ int run_far(const lb_opset* h, const double* pack, SkLayout* out, cudaStream_t s
   const SkLayout L = far_layout<F>(h);
   if (L.tiles * L.kmax * F::NOUT * L.tt > h->part_cap)
     return fail(LB_ERR_ARG, "opset: partial buffer too small");
-  opfar_kernel<F, TPT, kFarBT, far_ts<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(
+  opfar_kernel<F, TPT, kFarBT, far_ts<F>(), true, far_ur<F>()><<<(unsigned)L.G, kFarBT, 0, st>>>(
       h->d.nodes + 3 * h->r0, h->d.normals + 3 * h->r0, h->nr, pack, L, h->part,
       h->d.curvature ? h->d.curvature + h->r0 : nullptr);
   LB_CHECK_LAUNCH();

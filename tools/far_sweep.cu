@@ -1,6 +1,7 @@
 // Tuning harness (not part of the library): times opfar_kernel variants
 // (functor x targets-per-thread x split policy) on a config-2-sized random
 // sphere problem.  Build: make -C tools far_sweep ; run on the GPU box.
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -73,7 +74,26 @@ int main(int argc, char** argv) {
   cudaMemcpy(dp, pack.data(), 8 * 8 * ns_pad, cudaMemcpyHostToDevice);
   // A3 call 2 uses the 8-double record; A3 call 1 reads the first 4 doubles
   // of a 4-double record: reuse the buffer (layout-only timing)
+  const bool only_a3a = argc > 3 && std::string(argv[3]) == "a3a";
   for (int w : {1}) {
+    if (only_a3a) {
+      run<FarA3a, 4, 64, 64, true, 4, 1>("A3a*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped
+      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 64, 32, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 64, 64, true, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 32, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, 2);
+      run<FarA3a, 3, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 3, 64, 32, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 64, 128, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 2, 64, 64, false, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3a, 4, 64, 64, true, 4, 1>("A3a*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped again
+      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3c, 2, 64, 128, true, 4, 1>("A3c*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped
+      run<FarA3c, 2, 64, 128, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+      run<FarA3c, 2, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+      continue;
+    }
     run<FarA1a, 4, 64, 64, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA1a, 2, 64, 128, true, 4, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
     run<FarA1a, 3, 64, 128, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
