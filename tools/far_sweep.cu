@@ -77,21 +77,16 @@ int main(int argc, char** argv) {
   const bool only_a3a = argc > 3 && std::string(argv[3]) == "a3a";
   for (int w : {1}) {
     if (only_a3a) {
-      run<FarA3a, 4, 64, 64, true, 4, 1>("A3a*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped
-      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 64, 32, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 64, 64, true, 4, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 32, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, 2);
-      run<FarA3a, 3, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 3, 64, 32, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 64, 128, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 2, 64, 64, false, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3a, 4, 64, 64, true, 4, 1>("A3a*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped again
-      run<FarA3a, 2, 64, 64, true, 8, 1>("A3a", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3c, 2, 64, 128, true, 4, 1>("A3c*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped
-      run<FarA3c, 2, 64, 128, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
-      run<FarA3c, 2, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+      for (int rep = 0; rep < 2; ++rep) {
+        run<FarA3c, 2, 64, 128, true, 4, 1>("A3c*", dn, dnn, n, dp, ns_pad, dpart, w);  // shipped
+        run<FarA3c, 2, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+        run<FarA3c, 2, 64, 64, true, 4, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+        run<FarA3c, 3, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+        run<FarA3c, 1, 128, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+        run<FarA3c, 2, 64, 32, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+        run<FarA3c, 2, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, 2);
+        run<FarA3c, 1, 64, 64, true, 8, 1>("A3c", dn, dnn, n, dp, ns_pad, dpart, w);
+      }
       continue;
     }
     run<FarA1a, 4, 64, 64, true, 2, 1>("A1a", dn, dnn, n, dp, ns_pad, dpart, w);
