@@ -20,7 +20,7 @@ from paper_2111_10743_b200.solver import _bind  # noqa: E402
 _build.build(verbose=False)
 b = bench.load_bundle()
 n = b["nodes"].shape[0]
-op = LayerOperatorSet.from_bundle(b, "a3")
+op = bench.with_corrections(b) or LayerOperatorSet.from_bundle(b, "a3")
 L = _bind()
 st = _lib.stream_handle()
 K = bench.K_ARNOLDI
