@@ -1,24 +1,29 @@
 """Benchmark of the GMRES operator-apply hot path (BASELINE.json metric:
 "fp64 Laplace pot+grad interactions/s; GMRES operator-apply time vs N").
 
-Workload (N=1): BASELINE config 2 — icosphere, reference order 7 (N=8,960
-nodes, 35,840 oversampled sources), A3 formulation (the reference default).
-One step = one GMRES iteration of the device solver: the A3 operator apply
-(oversample -> far sweep 1 -> 2 corrected SpMVs -> oversample -> far sweep 2 ->
-4 corrected SpMVs + glue + W-average) followed by the modified Gram-Schmidt
-Arnoldi update against K_ARNOLDI=4 basis vectors (the reference converges in
-4 iterations here).  Interactions per step = sum over the two far sweeps of
-(densities x N x N_over): 1 + 3 = 4 density-sweeps.
+Headline workload (N=1): BASELINE config 3 -- the torus build_torus(7, 64,
+32, 2, 1) (reference order 7: N = 114,688 nodes, N_over = 458,752
+oversampled sources), A3 (the reference default and config 3's Hodge
+solves), FMM far field at eps 5e-8 (the paper's Hodge setting), near-field
+corrections built ON THE DEVICE (eta 2, cap 256: 3.2e8 nnz per kind, 3 kinds).
+Every input is generated on the box (paper_2111_10743_b200/shapes.py hands
+the device geometry build the reference's own chart coefficients).
 
-Geometry + corrections come from data/config2.npz (built by running the
-reference, scripts/make_golden.py config2; git-ignored, travels with the
-snapshot).  Without it the committed geometry bundle
-tests/golden/config2_geom.npz (the reference's geometry arrays, near map, the
-seeded tau and the reference's own A3 apply of it) is used and the
-corrections are built on the device (csrc/quad.cu, eps 1e-10, the same
-adaptive quadrature), which the JSON line then says.
+One step = one GMRES iteration of the device solver: the A3 operator apply
+(oversample -> FMM call 1 -> 2 corrected SpMVs -> oversample -> FMM call 2
+-> 3 corrected SpMVs + glue + W-average) and the modified Gram-Schmidt
+Arnoldi update against K_ARNOLDI basis vectors.  Interactions per step
+(effective, the metric's unit) = density-sweeps x N x N_over = (1 + 3) x N x
+N_over: the reference's two far calls (operators.py:229-266).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the oracle port of the reference's CPU path on the
+host cores (the reference is Python and does not travel to the GPU box):
+the same config-3 step, row-sampled (every ROW_STRIDE-th target: both far
+calls as exact fp64 sums over ALL sources at the sampled targets, the
+sampled CSR rows, the full-length oversampling and MGS), scaled by
+N / rows.  It never loads libb200lb.so.
 """
 
 from __future__ import annotations
@@ -36,50 +41,26 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-CONFIG2 = os.path.join(ROOT, "data", "config2.npz")
-CONFIG2_GEOM = os.path.join(ROOT, "tests", "golden", "config2_geom.npz")
-K_ARNOLDI = 4
 METRIC = "fp64 Laplace pot+grad interactions/s; GMRES operator-apply time vs N"
 UNIT = "interactions/s"
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+K_ARNOLDI = 8               # MGS basis size in the timed step
+CONFIG3 = {"order": 7, "nu": 64, "nv": 32, "R": 2.0, "r": 1.0, "eps": 5e-8,
+           "eta": 2.0, "cap": 256, "ncrit": 300}
+ROW_STRIDE = 128            # CPU arms: every 128th target (896 rows of 114,688)
+WORKLOAD = "config3-torus64x32-o7-A3-fmm5e-8-apply+MGS(k=8)"
 
 
 def _dist():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def load_bundle():
-    """Config-2 bundle: the reference-built one when present, else the
-    committed geometry bundle (corrections then come from the device build,
-    see with_corrections)."""
-    path = CONFIG2 if os.path.exists(CONFIG2) else CONFIG2_GEOM
-    z = np.load(path)
-    keys = [k for k in z.files if not k.startswith(("a2_", "a3_"))]
-    b = {k: z[k] for k in keys} | {k: z[k] for k in z.files if k in ("a3_apply",)}
-    b["_corrections"] = "reference" if "corr_indptr" in b else "device"
-    return b
-
-
-def with_corrections(b):
-    """Fill corr_* from the device correction build (quadrature.py mirror,
-    csrc/quad.cu) when the bundle carries none; returns the operator built on
-    the way (None when the bundle had the reference's corrections)."""
-    if "corr_indptr" in b:
-        return None
-    from paper_2111_10743_b200 import Geometry, LayerOperatorSet
-    op = LayerOperatorSet(Geometry.from_arrays(b), "a3", float(b["eps"]))
-    cs = op._cset
-
-    def host(a):
-        return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
-    b["corr_indptr"] = host(cs.indptr)
-    b["corr_indices"] = host(cs.indices)
-    for k, v in cs.values.items():
-        b["corr_" + k.value] = host(v)
-    return op
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
 
 
 class ClockSampler:
@@ -87,17 +68,12 @@ class ClockSampler:
     (B200_PROFILING.md clocks line) through NVML every 5 ms; nvidia-smi when
     NVML is unavailable."""
 
-    REASONS = {  # nvmlClocksEventReason bits
-        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown",
-        0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
-    }
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown",
+               0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index=0, period=0.005):
-        self.index = index
-        self.period = period
-        self.sm = []
-        self.reasons = set()
-        self.max_mhz = None
+        self.index, self.period = index, period
+        self.sm, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
         self._t = None
 
@@ -120,10 +96,9 @@ class ClockSampler:
             while not self._stop.is_set():
                 try:
                     out = subprocess.run(
-                        ["nvidia-smi", f"--id={self.index}",
-                         "--query-gpu=clocks.sm,clocks.max.sm",
-                         "--format=csv,noheader,nounits"], capture_output=True,
-                        text=True, timeout=5).stdout.strip().split(",")
+                        ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip().split(",")
                     self.sm.append(float(out[0]))
                     self.max_mhz = float(out[1])
                 except Exception:
@@ -145,104 +120,278 @@ class ClockSampler:
                 "samples": len(self.sm)}
 
 
+# ---------------------------------------------------------------------------
+# CPU side (oracle port): the reference arm and the cpu_baseline leg
+
+
+def cpu_config3_setup(nthreads, stride=ROW_STRIDE):
+    """Config-3 geometry on the host (oracle/geometry.py over the chart
+    coefficients of shapes.build_torus), the near lists of every
+    stride-th target and seeded correction values on the reference's CSR
+    pattern for those rows (timing only)."""
+    import oracle
+    from oracle import geometry as og
+    from oracle.sampled import SampledA3, synthetic_rows
+    from paper_2111_10743_b200.shapes import build_torus
+    c = CONFIG3
+    coeffs = build_torus(c["order"], c["nu"], c["nv"], c["R"], c["r"], coefficients_only=True)
+    geo = og.evaluate(c["order"], *coeffs)
+    n = geo["nodes"].shape[0]
+    rows = np.arange(0, n, stride)
+    near = og.near_patches(geo["nodes"], geo["npatches"], geo["nb"], geo["over_nodes"], rows,
+                           c["eta"])
+    corr = synthetic_rows(near, geo["nb"])
+    op = SampledA3(geo, rows, corr, nthreads=nthreads)
+    rng = np.random.default_rng(2)
+    tau = rng.standard_normal(n)
+    Q = np.linalg.qr(rng.standard_normal((n, K_ARNOLDI + 1)))[0].T.copy()
+    return op, tau, Q, n, geo["over_nodes"].shape[0], oracle.max_threads() if nthreads <= 0 \
+        else nthreads
+
+
+def cpu_step(op, tau, Q):
+    """One sampled step: pass 1 + pass 2 at the sampled rows (pass 2's
+    full-length sources from tau-sized substitutes, same cost), then the
+    MGS update of a full-length vector against K_ARNOLDI basis rows
+    (solver.py:74-81)."""
+    res, (s, sp) = op.step(tau, tau, tau, 0.0)
+    v = tau.copy()
+    v[op.rows] = res
+    h = np.empty(Q.shape[0])
+    for j in range(Q.shape[0] - 1):
+        h[j] = Q[j] @ v
+        v -= h[j] * Q[j]
+    nrm = np.linalg.norm(v)
+    return v / nrm
+
+
+def cpu_time(op, tau, Q, reps):
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        cpu_step(op, tau, Q)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return  # rank 0 alone times the host-core baseline
+    nthreads = os.cpu_count() or 1
+    op, tau, Q, n, nover, cores = cpu_config3_setup(nthreads)
+    inter = 4 * n * nover
+    scale = n / len(op.rows)
+    cpu_time(op, tau, Q, max(args.warmup, 1))
+    ts = cpu_time(op, tau, Q, args.steps)
+    t = scale * sum(ts) / len(ts)
+    v = inter / t
+    sample = (f"every {ROW_STRIDE}th target ({len(op.rows)} of {n} rows): both A3 far calls as "
+              "exact fp64 sums over all 458,752 sources (oracle C port, OpenMP), the sampled "
+              "CSR rows (seeded values on the reference's pattern), full-length oversampling "
+              f"and MGS(k={K_ARNOLDI}); time x N/rows")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-3 geometry from the chart; correction values seeded on the "
+                "reference's sparsity pattern)",
+        "config": {"workload": WORKLOAD, "N": n, "N_over": nover, "formulation": "a3",
+                   "interactions_per_step": inter, "eps": CONFIG3["eps"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+
+
 def fp64_peak_tflops(torch, lib, _lib):
-    """Measured FP64 FMA-pipe peak (lb_probe_dfma), best of 3."""
+    """Measured FP64 FMA-pipe peak (lb_probe_dfma), best of 4."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = sms * 8, 4000
     scr = torch.zeros(blocks, dtype=torch.float64, device="cuda")
-    st = _lib.stream_handle()
     best = 0.0
     for _ in range(4):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(lib.lb_probe_dfma(_lib.ptr(scr), blocks, iters, st))
+        _lib.check(lib.lb_probe_dfma(_lib.ptr(scr), blocks, iters, _lib.stream_handle()))
         e1.record()
         torch.cuda.synchronize()
         best = max(best, blocks * 256 * iters * 256 / (e0.elapsed_time(e1) / 1e3))
     return best / 1e12
 
 
-def cpu_baseline_apply(b, nthreads, reps=1):
-    """The oracle port (C restatement of the reference's direct sums + numpy
-    glue, oracle/apply.py) timed on this host: full A3 applies."""
-    import oracle
-    op = oracle.OracleOperator(b, nthreads=nthreads)
-    tau = np.asarray(b["tau"])
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        op.apply_a3(tau)
-        ts.append(time.perf_counter() - t0)
-    return min(ts), oracle.max_threads() if nthreads <= 0 else nthreads
+def dmma_peak_tflops(torch, lib, _lib):
+    """Measured FP64 tensor-core peak (lb_probe_dmma: DMMA 8x8x4 chains), best of 4."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 4, 2000
+    scr = torch.zeros(blocks, dtype=torch.float64, device="cuda")
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.lb_probe_dmma(_lib.ptr(scr), blocks, iters, _lib.stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, blocks * 8 * iters * 8 * 512 / (e0.elapsed_time(e1) / 1e3))
+    return best / 1e12
 
 
-def run_reference(args):
-    rank, world, _ = _dist()
-    if rank != 0:
-        return
-    b = load_bundle()
-    if b["_corrections"] == "device":
-        import torch
-        torch.cuda.set_device(0)
-        with_corrections(b)
-    n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
-    inter = 4 * n * nover
-    nthreads = os.cpu_count() or 1
-    import oracle
-    op = oracle.OracleOperator(b, nthreads=nthreads)
-    tau = np.asarray(b["tau"])
-    for _ in range(max(args.warmup, 1) if args.warmup < 3 else 1):
-        op.apply_a3(tau)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        op.apply_a3(tau)
-        ts.append(time.perf_counter() - t0)
-    t = sum(ts) / len(ts)
-    v = inter / t
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2-A3-operator-apply", "N": n,
-                   "N_over": nover, "formulation": "a3",
-                   "interactions_per_step": inter},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads,
-                         "kind": "port",
-                         "sample": "full A3 apply of config 2 per step (oracle/"
-                                   "apply.py: C direct sums + numpy glue; corrections "
-                                   f"built by the {b['_corrections']})"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }), flush=True)
+def build_config3(torch):
+    """Geometry (device), near map (device, eta 2, cap 256), corrections
+    (device, eps 5e-8, S / S' / S''+D')."""
+    from paper_2111_10743_b200 import shapes
+    from paper_2111_10743_b200.operators import KernelKind
+    from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map
+    c = CONFIG3
+    t0 = time.perf_counter()
+    geom = shapes.build_torus(c["order"], c["nu"], c["nv"], c["R"], c["r"])
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    near = build_near_map(geom, c["eta"], cap=c["cap"])
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    kinds = [KernelKind.SINGLE_LAYER, KernelKind.SPRIME, KernelKind.SPP_PLUS_DPRIME]
+    cset, t_q = build_correction_set(geom, near, kinds, c["eps"])
+    torch.cuda.synchronize()
+    return geom, near, cset, {"geometry_s": t1 - t0, "near_map_s": t2 - t1, "t_q_s": t_q}
+
+
+class Timer:
+    def __init__(self, torch, world, local, flush):
+        self.torch, self.world, self.local, self.flush = torch, world, local, flush
+
+    def __call__(self, fn, k):
+        torch = self.torch
+        times = []
+        if self.world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(self.local) as cs:
+            for _ in range(k):
+                self.flush.zero_()  # L2 flush between timed iterations (untimed)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) / 1e3)
+        if self.world > 1:
+            torch.distributed.barrier()
+        return times, cs.summary()
+
+    def max_over_ranks(self, t):
+        if self.world == 1:
+            return t
+        tt = self.torch.tensor([t], dtype=self.torch.float64, device="cuda")
+        self.torch.distributed.all_reduce(tt, op=self.torch.distributed.ReduceOp.MAX)
+        return float(tt.item())
+
+
+def capture(torch, step, lib, _lib):
+    """The step as a CUDA graph (same launches, no host gaps) and its kernel
+    count (lb_graph_kernel_nodes); eager with a count of None if capture fails."""
+    import ctypes
+    try:
+        s_cap = torch.cuda.Stream()
+        s_cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cap):
+            step()
+        torch.cuda.current_stream().wait_stream(s_cap)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(g):
+            step()
+        nk, nn = ctypes.c_int64(), ctypes.c_int64()
+        raw = g.raw_cuda_graph()
+        _lib.check(lib.lb_graph_kernel_nodes(ctypes.c_void_p(raw), ctypes.byref(nk),
+                                             ctypes.byref(nn)), "lb_graph_kernel_nodes")
+        g.instantiate()
+        g.replay()
+        torch.cuda.synchronize()
+        return g.replay, True, int(nk.value)
+    except Exception as exc:  # noqa: BLE001 - report and time eagerly
+        print(f"bench: CUDA graph capture failed ({exc}); timing eagerly", file=sys.stderr)
+        torch.cuda.synchronize()
+        return step, False, None
+
+
+def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib):
+    """Per-stage device times of one apply (lb_opset stage events) and of one
+    pot+grad FMM call (lb_fmm stage events) with their rooflines: SpMV passes
+    against HBM (algorithmic bytes = nnz x (kinds x 8 + 4) + 8 (N + 1)), the
+    FMM's pairwise stages against the FP64 pipe (20 flop per pot+grad pair:
+    SURVEY §8(d)), the M2L against FP64 by its algorithmic flops."""
+    tau = torch.from_numpy(np.random.default_rng(2).standard_normal(n)).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    op.dev.set_timing(True)
+    op.apply_device(tau, out)
+    torch.cuda.synchronize()
+    st = op.dev.stage_times()
+    op.dev.set_timing(False)
+    b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
+    b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
+    stages = {
+        "fmm_call1_ms": st[0], "fmm_call2_ms": st[2],
+        "spmv1": {"ms": st[1], "bytes": b1, "GBps": b1 / st[1] / 1e6,
+                  "frac_hbm": b1 / st[1] / 1e6 / hbm_gbs},
+        "spmv2_glue": {"ms": st[3], "bytes": b2, "GBps": b2 / st[3] / 1e6,
+                       "frac_hbm": b2 / st[3] / 1e6 / hbm_gbs},
+        "apply_ms": st[7]}
+    # one charge pot+grad call of the plan (the metric's unit), stage split
+    w = torch.from_numpy(np.random.default_rng(3).standard_normal((1, nover))).cuda()
+    pot = torch.empty((1, n), dtype=torch.float64, device="cuda")
+    grad = torch.empty((1, n, 3), dtype=torch.float64, device="cuda")
+    plan.set_timing(True)
+    plan.apply_device(w, None, 1, 1, 0, 1, pot, grad)
+    torch.cuda.synchronize()
+    fs = plan.stage_times()
+    plan.set_timing(False)
+    wc = plan.work_counts()
+    leaf_pairs = wc["u_pairs"] + wc["w_pairs"] + wc["de_pairs"]
+
+    def fp(ms, flops):
+        tf = flops / (ms / 1e3) / 1e12 if ms > 0 else None
+        return {"ms": ms, "flops": flops, "TFLOPs": tf,
+                "frac_fp64": tf / peak_tf if tf else None}
+    fmm = {"p2m": fp(fs["p2m"], 11.0 * wc["p2m_pairs"]),
+           "m2m_ms": fs["m2m"], "m2l": fp(fs["m2l"], wc["m2l_flops"]),
+           "x_list": fp(fs["x"], 11.0 * wc["x_pairs"]), "l2l_ms": fs["l2l"],
+           "leaf": fp(fs["leaf"], 20.0 * leaf_pairs), "total_ms": fs["total"],
+           "pairs": {k: wc[k] for k in ("u_pairs", "w_pairs", "de_pairs", "x_pairs",
+                                         "p2m_pairs", "v_pairs")},
+           "flop_convention": "pairwise 1/r: 20 flop per pot+grad pair (leaf), 11 per pot-only "
+                              "lattice pair (P2M, X); M2L 4 nrep r_k per V pair (low-rank)"}
+    stages["fmm_call1_stages"] = fmm
+    return stages
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time the step without a CUDA graph")
-    ap.add_argument("--no-fmm", action="store_true",
-                    help="skip the secondary FMM line (config 5, N = 1e6 on the sphere)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the secondary lines (config 2 exact sweeps, config 5 FMM)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
     import torch
     rank, world, local = _dist()
-    # BENCH_SHARE_GPU=1: every rank on cuda:0 (a functional check of the sharded
-    # path on a one-GPU box with BENCH_DIST_BACKEND=gloo; never a measurement)
-    if os.environ.get("BENCH_SHARE_GPU") == "1":
+    if os.environ.get("BENCH_SHARE_GPU") == "1":  # functional multi-rank check on one GPU
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: functional checks only
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -253,210 +402,196 @@ def main():
     from paper_2111_10743_b200 import LayerOperatorSet
     from paper_2111_10743_b200.solver import _bind
 
-    b = load_bundle()
-    op1 = with_corrections(b)
-    n, nover = b["nodes"].shape[0], b["over_nodes"].shape[0]
-    inter = 4 * n * nover  # density-sweeps x targets x sources per step
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6547.2))
+    geom, near, cset, setup = build_config3(torch)
+    n, nover = geom.nnodes, geom.noversampled
+    inter = 4 * n * nover
+    c = CONFIG3
+    t0 = time.perf_counter()
     if world > 1:
-        # target rows sharded over the ranks, densities all-gathered between
-        # the apply's phases over NCCL (sharding.py); GMRES replicated
-        from paper_2111_10743_b200 import CorrectionSet, Geometry
         from paper_2111_10743_b200.sharding import ShardedOperatorSet
-        op = ShardedOperatorSet(Geometry.from_arrays(b), "a3", float(b["eps"]),
-                                CorrectionSet.from_arrays(b))
+        op = ShardedOperatorSet(geom, "a3", c["eps"], cset, far="fmm", near=near,
+                                fmm_ncrit=c["ncrit"])
     else:
-        op = op1 if op1 is not None else LayerOperatorSet.from_bundle(b, "a3")
+        op = LayerOperatorSet(geom, "a3", c["eps"], corrections=cset, near=near, far="fmm",
+                              fmm_ncrit=c["ncrit"])
+    torch.cuda.synchronize()
+    setup["plan_s"] = time.perf_counter() - t0
     L = _bind()
-    st = _lib.stream_handle()
-
-    # Krylov state for the Arnoldi part of the step
+    nloc = op.nloc if world > 1 else n
     rng = np.random.default_rng(2)
-    Q = torch.from_numpy(np.linalg.qr(rng.standard_normal((n, K_ARNOLDI + 1)))[0].T
+    Q = torch.from_numpy(np.linalg.qr(rng.standard_normal((nloc, K_ARNOLDI + 1)))[0].T
                          .copy()).cuda().contiguous()
     hdev = torch.zeros(K_ARNOLDI + 2, dtype=torch.float64, device="cuda")
-    v = torch.empty(n, dtype=torch.float64, device="cuda")
-    tau = torch.from_numpy(np.asarray(b["tau"])).cuda()
+    v = torch.empty(nloc, dtype=torch.float64, device="cuda")
+    tau_h = rng.standard_normal(n)
+    tau = torch.from_numpy(tau_h if world == 1 else tau_h[op.row_slice]).cuda()
+
+    def mgs():
+        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), nloc, K_ARNOLDI - 1, nloc, _lib.ptr(v),
+                                    _lib.ptr(hdev), _lib.stream_handle()))
 
     def step():
         op.apply_device(tau, out=v)
-        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
-                                    _lib.ptr(hdev), st))
+        mgs()
 
-    # apply: 2 x (oversample, far sweep, CSR+epilogue) [+ add_scalar unless the
-    # second sweep is fused]; MGS: one single-CTA kernel (n <= 12288)
-    launches_per_step = (6 if op.dev.keep.get("phi_eta") is not None else 7) + 1
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-
-    # parity spot check against the reference's own A3 apply
-    y = op.apply(np.asarray(b["tau"]))
-    parity = float(np.abs(y - b["a3_apply"]).max() / np.abs(b["a3_apply"]).max()) \
-        if "a3_apply" in b else None
-
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-
-    # the device-resident step replayed as a CUDA graph (the same 6 + 1
-    # launches per step, without the host launch gaps: -1.7% measured,
-    # scripts/graph_probe.py, bit-identical results); eager if capture fails
-    run_step, graphed = step, False
+    ref_v = v.clone()
+    run_step, graphed, nkern = (step, False, None)
     if world == 1 and not args.eager:
-        try:
-            s_cap = torch.cuda.Stream()
-            s_cap.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s_cap):
-                step()
-            torch.cuda.current_stream().wait_stream(s_cap)
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                step()
-            graph.replay()
+        run_step, graphed, nkern = capture(torch, step, lib, _lib)
+        if graphed:  # the replay must reproduce the eager step
+            op.apply_device(tau, out=v)
+            mgs()
+            eager_v = v.clone()
+            run_step()
             torch.cuda.synchronize()
-            run_step, graphed = graph.replay, True
-        except Exception as exc:  # noqa: BLE001 - report and time eagerly
-            print(f"bench: CUDA graph capture failed ({exc}); timing eagerly", file=sys.stderr)
-            torch.cuda.synchronize()
+            if not torch.equal(v, eager_v):
+                print("bench: graph replay differs from the eager step; timing eagerly",
+                      file=sys.stderr)
+                run_step, graphed = step, False
+    timer = Timer(torch, world, local, flush)
+    times, clocks = timer(run_step, args.steps)
+    t_step = timer.max_over_ranks(sum(times) / len(times))
+    value = inter / t_step
 
-    def timed(fn, k):
-        times = []
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        with ClockSampler(local) as cs:
-            for _ in range(k):
-                flush.zero_()  # L2 flush between timed iterations (untimed)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                fn()
-                e1.record()
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1) / 1e3)
-        if world > 1:
-            torch.distributed.barrier()
-        return times, cs.summary()
-
-    times, clocks = timed(run_step, args.steps)
-    t_step = sum(times) / len(times)
-    if world > 1:
-        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_step = float(tt.item())
-    value = inter / t_step  # one apply per step, shared by all ranks (strong scaling)
-
-    # dominant kernel: far sweep 2, timed alone
-    from paper_2111_10743_b200.operators import _bind_opset  # noqa: F401
-    far_t = far2_time(torch, op, tau, lib, _lib)
-    nloc = op.dev.nrows if world > 1 else n
-
-    # e2e through the public API with host buffers: H2D tau, apply, D2H result
-    tau_h = torch.from_numpy(np.asarray(b["tau"])).pin_memory()
-    out_h = torch.empty(n, dtype=torch.float64).pin_memory()
-    tau_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    # e2e: the public API with host buffers (pinned tau in, result out)
+    tau_pin = torch.from_numpy(np.ascontiguousarray(tau.cpu().numpy())).pin_memory()
+    out_pin = torch.empty(nloc, dtype=torch.float64).pin_memory()
+    tau_d = torch.empty_like(tau)
 
     def e2e_step():
-        tau_d.copy_(tau_h, non_blocking=True)
+        tau_d.copy_(tau_pin, non_blocking=True)
         op.apply_device(tau_d, out=v)
-        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, K_ARNOLDI - 1, n, _lib.ptr(v),
-                                    _lib.ptr(hdev), st))
-        out_h.copy_(v, non_blocking=True)
-    e2e_times, _ = timed(e2e_step, args.steps)
-    e2e_t = sum(e2e_times) / len(e2e_times)
-    if world > 1:
-        tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_t = float(tt.item())
+        mgs()
+        out_pin.copy_(v, non_blocking=True)
+    e2e_times, _ = timer(e2e_step, args.steps)
+    e2e_t = timer.max_over_ranks(sum(e2e_times) / len(e2e_times))
 
     peak = fp64_peak_tflops(torch, lib, _lib)
-    # dominant kernel: the second far sweep.  Fused A3 (exact sweeps + Phi):
-    # opfar_kernel<FarA3c>, 39 algorithmic flop per pair; otherwise
-    # opfar_kernel<FarA3b>, 44 (DESIGN.md §3 tables)
-    fused = op.dev.keep.get("phi_eta") is not None
-    kname = "FarA3c" if fused else "FarA3b"
-    flops_pair = 39.0 if fused else 44.0
-    traffic = None  # dram read+write bytes per launch of that kernel (ncu --set full)
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "round1",
-                                           "ncu_full_config2_far_csr.json")))
-        for k in prof:
-            if kname in k["kernel"]:
-                tb = [float(k[m].split()[0]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
-                                                "Gbyte": 1e9}[k[m].split()[1]]
-                      for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")]
-                traffic = sum(tb)
-    except (OSError, KeyError, ValueError):
-        pass
-    far_flops = flops_pair * nloc * nover  # algorithmic flops per launch
-    achieved = far_flops / far_t / 1e12
-
+    peak_tc = dmma_peak_tflops(torch, lib, _lib)
+    stages = roofline = None
+    if world == 1:
+        stages = stage_rooflines(torch, op, op._plan, n, nover, cset.nnz, peak, hbm, _lib)
+        f = stages["fmm_call1_stages"]
+        cands = [("spmv", stages["spmv2_glue"]["ms"], "hbm"),
+                 ("leaf", f["leaf"]["ms"], "fp64"), ("m2l", f["m2l"]["ms"], "fp64")]
+        dom = max(cands, key=lambda x: x[1])[0]
+        if dom == "spmv":
+            s2 = stages["spmv2_glue"]
+            roofline = {"bound": "hbm", "kernel": "csr_epi_kernel (A3 pass 2: 3 kinds + glue)",
+                        "achieved": s2["GBps"], "peak": hbm, "unit": "GB/s",
+                        "frac": s2["frac_hbm"], "traffic": None,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        else:
+            s = f[dom]
+            roofline = {"bound": "fp64", "kernel": {"leaf": "leaf_kernel (FMM U/W/DE lists)",
+                                                     "m2l": "FMM M2L"}[dom],
+                        "achieved": s["TFLOPs"], "peak": peak, "unit": "TFLOP/s",
+                        "frac": s["frac_fp64"], "traffic": None,
+                        "peak_source": f"measured in-run (lb_probe_dfma); nominal "
+                                       f"{NOMINAL_FP64_TFLOPS}"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_cpu, cores = cpu_baseline_apply(b, os.cpu_count() or 1)
-        cpu = {"value": inter / t_cpu, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": "one full A3 apply of config 2 (oracle/apply.py: C direct "
-                         "sums + numpy glue; MGS excluded)"}
-
-    fmm = None
-    if rank == 0 and world == 1 and not args.no_fmm:
-        fmm = fmm_config5(torch)
-
+        cop, ctau, cQ, _, _, cores = cpu_config3_setup(os.cpu_count() or 1)
+        cpu_time(cop, ctau, cQ, 1)
+        ts = cpu_time(cop, ctau, cQ, 2)
+        tc = n / len(cop.rows) * min(ts)
+        cpu = {"value": inter / tc, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"every {ROW_STRIDE}th target ({len(cop.rows)} rows): both far calls "
+                         "as exact sums over all sources (oracle C port), sampled CSR rows, "
+                         "full oversampling + MGS; time x N/rows (bench.py --impl reference)"}
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra["config2"] = config2_line(torch, lib, _lib, peak, flush)
+        extra["config5_fmm"] = fmm_config5(torch)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": t_step * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (config 2 geometry + corrections built by the "
-                    f"{'reference' if b['_corrections'] == 'reference' else 'device (csrc/quad.cu)'})",
-            "config": {"workload": "config2-A3-operator-apply+MGS(k=4)",
-                       "N": n, "N_over": nover, "formulation": "a3",
-                       "interactions_per_step": inter,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (config-3 torus from its chart; near map and corrections built "
+                    "on the device, csrc/quad.cu)",
+            "config": {"workload": WORKLOAD, "N": n, "N_over": nover, "formulation": "a3",
+                       "far_field": f"FMM eps {c['eps']} ncrit {c['ncrit']} (surface m=10, "
+                                    "low-rank M2L)",
+                       "nnz_per_kind": cset.nnz, "interactions_per_step": inter,
                        "parallelism": f"target-shard{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (256 MB write)",
-                       "cuda_graph": graphed,
-                       "apply_parity_vs_reference": parity},
-            "roofline": {"bound": "fp64", "kernel": f"opfar_kernel<{kname}>",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak,
-                         "peak_source": "measured in-run (lb_probe_dfma); nominal "
-                                        f"{NOMINAL_FP64_TFLOPS}",
-                         "far2_ms": far_t * 1e3, "flops_per_pair": flops_pair,
-                         "traffic": traffic,
-                         "traffic_note": "bytes/launch from profiles/round1 ncu --set full: "
-                                         "the kernel is FP64-bound, DRAM traffic is the "
-                                         "2.3 MB packed source array plus outputs"},
-            "cpu_baseline": cpu,
-            "e2e": {"value": inter / e2e_t, "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-                    "ms_per_step": e2e_t * 1e3},
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks,
-            "fmm_config5": fmm,
+                       "l2": "flushed between timed steps (256 MB write); CSR 11.6 GB > L2",
+                       "cuda_graph": graphed, "setup_s": setup},
+            "roofline": roofline, "stages": stages, "cpu_baseline": cpu,
+            "e2e": {"value": inter / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 8 * nloc,
+                    "d2h_bytes_per_step": 8 * nloc, "ms_per_step": e2e_t * 1e3},
+            "gpu_launches": nkern * args.steps if nkern is not None else None,
+            "launches_per_step": nkern,
+            "clocks": clocks, "fp64_peaks_tflops": {"dfma": peak, "dmma": peak_tc},
+            **extra,
         }), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
+def config2_line(torch, lib, _lib, peak, flush, steps=20):
+    """Secondary: BASELINE config 2 (icosphere order 7, N = 8,960) with exact
+    fp64 far sweeps (the fused A3 path), device corrections at eps 1e-10; the
+    apply + MGS(k=4) step as a CUDA graph; roofline of the dominant kernel
+    (opfar_kernel<FarA3c>, 39 flop per pair)."""
+    import ctypes
+    from paper_2111_10743_b200 import LayerOperatorSet, shapes
+    from paper_2111_10743_b200.solver import _bind
+    geom = shapes.icosphere(7)
+    op = LayerOperatorSet(geom, "a3", 1e-10, far="direct")
+    n, nover = geom.nnodes, geom.noversampled
+    L = _bind()
+    rng = np.random.default_rng(2)
+    Q = torch.from_numpy(np.linalg.qr(rng.standard_normal((n, 5)))[0].T.copy()).cuda()
+    h = torch.zeros(6, dtype=torch.float64, device="cuda")
+    v = torch.empty(n, dtype=torch.float64, device="cuda")
+    tau = torch.from_numpy(rng.standard_normal(n)).cuda()
+
+    def step():
+        op.apply_device(tau, out=v)
+        _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), n, 3, n, _lib.ptr(v), _lib.ptr(h),
+                                    _lib.stream_handle()))
+    for _ in range(3):
+        step()
+    run, graphed, nk = capture(torch, step, lib, _lib)
+    ts, _ = Timer(torch, 1, 0, flush)(run, steps)
+    t = sum(ts) / len(ts)
+    sec = ctypes.c_double(0.0)
+    op.apply_device(tau)
+    torch.cuda.synchronize()
+    _lib.check(lib.lb_opset_time_far(op.dev.handle, 2, 20, ctypes.byref(sec),
+                                     _lib.stream_handle()))
+    achieved = 39.0 * n * nover / sec.value / 1e12
+    return {"workload": "config2-icosphere-o7-A3-exact-sweeps+MGS(k=4)", "N": n,
+            "N_over": nover, "ms_per_step": t * 1e3, "value": 4 * n * nover / t, "unit": UNIT,
+            "cuda_graph": graphed, "launches_per_step": nk,
+            "roofline": {"bound": "fp64", "kernel": "opfar_kernel<FarA3c>", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "far2_ms": sec.value * 1e3, "flops_per_pair": 39.0}}
+
+
 def fmm_config5(torch, n=1_000_000, eps=1e-6, reps=5):
-    """Secondary evidence for the 'apply time vs N' half of the metric:
-    BASELINE config 5's FMM (N = 1e6 unit-sphere cloud, sources = targets,
-    seed 105, charge pot+grad) through the device FmmPlan -- plan setup
-    (device tree, lists, operators) and the event-timed apply."""
-    import time
+    """Secondary: BASELINE config 5's FMM (N = 1e6 unit-sphere cloud, sources
+    = targets, seed 105, charge pot+grad) through the device FmmPlan."""
     from paper_2111_10743_b200.fmm_plan import FmmPlan
-    rng = np.random.default_rng(105)
-    x = rng.standard_normal((n, 3))
-    x /= np.linalg.norm(x, axis=1)[:, None]
-    q = torch.from_numpy(rng.standard_normal((1, n))).cuda()
+    from paper_2111_10743_b200.shapes import sphere_cloud
+    x = sphere_cloud(n)
+    q = torch.from_numpy(np.random.default_rng(5).standard_normal((1, n))).cuda()
     FmmPlan(x[:1000], x[:1000], eps)  # unit operators (cached), as a user's first plan
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan = FmmPlan(x, x, eps)
     pot = torch.empty((1, n), dtype=torch.float64, device="cuda")
     grad = torch.empty((1, n, 3), dtype=torch.float64, device="cuda")
-    plan.apply_device(q, None, 1, 1, 0, 1, pot, grad)  # builds the device state
+    plan.apply_device(q, None, 1, 1, 0, 1, pot, grad)
     torch.cuda.synchronize()
-    t_setup_first = time.perf_counter() - t0
+    t_setup = time.perf_counter() - t0
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -466,22 +601,12 @@ def fmm_config5(torch, n=1_000_000, eps=1e-6, reps=5):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3)
     t = sum(ts) / len(ts)
+    plan.set_timing(True)
+    plan.apply_device(q, None, 1, 1, 0, 1, pot, grad)
+    torch.cuda.synchronize()
     return {"workload": "config5-fmm", "N": n, "eps": eps, "rep": plan.rep, "m": plan.m,
             "apply_ms": t * 1e3, "effective_interactions_per_s": n * (n - 1) / t,
-            "plan_plus_first_apply_s": t_setup_first, "setup_ms": plan.setup_times()}
-
-
-def far2_time(torch, op, tau, lib, _lib, which=2, reps=20):
-    """Average device duration of one far sweep (default: A3 call 2,
-    FarA3c when fused, else FarA3b) timed with CUDA events on its launching stream
-    (lb_opset_time_far); the packed sources are the last apply's."""
-    import ctypes
-    op.apply_device(tau)
-    torch.cuda.synchronize()
-    sec = ctypes.c_double(0.0)
-    _lib.check(lib.lb_opset_time_far(op.dev.handle, which, reps, ctypes.byref(sec),
-                                     _lib.stream_handle()))
-    return sec.value
+            "plan_plus_first_apply_s": t_setup, "stages_ms": plan.stage_times()}
 
 
 if __name__ == "__main__":

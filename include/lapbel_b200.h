@@ -51,6 +51,9 @@ int lb_abi_version(void);
 const char* lb_last_error_string(void);
 /* Host-side query: SM count and compute capability of the current device. */
 int lb_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* Kernel nodes (and all nodes) of a captured CUDA graph (a cudaGraph_t):
+ * how many kernels one captured step launches (bench.py gpu_launches). */
+int lb_graph_kernel_nodes(void* graph, int64_t* nkernels, int64_t* nnodes);
 
 /* ------------------------------------------------------------------------
  * Direct pairwise sums.
@@ -120,8 +123,9 @@ typedef struct {
   const double* corr[LB_NKINDS];
   double weight_sum;
   const double* phi0;
-  /* owned target rows [row0, row0 + nrows) for a sharded apply (nrows = 0:
-   * all rows).  Densities stay full length; only owned rows are written. */
+  /* owned target rows [row0, row0 + nrows) for a sharded apply (nrows < 0:
+   * all rows; nrows = 0 is rejected with LB_ERR_SHAPE).  Densities stay full
+   * length; only owned rows are written. */
   int64_t row0, nrows;
 } lb_opset_desc;
 
@@ -412,6 +416,8 @@ int lb_geom_build(const lb_geom_desc* desc, void* stream);
  * (flops = blocks*256*iters*256) and the 1/sqrt seed/refinement, used to state
  * the measured fp64 roofline and the kernel's rsqrt accuracy. */
 int lb_probe_dfma(double* scratch, int blocks, int iters, void* stream);
+/* FP64 tensor-core peak: DMMA 8x8x4 chains, flops = blocks*8*iters*8*512. */
+int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream);
 int lb_probe_rsqrt(const double* x, double* y, int64_t n, int mode,
                    void* stream);
 

@@ -82,7 +82,7 @@ def build(force=False, verbose=True, extra=()):
     with ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 1))) as ex:
         list(ex.map(compile_one, todo))
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-           "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp", *[_obj(s) for s in sources()], "-lcudart", "-lcublas", "-lgomp",
+           "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp", *[_obj(s) for s in sources()], "-lcudart", "-lgomp",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -39,6 +39,7 @@ SIGNATURES = {
     "lb_abi_version": [],
     "lb_last_error_string": [],
     "lb_device_info": [_P, _P, _P],
+    "lb_graph_kernel_nodes": [_P, _P, _P],
     "lb_p2p": [_P, _I64, _P, _I64, _P, _P, _I32, _U32, _U32, _I32, _P, _P, _P,
                _I32, _P],
     "lb_p2p_grouped": [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _I64, _I32,
@@ -81,6 +82,7 @@ SIGNATURES = {
     "lb_fmm_stage_times": [_P, _P],
     "lb_fmm_setup_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
+    "lb_probe_dmma": [_P, _I32, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],
 }
 _RES = {"lb_last_error_string": ctypes.c_char_p}

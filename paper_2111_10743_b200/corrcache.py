@@ -102,6 +102,8 @@ def load_corrections(path, mhash: bytes, kinds, eps: float, eta: float) -> Corre
         if magic != MAGIC:
             raise CacheKeyMismatch(f"{path}: not a correction cache (version 1)")
         codes = fh.read(nk)
+        if len(codes) < nk or any(c not in _CODE_KIND for c in codes):
+            raise CacheKeyMismatch(f"{path}: truncated or unknown kind codes")
         have = [_CODE_KIND[c] for c in codes]
         if h != mhash or e != float(eps) or et != float(eta) or \
                 any(k not in have for k in want):
@@ -131,6 +133,9 @@ def cached_correction_set(path, disc, near, kinds, eps: float, eta: float = 2.0)
     `path`.  Returns (cset, t_q seconds, hit)."""
     from .quadrature import build_correction_set
     mh = mesh_hash(disc)
+    # the pattern comes from `near`, so the key carries the near map's own eta
+    # (a map built with another tolerance must never hit this entry)
+    eta = float(getattr(near, "eta", eta))
     try:
         return load_corrections(path, mh, kinds, eps, eta), 0.0, True
     except (FileNotFoundError, CacheKeyMismatch):

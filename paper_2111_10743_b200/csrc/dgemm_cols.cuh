@@ -1,0 +1,253 @@
+// FP64 "gather - GEMM - scatter" on the FP64 tensor cores (DMMA 8x8x4,
+// mma.sync.m8n8k4.f64), the one GEMM shape every FMM translation has:
+//
+//   Y[:, out(c)] (=|+=) alpha(c) * sum_{s < S} A_s * X[perm_c(:), in_s(c)]
+//
+// A_s row-major (M x K, lda), X / Y column vectors of an expansion array
+// (one vector of K (X) or M (Y) doubles per (box, density)).  Logical column
+// c = q * nd + l walks the launch's box / pair list q and the densities l.
+// Per column the input vector of segment s is X + (in[s](q) * nd + l) * ldx
+// (in == nullptr: q itself; an index of -1 skips that segment for the
+// column), optionally read through a K-permutation (kperm + kp(q) * K: the
+// M2L's cube-symmetry gather), and the output is Y + (out(q) * nd + l) * ldy.
+// Batches (blockIdx.z) select A_z = A + z * a_batch and the box range
+// [boff[z], boff[z+1]) (the L2L's per-octant child groups).
+//
+// Every FMM stage maps onto it (fmm.py:823-935): P2M (pinv_up, S = 1), M2M
+// (the 8 child-octant operators of one parent as 8 K-segments: one launch per
+// level, each parent summed in octant order -- deterministic, no atomics),
+// L2L (pinv_dn, then l2l[octant] in 8 batches), and the M2L's low-rank
+// factors (B_k on the permuted, 1/h-scaled multipoles, then A_k).
+//
+// Tiles: BM x 32 columns per CTA, 4 warps; warp w owns BM/32 M-tiles of 8 rows
+// (rows w*8*(BM/32) ...) and all four 8-column N-tiles.  K runs in chunks of
+// 32 through a two-stage cp.async pipeline (A rows 256 B coalesced, X
+// elements 8 B gathered through the column pointers / permutation, zero
+// filled past K); fragments come from shared memory (stride 36 doubles: two
+// wavefronts per 8-byte fragment load, the minimum).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lb {
+namespace dg {
+
+constexpr int kBN = 32;      // columns per CTA
+constexpr int kKC = 32;      // K chunk
+constexpr int kLD = 36;      // smem row stride (doubles)
+constexpr int kThreads = 128;
+constexpr int kMaxSeg = 8;
+
+struct Args {
+  const double* A;           // segment s of batch z at A + z*a_batch + s*a_seg
+  int64_t a_batch, a_seg;
+  int lda, M, K, S, nd;
+  const double* X;           // input expansion array
+  int64_t ldx;
+  const int64_t* in;         // (nq_total x S) box index per segment, -1 = none; nullptr = q
+  const int32_t* kperm;      // optional (nperm x K) K-permutations
+  const int32_t* kp;         // per box/pair q: permutation index (with kperm)
+  double* Y;
+  int64_t ldy;
+  const int64_t* out;        // per q output box; nullptr = q
+  const double* alpha_q;     // optional per-q scale
+  double alpha;
+  int add;                   // 1: Y += ..., 0: Y = ...
+  int64_t nq;                // boxes/pairs (no batches)
+  const int64_t* boff;       // batches: q range [boff[z], boff[z+1])
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// src-size below the copy size zero-fills the rest (0: all zeros, src unread)
+__device__ __forceinline__ void cp8(double* s, const double* g, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp16(double* s, const double* g, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int BM>
+__global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
+  constexpr int MT = BM / 32;  // M-tiles per warp
+  extern __shared__ __align__(16) double dsm[];
+  // stage b: A tile at dsm + b * BM * kLD, X tile at dsm + 2 * BM * kLD + b * kBN * kLD
+  auto As = [&](int b) { return dsm + b * BM * kLD; };
+  auto Xs = [&](int b) { return dsm + 2 * BM * kLD + b * kBN * kLD; };
+  __shared__ const double* xin[kMaxSeg][kBN];
+  __shared__ const int32_t* kpp[kBN];
+  __shared__ double* yout[kBN];
+  __shared__ double alph[kBN];
+  __shared__ int seg_used[kMaxSeg];
+
+  const int z = blockIdx.z;
+  const int64_t q0 = g.boff ? g.boff[z] : 0;
+  const int64_t q1 = g.boff ? g.boff[z + 1] : g.nq;
+  const int64_t ncols = (q1 - q0) * g.nd;
+  const int64_t c0 = (int64_t)blockIdx.y * kBN;
+  if (c0 >= ncols) return;
+  const int m0 = blockIdx.x * BM;
+  const double* A = g.A + (int64_t)z * g.a_batch;
+  // 16-byte A copies need even row strides / offsets and an aligned base
+  const bool a16 = ((g.lda | g.a_seg | g.a_batch) & 1) == 0 && (((uintptr_t)g.A) & 15) == 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  if (tid < kMaxSeg) seg_used[tid] = 0;
+  __syncthreads();
+  if (tid < kBN) {
+    const int64_t c = c0 + tid;
+    const bool ok = c < ncols;
+    const int64_t q = q0 + (ok ? c / g.nd : 0);
+    const int l = ok ? (int)(c % g.nd) : 0;
+    for (int s = 0; s < g.S; ++s) {
+      const int64_t b = g.in ? g.in[q * g.S + s] : q;
+      xin[s][tid] = (ok && b >= 0) ? g.X + (b * g.nd + l) * g.ldx : nullptr;
+      if (ok && b >= 0) seg_used[s] = 1;  // benign race: all writers store 1
+    }
+    kpp[tid] = (ok && g.kperm) ? g.kperm + (int64_t)g.kp[q] * g.K : nullptr;
+    const int64_t ob = g.out ? g.out[q] : q;
+    yout[tid] = ok ? g.Y + (ob * g.nd + l) * g.ldy : nullptr;
+    alph[tid] = ok ? g.alpha * (g.alpha_q ? g.alpha_q[q] : 1.0) : 0.0;
+  }
+  __syncthreads();
+
+  double acc[MT][4][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // the (segment, chunk) sequence, skipping segments no column uses
+  const int nchunk = (g.K + kKC - 1) / kKC;
+  int nstep = 0;
+  for (int s = 0; s < g.S; ++s) nstep += seg_used[s] ? nchunk : 0;
+  auto step_at = [&](int i, int& s, int& k0) {
+    for (s = 0; s < g.S; ++s) {
+      if (!seg_used[s]) continue;
+      if (i < nchunk) break;
+      i -= nchunk;
+    }
+    k0 = i * kKC;
+  };
+  auto load = [&](int buf, int s, int k0) {
+    const double* As_src = A + (int64_t)s * g.a_seg;
+    // A tile: BM rows x 32 doubles = BM * 16 chunks of 16 B
+    if (a16) {
+      for (int e = tid; e < BM * (kKC / 2); e += kThreads) {
+        const int r = e / (kKC / 2), kk = (e % (kKC / 2)) * 2;
+        const int row = m0 + r, k = k0 + kk;
+        int bytes = 0;
+        if (row < g.M && k < g.K) bytes = (k + 1 < g.K) ? 16 : 8;
+        cp16(As(buf) + r * kLD + kk, bytes ? As_src + (int64_t)row * g.lda + k : g.A, bytes);
+      }
+    } else {
+      for (int e = tid; e < BM * kKC; e += kThreads) {
+        const int r = e / kKC, kk = e % kKC;
+        const int row = m0 + r, k = k0 + kk;
+        const bool ok = row < g.M && k < g.K;
+        cp8(As(buf) + r * kLD + kk, ok ? As_src + (int64_t)row * g.lda + k : g.A, ok);
+      }
+    }
+    // X tile: 32 columns x 32 k, one 8-byte gather each
+    for (int e = tid; e < kBN * kKC; e += kThreads) {
+      const int c = e >> 5, kk = e & 31, k = k0 + kk;
+      const double* base = xin[s][c];
+      const bool ok = base != nullptr && k < g.K;
+      const int32_t* pp = kpp[c];
+      const double* src = ok ? base + (pp ? pp[k] : k) : g.X;
+      cp8(Xs(buf) + c * kLD + kk, src, ok);
+    }
+    cp_commit();
+  };
+
+  if (nstep > 0) {
+    int s, k0;
+    step_at(0, s, k0);
+    load(0, s, k0);
+  }
+  for (int i = 0; i < nstep; ++i) {
+    const int buf = i & 1;
+    if (i + 1 < nstep) {
+      int s, k0;
+      step_at(i + 1, s, k0);
+      load(buf ^ 1, s, k0);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As(buf);
+    const double* xs = Xs(buf);
+#pragma unroll
+    for (int ks = 0; ks < kKC / 4; ++ks) {
+      const int kk = ks * 4 + tq;
+      double a[MT], b[4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = as[((warp * MT + mt) * 8 + gq) * kLD + kk];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) b[nt] = xs[(nt * 8 + gq) * kLD + kk];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    }
+    __syncthreads();
+  }
+  // epilogue: D[row][col] with row = gq, cols = 2 tq, 2 tq + 1 of each tile
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int row = m0 + (warp * MT + mt) * 8 + gq;
+    if (row >= g.M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = nt * 8 + 2 * tq + h;
+        double* y = yout[c];
+        if (!y) continue;
+        const double v = alph[c] * acc[mt][nt][h];
+        y[row] = g.add ? y[row] + v : v;
+      }
+    }
+  }
+}
+
+template <int BM>
+constexpr size_t smem_bytes() { return sizeof(double) * 2 * (BM + kBN) * kLD; }
+
+// host launcher: grid = (M tiles, column tiles, batches)
+inline cudaError_t gemm_cols(const Args& a, int64_t max_cols_per_batch, int batches, cudaStream_t st) {
+  if (max_cols_per_batch <= 0 || batches <= 0 || a.M <= 0) return cudaSuccess;
+  if (a.S < 1 || a.S > kMaxSeg) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_cols_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_bytes<32>());
+    cudaFuncSetAttribute(gemm_cols_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_bytes<64>());
+    attr = true;
+  }
+  const unsigned gy = (unsigned)((max_cols_per_batch + kBN - 1) / kBN);
+  if (a.M <= 32) {
+    gemm_cols_kernel<32><<<dim3((unsigned)((a.M + 31) / 32), gy, (unsigned)batches), kThreads,
+                           smem_bytes<32>(), st>>>(a);
+  } else {
+    gemm_cols_kernel<64><<<dim3((unsigned)((a.M + 63) / 64), gy, (unsigned)batches), kThreads,
+                           smem_bytes<64>(), st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dg
+}  // namespace lb

@@ -20,7 +20,9 @@
 //              charges, exactly the fused leaf stage of fmm.py:937-988
 //   scatter  : sorted targets -> reference layout (pot, grad, full hess)
 //
-// DGEMMs are plain cuBLAS calls; every other stage is a hand-written kernel.
+// Every GEMM-shaped stage (surface P2M / M2M / L2L, the M2L factors) runs on
+// the FP64 tensor cores through dgemm_cols.cuh (DMMA 8x8x4, gathers and
+// scatters fused into the operand loads and the epilogue); no library GEMM.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -33,6 +35,7 @@
 #include <tuple>
 #include <vector>
 
+#include "dgemm_cols.cuh"
 #include "fmm_plan.h"
 #include "lb_common.cuh"
 #include "ozaki.cuh"
@@ -42,11 +45,12 @@ namespace lb {
 
 constexpr int kStages = 8;  // p2m m2m m2l x l2l l2t leaf scatter (+ total)
 
-#define LB_BLAS(expr)                                                              \
+#define LB_DG(expr)                                                                \
   do {                                                                             \
-    cublasStatus_t _s = (expr);                                                    \
-    if (_s != CUBLAS_STATUS_SUCCESS)                                               \
-      return fail(LB_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string((int)_s)); \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return fail(LB_ERR_CUDA, std::string("dgemm_cols (") + __FILE__ + ":" +      \
+                                   std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
   } while (0)
 
 // ---------------------------------------------------------------------------
@@ -67,30 +71,6 @@ __global__ void gather_sources_kernel(const double* __restrict__ charges,
     for (int k = 0; k < 3; ++k)
       vs[((int64_t)l * ns + p) * 3 + k] = on ? dipoles[((int64_t)d * ns + o) * 3 + k] : 0.0;
   }
-}
-
-// dst[cols[c]*ld + r] (+)= src[c*ld + r] for c < ncols, r < ld
-__global__ void scatter_cols_kernel(const double* __restrict__ src, const int64_t* __restrict__ boxes,
-                                    int64_t nbox_list, int nd, int ld, double* __restrict__ dst,
-                                    int add) {
-  const int64_t c = blockIdx.x;  // (box, density) column
-  if (c >= nbox_list * nd) return;
-  const int64_t b = boxes[c / nd];
-  const int l = (int)(c % nd);
-  const double* s = src + c * ld;
-  double* d = dst + (b * nd + l) * (int64_t)ld;
-  for (int r = threadIdx.x; r < ld; r += blockDim.x) d[r] = add ? d[r] + s[r] : s[r];
-}
-
-__global__ void gather_cols_kernel(const double* __restrict__ src, const int64_t* __restrict__ boxes,
-                                   int64_t nbox_list, int nd, int ld, double* __restrict__ dst) {
-  const int64_t c = blockIdx.x;
-  if (c >= nbox_list * nd) return;
-  const int64_t b = boxes[c / nd];
-  const int l = (int)(c % nd);
-  const double* s = src + (b * nd + l) * (int64_t)ld;
-  double* d = dst + c * ld;
-  for (int r = threadIdx.x; r < ld; r += blockDim.x) d[r] = s[r];
 }
 
 // ---------------------------------------------------------------------------
@@ -364,22 +344,6 @@ __global__ void __launch_bounds__(256) grid_tensor_kernel(const int64_t* __restr
 
 // ---------------------------------------------------------------------------
 // M2L staging
-
-// X[(pi*nd+l)*nrep + p] = scale(pi) * up[src(pi), l, perm_inv[off(pi), p]]
-__global__ void m2l_gather_kernel(const double* __restrict__ up, const int64_t* __restrict__ vsrc,
-                                  const int32_t* __restrict__ voff, const double* __restrict__ vscale,
-                                  const int32_t* __restrict__ perm_inv, int64_t p0, int64_t np, int nd,
-                                  int nrep, double* __restrict__ X) {
-  const int64_t col = blockIdx.x;  // local pair*nd + l
-  if (col >= np * nd) return;
-  const int64_t pi = p0 + col / nd;
-  const int l = (int)(col % nd);
-  const double* u = up + (vsrc[pi] * nd + l) * (int64_t)nrep;
-  const int32_t* pv = perm_inv + (int64_t)voff[pi] * nrep;
-  const double s = vscale[pi];
-  double* x = X + col * (int64_t)nrep;
-  for (int p = threadIdx.x; p < nrep; p += blockDim.x) x[p] = s * u[pv[p]];
-}
 
 // per unique target t of the chunk: dc[t,l,i] += sum over its pairs (fixed
 // order) of Y[(pi-p0)*nd+l, perm[off(pi), i]]
@@ -1113,6 +1077,17 @@ int build_device(lb_fmm_plan* P) {
     LB_TRY(upload(&D.pinv_up, P->pinv_up));
     LB_TRY(upload(&D.pinv_dn, P->pinv_dn));
     LB_TRY(upload(&D.l2l, P->l2l));
+    // the 8 child-octant operators in octant order (x | y<<1 | z<<2): the
+    // reference lists them by 4*ox + 2*oy + oz (fmm.py:307-317)
+    const int64_t nn = (int64_t)nrep * nrep;
+    std::vector<double> mo(8 * nn), lo(8 * nn);
+    for (int oct = 0; oct < 8; ++oct) {
+      const int r = ((oct & 1) << 2) | (oct & 2) | ((oct >> 2) & 1);
+      std::copy(P->m2m.begin() + r * nn, P->m2m.begin() + (r + 1) * nn, mo.begin() + oct * nn);
+      std::copy(P->l2l.begin() + r * nn, P->l2l.begin() + (r + 1) * nn, lo.begin() + oct * nn);
+    }
+    LB_TRY(upload(&D.m2m_oct, mo));
+    LB_TRY(upload(&D.l2l_oct, lo));
   } else {
     LB_TRY(upload(&D.vinv, P->vinv));
   }
@@ -1130,12 +1105,33 @@ int build_device(lb_fmm_plan* P) {
     if (t.is_leaf[b] && t.src_hi[b] > t.src_lo[b]) p2m.push_back(S[b]);
   D.n_p2m = (int64_t)p2m.size();
   LB_TRY(upload(&D.p2m_leaves, p2m));
-  std::vector<int64_t> uc, upar, dch, dpar;
+  std::vector<int64_t> uc, upar, dch, dpar, mpar, mch8;
   D.up_off.assign(1, 0);
   D.dn_off.assign(1, 0);
+  D.up_par_off.assign(1, 0);
   {  // buckets per (level, octant), boxes in ascending id within a level
     std::vector<std::vector<int64_t>> bu(8), bd(8);
     for (int l = 0; l < t.nlev; ++l) {
+      if (l > 0) {  // surface M2M: this level's parents (slots ascending), 8 child slots each
+        std::map<int64_t, int64_t> row;
+        for (int64_t b : t.levels[l]) {
+          const int64_t p = t.parent[b];
+          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) row.emplace(S[p], 0);
+        }
+        int64_t i = 0;
+        for (auto& kv : row) {
+          kv.second = i++;
+          mpar.push_back(kv.first);
+        }
+        const size_t base = mch8.size();
+        mch8.resize(base + 8 * row.size(), -1);
+        for (int64_t b : t.levels[l]) {
+          const int64_t p = t.parent[b];
+          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0)
+            mch8[base + 8 * row[S[p]] + octant[S[b]]] = S[b];
+        }
+      }
+      D.up_par_off.push_back((int64_t)mpar.size());
       for (auto& v : bu) v.clear();
       for (auto& v : bd) v.clear();
       if (l > 0)
@@ -1168,6 +1164,9 @@ int build_device(lb_fmm_plan* P) {
   LB_TRY(upload(&D.up_parent, upar));
   LB_TRY(upload(&D.dn_child, dch));
   LB_TRY(upload(&D.dn_parent, dpar));
+  LB_TRY(upload(&D.up_par, mpar));
+  LB_TRY(upload(&D.up_child8, mch8));
+  LB_TRY(upload(&D.dn_off_dev, D.dn_off));
   mark("m2m/l2l");
   // M2L pairs grouped by canonical key, each group in target-slot order (the
   // walk below visits targets in slot order, so no sort is needed).  Lattice
@@ -1384,8 +1383,6 @@ int build_device(lb_fmm_plan* P) {
   D.btgt_oct = doct;
   D.level_slot_off = level_slot_off;
   mark("leaf upload");
-  if (cublasCreate(&D.blas) != CUBLAS_STATUS_SUCCESS) return fail(LB_ERR_CUDA, "cublasCreate failed");
-  mark("cublas");
   LB_CUDA(cudaStreamSynchronize(0));  // the setup kernels above ran on the legacy stream
   D.ready = true;
   return LB_OK;
@@ -1464,33 +1461,15 @@ int ensure_oz(lb_fmm_plan* P, int nd, cudaStream_t st) {
   return LB_OK;
 }
 
-// child octant (x | y<<1 | z<<2, the children order of fmm.py:624-628) ->
-// index of the reference's m2m/l2l operator lists, k = 4*ox + 2*oy + oz
-// (fmm.py:307-317, 870, 934)
-inline int ref_octant(int oct) { return ((oct & 1) << 2) | (oct & 2) | ((oct >> 2) & 1); }
 
-// Y(nrep x ncols) = alpha * A(nrep x nrep, row-major) * X(nrep x ncols, col-major)
-int gemm_rm(cublasHandle_t h, const double* A, const double* X, double* Y, int nrep, int64_t ncols,
-            double alpha, double beta) {
-  if (ncols <= 0) return LB_OK;
-  LB_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nrep, (int)ncols, nrep, &alpha, A, nrep, X, nrep,
-                      &beta, Y, nrep));
-  // cuBLAS reports through its status; do not let an internal runtime error
-  // it tolerated surface at our next launch check
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess)
-    return fail(LB_ERR_CUDA, std::string("after cublasDgemm: ") + cudaGetErrorString(e));
-  return LB_OK;
-}
-
-// Y (m, ncols) = A (m, k) row-major  X (k, ncols) column-major
-int gemm_rm2(cublasHandle_t h, const double* A, const double* X, double* Y, int m, int k, int64_t ncols,
-             double alpha, double beta) {
-  if (ncols <= 0) return LB_OK;
-  LB_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, m, (int)ncols, k, &alpha, A, k, X, k, &beta, Y, m));
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess)
-    return fail(LB_ERR_CUDA, std::string("after cublasDgemm: ") + cudaGetErrorString(e));
+// Y[:, cols] = alpha * A * X[:, cols] for contiguous column blocks (the
+// M2L's second low-rank factor, L2L's pinv_dn): dgemm_cols.cuh
+int gemm_contig(const double* A, int lda, int M, int K, const double* X, int64_t ldx, double* Y,
+                int64_t ldy, int64_t ncols, double alpha, cudaStream_t st) {
+  dg::Args a{};
+  a.A = A; a.lda = lda; a.M = M; a.K = K; a.S = 1; a.nd = 1;
+  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.alpha = alpha; a.add = 0; a.nq = ncols;
+  LB_DG(dg::gemm_cols(a, ncols, 1, st));
   return LB_OK;
 }
 
@@ -1543,10 +1522,12 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       LB_TRY(launch_lattice<ND>((unsigned)D.n_p2m, st, D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf,
                                 D.bsrc, D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1,
                                 D.tmpA, 0, 0));
-      LB_TRY(gemm_rm(D.blas, D.pinv_up, D.tmpA, D.tmpB, nrep, D.n_p2m * ND, 1.0, 0.0));
-      scatter_cols_kernel<<<(unsigned)(D.n_p2m * ND), 128, 0, st>>>(D.tmpB, D.p2m_leaves, D.n_p2m, ND,
-                                                                    nrep, D.up, 0);
-      LB_CHECK_LAUNCH();
+      // upward[b] = pinv_up @ (h phi) straight into the leaves' slots (fmm.py:852)
+      dg::Args a{};
+      a.A = D.pinv_up; a.lda = nrep; a.M = nrep; a.K = nrep; a.S = 1; a.nd = ND;
+      a.X = D.tmpA; a.ldx = nrep; a.Y = D.up; a.ldy = nrep; a.out = D.p2m_leaves;
+      a.alpha = 1.0; a.add = 0; a.nq = D.n_p2m;
+      LB_DG(dg::gemm_cols(a, D.n_p2m * ND, 1, st));
     } else {
       p2m_grid_kernel<ND><<<(unsigned)D.n_p2m, 256, 0, st>>>(D.p2m_leaves, D.bctr, D.bhalf, D.bsrc,
                                                              D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, n,
@@ -1558,18 +1539,24 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   // ---- M2M (fmm.py:853-871), deepest level first, octants in order
   const size_t grid_smem = sizeof(double) * 2 * nrep;
   for (int l = t.nlev - 1; l >= 1; --l) {
+    if (surface) {
+      // every parent of level l-1 sums its children's m2m[octant] @ up[child]
+      // in octant order: the 8 operators are 8 K-segments of one GEMM
+      const int64_t p0 = D.up_par_off[l], p1 = D.up_par_off[l + 1];
+      if (p1 > p0) {
+        dg::Args a{};
+        a.A = D.m2m_oct; a.a_seg = (int64_t)nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
+        a.S = 8; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.up_child8 + 8 * p0;
+        a.Y = D.up; a.ldy = nrep; a.out = D.up_par + p0; a.alpha = 1.0; a.add = 1; a.nq = p1 - p0;
+        LB_DG(dg::gemm_cols(a, (p1 - p0) * ND, 1, st));
+      }
+      continue;
+    }
     for (int oct = 0; oct < 8; ++oct) {
       const int64_t g0 = D.up_off[8 * l + oct], g1 = D.up_off[8 * l + oct + 1];
       const int64_t cnt = g1 - g0;
       if (cnt == 0) continue;
-      if (surface) {
-        gather_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.up, D.up_child + g0, cnt, ND, nrep,
-                                                                D.tmpA);
-        LB_TRY(gemm_rm(D.blas, D.m2m + (int64_t)ref_octant(oct) * nrep * nrep, D.tmpA, D.tmpB, nrep,
-                       cnt * ND, 1.0, 0.0));
-        scatter_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.tmpB, D.up_parent + g0, cnt, ND,
-                                                                 nrep, D.up, 1);
-      } else {
+      {
         grid_tensor_kernel<ND><<<(unsigned)cnt, 256, grid_smem, st>>>(
             D.up_child + g0, D.up_parent + g0, D.btgt_oct, D.m2m, n, D.up, D.up, 0);
       }
@@ -1600,16 +1587,21 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
                                            np * ND, D.oz_b, D.oz_cs, D.tmpB, st);
         if (e != cudaSuccess) return fail(LB_ERR_CUDA, std::string("m2l tcgen05 gemm: ") + cudaGetErrorString(e));
       } else {
-        m2l_gather_kernel<<<(unsigned)(np * ND), 128, 0, st>>>(D.up, D.v_src, D.v_off_idx, D.v_scale,
-                                                               D.perm_inv, p0, np, ND, nrep, D.tmpA);
-        LB_CHECK_LAUNCH();
-        if (P->m2l_slices < 0) {  // K_k ~= A_k B_k: two thin DGEMMs through the rank-r_k staging
+        // the gathered column: scale(pi) * up[src(pi), l, perm_inv[off(pi), p]]
+        dg::Args a{};
+        a.S = 1; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.v_src + p0;
+        a.kperm = D.perm_inv; a.kp = D.v_off_idx + p0; a.alpha_q = D.v_scale + p0;
+        a.alpha = 1.0; a.add = 0; a.nq = np;
+        if (P->m2l_slices < 0) {  // K_k ~= A_k B_k: T = B_k X (r_k x cols), Y = A_k T
           const int r = P->lr_rank[k];
           const int64_t o = P->lr_off[k] * nrep;
-          LB_TRY(gemm_rm2(D.blas, D.lr_b + o, D.tmpA, D.lr_t, r, nrep, np * ND, 1.0, 0.0));
-          LB_TRY(gemm_rm2(D.blas, D.lr_a + o, D.lr_t, D.tmpB, nrep, r, np * ND, 1.0, 0.0));
-        } else {
-          LB_TRY(gemm_rm(D.blas, D.canon + (int64_t)k * nrep * nrep, D.tmpA, D.tmpB, nrep, np * ND, 1.0, 0.0));
+          a.A = D.lr_b + o; a.lda = nrep; a.M = r; a.K = nrep; a.Y = D.lr_t; a.ldy = r;
+          LB_DG(dg::gemm_cols(a, np * ND, 1, st));
+          LB_TRY(gemm_contig(D.lr_a + o, r, nrep, r, D.lr_t, r, D.tmpB, nrep, np * ND, 1.0, st));
+        } else {  // the dense canonical operator (the reference's arithmetic)
+          a.A = D.canon + (int64_t)k * nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
+          a.Y = D.tmpB; a.ldy = nrep;
+          LB_DG(dg::gemm_cols(a, np * ND, 1, st));
         }
       }
       m2l_accum_kernel<<<(unsigned)(tj - ti), 128, 0, st>>>(D.tmpB, D.v_tgts, D.v_tgt_pair_off,
@@ -1630,25 +1622,33 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   // ---- L2L (fmm.py:913-935)
   for (int l = 0; l < t.nlev; ++l) {
     const int64_t s0 = D.level_slot_off[l], s1 = D.level_slot_off[l + 1];
-    if (surface) {
+    if (surface) {  // local = h pinv_dn @ dcheck over the level's slots (fmm.py:920)
       const double hl = t.half / std::ldexp(1.0, l);
-      LB_TRY(gemm_rm(D.blas, D.pinv_dn, D.dc + s0 * ND * nrep, D.loc + s0 * ND * nrep, nrep,
-                     (s1 - s0) * ND, hl, 0.0));
+      LB_TRY(gemm_contig(D.pinv_dn, nrep, nrep, nrep, D.dc + s0 * ND * nrep, nrep,
+                         D.loc + s0 * ND * nrep, nrep, (s1 - s0) * ND, hl, st));
     }
     if (l + 1 >= t.nlev) break;
+    if (surface) {
+      // dcheck[c] += l2l[octant] @ local[parent] / h_c (fmm.py:931-935): the
+      // eight octant groups of level l+1 are the eight batches of one launch
+      const double hc = t.half / std::ldexp(1.0, l + 1);
+      int64_t mx = 0;
+      for (int oct = 0; oct < 8; ++oct)
+        mx = std::max(mx, D.dn_off[8 * (l + 1) + oct + 1] - D.dn_off[8 * (l + 1) + oct]);
+      if (mx > 0) {
+        dg::Args a{};
+        a.A = D.l2l_oct; a.a_batch = (int64_t)nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
+        a.S = 1; a.nd = ND; a.X = D.loc; a.ldx = nrep; a.in = D.dn_parent; a.Y = D.dc; a.ldy = nrep;
+        a.out = D.dn_child; a.alpha = 1.0 / hc; a.add = 1; a.boff = D.dn_off_dev + 8 * (l + 1);
+        LB_DG(dg::gemm_cols(a, mx * ND, 8, st));
+      }
+      continue;
+    }
     for (int oct = 0; oct < 8; ++oct) {
       const int64_t g0 = D.dn_off[8 * (l + 1) + oct], g1 = D.dn_off[8 * (l + 1) + oct + 1];
       const int64_t cnt = g1 - g0;
       if (cnt == 0) continue;
-      if (surface) {
-        const double hc = t.half / std::ldexp(1.0, l + 1);
-        gather_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.loc, D.dn_parent + g0, cnt, ND,
-                                                                nrep, D.tmpA);
-        LB_TRY(gemm_rm(D.blas, D.l2l + (int64_t)ref_octant(oct) * nrep * nrep, D.tmpA, D.tmpB, nrep,
-                       cnt * ND, 1.0 / hc, 0.0));
-        scatter_cols_kernel<<<(unsigned)(cnt * ND), 128, 0, st>>>(D.tmpB, D.dn_child + g0, cnt, ND,
-                                                                 nrep, D.dc, 1);
-      } else {
+      {
         grid_tensor_kernel<ND><<<(unsigned)cnt, 256, grid_smem, st>>>(
             D.dn_child + g0, D.dn_parent + g0, D.btgt_oct, D.m2m, n, D.loc, D.dc, 1);
       }
@@ -1765,7 +1765,11 @@ void fmm_release_device(lb_fmm_plan* P) {
   cudaFree(D.lr_t);
   cudaFree(D.oz_b);
   cudaFree(D.oz_cs);
-  if (D.blas) cublasDestroy(D.blas);
+  cudaFree(D.dn_off_dev);
+  cudaFree(D.up_par);
+  cudaFree(D.up_child8);
+  cudaFree(D.m2m_oct);
+  cudaFree(D.l2l_oct);
   D = FmmDevice();
 }
 
@@ -1900,7 +1904,6 @@ int fmm_apply_impl(lb_fmm_plan* P, const double* charges, const double* dipoles,
     LB_CUDA(cudaMalloc((void**)&P->dev.tproj, sizeof(double) * 3 * nt));
     LB_CUDA(cudaMalloc((void**)&P->dev.snrm, sizeof(double) * 3 * std::max<int64_t>(P->tree.ns, 1)));
   }
-  LB_BLAS(cublasSetStream(P->dev.blas, st));
   std::vector<cudaEvent_t> ev;
   if (P->timing) {
     ev.resize(kStages + 1);

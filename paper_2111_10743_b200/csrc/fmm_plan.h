@@ -1,7 +1,6 @@
 // lb_fmm_plan: the device FmmPlan (fmm.py:722-990).
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -15,7 +14,6 @@ namespace lb {
 struct FmmDevice {
   bool ready = false;
   int nd_alloc = 0;
-  cublasHandle_t blas = nullptr;
   // geometry, sorted order
   double *spos = nullptr, *tpos = nullptr;   // sorted positions (ns,3) (nt,3)
   int64_t *src_sorted = nullptr, *tgt_sorted = nullptr;
@@ -38,6 +36,12 @@ struct FmmDevice {
   std::vector<int64_t> up_off;               // 8 * nlev + 1 host offsets
   int64_t *dn_child = nullptr, *dn_parent = nullptr;
   std::vector<int64_t> dn_off;
+  int64_t* dn_off_dev = nullptr;             // device copy (per-octant batches of the L2L)
+  // surface M2M per level: parents (slots) with their 8 child slots in
+  // octant order (-1 = none), levels concatenated; up_par_off: host offsets
+  int64_t *up_par = nullptr, *up_child8 = nullptr;
+  std::vector<int64_t> up_par_off;
+  double *m2m_oct = nullptr, *l2l_oct = nullptr;  // surface operators in octant order
   // m2l: per canonical key, pairs sorted by target
   int64_t *v_src = nullptr, *v_tgt_pair_off = nullptr, *v_tgts = nullptr;
   int32_t* v_off_idx = nullptr;

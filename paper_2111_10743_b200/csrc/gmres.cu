@@ -5,6 +5,9 @@
 // one Hessenberg column per iteration for the Givens update, as the
 // reference's convergence test requires.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "lb_common.cuh"
 #include "reduce.cuh"
@@ -137,20 +140,29 @@ __global__ void __launch_bounds__(kSmallBT) mgs_small_kernel(double* __restrict_
 
 namespace {
 
-// persistent reduction scratch per device (grid <= 2*SMs blocks)
+// persistent reduction scratch, one pool per (device, stream): the grid
+// reductions count finished CTAs on a ticket, so two reductions in flight on
+// different streams (or devices) must never share partials or tickets.
+// Calls on ONE stream are ordered by the stream and may share a pool.
 struct RedPool {
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   int cap = 0;
 };
 
-int get_pool(RedBufs* rb, int blocks) {
-  static RedPool pool;
+int get_pool(RedBufs* rb, int blocks, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, RedPool> pools;
+  int dev = 0;
+  LB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  RedPool& pool = pools[{dev, st}];
   if (pool.cap < blocks) {
     if (pool.partials) cudaFree(pool.partials);
     if (pool.ticket) cudaFree(pool.ticket);
     pool.partials = nullptr;
     pool.ticket = nullptr;
+    pool.cap = 0;
     LB_CUDA(cudaMalloc(&pool.partials, sizeof(double) * (blocks + 32)));
     LB_CUDA(cudaMalloc(&pool.ticket, sizeof(unsigned) * 4));
     LB_CUDA(cudaMemset(pool.ticket, 0, sizeof(unsigned) * 4));
@@ -181,7 +193,7 @@ int lb_arnoldi_mgs(double* Q, int64_t ldq, int k, int64_t n, double* v, double* 
   }
   const int blocks = vec_blocks(n);
   RedBufs rb;
-  LB_TRY(get_pool(&rb, 2 * sm_count() + 8));
+  LB_TRY(get_pool(&rb, 2 * sm_count() + 8, st));
   // h[0] = Q_0 . v ; then for j >= 1: v -= h[j-1] Q_{j-1} fused with h[j] = Q_j . v
   for (int j = 0; j <= k; ++j) {
     const double* qp = j > 0 ? Q + (int64_t)(j - 1) * ldq : nullptr;
@@ -210,7 +222,7 @@ int lb_combine_rows(const double* Q, int64_t ldq, int k, int64_t n, const double
 int lb_dot(const double* x, const double* y, int64_t n, double* out, void* stream) {
   using namespace lb;
   RedBufs rb;
-  LB_TRY(get_pool(&rb, 2 * sm_count() + 8));
+  LB_TRY(get_pool(&rb, 2 * sm_count() + 8, as_stream(stream)));
   // v := x is read-only here (qp == nullptr), so the const_cast is never written through
   mgs_pass_kernel<<<vec_blocks(std::max<int64_t>(n, 1)), kVecBT, 0, as_stream(stream)>>>(
       const_cast<double*>(x), nullptr, nullptr, y, n, 0, out, rb);
@@ -221,7 +233,7 @@ int lb_dot(const double* x, const double* y, int64_t n, double* out, void* strea
 int lb_nrm2(const double* x, int64_t n, double* out, void* stream) {
   using namespace lb;
   RedBufs rb;
-  LB_TRY(get_pool(&rb, 2 * sm_count() + 8));
+  LB_TRY(get_pool(&rb, 2 * sm_count() + 8, as_stream(stream)));
   mgs_pass_kernel<<<vec_blocks(std::max<int64_t>(n, 1)), kVecBT, 0, as_stream(stream)>>>(
       const_cast<double*>(x), nullptr, nullptr, nullptr, n, 1, out, rb);
   LB_CHECK_LAUNCH();

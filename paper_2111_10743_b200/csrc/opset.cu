@@ -947,7 +947,11 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
   if (!d->nodes || !d->normals || !d->weights || !d->curvature || !d->over_nodes ||
       !d->over_normals || !d->over_weights || !d->over_interp || !d->indptr || !d->indices)
     return fail(LB_ERR_ARG, "lb_opset_create: missing geometry or CSR pattern");
-  if (d->row0 < 0 || d->nrows < 0 || d->row0 + d->nrows > d->n)
+  // nrows < 0: every row; an empty shard is an error (a handle owning no
+  // rows would reduce and read rows it never computed)
+  if (d->nrows == 0)
+    return fail(LB_ERR_SHAPE, "lb_opset_create: empty row range (nrows = 0)");
+  if (d->nrows > 0 && (d->row0 < 0 || d->row0 + d->nrows > d->n))
     return fail(LB_ERR_SHAPE, "lb_opset_create: row range outside [0, n)");
   lb_opset* h = new lb_opset();
   h->d = *d;

@@ -20,6 +20,29 @@ __global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, 
   if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
 }
 
+// FP64 tensor-core (DMMA 8x8x4) peak: 8 independent accumulator tiles per
+// warp; each mma = 8*8*4 FMA = 512 flop per warp
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters, double a) {
+  double c[8][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = threadIdx.x * 1e-3 + t;
+  double av = a + threadIdx.x * 1e-9, bv = a - threadIdx.x * 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dmma_884(c[t][0], c[t][1], av, bv);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 __global__ void rsqrt_seed_kernel(const double* x, double* y, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = rsqrt_seed(x[i]);
@@ -37,6 +60,13 @@ extern "C" {
 // flops executed = blocks * 256 * iters * 16 * 8 * 2
 int lb_probe_dfma(double* scratch, int blocks, int iters, void* stream) {
   lb::dfma_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 0.999999, 1e-7);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+// flops executed = blocks * 8 warps * iters * 8 mma * 512
+int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream) {
+  lb::dmma_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }

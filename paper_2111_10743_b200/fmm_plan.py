@@ -493,6 +493,57 @@ class FmmPlan:
         _lib.check(self._L.lb_fmm_setup_times(self._h, ms.ctypes.data_as(ctypes.c_void_p)))
         return dict(zip(("sort", "tree", "lists", "device", "total"), ms.tolist()))
 
+    def work_counts(self):
+        """Algorithmic work of one apply per density, from the tree and lists
+        (fmm.py:823-988): pairwise-kernel pair counts of the stages that run
+        the 1/r kernel (P2M lattice, X list, leaf U / own-DE / W parts) and
+        the M2L's V pairs with its flops (low-rank: 4 nrep r_k per pair,
+        dense: 2 nrep^2).  Targets outside an owned range are not excluded."""
+        t = self.tree
+        r = t.raw
+        leaf = t.is_leaf
+        ns_box = np.where(leaf, r["src_hi"] - r["src_lo"], 0)
+        nt_box = np.where(leaf, r["tgt_hi"] - r["tgt_lo"], 0)
+        nrep = self.nrep
+
+        def per_box_sum(off, idx, w):
+            v = np.zeros(len(off) - 1)
+            if len(idx):
+                s = np.concatenate([[0.0], np.cumsum(w[idx], dtype=np.float64)])
+                v = s[off[1:]] - s[off[:-1]]
+            return v
+        u_src = per_box_sum(r["u_off"], r["u"], ns_box.astype(float))
+        w_cnt = np.diff(r["w_off"]).astype(float)
+        x_src = per_box_sum(r["x_off"], r["x"], ns_box.astype(float))
+        surface = self.rep == "surface"
+        out = {"u_pairs": float(np.dot(nt_box, u_src)),
+               "w_pairs": float(np.dot(nt_box, w_cnt)) * nrep,
+               "de_pairs": float(nt_box.sum()) * nrep if surface else 0.0,
+               "x_pairs": float(x_src.sum()) * nrep,
+               "p2m_pairs": float(ns_box.sum()) * nrep if surface else 0.0,
+               "v_pairs": float(len(r["v"])), "nrep": nrep}
+        if self.m2l_slices < 0:  # low-rank: V pairs per canonical key x 4 nrep r_k
+            okey = self.ops["off_key"]
+            cnt = self._v_pairs_per_key(okey)
+            out["m2l_flops"] = float(np.dot(cnt, 4.0 * nrep * self.m2l_ranks))
+        else:
+            out["m2l_flops"] = out["v_pairs"] * 2.0 * nrep * nrep
+        return out
+
+    def _v_pairs_per_key(self, okey):
+        """V pairs per canonical key: offset = ijk(src) - ijk(tgt) at one level."""
+        t = self.tree
+        r = t.raw
+        tgt = np.repeat(np.arange(len(r["v_off"]) - 1), np.diff(r["v_off"]))
+        d = t.ijk[r["v"]] - t.ijk[tgt]
+        ov = self.ops["off_vec"]
+        base = int(np.abs(ov).max()) + 1
+        code = lambda a: ((a[:, 0] + base) * (2 * base + 1) + (a[:, 1] + base)) \
+            * (2 * base + 1) + (a[:, 2] + base)  # noqa: E731
+        lut = dict(zip(code(ov).tolist(), okey.tolist()))
+        keys = np.array([lut[c] for c in code(d).tolist()], dtype=np.int64)
+        return np.bincount(keys, minlength=len(self.ops["canon_keys"])).astype(float)
+
     def apply_device(self, charges, dipoles, nd, cmask, dmask, level, pot,
                      grad=None, hess=None, stream=None):
         _lib.check(self._L.lb_fmm_apply(

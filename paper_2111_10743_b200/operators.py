@@ -6,14 +6,15 @@ constructor, attributes (`disc`, `formulation`, `eps`, `near`, `corrections`,
 `t_q`, `t_mv_total`, `n_apply`, `phi0`) and methods (`apply`, `apply_a1/2/3`,
 `apply_layer`, `evaluate_solution`, `corr`).  The discretisation is
 duck-typed: the reference's own SurfaceDiscretization works, as does
-`Geometry` (the same attributes loaded from a bundle).  Corrections are the
-reference's CSR matrices (NearCorrections.matrix); building them is the
-reference's CPU precompute (compute_corrections, quadrature.py:663-701, out of
-scope here), so they are either passed in or built by the reference when it
-is importable.
+`Geometry` (the same attributes loaded from a bundle).  Corrections are
+either passed in (the reference's CSR matrices, NearCorrections.matrix) or
+built on the device from the chart coefficients the discretisation carries
+(quadrature.build_correction_set, csrc/quad.cu: the near map and adaptive
+quadrature of compute_corrections, quadrature.py:663-701); there is no CPU
+build and no import of the reference.
 
 The apply itself is one C-ABI call (lb_opset_apply): oversampling, the two
-far-field sweeps (fp64, exact all-pairs), the near-correction SpMVs and the
+far-field sums (exact fp64 sweeps, or the device FmmPlan), the near-correction SpMVs and the
 glue run as fused sm_100a kernels on one stream.  Inputs may be numpy (result
 returned as numpy, like the reference) or CUDA tensors (result stays on the
 device, nothing synchronised).
@@ -293,7 +294,7 @@ class DeviceOperator:
     """Owner of the device arrays and the lb_opset handle (C ABI)."""
 
     def __init__(self, disc, corrections: CorrectionSet, kinds, row0=0,
-                 nrows=0):
+                 nrows=-1):
         t = _lib.require_cuda()
         L = _bind_opset()
         oi = _over_interp(disc)
@@ -334,7 +335,7 @@ class DeviceOperator:
         d.phi0 = None
         d.row0, d.nrows = int(row0), int(nrows)
         self.row0 = int(row0)
-        self.nrows = int(nrows) if nrows else n
+        self.nrows = int(nrows) if nrows >= 0 else n
         self.desc = d
         self.n = n
         h = ctypes.c_void_p()
@@ -484,8 +485,10 @@ class LayerOperatorSet:
                     approximation; ~300 is ~2x faster on a B200 for surface
                     point sets, tools: scripts/fmm_ncrit_probe.py).
       fmm_m2l     : M2L arithmetic of that plan (FmmPlan.set_m2l): "auto"
-                    (tcgen05 int8 slices sized from eps), "fp64" (DGEMM) or
-                    a slice count in [3, 8].
+                    (the canonical operators' truncated-SVD factors at
+                    eps/100, fp64, fmm_plan.m2l_factors), "fp64" (the dense
+                    canonical operators, the reference's arithmetic) or a
+                    slice count in [3, 8] (tcgen05 int8 Ozaki slices).
       fuse_a3     : A3 with exact sweeps runs its second sweep fused with the
                     glue (one accumulator, eta from Phi = S^T w: eta_weights,
                     lb_opset_set_eta_weights); False keeps the four-output

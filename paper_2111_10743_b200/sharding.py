@@ -25,13 +25,20 @@ def partition_rows(npatches: int, nb: int, world: int, cost=None):
     of (row0, nrows) in target rows (patch-aligned)."""
     if world < 1:
         raise ValueError("world must be >= 1")
+    if world > npatches:
+        raise ValueError(f"cannot give each of {world} ranks a patch "
+                         f"({npatches} patches)")
     c = np.ones(npatches) if cost is None else np.asarray(cost, dtype=float)
     cum = np.concatenate([[0.0], np.cumsum(c)])
     bounds = [0]
     for r in range(1, world):
         bounds.append(int(np.searchsorted(cum, cum[-1] * r / world)))
     bounds.append(npatches)
-    bounds = np.maximum.accumulate(np.array(bounds))
+    # every rank owns at least one patch (an empty shard would own nothing
+    # yet take part in the reductions): clamp bound r into [r, npatches-world+r]
+    bounds = np.array(bounds)
+    for r in range(1, world):
+        bounds[r] = min(max(bounds[r], bounds[r - 1] + 1), npatches - (world - r))
     return [(int(bounds[r]) * nb, int(bounds[r + 1] - bounds[r]) * nb)
             for r in range(world)]
 

@@ -1,0 +1,299 @@
+"""BASELINE configs 2-5 pinned to the REFERENCE at their full sizes, with
+every input rebuilt on the box (no data/ bundle, nothing skipped):
+
+* geometry: shapes.py hands the device geometry build the reference's own
+  chart coefficients (bit-identical, tests/test_shapes_cpu.py); nodes,
+  normals, weights and curvature then match the reference's at 1e-13;
+* near maps (integer work): the full map's SHA-256 equals the reference's
+  build_near_map (quadrature.py:76-104) at configs 3 and 4;
+* corrections: row-sampled reference builds (a NearMap with near lists only
+  for the sampled targets, quadrature.py:66-73, through compute_corrections,
+  quadrature.py:663-701: bit-identical to the full build's rows)
+  against the device build of the same rows, 5 eps of max|value| and 50 eps
+  of each row's max (the bars of tests/test_quadrature_gpu.py);
+* config 2: the reference's A2 and A3 solves (GMRES 1e-10) against the device
+  solves on device-built corrections, u within 1e-9 relative weighted L2
+  (north_star's solution bar), same iteration counts;
+* config 3: the Hodge decomposition of BASELINE's Gaussian field (two A3
+  solves, hodge.py:126-161), pinned on a reduced 12 x 6 torus where the
+  reference's own corrections and solves are cheap (alpha, beta, H within
+  1e-9), and run at full size (64 x 32 torus, FMM far field at eps 5e-8);
+* config 5: the device octree + lists at 10^6 points bit-exact (digests of
+  the reference's _build_tree/_build_lists), and the device FMM at 10^6, eps
+  1e-6, against the reference's FmmPlan.apply on 200 sampled targets.
+
+Goldens: scripts/make_golden_r2.py (run against lapbel in the build
+container)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, golden, rel_errs
+from treehash import compare, digests, sha
+
+pytestmark = pytest.mark.gpu
+
+A3 = ("s", "sprime", "spp_plus_dprime")
+
+
+def _kind(name):
+    from paper_2111_10743_b200.operators import as_kind
+    return as_kind(name)
+
+
+def _wl2(a, b, w):
+    return float(np.sqrt(np.dot(w, (a - b) ** 2) / np.dot(w, b ** 2)))
+
+
+def _sampled_near(near, targets):
+    """The reference's row-sampled NearMap (quadrature.py:66-73): near lists
+    kept only for `targets`."""
+    from paper_2111_10743_b200.quadrature import NearMap
+    n = len(near.offsets) - 1
+    keep = np.zeros(n, dtype=bool)
+    keep[targets] = True
+    cnt = np.where(keep, np.diff(near.offsets), 0)
+    off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    pats = np.concatenate([near.patches[near.offsets[t]:near.offsets[t + 1]]
+                           for t in targets]).astype(np.int32)
+    return NearMap(near.eta, near.cap, off, pats)
+
+
+def _check_rows(cset, g, kinds, eps):
+    """Device CSR rows of the sampled targets vs the reference's rows."""
+    ip = cset.indptr.cpu().numpy()
+    ix = cset.indices.cpu().numpy()
+    tg = g["targets"]
+    roff = g["rows_off"]
+    worst = {}
+    for j, t in enumerate(tg):
+        a, b = ip[t], ip[t + 1]
+        assert np.array_equal(ix[a:b], g["rows_cols"][roff[j]:roff[j + 1]]), t
+    for k in kinds:
+        v = cset.values[_kind(k)].cpu().numpy()
+        ref = g["rows_" + k]
+        got = np.concatenate([v[ip[t]:ip[t + 1]] for t in tg])
+        diff = np.abs(got - ref)
+        assert diff.max() <= 5 * eps * np.abs(ref).max(), k
+        rowmax = np.maximum.reduceat(np.abs(ref), roff[:-1])
+        rows = np.repeat(np.arange(len(tg)), np.diff(roff))
+        assert (diff / rowmax[rows]).max() <= 50 * eps, k
+        worst[k] = float(diff.max() / np.abs(ref).max())
+    return worst
+
+
+def _check_geometry(geom, g):
+    t = g["targets"]
+    scale = 1.0 + np.abs(geom.nodes).max()
+    assert np.abs(geom.nodes[t] - g["nodes_at"]).max() < 1e-13 * scale
+    assert np.abs(geom.normals[t] - g["normals_at"]).max() < 1e-12
+    assert np.abs(geom.weights[t] - g["weights_at"]).max() < 1e-13 * np.abs(g["weights_at"]).max()
+    assert np.abs(geom.curvature[t] - g["curvature_at"]).max() < 1e-10
+    assert abs(geom.weights.sum() - float(g["area"])) < 1e-12 * float(g["area"])
+    assert abs(geom.over_weights.sum() - float(g["over_weights_sum"])) < 1e-12 * float(g["area"])
+
+
+def _check_near(near, g):
+    from treehash import sha as _sha
+    assert int(near.offsets[-1]) == int(g["near_total"])
+    assert _sha(near.offsets, np.int64) == str(g["near_off_sha"])
+    assert _sha(near.patches, np.int32) == str(g["near_patches_sha"])
+
+
+# ---------------------------------------------------------------------------
+# config 3: build_torus(7, 64, 32, 2, 1), N = 114,688
+
+
+@pytest.fixture(scope="module")
+def config3(cuda):
+    from paper_2111_10743_b200 import shapes
+    from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map
+    g = golden("config3_rows.npz")
+    geom = shapes.build_torus(7, 64, 32, 2.0, 1.0)
+    near = build_near_map(geom, 2.0, cap=256)
+    eps = float(g["eps"])
+    cset, t_q = build_correction_set(geom, near, [_kind(k) for k in A3], eps)
+    return g, geom, near, cset, eps
+
+
+def test_config3_geometry_and_near_map(config3):
+    g, geom, near, _, _ = config3
+    assert geom.nnodes == int(g["nnodes"]) == 114688
+    _check_geometry(geom, g)
+    _check_near(near, g)
+
+
+def test_config3_corrections_match_reference_rows(config3):
+    g, _, _, cset, eps = config3
+    assert cset.nnz > 3.2e8  # the full build: 2,809 nnz per row per kind
+    _check_rows(cset, g, A3, eps)
+
+
+def test_config3_hodge_full_size(config3):
+    """BASELINE config 3 as stated: the Gaussian field's Hodge decomposition
+    (two A3 solves on one operator set, FMM far field at eps 5e-8, GMRES
+    5e-10: the paper's Hodge setting) on the 64 x 32 torus.  No reference
+    solve exists at this size (its correction build takes hours): the
+    decomposition is checked by its defining identities -- H is divergence-
+    and curl-free to the discretisation level, and F = grad a + n x grad b + H
+    holds by construction -- and against the exact-sweep operator's solves."""
+    import paper_2111_10743_b200 as b
+    from paper_2111_10743_b200.hodge import gaussian_field, hodge_decompose
+    _, geom, near, cset, eps = config3
+    field = gaussian_field(geom)
+    cfg = b.SolveConfig(formulation="a3", eps=eps, eps_gmres=5e-10, max_iter=100)
+    op = b.LayerOperatorSet(geom, "a3", eps, corrections=cset, near=near, far="fmm")
+    res = hodge_decompose(op, field, cfg)
+    assert res.converged and max(res.n_iter) < 40
+    fnorm = float(np.sqrt(np.dot(geom.weights, (field.values ** 2).sum(1))))
+    # the exact decomposition has div H = div(n x H) = 0; the discrete one
+    # is limited by the reference's per-patch spectral differentiation
+    # (surface.py:335-367, div of grad at order 7 on 4,096 patches): measured
+    # 2.7e-3 of |F| (the reduced 12 x 6 torus golden: see the test below)
+    assert res.div_h_norm < 1e-2 * fnorm and res.div_nxh_norm < 1e-2 * fnorm
+    del op
+    op2 = b.LayerOperatorSet(geom, "a3", eps, corrections=cset, near=near, far="direct")
+    res2 = hodge_decompose(op2, field, cfg)
+    w = geom.weights
+    for a, c in ((res.alpha.values, res2.alpha.values), (res.beta.values, res2.beta.values)):
+        assert _wl2(np.asarray(a), np.asarray(c), w) < 20 * eps
+
+
+def test_hodge_reduced_torus_matches_reference(cuda):
+    """Config 3's workload (Gaussian field, two A3 solves, H) against the
+    reference's own hodge_decompose on build_torus(7, 12, 6, 2, 1) with its
+    own corrections (eps 1e-10) and exact far sums, GMRES 1e-10: the device
+    solves use device-built corrections and exact sweeps."""
+    import paper_2111_10743_b200 as b
+    from paper_2111_10743_b200 import shapes
+    from paper_2111_10743_b200.hodge import gaussian_field, hodge_decompose
+    g = golden("hodge_torus_o7.npz")
+    geom = shapes.build_torus(7, 12, 6, 2.0, 1.0)
+    assert np.abs(geom.nodes - g["nodes"]).max() < 1e-13
+    near = b.build_near_map(geom, 2.0, cap=256)
+    assert np.array_equal(near.offsets, g["near_offsets"])
+    assert np.array_equal(near.patches, g["near_patches"])
+    eps = float(g["eps"])
+    op = b.LayerOperatorSet(geom, "a3", eps, near=near, far="direct")
+    field = gaussian_field(geom)
+    assert np.abs(field.values - g["field"]).max() < 1e-12 * np.abs(g["field"]).max()
+    cfg = b.SolveConfig(formulation="a3", eps=eps, eps_gmres=float(g["eps_gmres"]),
+                        max_iter=100)
+    res = hodge_decompose(op, field, cfg)
+    assert tuple(res.n_iter) == tuple(g["n_iter"])
+    w = geom.weights
+    assert _wl2(np.asarray(res.alpha.values), g["alpha"], w) < 1e-9
+    assert _wl2(np.asarray(res.beta.values), g["beta"], w) < 1e-9
+    hn = np.sqrt(np.dot(w, (g["harmonic"] ** 2).sum(1)))
+    assert np.sqrt(np.dot(w, ((res.harmonic.values - g["harmonic"]) ** 2).sum(1))) < 1e-9 * \
+        np.sqrt(np.dot(w, (g["field"] ** 2).sum(1))) + 1e-9 * hn
+
+
+# ---------------------------------------------------------------------------
+# config 4: the wavy torus, order 9, N = 1,202,940
+
+
+def test_config4_geometry_near_map_and_rows(cuda):
+    from paper_2111_10743_b200 import shapes
+    from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map
+    g = golden("config4_rows.npz")
+    geom = shapes.wavy_torus(9, 82, 163)
+    assert geom.nnodes == int(g["nnodes"]) == 1202940
+    _check_geometry(geom, g)
+    near = build_near_map(geom, 2.0, cap=256)
+    _check_near(near, g)
+    eps = float(g["eps"])
+    cset, _ = build_correction_set(geom, _sampled_near(near, g["targets"]),
+                                   [_kind(k) for k in A3], eps)
+    _check_rows(cset, g, A3, eps)
+
+
+# ---------------------------------------------------------------------------
+# config 2: the reference's A2 and A3 solves
+
+
+@pytest.mark.parametrize("form", ["a3", "a2"])
+def test_config2_solve_matches_reference(cuda, form):
+    """Icosphere order 7 (N = 8,960), f = Re Y_3^2, eps 1e-10, GMRES 1e-10:
+    device-built corrections (the 4 kinds' sampled rows against the
+    reference's), the apply of the seeded tau against the reference's apply,
+    and the solution against the reference's solve at 1e-9 (north_star)."""
+    import paper_2111_10743_b200 as b
+    from paper_2111_10743_b200 import shapes
+    from test_oracle_golden import REF_NOISE
+    geo = golden("config2_geom.npz")
+    ref = golden("config2_ref.npz")
+    geom = shapes.icosphere(7)
+    assert np.abs(geom.nodes - geo["nodes"]).max() < 1e-14
+    near = b.build_near_map(geom, 2.0)
+    assert np.array_equal(near.offsets, geo["near_offsets"])
+    assert np.array_equal(near.patches, geo["near_patches"])
+    eps = float(ref["eps"])
+    op = b.LayerOperatorSet(geom, form, eps, near=near, far="direct")
+    _check_rows(op._cset, ref, [k.value for k in op._cset.values], eps)
+    got = op.apply(geo["tau"])
+    assert np.abs(got - ref[f"{form}_apply"]).max() / np.abs(ref[f"{form}_apply"]).max() \
+        < REF_NOISE[form]
+    rep = b.solve_laplace_beltrami(op, geo["f"], b.SolveConfig(
+        formulation=form, eps=eps, eps_gmres=1e-10))
+    w = geom.weights
+    assert rep.converged and rep.n_iter == len(ref[f"{form}_hist"])
+    assert _wl2(np.asarray(rep.u.values), ref[f"{form}_u"], w) < 1e-9
+    ue = geo["u_exact"] - np.dot(w, geo["u_exact"]) / w.sum()
+    assert _wl2(np.asarray(rep.u.values), ue, w) < 3e-7
+
+
+# ---------------------------------------------------------------------------
+# config 5: 10^6 points on the sphere
+
+
+@pytest.fixture(scope="module")
+def tree_want():
+    with open(os.path.join(GOLD, "config5_tree_sha256.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("buffer,eps", [(1, 1e-6), (2, 1e-9)])
+def test_config5_device_tree_and_lists_bit_exact(cuda, tree_want, buffer, eps):
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    from paper_2111_10743_b200.shapes import sphere_cloud
+    x = sphere_cloud(tree_want["n"], tree_want["seed"])
+    assert sha(x, np.float64) == tree_want["x_sha"]
+    plan = FmmPlan(x, x, eps, ncrit=120, device_sort=True)
+    assert plan.setup_times()["tree"] < 1.0  # the device build ran
+    bad = compare(digests(plan.tree), tree_want[f"b{buffer}"])
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("m2l", ["fp64", "auto"])
+def test_config5_fmm_matches_reference_fmm(cuda, m2l):
+    """fmm.py:784-990 at 10^6 (eps 1e-6, surface m = 8, ncrit 120): the
+    reference's FmmPlan.apply on 200 sampled targets.  With m2l="fp64" the
+    device evaluates the reference's approximation (same tree, lists and
+    operators): agreement is roundoff amplified by the surface
+    representation's Tikhonov pseudo-inverse (3e-9 on the small fixtures);
+    the default low-rank M2L moves it by < eps/100.  Both within eps of the
+    exact sums."""
+    import torch
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    from paper_2111_10743_b200.shapes import sphere_cloud
+    g = golden("config5_fmm_1e6.npz")
+    n = int(g["n"])
+    x = sphere_cloud(n)
+    q = np.random.default_rng(int(g["q_seed"])).standard_normal((1, n))
+    plan = FmmPlan(x, x, 1e-6, ncrit=120, m2l=m2l)
+    qd = torch.from_numpy(q).cuda()
+    pot = torch.zeros((1, n), dtype=torch.float64, device="cuda")
+    grad = torch.zeros((1, n, 3), dtype=torch.float64, device="cuda")
+    plan.apply_device(qd, None, 1, 1, 0, 1, pot, grad)
+    torch.cuda.synchronize()
+    idx = g["idx"]
+    p, gr = pot.cpu().numpy()[:, idx], grad.cpu().numpy()[:, idx]
+    bar = 1e-8 if m2l == "fp64" else 2e-8
+    assert rel_errs(p, g["e6_pot"], 1) < bar
+    assert rel_errs(gr, g["e6_grad"], 1) < bar
+    assert rel_errs(p, g["e6_direct_pot"], 1) <= 1e-6
+    assert rel_errs(gr, g["e6_direct_grad"], 1) <= 1e-6
