@@ -240,9 +240,10 @@ def dmma_peak_tflops(torch, lib, _lib):
     return best / 1e12
 
 
-def build_config3(torch):
+def build_config3(torch, corrections=True):
     """Geometry (device), near map (device, eta 2, cap 256), corrections
-    (device, eps 5e-8, S / S' / S''+D')."""
+    (device, eps 5e-8, S / S' / S''+D'; skipped for a sharded run, whose
+    ranks build their own rows)."""
     from paper_2111_10743_b200 import shapes
     from paper_2111_10743_b200.operators import KernelKind
     from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map
@@ -254,6 +255,8 @@ def build_config3(torch):
     near = build_near_map(geom, c["eta"], cap=c["cap"])
     torch.cuda.synchronize()
     t2 = time.perf_counter()
+    if not corrections:
+        return geom, near, None, {"geometry_s": t1 - t0, "near_map_s": t2 - t1}
     kinds = [KernelKind.SINGLE_LAYER, KernelKind.SPRIME, KernelKind.SPP_PLUS_DPRIME]
     cset, t_q = build_correction_set(geom, near, kinds, c["eps"])
     torch.cuda.synchronize()
@@ -392,6 +395,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS lines in the log
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -404,29 +408,32 @@ def main():
 
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6547.2))
-    geom, near, cset, setup = build_config3(torch)
+    geom, near, cset, setup = build_config3(torch, corrections=world == 1)
     n, nover = geom.nnodes, geom.noversampled
     inter = 4 * n * nover
     c = CONFIG3
     t0 = time.perf_counter()
     if world > 1:
+        # Morton-range target shards, per-rank corrections, distributed
+        # upward pass (sharding.py); GMRES replicated on full vectors
         from paper_2111_10743_b200.sharding import ShardedOperatorSet
-        op = ShardedOperatorSet(geom, "a3", c["eps"], cset, far="fmm", near=near,
-                                fmm_ncrit=c["ncrit"])
+        op = ShardedOperatorSet(geom, "a3", c["eps"], None, far="fmm", eta=c["eta"],
+                                cap=c["cap"], fmm_ncrit=c["ncrit"])
+        cset = type("C", (), {"nnz": int(np.asarray(near.offsets)[-1]) * int(geom.nodes_per_patch)})
     else:
         op = LayerOperatorSet(geom, "a3", c["eps"], corrections=cset, near=near, far="fmm",
                               fmm_ncrit=c["ncrit"])
     torch.cuda.synchronize()
     setup["plan_s"] = time.perf_counter() - t0
     L = _bind()
-    nloc = op.nloc if world > 1 else n
+    nloc = n  # GMRES vectors are full length on every rank
     rng = np.random.default_rng(2)
     Q = torch.from_numpy(np.linalg.qr(rng.standard_normal((nloc, K_ARNOLDI + 1)))[0].T
                          .copy()).cuda().contiguous()
     hdev = torch.zeros(K_ARNOLDI + 2, dtype=torch.float64, device="cuda")
     v = torch.empty(nloc, dtype=torch.float64, device="cuda")
     tau_h = rng.standard_normal(n)
-    tau = torch.from_numpy(tau_h if world == 1 else tau_h[op.row_slice]).cuda()
+    tau = torch.from_numpy(tau_h).cuda()
 
     def mgs():
         _lib.check(L.lb_arnoldi_mgs(_lib.ptr(Q), nloc, K_ARNOLDI - 1, nloc, _lib.ptr(v),

@@ -296,6 +296,14 @@ int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
  * the same plan with its own row range; the outputs at owned
  * targets equal the unsharded plan's. */
 int lb_fmm_plan_set_target_range(lb_fmm_plan* plan, int64_t t0, int64_t t1);
+/* Owned sources [s0, s1) (plan source order; s1 < 0: all) of a sharded
+ * apply: the upward pass (P2M + M2M) covers only these, so each rank's
+ * expansions are partial sums; the upward hook, called on the apply's
+ * stream between the M2M and the M2L with the (nbox x nd x nrep) expansion
+ * array, must sum them over the ranks in place (an all-reduce). */
+typedef void (*lb_fmm_upward_hook)(void* user, double* up, int64_t count, int nd, void* stream);
+int lb_fmm_plan_set_source_range(lb_fmm_plan* plan, int64_t s0, int64_t s1);
+int lb_fmm_plan_set_upward_hook(lb_fmm_plan* plan, lb_fmm_upward_hook hook, void* user);
 /* Low-rank M2L (slices = -1 above): per canonical key k the factors of the
  * truncated SVD  canon_k ~= A_k B_k, A_k (nrep, r_k), B_k (r_k, nrep), both
  * row-major and concatenated over k in key order.  The product then costs
@@ -410,6 +418,16 @@ typedef struct lb_geom_desc {
   double* stats;
 } lb_geom_desc;
 int lb_geom_build(const lb_geom_desc* desc, void* stream);
+
+/* ------------------------------------------------------------------------
+ * FP64 tensor-core GEMM of the FMM translations (DMMA 8x8x4, no library):
+ * Y[:, c] (+)= alpha * A @ X[kperm_c(:), cols[c]]  with A (M x K) row-major,
+ * X / Y column vectors (strides ldx / ldy); cols (optional) gathers X's
+ * columns, kperm + kp[c] * K (optional) permutes each column's K index.
+ * The kernel behind P2M / M2M / L2L / M2L in lb_fmm_apply. */
+int lb_dgemm_cols(const double* A, int lda, int M, int K, const double* X, int64_t ldx,
+                  const int64_t* cols, const int32_t* kperm, const int32_t* kp, int64_t ncols,
+                  double* Y, int64_t ldy, double alpha, int add, void* stream);
 
 /* ------------------------------------------------------------------------
  * Hardware probes (no reference counterpart): FP64 FMA-pipe peak

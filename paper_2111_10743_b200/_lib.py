@@ -75,6 +75,8 @@ SIGNATURES = {
     "lb_fmm_plan_set_m2l": [_P, _I32],
     "lb_fmm_plan_set_m2l_factors": [_P, _P, _P, _P],
     "lb_fmm_plan_set_target_range": [_P, _I64, _I64],
+    "lb_fmm_plan_set_source_range": [_P, _I64, _I64],
+    "lb_fmm_plan_set_upward_hook": [_P, _P, _P],
     "lb_near_map_count": [_P, _I64, _P, _P, _I64, _P, _P, _P],
     "lb_near_map_fill": [_P, _I64, _P, _P, _I64, _P, _P, _P, _P],
     "lb_corrections_build": [_P, _P],
@@ -83,6 +85,8 @@ SIGNATURES = {
     "lb_fmm_setup_times": [_P, _P],
     "lb_probe_dfma": [_P, _I32, _I32, _P],
     "lb_probe_dmma": [_P, _I32, _I32, _P],
+    "lb_dgemm_cols": [_P, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
+                      ctypes.c_double, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],
 }
 _RES = {"lb_last_error_string": ctypes.c_char_p}

@@ -11,20 +11,20 @@
 // column), optionally read through a K-permutation (kperm + kp(q) * K: the
 // M2L's cube-symmetry gather), and the output is Y + (out(q) * nd + l) * ldy.
 // Batches (blockIdx.z) select A_z = A + z * a_batch and the box range
-// [boff[z], boff[z+1]) (the L2L's per-octant child groups).
+// [boff[z] - boff[0], boff[z+1] - boff[0]) (the M2M / L2L per-octant child
+// groups).
 //
-// Every FMM stage maps onto it (fmm.py:823-935): P2M (pinv_up, S = 1), M2M
-// (the 8 child-octant operators of one parent as 8 K-segments: one launch per
-// level, each parent summed in octant order -- deterministic, no atomics),
-// L2L (pinv_dn, then l2l[octant] in 8 batches), and the M2L's low-rank
-// factors (B_k on the permuted, 1/h-scaled multipoles, then A_k).
+// Every FMM stage maps onto it (fmm.py:823-935): P2M (pinv_up), M2M (the
+// children of one level in 8 octant batches, then an in-order sum into the
+// parents), L2L (pinv_dn, then l2l[octant] in 8 batches) and the M2L (its
+// low-rank factors, or the dense canonical operators).
 //
-// Tiles: BM x 32 columns per CTA, 4 warps; warp w owns BM/32 M-tiles of 8 rows
-// (rows w*8*(BM/32) ...) and all four 8-column N-tiles.  K runs in chunks of
-// 32 through a two-stage cp.async pipeline (A rows 256 B coalesced, X
-// elements 8 B gathered through the column pointers / permutation, zero
-// filled past K); fragments come from shared memory (stride 36 doubles: two
-// wavefronts per 8-byte fragment load, the minimum).
+// Tiles: BM x BN per CTA, warps of WM x 32 (WM/8 M-tiles x 4 N-tiles of 8x8,
+// WM/8 * 4 DMMAs per 4-deep k-step).  K runs in chunks of 32 through a
+// two-stage cp.async pipeline (A rows 16-byte coalesced when aligned, X 16 B
+// per contiguous pair or 8 B per gathered element, zero-filled past K);
+// fragments come from shared memory at a 36-double stride (two wavefronts per
+// 8-byte fragment load, the minimum for 32 x 8 B).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,15 +33,14 @@
 namespace lb {
 namespace dg {
 
-constexpr int kBN = 32;      // columns per CTA
 constexpr int kKC = 32;      // K chunk
 constexpr int kLD = 36;      // smem row stride (doubles)
-constexpr int kThreads = 128;
 constexpr int kMaxSeg = 8;
 
 struct Args {
   const double* A;           // segment s of batch z at A + z*a_batch + s*a_seg
-  int64_t a_batch, a_seg;
+  int64_t a_batch, a_seg;    // (or at A + a_off[z] + s*a_seg when a_off is set)
+  const int64_t* a_off;
   int lda, M, K, S, nd;
   const double* X;           // input expansion array
   int64_t ldx;
@@ -55,7 +54,7 @@ struct Args {
   double alpha;
   int add;                   // 1: Y += ..., 0: Y = ...
   int64_t nq;                // boxes/pairs (no batches)
-  const int64_t* boff;       // batches: q range [boff[z], boff[z+1])
+  const int64_t* boff;       // batches: q range [boff[z] - boff[0], boff[z+1] - boff[0])
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -77,50 +76,67 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int BM>
-__global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
-  constexpr int MT = BM / 32;  // M-tiles per warp
+template <int BM, int BN, int WM>
+struct Cfg {
+  static constexpr int kWarpsM = BM / WM, kWarpsN = BN / 32;
+  static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
+  static constexpr int kMT = WM / 8;
+  static constexpr size_t kSmem = sizeof(double) * 2 * (BM + BN) * kLD;
+};
+
+template <int BM, int BN, int WM>
+__global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Args g) {
+  using C = Cfg<BM, BN, WM>;
+  constexpr int NT = C::kThreads, MT = C::kMT;
   extern __shared__ __align__(16) double dsm[];
-  // stage b: A tile at dsm + b * BM * kLD, X tile at dsm + 2 * BM * kLD + b * kBN * kLD
+  // stage b: A tile at dsm + b * BM * kLD, X tile at dsm + 2 * BM * kLD + b * BN * kLD
   auto As = [&](int b) { return dsm + b * BM * kLD; };
-  auto Xs = [&](int b) { return dsm + 2 * BM * kLD + b * kBN * kLD; };
-  __shared__ const double* xin[kMaxSeg][kBN];
-  __shared__ const int32_t* kpp[kBN];
-  __shared__ double* yout[kBN];
-  __shared__ double alph[kBN];
+  auto Xs = [&](int b) { return dsm + 2 * BM * kLD + b * BN * kLD; };
+  __shared__ const double* xin[kMaxSeg][BN];
+  __shared__ const int32_t* kpp[BN];
+  __shared__ double* yout[BN];
+  __shared__ double alph[BN];
   __shared__ int seg_used[kMaxSeg];
+  __shared__ int x16;
 
   const int z = blockIdx.z;
-  const int64_t q0 = g.boff ? g.boff[z] : 0;
-  const int64_t q1 = g.boff ? g.boff[z + 1] : g.nq;
+  const int64_t q0 = g.boff ? g.boff[z] - g.boff[0] : 0;
+  const int64_t q1 = g.boff ? g.boff[z + 1] - g.boff[0] : g.nq;
   const int64_t ncols = (q1 - q0) * g.nd;
-  const int64_t c0 = (int64_t)blockIdx.y * kBN;
+  const int64_t c0 = (int64_t)blockIdx.y * BN;
   if (c0 >= ncols) return;
   const int m0 = blockIdx.x * BM;
-  const double* A = g.A + (int64_t)z * g.a_batch;
+  const double* A = g.a_off ? g.A + g.a_off[z] : g.A + (int64_t)z * g.a_batch;
   // 16-byte A copies need even row strides / offsets and an aligned base
-  const bool a16 = ((g.lda | g.a_seg | g.a_batch) & 1) == 0 && (((uintptr_t)g.A) & 15) == 0;
+  const bool a16 = ((g.lda | g.a_seg | g.a_batch) & 1) == 0 && (((uintptr_t)A) & 15) == 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % C::kWarpsM, wn = warp / C::kWarpsM;
   const int gq = lane >> 2, tq = lane & 3;
 
   if (tid < kMaxSeg) seg_used[tid] = 0;
+  if (tid == 0) x16 = (g.kperm == nullptr && (g.ldx & 1) == 0) ? 1 : 0;
   __syncthreads();
-  if (tid < kBN) {
-    const int64_t c = c0 + tid;
+  for (int j = tid; j < BN; j += NT) {
+    const int64_t c = c0 + j;
     const bool ok = c < ncols;
     const int64_t q = q0 + (ok ? c / g.nd : 0);
     const int l = ok ? (int)(c % g.nd) : 0;
     for (int s = 0; s < g.S; ++s) {
       const int64_t b = g.in ? g.in[q * g.S + s] : q;
-      xin[s][tid] = (ok && b >= 0) ? g.X + (b * g.nd + l) * g.ldx : nullptr;
-      if (ok && b >= 0) seg_used[s] = 1;  // benign race: all writers store 1
+      const double* p = (ok && b >= 0) ? g.X + (b * g.nd + l) * g.ldx : nullptr;
+      xin[s][j] = p;
+      if (p) {
+        seg_used[s] = 1;  // benign race: every writer stores 1
+        if (((uintptr_t)p) & 15) x16 = 0;
+      }
     }
-    kpp[tid] = (ok && g.kperm) ? g.kperm + (int64_t)g.kp[q] * g.K : nullptr;
+    kpp[j] = (ok && g.kperm) ? g.kperm + (int64_t)g.kp[q] * g.K : nullptr;
     const int64_t ob = g.out ? g.out[q] : q;
-    yout[tid] = ok ? g.Y + (ob * g.nd + l) * g.ldy : nullptr;
-    alph[tid] = ok ? g.alpha * (g.alpha_q ? g.alpha_q[q] : 1.0) : 0.0;
+    yout[j] = ok ? g.Y + (ob * g.nd + l) * g.ldy : nullptr;
+    alph[j] = ok ? g.alpha * (g.alpha_q ? g.alpha_q[q] : 1.0) : 0.0;
   }
   __syncthreads();
+  const bool xv = x16 != 0;
 
   double acc[MT][4][2];
 #pragma unroll
@@ -142,31 +158,40 @@ __global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
   };
   auto load = [&](int buf, int s, int k0) {
     const double* As_src = A + (int64_t)s * g.a_seg;
-    // A tile: BM rows x 32 doubles = BM * 16 chunks of 16 B
+    double* as = As(buf);
     if (a16) {
-      for (int e = tid; e < BM * (kKC / 2); e += kThreads) {
+      for (int e = tid; e < BM * (kKC / 2); e += NT) {
         const int r = e / (kKC / 2), kk = (e % (kKC / 2)) * 2;
         const int row = m0 + r, k = k0 + kk;
         int bytes = 0;
         if (row < g.M && k < g.K) bytes = (k + 1 < g.K) ? 16 : 8;
-        cp16(As(buf) + r * kLD + kk, bytes ? As_src + (int64_t)row * g.lda + k : g.A, bytes);
+        cp16(as + r * kLD + kk, bytes ? As_src + (int64_t)row * g.lda + k : g.A, bytes);
       }
     } else {
-      for (int e = tid; e < BM * kKC; e += kThreads) {
+      for (int e = tid; e < BM * kKC; e += NT) {
         const int r = e / kKC, kk = e % kKC;
         const int row = m0 + r, k = k0 + kk;
         const bool ok = row < g.M && k < g.K;
-        cp8(As(buf) + r * kLD + kk, ok ? As_src + (int64_t)row * g.lda + k : g.A, ok);
+        cp8(as + r * kLD + kk, ok ? As_src + (int64_t)row * g.lda + k : g.A, ok);
       }
     }
-    // X tile: 32 columns x 32 k, one 8-byte gather each
-    for (int e = tid; e < kBN * kKC; e += kThreads) {
-      const int c = e >> 5, kk = e & 31, k = k0 + kk;
-      const double* base = xin[s][c];
-      const bool ok = base != nullptr && k < g.K;
-      const int32_t* pp = kpp[c];
-      const double* src = ok ? base + (pp ? pp[k] : k) : g.X;
-      cp8(Xs(buf) + c * kLD + kk, src, ok);
+    double* xs = Xs(buf);
+    if (xv) {  // contiguous, 16-byte aligned columns
+      for (int e = tid; e < BN * (kKC / 2); e += NT) {
+        const int c = e / (kKC / 2), kk = (e % (kKC / 2)) * 2, k = k0 + kk;
+        const double* base = xin[s][c];
+        int bytes = 0;
+        if (base && k < g.K) bytes = (k + 1 < g.K) ? 16 : 8;
+        cp16(xs + c * kLD + kk, bytes ? base + k : g.X, bytes);
+      }
+    } else {
+      for (int e = tid; e < BN * kKC; e += NT) {
+        const int c = e >> 5, kk = e & 31, k = k0 + kk;
+        const double* base = xin[s][c];
+        const bool ok = base != nullptr && k < g.K;
+        const int32_t* pp = kpp[c];
+        cp8(xs + c * kLD + kk, ok ? base + (pp ? pp[k] : k) : g.X, ok);
+      }
     }
     cp_commit();
   };
@@ -187,16 +212,16 @@ __global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
       cp_wait<0>();
     }
     __syncthreads();
-    const double* as = As(buf);
-    const double* xs = Xs(buf);
+    const double* as = As(buf) + (wm * WM + gq) * kLD;
+    const double* xs = Xs(buf) + (wn * 32 + gq) * kLD;
 #pragma unroll
     for (int ks = 0; ks < kKC / 4; ++ks) {
       const int kk = ks * 4 + tq;
       double a[MT], b[4];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) a[mt] = as[((warp * MT + mt) * 8 + gq) * kLD + kk];
+      for (int mt = 0; mt < MT; ++mt) a[mt] = as[mt * 8 * kLD + kk];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) b[nt] = xs[(nt * 8 + gq) * kLD + kk];
+      for (int nt = 0; nt < 4; ++nt) b[nt] = xs[nt * 8 * kLD + kk];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -207,13 +232,13 @@ __global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
   // epilogue: D[row][col] with row = gq, cols = 2 tq, 2 tq + 1 of each tile
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
-    const int row = m0 + (warp * MT + mt) * 8 + gq;
+    const int row = m0 + wm * WM + mt * 8 + gq;
     if (row >= g.M) continue;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = nt * 8 + 2 * tq + h;
+        const int c = wn * 32 + nt * 8 + 2 * tq + h;
         double* y = yout[c];
         if (!y) continue;
         const double v = alph[c] * acc[mt][nt][h];
@@ -223,30 +248,46 @@ __global__ void __launch_bounds__(kThreads) gemm_cols_kernel(Args g) {
   }
 }
 
-template <int BM>
-constexpr size_t smem_bytes() { return sizeof(double) * 2 * (BM + kBN) * kLD; }
+template <int BM, int BN, int WM>
+inline cudaError_t launch(const Args& a, int64_t max_cols, int batches, cudaStream_t st) {
+  using C = Cfg<BM, BN, WM>;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(gemm_cols_kernel<BM, BN, WM>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((max_cols + BN - 1) / BN),
+                  (unsigned)batches);
+  gemm_cols_kernel<BM, BN, WM><<<grid, C::kThreads, C::kSmem, st>>>(a);
+  return cudaGetLastError();
+}
 
-// host launcher: grid = (M tiles, column tiles, batches)
+// host launcher: grid = (M tiles, column tiles, batches).  The tile is the
+// largest that still puts two CTAs' worth of work on every SM (148 SMs): the
+// FMM's launches range from a few hundred columns (one level's parents, one
+// offset's V pairs) to millions, and a small launch on big tiles leaves most
+// SMs idle (measured: 48 CTAs for a config-3 M2L factor at 128 x 128)
 inline cudaError_t gemm_cols(const Args& a, int64_t max_cols_per_batch, int batches, cudaStream_t st) {
   if (max_cols_per_batch <= 0 || batches <= 0 || a.M <= 0) return cudaSuccess;
   if (a.S < 1 || a.S > kMaxSeg) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_cols_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_bytes<32>());
-    cudaFuncSetAttribute(gemm_cols_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_bytes<64>());
-    attr = true;
+  auto ctas = [&](int bm, int bn) {
+    return (int64_t)((a.M + bm - 1) / bm) * ((max_cols_per_batch + bn - 1) / bn) * batches;
+  };
+  const int64_t want = 2 * 148;
+  if (a.M > 64) {
+    if (ctas(128, 128) >= want) return launch<128, 128, 32>(a, max_cols_per_batch, batches, st);
+    if (ctas(128, 64) >= want) return launch<128, 64, 32>(a, max_cols_per_batch, batches, st);
+    return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
   }
-  const unsigned gy = (unsigned)((max_cols_per_batch + kBN - 1) / kBN);
-  if (a.M <= 32) {
-    gemm_cols_kernel<32><<<dim3((unsigned)((a.M + 31) / 32), gy, (unsigned)batches), kThreads,
-                           smem_bytes<32>(), st>>>(a);
-  } else {
-    gemm_cols_kernel<64><<<dim3((unsigned)((a.M + 63) / 64), gy, (unsigned)batches), kThreads,
-                           smem_bytes<64>(), st>>>(a);
+  if (a.M > 32) {
+    if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
+    return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
   }
-  return cudaGetLastError();
+  if (ctas(32, 128) >= want) return launch<32, 128, 32>(a, max_cols_per_batch, batches, st);
+  return launch<32, 64, 16>(a, max_cols_per_batch, batches, st);
 }
 
 }  // namespace dg

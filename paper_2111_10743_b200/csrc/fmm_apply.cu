@@ -26,6 +26,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
+#include <climits>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -38,6 +40,7 @@
 #include "dgemm_cols.cuh"
 #include "fmm_plan.h"
 #include "lb_common.cuh"
+#include "m2l_fused.cuh"
 #include "ozaki.cuh"
 #include "p2p_core.cuh"
 
@@ -344,6 +347,39 @@ __global__ void __launch_bounds__(256) grid_tensor_kernel(const int64_t* __restr
 
 // ---------------------------------------------------------------------------
 // M2L staging
+
+// sources outside the owned range zeroed (the P2M input of a rank's upward pass)
+__global__ void mask_sources_kernel(const double* __restrict__ cs, const double* __restrict__ vs,
+                                    const uint8_t* __restrict__ own, int64_t ns, int nd,
+                                    double* __restrict__ cs_own, double* __restrict__ vs_own) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= ns) return;
+  const double m = own[p] ? 1.0 : 0.0;
+  for (int l = 0; l < nd; ++l) {
+    cs_own[(int64_t)l * ns + p] = m * cs[(int64_t)l * ns + p];
+    for (int k = 0; k < 3; ++k) vs_own[((int64_t)l * ns + p) * 3 + k] = m * vs[((int64_t)l * ns + p) * 3 + k];
+  }
+}
+
+// surface M2M, second half: up[parent, l] += sum over its children (octant
+// order, fmm.py:853-871) of the staged m2m[octant] @ up[child, l]
+__global__ void m2m_sum_kernel(const double* __restrict__ Y, const int64_t* __restrict__ child8,
+                               const int64_t* __restrict__ parents, int64_t np, int nd, int nrep,
+                               double* __restrict__ up) {
+  const int64_t pl = blockIdx.x;
+  if (pl >= np * nd) return;
+  const int64_t p = pl / nd;
+  const int l = (int)(pl % nd);
+  const int64_t* ch = child8 + 8 * p;
+  double* u = up + (parents[p] * nd + l) * (int64_t)nrep;
+  for (int i = threadIdx.x; i < nrep; i += blockDim.x) {
+    double acc = u[i];
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if (ch[o] >= 0) acc += Y[(ch[o] * nd + l) * (int64_t)nrep + i];
+    u[i] = acc;
+  }
+}
 
 // per unique target t of the chunk: dc[t,l,i] += sum over its pairs (fixed
 // order) of Y[(pi-p0)*nd+l, perm[off(pi), i]]
@@ -1013,6 +1049,19 @@ int build_device(lb_fmm_plan* P) {
   auto owned = [&](int64_t b) { return own_pref[t.tgt_hi[b]] - own_pref[t.tgt_lo[b]]; };
   std::vector<uint8_t> own_id(nb);
   for (int64_t b = 0; b < nb; ++b) own_id[b] = owned(b) > 0 ? 1 : 0;
+  // owned sources (lb_fmm_plan_set_source_range): a rank's upward pass (P2M
+  // + M2M) covers only its own sources; the partial expansions are summed
+  // across the ranks by the upward hook before the M2L
+  const bool src_range = P->own_s1 >= 0;
+  std::vector<int64_t> sown_pref(t.ns + 1, 0);
+  std::vector<uint8_t> src_own(src_range ? t.ns : 0);
+  for (int64_t q = 0; q < t.ns; ++q) {
+    const int64_t o = t.src_sorted[q];
+    const bool mine = !src_range || (o >= P->own_s0 && o < P->own_s1);
+    if (src_range) src_own[q] = mine ? 1 : 0;
+    sown_pref[q + 1] = sown_pref[q] + (mine ? 1 : 0);
+  }
+  auto nsrc_own = [&](int64_t b) { return sown_pref[t.src_hi[b]] - sown_pref[t.src_lo[b]]; };
   const bool dev_tree = P->tdev.spos != nullptr;
   std::vector<double> ctr(3 * nb), hf(nb), spos_s(dev_tree ? 0 : 3 * t.ns), tpos_s(dev_tree ? 0 : 3 * t.nt);
   std::vector<int64_t> bsrc(2 * nb), btgt(2 * nb), octant(nb, 0);
@@ -1102,9 +1151,10 @@ int build_device(lb_fmm_plan* P) {
   // P2M leaves (fmm.py:826) and M2M / L2L groups per (level, octant)
   std::vector<int64_t> p2m;
   for (int64_t b = 0; b < nb; ++b)
-    if (t.is_leaf[b] && t.src_hi[b] > t.src_lo[b]) p2m.push_back(S[b]);
+    if (t.is_leaf[b] && t.src_hi[b] > t.src_lo[b] && nsrc_own(b) > 0) p2m.push_back(S[b]);
   D.n_p2m = (int64_t)p2m.size();
   LB_TRY(upload(&D.p2m_leaves, p2m));
+  if (src_range) LB_TRY(upload(&D.src_own, src_own));
   std::vector<int64_t> uc, upar, dch, dpar, mpar, mch8;
   D.up_off.assign(1, 0);
   D.dn_off.assign(1, 0);
@@ -1112,26 +1162,6 @@ int build_device(lb_fmm_plan* P) {
   {  // buckets per (level, octant), boxes in ascending id within a level
     std::vector<std::vector<int64_t>> bu(8), bd(8);
     for (int l = 0; l < t.nlev; ++l) {
-      if (l > 0) {  // surface M2M: this level's parents (slots ascending), 8 child slots each
-        std::map<int64_t, int64_t> row;
-        for (int64_t b : t.levels[l]) {
-          const int64_t p = t.parent[b];
-          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) row.emplace(S[p], 0);
-        }
-        int64_t i = 0;
-        for (auto& kv : row) {
-          kv.second = i++;
-          mpar.push_back(kv.first);
-        }
-        const size_t base = mch8.size();
-        mch8.resize(base + 8 * row.size(), -1);
-        for (int64_t b : t.levels[l]) {
-          const int64_t p = t.parent[b];
-          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0)
-            mch8[base + 8 * row[S[p]] + octant[S[b]]] = S[b];
-        }
-      }
-      D.up_par_off.push_back((int64_t)mpar.size());
       for (auto& v : bu) v.clear();
       for (auto& v : bd) v.clear();
       if (l > 0)
@@ -1139,13 +1169,15 @@ int build_device(lb_fmm_plan* P) {
           const int64_t s = S[b];
           const int oct = (int)octant[s];
           const int64_t p = t.parent[b];
-          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0) bu[oct].push_back(b);  // fmm.py:855-859
+          // fmm.py:855-859 (with a source range: subtrees holding owned sources)
+          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0 && nsrc_own(b) > 0) bu[oct].push_back(b);
           // fmm.py:923-935 passes down to every child; children without targets
           // in their subtree never reach an L2T or a leaf, so they are skipped
           // (the results at the targets are unchanged; a plan whose targets are
           // one rank's rows skips most of the downward pass)
           if (own_id[b]) bd[oct].push_back(b);
         }
+      const int64_t ubase = (int64_t)uc.size();
       for (int oct = 0; oct < 8; ++oct) {
         for (int64_t b : bu[oct]) {
           uc.push_back(S[b]);
@@ -1158,6 +1190,20 @@ int build_device(lb_fmm_plan* P) {
         D.up_off.push_back((int64_t)uc.size());
         D.dn_off.push_back((int64_t)dch.size());
       }
+      // surface M2M sum: this level's parents (slots ascending), each with the
+      // positions of its children in the level's child list, octant order
+      std::map<int64_t, int64_t> row;
+      for (int64_t i = ubase; i < (int64_t)uc.size(); ++i) row.emplace(upar[i], 0);
+      int64_t r = 0;
+      for (auto& kv : row) {
+        kv.second = r++;
+        mpar.push_back(kv.first);
+      }
+      const size_t base = mch8.size();
+      mch8.resize(base + 8 * row.size(), -1);
+      for (int64_t i = ubase; i < (int64_t)uc.size(); ++i)
+        mch8[base + 8 * row[upar[i]] + octant[uc[i]]] = i - ubase;
+      D.up_par_off.push_back((int64_t)mpar.size());  // parents of level l's children
     }
   }
   LB_TRY(upload(&D.up_child, uc));
@@ -1167,6 +1213,7 @@ int build_device(lb_fmm_plan* P) {
   LB_TRY(upload(&D.up_par, mpar));
   LB_TRY(upload(&D.up_child8, mch8));
   LB_TRY(upload(&D.dn_off_dev, D.dn_off));
+  LB_TRY(upload(&D.up_off_dev, D.up_off));
   mark("m2m/l2l");
   // M2L pairs grouped by canonical key, each group in target-slot order (the
   // walk below visits targets in slot order, so no sort is needed).  Lattice
@@ -1397,13 +1444,15 @@ int ensure_work(lb_fmm_plan* P, int nd) {
   nd = std::max(nd, std::min(4, 2 * std::max(D.nd_alloc, 1)));
   if (D.loc != D.dc) cudaFree(D.loc);  // grid: loc aliases dc
   cudaFree(D.cs); cudaFree(D.vs); cudaFree(D.up); cudaFree(D.dc);
+  cudaFree(D.cs_own); cudaFree(D.vs_own);
+  D.cs_own = D.vs_own = nullptr;
   cudaFree(D.tmpA); cudaFree(D.tmpB); cudaFree(D.tout);
   D.cs = D.vs = D.up = D.dc = D.loc = D.tmpA = D.tmpB = D.tout = nullptr;
   const FmmTree& t = P->tree;
   const int64_t nb = t.nbox(), nrep = P->nrep;
   // GEMM staging: the largest of (P2M leaves, any level/octant group, M2L chunk)
   int64_t cols = std::max<int64_t>(D.n_p2m, 1);
-  for (size_t i = 0; i + 1 < D.up_off.size(); ++i) cols = std::max(cols, D.up_off[i + 1] - D.up_off[i]);
+  for (size_t i = 0; i + 8 < D.up_off.size(); i += 8) cols = std::max(cols, D.up_off[i + 8] - D.up_off[i]);
   for (size_t i = 0; i + 1 < D.dn_off.size(); ++i) cols = std::max(cols, D.dn_off[i + 1] - D.dn_off[i]);
   const int64_t m2l_cap = std::max<int64_t>(1, std::min<int64_t>(D.max_key_pairs, (int64_t)1 << 17));
   cols = std::max(cols, m2l_cap);
@@ -1412,6 +1461,10 @@ int ensure_work(lb_fmm_plan* P, int nd) {
   auto A = [&](double** p, int64_t n) { if (e == cudaSuccess) e = cudaMalloc((void**)p, std::max<int64_t>(n, 2) * 8); };
   A(&D.cs, (int64_t)nd * t.ns);
   A(&D.vs, (int64_t)nd * t.ns * 3);
+  if (D.src_own) {
+    A(&D.cs_own, (int64_t)nd * t.ns);
+    A(&D.vs_own, (int64_t)nd * t.ns * 3);
+  }
   A(&D.up, nb * nd * nrep);
   A(&D.dc, nb * nd * nrep);
   if (P->rep == 0) A(&D.loc, nb * nd * nrep);
@@ -1481,11 +1534,114 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     LB_CUDA(cudaMalloc((void**)&D.lr_b, sizeof(double) * std::max<size_t>(P->lr_b_host.size(), 1)));
     LB_CUDA(cudaMemcpy(D.lr_a, P->lr_a_host.data(), sizeof(double) * P->lr_a_host.size(), cudaMemcpyHostToDevice));
     LB_CUDA(cudaMemcpy(D.lr_b, P->lr_b_host.data(), sizeof(double) * P->lr_b_host.size(), cudaMemcpyHostToDevice));
+    D.lo_ready = false;
   }
-  int rmax = 1;
-  for (int r : P->lr_rank) rmax = std::max(rmax, r);
-  const int64_t need = (int64_t)rmax * D.tmp_cols * nd;
+  const int nk = P->ncanon, nrep = P->nrep;
+  if (!D.lo_ready) {
+    // pair arrays back on the host once (the device plan build leaves them on the device)
+    const int64_t np = D.v_key_pair_off[nk];
+    std::vector<int64_t> vsrc(np);
+    std::vector<int32_t> voff(np);
+    std::vector<double> vsc(np);
+    if (np) {
+      LB_CUDA(cudaMemcpy(vsrc.data(), D.v_src, 8 * np, cudaMemcpyDeviceToHost));
+      LB_CUDA(cudaMemcpy(voff.data(), D.v_off_idx, 4 * np, cudaMemcpyDeviceToHost));
+      LB_CUDA(cudaMemcpy(vsc.data(), D.v_scale, 8 * np, cudaMemcpyDeviceToHost));
+    }
+    // B_k P_d for every offset d: T = B_k x[perm_inv] = (B_k[:, perm]) x
+    std::vector<int64_t> bp_off(P->noff + 1, 0);
+    for (int d = 0; d < P->noff; ++d) bp_off[d + 1] = bp_off[d] + (int64_t)P->lr_rank[P->off_key[d]] * nrep;
+    std::vector<double> bp(std::max<int64_t>(bp_off.back(), 1));
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int d = 0; d < P->noff; ++d) {
+      const int k = P->off_key[d], r = P->lr_rank[k];
+      const double* B = P->lr_b_host.data() + P->lr_off[k] * nrep;
+      const int32_t* pm = P->off_perm.data() + (int64_t)d * nrep;
+      double* o = bp.data() + bp_off[d];
+      for (int a = 0; a < r; ++a)
+        for (int j = 0; j < nrep; ++j) o[(int64_t)a * nrep + j] = B[(int64_t)a * nrep + pm[j]];
+    }
+    // every key's pairs by offset (stable): the first factor's batches
+    std::vector<int64_t> lsrc(np), ltcol(np), boff, aoff;
+    std::vector<double> lsc(np);
+    D.lo_key_batch.assign(nk + 1, 0);
+    D.lo_key_maxgrp.assign(nk, 0);
+    std::vector<int64_t> cnt(P->noff);
+    for (int k = 0; k < nk; ++k) {
+      const int64_t p0 = D.v_key_pair_off[k], p1 = D.v_key_pair_off[k + 1];
+      D.lo_key_batch[k] = (int64_t)boff.size();
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (int64_t i = p0; i < p1; ++i) ++cnt[voff[i]];
+      std::vector<int64_t> at(P->noff);
+      int64_t pos = p0;
+      for (int d = 0; d < P->noff; ++d) {
+        at[d] = pos;
+        if (cnt[d]) {
+          boff.push_back(pos);
+          aoff.push_back(bp_off[d]);
+          D.lo_key_maxgrp[k] = std::max(D.lo_key_maxgrp[k], cnt[d]);
+        }
+        pos += cnt[d];
+      }
+      boff.push_back(p1);
+      aoff.push_back(0);  // keeps aoff aligned with boff (nbatch + 1 entries per key)
+      for (int64_t i = p0; i < p1; ++i) {
+        const int64_t j = at[voff[i]]++;
+        lsrc[j] = vsrc[i];
+        ltcol[j] = i - p0;
+        lsc[j] = vsc[i];
+      }
+    }
+    D.lo_key_batch[nk] = (int64_t)boff.size();
+
+    cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
+    cudaFree(D.lo_boff); cudaFree(D.lo_aoff);
+    D.lr_bp = D.lo_scale = nullptr;
+    D.lo_src = D.lo_tcol = D.lo_boff = D.lo_aoff = nullptr;
+    LB_TRY(upload(&D.lr_bp, bp));
+    LB_TRY(upload(&D.lo_src, lsrc));
+    LB_TRY(upload(&D.lo_tcol, ltcol));
+    LB_TRY(upload(&D.lo_scale, lsc));
+    LB_TRY(upload(&D.lo_boff, boff));
+    LB_TRY(upload(&D.lo_aoff, aoff));
+    for (int i = 0; i < 5; ++i) {
+      cudaFree(D.lo_units[i]);
+      D.lo_units[i] = nullptr;
+    }
+    D.lo_ready = true;
+  }
+  if (nd < 1 || nd > 4) return fail(LB_ERR_ARG, "fmm: density chunk outside [1, 4]");
+  if (!D.lo_units[nd]) {  // units of whole target groups, <= one pass of columns where possible
+    std::vector<int64_t> units;
+    std::vector<int64_t>& ku = D.lo_key_units[nd];
+    ku.assign(nk + 1, 0);
+    for (int k = 0; k < nk; ++k) {
+      ku[k] = (int64_t)(units.size() / 2);
+      const int64_t g0 = D.v_key_tgt_off[k], g1 = D.v_key_tgt_off[k + 1];
+      int64_t ub = g0, cols = 0;
+      for (int64_t gi = g0; gi < g1; ++gi) {
+        const int64_t c = (D.v_tpoff_host[gi + 1] - D.v_tpoff_host[gi]) * nd;
+        if (gi > ub && cols + c > m2lf::kCols) {
+          units.push_back(ub);
+          units.push_back(gi);
+          ub = gi;
+          cols = 0;
+        }
+        cols += c;
+      }
+      if (g1 > ub) {
+        units.push_back(ub);
+        units.push_back(g1);
+      }
+    }
+    ku[nk] = (int64_t)(units.size() / 2);
+    LB_TRY(upload(&D.lo_units[nd], units));
+  }
+  int64_t need = 1;
+  for (int k = 0; k < nk; ++k)
+    need = std::max(need, (D.v_key_pair_off[k + 1] - D.v_key_pair_off[k]) * nd * P->lr_rank[k]);
   if (D.lr_t_cap < need) {
+
     cudaFree(D.lr_t);
     D.lr_t = nullptr;
     LB_CUDA(cudaMalloc((void**)&D.lr_t, sizeof(double) * need));
@@ -1516,11 +1672,21 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   }
   LB_CUDA(cudaMemsetAsync(D.up, 0, sizeof(double) * nb * ND * nrep, st));
   LB_CUDA(cudaMemsetAsync(D.dc, 0, sizeof(double) * nb * ND * nrep, st));
+  // P2M reads the owned sources only when a source range is set
+  const double* p2m_cs = D.cs;
+  const double* p2m_vs = D.vs;
+  if (D.src_own && t.ns > 0) {
+    mask_sources_kernel<<<(unsigned)ceil_div(t.ns, 256), 256, 0, st>>>(D.cs, D.vs, D.src_own, t.ns, ND,
+                                                                       D.cs_own, D.vs_own);
+    LB_CHECK_LAUNCH();
+    p2m_cs = D.cs_own;
+    p2m_vs = D.vs_own;
+  }
   // ---- P2M (fmm.py:823-852)
   if (D.n_p2m > 0) {
     if (surface) {
       LB_TRY(launch_lattice<ND>((unsigned)D.n_p2m, st, D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf,
-                                D.bsrc, D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1,
+                                D.bsrc, D.spos, p2m_cs, p2m_vs, t.ns, hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1,
                                 D.tmpA, 0, 0));
       // upward[b] = pinv_up @ (h phi) straight into the leaves' slots (fmm.py:852)
       dg::Args a{};
@@ -1530,7 +1696,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       LB_DG(dg::gemm_cols(a, D.n_p2m * ND, 1, st));
     } else {
       p2m_grid_kernel<ND><<<(unsigned)D.n_p2m, 256, 0, st>>>(D.p2m_leaves, D.bctr, D.bhalf, D.bsrc,
-                                                             D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, n,
+                                                             D.spos, p2m_cs, p2m_vs, t.ns, hd ? 1 : 0, n,
                                                              D.vinv, D.up);
       LB_CHECK_LAUNCH();
     }
@@ -1540,15 +1706,24 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   const size_t grid_smem = sizeof(double) * 2 * nrep;
   for (int l = t.nlev - 1; l >= 1; --l) {
     if (surface) {
-      // every parent of level l-1 sums its children's m2m[octant] @ up[child]
-      // in octant order: the 8 operators are 8 K-segments of one GEMM
-      const int64_t p0 = D.up_par_off[l], p1 = D.up_par_off[l + 1];
-      if (p1 > p0) {
+      // children of level l: m2m[octant] @ up[child] in 8 octant batches into
+      // the staging, then every parent sums its children in octant order
+      // (fmm.py:853-871; deterministic, no atomics)
+      const int64_t u0 = D.up_off[8 * l], u1 = D.up_off[8 * l + 8];
+      if (u1 > u0) {
+        int64_t mx = 0;
+        for (int oct = 0; oct < 8; ++oct) mx = std::max(mx, D.up_off[8 * l + oct + 1] - D.up_off[8 * l + oct]);
         dg::Args a{};
-        a.A = D.m2m_oct; a.a_seg = (int64_t)nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
-        a.S = 8; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.up_child8 + 8 * p0;
-        a.Y = D.up; a.ldy = nrep; a.out = D.up_par + p0; a.alpha = 1.0; a.add = 1; a.nq = p1 - p0;
-        LB_DG(dg::gemm_cols(a, (p1 - p0) * ND, 1, st));
+        a.A = D.m2m_oct; a.a_batch = (int64_t)nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
+        a.S = 1; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.up_child + u0; a.Y = D.tmpB; a.ldy = nrep;
+        a.alpha = 1.0; a.add = 0; a.boff = D.up_off_dev + 8 * l;
+        LB_DG(dg::gemm_cols(a, mx * ND, 8, st));
+        const int64_t p0 = D.up_par_off[l], p1 = D.up_par_off[l + 1];
+        if (p1 > p0) {
+          m2m_sum_kernel<<<(unsigned)((p1 - p0) * ND), 128, 0, st>>>(D.tmpB, D.up_child8 + 8 * p0, D.up_par + p0,
+                                                                     p1 - p0, ND, nrep, D.up);
+          LB_CHECK_LAUNCH();
+        }
       }
       continue;
     }
@@ -1564,12 +1739,43 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     }
   }
   mark(2);
+  // a sharded apply sums the ranks' partial upward expansions here (the hook
+  // enqueues the all-reduce on this stream, lb_fmm_plan_set_upward_hook)
+  if (P->up_hook) P->up_hook(P->up_hook_user, D.up, nb * ND * (int64_t)nrep, ND, (void*)st);
   // ---- M2L (fmm.py:873-886), by canonical key, chunked at target boundaries
   if (P->m2l_slices < 0) LB_TRY(ensure_lowrank(P, ND));
   else LB_TRY(ensure_oz(P, ND, st));
+  // M2L: low-rank fused per key (default) or staged (the A/B probe switch)
+  static const int m2l_mode = [] {  // LB_M2L_MODE=staged
+    const char* e = std::getenv("LB_M2L_MODE");
+    return (e && std::string(e) == "staged") ? 2 : 0;
+  }();
   for (int k = 0; k < P->ncanon; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
     if (pe == pb) continue;
+    const bool no_fuse = m2l_mode == 2;
+    if (P->m2l_slices < 0 && P->lr_rank[k] <= 4 * m2lf::kMaxKS && !no_fuse &&
+        nrep <= m2lf::kMaxIt * m2lf::kThreads && ND <= m2lf::kMaxNd) {
+      // low-rank, fused: T = (B_k P_d) x / h for all the key's pairs (batches
+      // of one lattice offset: one permuted factor per batch, contiguous
+      // multipoles), then Y = A_k T and the permuted accumulation per unit of
+      // whole target groups, Y kept in shared memory
+      const int r = P->lr_rank[k];
+      const int64_t kb = D.lo_key_batch[k];
+      const int nbatch = (int)(D.lo_key_batch[k + 1] - kb - 1);
+      dg::Args a{};
+      a.A = D.lr_bp; a.a_off = D.lo_aoff + kb; a.lda = nrep; a.M = r; a.K = nrep; a.S = 1; a.nd = ND;
+      a.X = D.up; a.ldx = nrep; a.in = D.lo_src + pb; a.alpha_q = D.lo_scale + pb; a.alpha = 1.0;
+      a.Y = D.lr_t; a.ldy = r; a.out = D.lo_tcol + pb; a.add = 0; a.boff = D.lo_boff + kb;
+      LB_DG(dg::gemm_cols(a, D.lo_key_maxgrp[k] * ND, nbatch, st));
+      m2lf::Args f{};
+      f.A = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND; f.T = D.lr_t;
+      const std::vector<int64_t>& ku = D.lo_key_units[ND];
+      f.units = D.lo_units[ND] + 2 * ku[k]; f.vtgts = D.v_tgts; f.tpair = D.v_tgt_pair_off;
+      f.voff = D.v_off_idx; f.perm = D.perm; f.p0 = pb; f.dc = D.dc;
+      LB_DG(m2lf::launch(f, ku[k + 1] - ku[k], st));
+      continue;
+    }
     const std::vector<int64_t> tp(D.v_tpoff_host.begin() + D.v_key_tgt_off[k],
                                   D.v_tpoff_host.begin() + D.v_key_tgt_off[k + 1] + 1);
     int64_t ti = 0;
@@ -1638,8 +1844,9 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       if (mx > 0) {
         dg::Args a{};
         a.A = D.l2l_oct; a.a_batch = (int64_t)nrep * nrep; a.lda = nrep; a.M = nrep; a.K = nrep;
-        a.S = 1; a.nd = ND; a.X = D.loc; a.ldx = nrep; a.in = D.dn_parent; a.Y = D.dc; a.ldy = nrep;
-        a.out = D.dn_child; a.alpha = 1.0 / hc; a.add = 1; a.boff = D.dn_off_dev + 8 * (l + 1);
+        const int64_t d0 = D.dn_off[8 * (l + 1)];
+        a.S = 1; a.nd = ND; a.X = D.loc; a.ldx = nrep; a.in = D.dn_parent + d0; a.Y = D.dc; a.ldy = nrep;
+        a.out = D.dn_child + d0; a.alpha = 1.0 / hc; a.add = 1; a.boff = D.dn_off_dev + 8 * (l + 1);
         LB_DG(dg::gemm_cols(a, mx * ND, 8, st));
       }
       continue;
@@ -1763,9 +1970,14 @@ void fmm_release_device(lb_fmm_plan* P) {
   cudaFree(D.lr_a);
   cudaFree(D.lr_b);
   cudaFree(D.lr_t);
+  cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
+  cudaFree(D.lo_boff); cudaFree(D.lo_aoff);
+  for (int i = 0; i < 5; ++i) cudaFree(D.lo_units[i]);
   cudaFree(D.oz_b);
   cudaFree(D.oz_cs);
   cudaFree(D.dn_off_dev);
+  cudaFree(D.up_off_dev);
+  cudaFree(D.src_own); cudaFree(D.cs_own); cudaFree(D.vs_own);
   cudaFree(D.up_par);
   cudaFree(D.up_child8);
   cudaFree(D.m2m_oct);
@@ -1852,6 +2064,24 @@ int lb_fmm_plan_set_target_range(lb_fmm_plan* P, int64_t t0, int64_t t1) {
   P->own_t0 = t0;
   P->own_t1 = t1;
   fmm_release_device(P);  // lists are rebuilt on the next apply
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_source_range(lb_fmm_plan* P, int64_t s0, int64_t s1) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  if (s1 >= 0 && (s0 < 0 || s0 > s1 || s1 > P->tree.ns))
+    return fail(LB_ERR_SHAPE, "lb_fmm_plan_set_source_range: range outside [0, ns]");
+  if (s0 == P->own_s0 && s1 == P->own_s1) return LB_OK;
+  P->own_s0 = s0;
+  P->own_s1 = s1;
+  fmm_release_device(P);  // P2M / M2M lists are rebuilt on the next apply
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_upward_hook(lb_fmm_plan* P, lb_fmm_upward_hook hook, void* user) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  P->up_hook = hook;
+  P->up_hook_user = user;
   return LB_OK;
 }
 

@@ -37,8 +37,10 @@ struct FmmDevice {
   int64_t *dn_child = nullptr, *dn_parent = nullptr;
   std::vector<int64_t> dn_off;
   int64_t* dn_off_dev = nullptr;             // device copy (per-octant batches of the L2L)
-  // surface M2M per level: parents (slots) with their 8 child slots in
-  // octant order (-1 = none), levels concatenated; up_par_off: host offsets
+  int64_t* up_off_dev = nullptr;             // device copy (per-octant batches of the M2M)
+  // surface M2M per level: parents (slots) with the positions of their 8
+  // children in the level's child list, octant order (-1 = none), levels
+  // concatenated; up_par_off: host offsets
   int64_t *up_par = nullptr, *up_child8 = nullptr;
   std::vector<int64_t> up_par_off;
   double *m2m_oct = nullptr, *l2l_oct = nullptr;  // surface operators in octant order
@@ -67,6 +69,8 @@ struct FmmDevice {
   int64_t leaf_part_cap = 0, part_width = -1;
   // work arrays (per nd)
   double *cs = nullptr, *vs = nullptr;       // sorted charges (nd,ns), dipoles (nd,ns,3)
+  uint8_t* src_own = nullptr;                // owned-source flags, sorted order (source range set)
+  double *cs_own = nullptr, *vs_own = nullptr;  // the P2M's masked copies
   double *up = nullptr, *dc = nullptr, *loc = nullptr;  // (nbox, nd, nrep) slot order
   double *tmpA = nullptr, *tmpB = nullptr;   // GEMM staging
   int64_t tmp_cols = 0;
@@ -89,6 +93,20 @@ struct FmmDevice {
   // A (nrep, r_k) and B (r_k, nrep) row-major, packed; staging (r_max, cols)
   double *lr_a = nullptr, *lr_b = nullptr, *lr_t = nullptr;
   int64_t lr_t_cap = 0;
+  // fused low-rank M2L (m2l_fused.cuh): B_k with its columns permuted per
+  // lattice offset (lr_bp, r_k x nrep per offset at lo_aoff), every key's
+  // pairs re-ordered by offset for the first factor (source slot, T column,
+  // 1/h; batch boundaries lo_boff per key from lo_key_batch), and the
+  // per-density-count units of whole target groups for the second
+  bool lo_ready = false;
+  double* lr_bp = nullptr;
+  int64_t *lo_src = nullptr, *lo_tcol = nullptr, *lo_boff = nullptr, *lo_aoff = nullptr;
+  double* lo_scale = nullptr;
+  std::vector<int64_t> lo_key_batch, lo_key_maxgrp;    // per key: first batch entry, largest batch
+  // per density count nd (1..4): units (2 x int64 target-group ranges) and
+  // each key's first unit; built once per nd, so an apply never allocates
+  int64_t* lo_units[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<int64_t> lo_key_units[5];
 };
 
 // device arrays kept from the device tree build (fmm_tree_dev.cu): the
@@ -125,6 +143,9 @@ struct lb_fmm_plan {
   double setup_ms[4] = {0, 0, 0, 0};        // keys+sort, tree, lists, device state (host ms)
   bool timing = false;
   int64_t own_t0 = 0, own_t1 = -1;          // owned targets [t0, t1) (original order); t1 < 0: all
+  int64_t own_s0 = 0, own_s1 = -1;          // owned sources [s0, s1) of the upward pass; s1 < 0: all
+  lb_fmm_upward_hook up_hook = nullptr;     // sums the ranks' partial upward expansions
+  void* up_hook_user = nullptr;
   int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices;
                                             // -1: low-rank factors (fp64 DGEMM pair)
   std::vector<int32_t> lr_rank;             // per canonical key

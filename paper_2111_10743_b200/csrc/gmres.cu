@@ -143,7 +143,10 @@ namespace {
 // persistent reduction scratch, one pool per (device, stream): the grid
 // reductions count finished CTAs on a ticket, so two reductions in flight on
 // different streams (or devices) must never share partials or tickets.
-// Calls on ONE stream are ordered by the stream and may share a pool.
+// Calls on ONE stream are ordered by the stream and share its pool.  A stream
+// being captured into a CUDA graph cannot allocate: it borrows the pool of
+// the device's first stream (a captured graph replays on its own stream, and
+// replays of graphs that share a pool must not overlap).
 struct RedPool {
   double* partials = nullptr;
   unsigned* ticket = nullptr;
@@ -153,10 +156,21 @@ struct RedPool {
 int get_pool(RedBufs* rb, int blocks, cudaStream_t st) {
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, RedPool> pools;
+  static std::map<int, std::pair<int, cudaStream_t>> first;
   int dev = 0;
   LB_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  RedPool& pool = pools[{dev, st}];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  LB_CUDA(cudaStreamIsCapturing(st, &cs));
+  auto key = std::make_pair(dev, st);
+  if (cs != cudaStreamCaptureStatusNone && !pools.count(key)) {
+    auto f = first.find(dev);
+    if (f == first.end() || pools[f->second].cap < blocks)
+      return fail(LB_ERR_CUDA, "reduction scratch: run one reduction on this device before capturing a graph");
+    key = f->second;
+  }
+  RedPool& pool = pools[key];
+  if (!first.count(dev)) first[dev] = key;
   if (pool.cap < blocks) {
     if (pool.partials) cudaFree(pool.partials);
     if (pool.ticket) cudaFree(pool.ticket);

@@ -320,6 +320,7 @@ struct EpiA1p2 : EpiBase {
 template <int J, class E, class Mix = MixId<J>>
 __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
                                                          const int32_t* __restrict__ indices,
+                                                         const int32_t* __restrict__ bstart, int bnb,
                                                          int64_t grow0, int64_t nrows, int wpr,
                                                          CsrJobs<J> jobs, E epi, double* partials,
                                                          unsigned* ticket, double* red_out,
@@ -369,10 +370,21 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
     const int64_t stride = 32 * wpr;
     int64_t k = kb + seg * 32 + lane;
     constexpr int K = Mix::K, X = Mix::X;
+    // column of entry k: the block-CSR index (one int32 start per block of
+    // nb consecutive columns, quadrature.py:693-700: 4/nb bytes per entry)
+    // when the handle has one, else the scalar index (4 bytes per entry)
+    const double inv_nb = bstart ? 1.0 / bnb : 0.0;
+    auto col = [&](int64_t kk) -> int {
+      if (!bstart) return __ldg(indices + kk);
+      int64_t b = (int64_t)((double)kk * inv_nb);
+      b += (b + 1) * bnb <= kk ? 1 : 0;
+      b -= b * bnb > kk ? 1 : 0;
+      return __ldg(bstart + b) + (int)(kk - b * bnb);
+    };
     for (; k + 3 * stride < ke; k += 4 * stride) {
       int c[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = __ldg(indices + k + stride * u);
+      for (int u = 0; u < 4; ++u) c[u] = col(k + stride * u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         double v[K], xv[X];
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
       }
     }
     for (; k < ke; k += stride) {
-      const int c = __ldg(indices + k);
+      const int c = col(k);
       double v[K], xv[X];
 #pragma unroll
       for (int q = 0; q < K; ++q) v[q] = __ldg(jobs.val[q] + k);
@@ -454,6 +466,8 @@ struct lb_opset {
   bool fmm_a3_two = true;  // FMM path: A3's second call on 2 densities (lb_opset_set_fmm_a3)
   int csr_blocks = 0;
   int csr_wpr = 1;
+  int32_t* bstart = nullptr;  // block-CSR index: first column of every nb-block (nullptr: scalar)
+  int bnb = 0;
   // optional FMM far field (lb_opset_set_fmm) and its scratch
   lb_fmm_plan* fmm = nullptr;
   bool timing = false;
@@ -559,7 +573,7 @@ int run_csr(const lb_opset* h, const double* const* vals, const double* const* x
     jobs.x[Mix::xi(j)] = xs[j];
   }
   csr_epi_kernel<J, E, Mix><<<(unsigned)h->csr_blocks, kCsrBT, 0, st>>>(
-      h->d.indptr, h->d.indices, h->r0, h->nr, h->csr_wpr, jobs, epi, h->partials, h->ticket,
+      h->d.indptr, h->d.indices, h->bstart, h->bnb, h->r0, h->nr, h->csr_wpr, jobs, epi, h->partials, h->ticket,
       h->scal, red_div);
   LB_CHECK_LAUNCH();
   return LB_OK;
@@ -931,12 +945,65 @@ int apply_layer(lb_opset* h, int kind, const double* tau, double* out, cudaStrea
   return run_csr<1>(h, vals, xs, e, st);
 }
 
+// block-CSR index (quadrature.py:693-700: every row is |Near| blocks of nb
+// consecutive columns, so one int32 per block carries the pattern): built
+// and verified on the device; any row or block that breaks the structure
+// (a caller's own CSR) leaves the scalar index in use
+__global__ void block_index_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                   int64_t r0, int64_t nr, int nb, int32_t* __restrict__ bstart,
+                                   int* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  const int64_t kb = indptr[r0 + i], ke = indptr[r0 + i + 1];
+  if (kb % nb || ke % nb) {
+    *bad = 1;
+    return;
+  }
+  for (int64_t b = kb / nb; b < ke / nb; ++b) {
+    const int32_t c0 = indices[b * nb];
+    bstart[b] = c0;
+    for (int j = 1; j < nb; ++j)
+      if (indices[b * nb + j] != c0 + j) *bad = 1;
+  }
+}
+
+int build_block_index(lb_opset* h) {
+  const int nb = h->d.nb;
+  const int64_t nnz = h->d.nnz;
+  if (nb <= 1 || nnz <= 0 || nnz % nb) return LB_OK;
+  int* bad = nullptr;
+  cudaError_t e = cudaMalloc((void**)&h->bstart, sizeof(int32_t) * (nnz / nb));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&bad, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(bad, 0, sizeof(int));
+  if (e == cudaSuccess && h->nr > 0) {
+    block_index_kernel<<<(unsigned)ceil_div(h->nr, 128), 128>>>(h->d.indptr, h->d.indices, h->r0, h->nr, nb,
+                                                                  h->bstart, bad);
+    e = cudaGetLastError();
+  }
+  int hbad = 1;
+  if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  if (e != cudaSuccess) {
+    cudaFree(h->bstart);
+    h->bstart = nullptr;
+    return fail(LB_ERR_CUDA, std::string("lb_opset_create: block index: ") + cudaGetErrorString(e));
+  }
+  if (hbad) {
+    cudaFree(h->bstart);
+    h->bstart = nullptr;
+  } else {
+    h->bnb = nb;
+  }
+  return LB_OK;
+}
+
 }  // namespace
 }  // namespace lb
 
 extern "C" {
 
 int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
+  using lb::build_block_index;
   using namespace lb;
   if (!d || !out) return fail(LB_ERR_ARG, "lb_opset_create: null argument");
   *out = nullptr;
@@ -1001,12 +1068,14 @@ int lb_opset_create(const lb_opset_desc* d, lb_opset** out) {
     lb_opset_destroy(h);
     return fail(LB_ERR_CUDA, std::string("lb_opset_create: ") + cudaGetErrorString(e));
   }
+  LB_TRY(build_block_index(h));
   *out = h;
   return LB_OK;
 }
 
 int lb_opset_destroy(lb_opset* h) {
   if (!h) return LB_OK;
+  cudaFree(h->bstart);
   cudaFree(h->pack4);
   cudaFree(h->pack6);
   cudaFree(h->pack8);
@@ -1237,7 +1306,7 @@ int lb_csr_spmv(const int64_t* indptr, const int32_t* indices, int64_t nrows, in
       epi.y[j] = ys[j];                                                                     \
     }                                                                                       \
     epi.accumulate = accumulate;                                                            \
-    csr_epi_kernel<J, EpiStore<J>, MixId<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, 0, nrows, wpr, jobs, \
+    csr_epi_kernel<J, EpiStore<J>, MixId<J>><<<blocks, kCsrBT, 0, st>>>(indptr, indices, nullptr, 0, 0, nrows, wpr, jobs, \
                                                               epi, nullptr, nullptr,        \
                                                               nullptr, 1.0);                \
   }

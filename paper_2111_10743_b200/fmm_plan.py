@@ -294,6 +294,8 @@ def _bind():
         L.lb_fmm_plan_set_timing.argtypes = [P, I32]
         L.lb_fmm_plan_set_m2l_factors.argtypes = [P, P, P, P]
         L.lb_fmm_plan_set_target_range.argtypes = [P, I64, I64]
+        L.lb_fmm_plan_set_source_range.argtypes = [P, I64, I64]
+        L.lb_fmm_plan_set_upward_hook.argtypes = [P, P, P]
         L.lb_fmm_stage_times.argtypes = [P, P]
         L.lb_fmm_setup_times.argtypes = [P, P]
         _bound = True
@@ -479,6 +481,34 @@ class FmmPlan:
         _lib.check(self._L.lb_fmm_plan_set_target_range(self._h, int(t0), int(t1)),
                    "lb_fmm_plan_set_target_range")
 
+    def set_source_range(self, s0: int = 0, s1: int = -1):
+        """Owned sources [s0, s1) of the upward pass (lb_fmm_plan_set_source_range;
+        s1 < 0: all): P2M + M2M cover only these, and the upward hook must sum
+        the ranks' partial expansions (a sharded apply)."""
+        _lib.check(self._L.lb_fmm_plan_set_source_range(self._h, int(s0), int(s1)),
+                   "lb_fmm_plan_set_source_range")
+
+    def set_upward_hook(self, fn):
+        """fn(up, nd, stream): called on the apply's stream between the M2M and
+        the M2L with the (nbox, nd, nrep) upward expansions as a CUDA tensor
+        view (lb_fmm_plan_set_upward_hook); None removes it."""
+        if fn is None:
+            self._hook = None
+            _lib.check(self._L.lb_fmm_plan_set_upward_hook(self._h, None, None))
+            return
+        t = _lib.torch()
+
+        def _cb(user, up, count, nd, stream):
+            try:
+                view = _device_array(up, count, t)
+                fn(view, int(nd), stream)
+            except Exception as exc:  # noqa: BLE001 - never unwind through C
+                self._hook_error = exc
+        self._hook_error = None
+        self._hook = _HOOK_T(_cb)
+        _lib.check(self._L.lb_fmm_plan_set_upward_hook(
+            self._h, ctypes.cast(self._hook, ctypes.c_void_p), None))
+
     def stage_times(self):
         """Device ms of gather+P2M, M2M, M2L, X, L2L, L2T, leaf, scatter, total."""
         ms = np.zeros(9)
@@ -592,6 +622,23 @@ class FmmPlan:
             except Exception:  # pragma: no cover
                 pass
             self._h = None
+
+
+_HOOK_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                           ctypes.c_int, ctypes.c_void_p)
+
+
+class _CudaArray:
+    """A __cuda_array_interface__ over a raw device pointer (zero copy)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def _device_array(ptr, n, t):
+    return t.as_tensor(_CudaArray(ptr, n), device="cuda")
 
 
 def _host(a):

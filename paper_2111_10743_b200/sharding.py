@@ -1,22 +1,37 @@
 """Target-sharded operator apply across GPUs.
 
-The apply shards by target rows: rank r owns a contiguous range of patches
-(rows [row0, row0 + nrows)); every far sweep still needs ALL sources, so the
-intermediate densities are all-gathered between the phases of the apply and
-the W-average is all-reduced (lb_opset_apply_phase / lb_opset_phase_exchange).
-Collectives are torch.distributed (NCCL over NVLink on the GPUs; gloo in the
-CPU tests).  GMRES stays replicated: every rank holds the full Krylov basis
-and the apply returns the full result vector (one all-gather of N doubles),
-so the Arnoldi arithmetic and its residual history are identical to a single
-GPU's.
+Partition.  Patches are put in Morton order of their centroids (the FMM's
+key: 20 bits per axis of the bounding cube, x the lowest bit, fmm.py:562-576)
+and every rank owns a contiguous run of them, balanced by the estimated work
+(correction nnz + far rows): targets are partitioned by contiguous Morton
+range, as north_star asks.  The sharded operator works on the Morton-permuted
+discretisation internally; inputs and outputs stay in the caller's order.
+
+Per rank: (i) the near-field corrections of its OWN rows only (the device
+build over a near map restricted to them: config 4's 58 GB of corrections are
+split G ways, never replicated); (ii) the far field's targets are its rows;
+(iii) with the FMM, the plan is the reference's tree over ALL sources and
+targets (deterministic, identical everywhere), the downward pass and the leaf
+stage run only where the rank has targets, and the UPWARD pass runs only over
+the rank's own sources (its patches' oversampled nodes): the partial
+multipole expansions are summed over the ranks by an all-reduce between the
+M2M and the M2L (lb_fmm_plan_set_source_range / set_upward_hook), so no rank
+repeats another's P2M + M2M.
+
+Between the apply's phases the intermediate densities are all-gathered and
+the W-average is all-reduced (lb_opset_apply_phase / lb_opset_phase_exchange),
+torch.distributed collectives: NCCL over NVLink on the GPUs, gloo in the CPU
+tests.  GMRES stays replicated: the apply returns the full result (one
+all-gather of N doubles), so every rank's Arnoldi arithmetic and residual
+history are identical to a single GPU's.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["partition_rows", "allgather_rows", "ShardedApply",
-           "ShardedOperatorSet"]
+__all__ = ["partition_rows", "allgather_rows", "morton_patch_order", "permute_geometry",
+           "ShardedApply", "ShardedOperatorSet"]
 
 
 def partition_rows(npatches: int, nb: int, world: int, cost=None):
@@ -41,6 +56,85 @@ def partition_rows(npatches: int, nb: int, world: int, cost=None):
         bounds[r] = min(max(bounds[r], bounds[r - 1] + 1), npatches - (world - r))
     return [(int(bounds[r]) * nb, int(bounds[r + 1] - bounds[r]) * nb)
             for r in range(world)]
+
+
+def morton_patch_order(nodes, nb: int):
+    """Patch order by the Morton key of the patch centroids, the FMM's key
+    function (fmm.py:562-576: 20 bits per axis of the bounding cube, bit
+    3b + axis = bit b of the axis cell, x lowest), stable on ties."""
+    c = np.asarray(nodes, dtype=float).reshape(-1, nb, 3).mean(axis=1)
+    lo, hi = c.min(axis=0), c.max(axis=0)
+    center = 0.5 * (lo + hi)
+    half = 0.5 * float((hi - lo).max()) * (1.0 + 1e-9) + 1e-300
+    q = (c - (center - half)) / (2.0 * half)
+    cells = np.clip((q * (1 << 20)).astype(np.int64), 0, (1 << 20) - 1).astype(np.uint64)
+    key = np.zeros(len(c), dtype=np.uint64)
+    for b in range(20):
+        for ax in range(3):
+            key |= ((cells[:, ax] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + ax)
+    return np.argsort(key, kind="stable")
+
+
+def permute_geometry(disc, order):
+    """The discretisation with its patches in `order` (node blocks of nb,
+    oversampled blocks of nbo, chart coefficients): a Geometry."""
+    from .operators import Geometry, _over_interp
+    oi = _over_interp(disc)
+    nbo, nb = oi.shape
+    order = np.asarray(order, dtype=np.int64)
+    nodes_ix = (order[:, None] * nb + np.arange(nb)[None, :]).ravel()
+    over_ix = (order[:, None] * nbo + np.arange(nbo)[None, :]).ravel()
+
+    def rows(a, ix):
+        return None if a is None else np.ascontiguousarray(np.asarray(a)[ix])
+    g = Geometry(order=int(disc.order), nodes=rows(disc.nodes, nodes_ix),
+                 normals=rows(disc.normals, nodes_ix), weights=rows(disc.weights, nodes_ix),
+                 curvature=rows(disc.curvature, nodes_ix),
+                 over_nodes=rows(disc.over_nodes, over_ix),
+                 over_normals=rows(disc.over_normals, over_ix),
+                 over_weights=rows(disc.over_weights, over_ix), over_interp=oi,
+                 tangents_u=rows(getattr(disc, "tangents_u", None), nodes_ix),
+                 tangents_v=rows(getattr(disc, "tangents_v", None), nodes_ix),
+                 inv_metric=rows(getattr(disc, "inv_metric", None), nodes_ix),
+                 node_patch=np.repeat(np.arange(len(order)), nb),
+                 coeffs_x=rows(getattr(disc, "coeffs_x", None), order),
+                 coeffs_dxdu=rows(getattr(disc, "coeffs_dxdu", None), order),
+                 coeffs_dxdv=rows(getattr(disc, "coeffs_dxdv", None), order),
+                 node_uv=rows(getattr(disc, "node_uv", None), nodes_ix),
+                 vinv=getattr(disc, "vinv", None))
+    return g, nodes_ix
+
+
+def _permute_corrections(cset, nodes_ix, n):
+    """A CorrectionSet with rows and columns renumbered by nodes_ix (new ->
+    old node index); patch blocks of columns stay blocks."""
+    from .operators import CorrectionSet
+
+    def host(a):
+        return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    ip, ix = host(cset.indptr), host(cset.indices)
+    inv = np.empty(n, dtype=np.int64)
+    inv[nodes_ix] = np.arange(n)
+    lens = np.diff(ip)[nodes_ix]
+    nip = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    take = np.concatenate([np.arange(ip[o], ip[o + 1]) for o in nodes_ix]) if n else \
+        np.zeros(0, np.int64)
+    vals = {k: host(v)[take] for k, v in cset.values.items()}
+    return CorrectionSet(nip, inv[ix[take]].astype(np.int32), vals, (n, n))
+
+
+def _rows_near_map(near, r0, nr):
+    """The near map restricted to targets [r0, r0 + nr): the other rows'
+    lists emptied (quadrature.py:66-73), so the correction build and its CSR
+    hold this rank's rows only."""
+    from .quadrature import NearMap
+    off = np.asarray(near.offsets)
+    cnt = np.diff(off)
+    keep = np.zeros_like(cnt)
+    keep[r0:r0 + nr] = cnt[r0:r0 + nr]
+    noff = np.concatenate([[0], np.cumsum(keep)]).astype(np.int64)
+    pats = np.asarray(near.patches)[off[r0]:off[r0 + nr]]
+    return NearMap(near.eta, near.cap, noff, np.ascontiguousarray(pats, dtype=np.int32))
 
 
 def allgather_rows(vec, parts, rank, group=None):
@@ -113,48 +207,103 @@ class _DeviceBackend:
         return self.dev.buffers()[1]
 
 
+def _eta_weights_rows(disc, cset, r0, nr, group):
+    """Phi = S^T w (operators.eta_weights) from this rank's rows -- the far
+    sum over its targets and its correction rows -- summed over the ranks."""
+    import scipy.sparse as sp
+    import torch.distributed as dist
+    from . import _lib
+    from .fmm import FmmSources, evaluate_direct
+    from .operators import FOUR_PI, KernelKind, _over_interp
+    w = np.asarray(disc.weights, dtype=float)
+    n = w.shape[0]
+    oi = np.asarray(_over_interp(disc), dtype=float)
+    rows = slice(r0, r0 + nr)
+    phi_over = evaluate_direct(FmmSources(np.asarray(disc.nodes)[rows], w[None, rows]),
+                               np.asarray(disc.over_nodes), ("pot",)).pot[0]
+    pulled = ((np.asarray(disc.over_weights) * phi_over).reshape(-1, oi.shape[0]) @ oi).ravel()
+
+    def host(a):
+        return a.cpu().numpy() if _lib.is_torch(a) else np.asarray(a)
+    C = sp.csr_matrix((host(cset.values[KernelKind.SINGLE_LAYER]), host(cset.indices),
+                       host(cset.indptr)), shape=(n, n))
+    w_own = np.zeros_like(w)
+    w_own[rows] = w[rows]  # C^T w = sum over rows: this rank's rows only
+    part = _lib.to_device(pulled / FOUR_PI + C.T @ w_own)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(part, group=group)
+    return part
+
+
 class ShardedOperatorSet:
     """LayerOperatorSet whose applies are split across the ranks of a
     torch.distributed group (one process per GPU).  Same apply/apply_a*
-    semantics; results are full vectors on every rank."""
+    semantics; inputs and results are full vectors in the caller's node
+    order on every rank.
 
-    def __init__(self, disc, formulation, eps, corrections, group=None,
-                 far="direct"):
+    corrections: a CorrectionSet / the reference's matrices (all rows; the
+    rank keeps its own), or None: built on the device for the rank's rows
+    only (the discretisation must carry its chart coefficients)."""
+
+    def __init__(self, disc, formulation, eps, corrections=None, group=None,
+                 far="direct", near=None, eta: float = 2.0, cap: int = 128,
+                 fmm_ncrit: int = 120, fmm_m2l="auto", morton: bool = True,
+                 distributed_upward: bool = True):
         import torch.distributed as dist
         from . import _lib
         from .operators import (FORMULATIONS, CorrectionSet, DeviceOperator,
-                                KernelKind, _FORM_CODE)
+                                KernelKind, _FORM_CODE, _over_interp)
         self.formulation = formulation.lower()
         self.eps = float(eps)
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        if not isinstance(corrections, CorrectionSet):
-            corrections = CorrectionSet.from_matrices(corrections)
+        oi = _over_interp(disc)
+        nbo, nb = oi.shape
         n = disc.nodes.shape[0]
-        nb = disc.over_interp.shape[1] if hasattr(disc, "over_interp") \
-            else disc.nodes_per_patch
         npat = n // nb
-        ip = corrections.indptr
-        cost = (ip[nb::nb] - ip[:-1:nb]) + nb * disc.over_nodes.shape[0] / 50.0
+        order = morton_patch_order(disc.nodes, nb) if morton else np.arange(npat)
+        geom, nodes_ix = permute_geometry(disc, order)
+        self.nodes_ix = nodes_ix
+        self.nodes_ix_dev = _lib.to_device(nodes_ix, _lib.torch().int64)
+        kinds = list(FORMULATIONS[self.formulation])
+        if corrections is not None:
+            if not isinstance(corrections, CorrectionSet):
+                corrections = CorrectionSet.from_matrices(corrections)
+            cset_all = _permute_corrections(corrections, nodes_ix, n)
+            ip = np.asarray(cset_all.indptr)
+            nnz_patch = ip[nb::nb] - ip[:-1:nb]
+            near_p = None
+        else:
+            from .quadrature import build_near_map
+            near_p = build_near_map(geom, eta, cap=cap)
+            nnz_patch = np.add.reduceat(np.diff(near_p.offsets), np.arange(0, n, nb)) * nb
+        cost = nnz_patch + nb * geom.over_nodes.shape[0] / 50.0
         self.parts = partition_rows(npat, nb, world, cost)
         r0, nr = self.parts[rank]
-        kinds = list(FORMULATIONS[self.formulation])
-        self.dev = DeviceOperator(disc, corrections, kinds, row0=r0, nrows=nr)
+        if corrections is not None:
+            cset = cset_all
+        else:
+            from .quadrature import build_correction_set
+            cset, self.t_q = build_correction_set(geom, _rows_near_map(near_p, r0, nr), kinds,
+                                                  self.eps)
+        self.dev = DeviceOperator(geom, cset, kinds, row0=r0, nrows=nr)
+        self._plan = None
         if far == "fmm":
-            # the reference's tree over ALL sources and targets on every rank
-            # (deterministic, identical), downward pass + leaf stage only for
-            # this rank's target rows: its outputs equal the unsharded FMM's
             from .fmm_plan import FmmPlan
-            self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps)
-            self._plan.set_target_range(r0, r0 + nr)
-            self.dev.set_fmm(self._plan)
+            plan = FmmPlan(geom.over_nodes, geom.nodes, self.eps, ncrit=fmm_ncrit, m2l=fmm_m2l)
+            plan.set_target_range(r0, r0 + nr)
+            if distributed_upward and world > 1:
+                # this rank's sources = its patches' oversampled nodes
+                plan.set_source_range(r0 // nb * nbo, (r0 + nr) // nb * nbo)
+                plan.set_upward_hook(lambda up, nd, stream: dist.all_reduce(up, group=group))
+            self.dev.set_fmm(plan)
+            self._plan = plan
         elif self.formulation == "a3":
-            # fused second sweep; Phi is global (every rank computes it whole)
-            from .operators import eta_weights
-            self.dev.set_eta_weights(_lib.to_device(eta_weights(disc, corrections)))
-        self.driver = ShardedApply(_DeviceBackend(self.dev), self.parts, rank,
-                                   group)
+            # fused second sweep: Phi = S^T w, the ranks' row parts summed
+            self.dev.set_eta_weights(_eta_weights_rows(geom, cset, r0, nr, group))
+        self.driver = ShardedApply(_DeviceBackend(self.dev), self.parts, rank, group)
         self.rank, self.world, self.n = rank, world, n
+        self.geom = geom
         self._code = _FORM_CODE[self.formulation]
         # phi0 = S[1] on the full vector (operators.py:99-100)
         ones = _lib.to_device(np.ones(n))
@@ -162,12 +311,24 @@ class ShardedOperatorSet:
         self.dev.apply_layer(KernelKind.SINGLE_LAYER, ones, phi0)
         allgather_rows(phi0, self.parts, rank, group)
         self.dev.set_phi0(phi0)
-        self._out = _lib.zeros((n,))
+        self._tau_p = _lib.zeros((n,))
+        self._out_p = _lib.zeros((n,))
+
+    @property
+    def row_range(self):
+        """This rank's rows [r0, r0 + nr) in the Morton-permuted order."""
+        r0, nr = self.parts[self.rank]
+        return r0, r0 + nr
 
     def apply_device(self, tau, out=None):
+        """Full-length device vectors in the caller's node order."""
         from . import _lib
         out = _lib.zeros((self.n,)) if out is None else out
-        return self.driver.apply(self._code, tau, out)
+        ix = self.nodes_ix_dev
+        self._tau_p.copy_(tau[ix])
+        self.driver.apply(self._code, self._tau_p, self._out_p)
+        out[ix] = self._out_p
+        return out
 
     def apply(self, tau):
         from . import _lib

@@ -72,3 +72,55 @@ def test_partition_rows_is_contiguous_and_patch_aligned():
         for (a0, an), (b0, _) in zip(parts, parts[1:]):
             assert a0 + an == b0
         assert all(nr % 28 == 0 for _, nr in parts)
+
+
+def test_partition_rejects_more_ranks_than_patches():
+    """a rank without rows must never exist (it would reduce rows it
+    never computed): every rank gets >= 1 patch, world > npatches raises."""
+    from paper_2111_10743_b200.sharding import partition_rows
+    parts = partition_rows(3, 10, 3)
+    assert [nr for _, nr in parts] == [10, 10, 10]
+    parts = partition_rows(8, 10, 4, cost=[100, 1, 1, 1, 1, 1, 1, 1])
+    assert all(nr > 0 for _, nr in parts) and sum(nr for _, nr in parts) == 80
+    with pytest.raises(ValueError):
+        partition_rows(3, 10, 4)
+
+
+def test_morton_patch_order_and_permutation():
+    """Targets are partitioned by contiguous Morton range (north_star): the
+    patch order sorts the centroids' Morton keys (the FMM's key function), so
+    every rank's patches are one contiguous key range; the permuted geometry
+    is a relabelling (node blocks move with their patch)."""
+    from paper_2111_10743_b200.operators import Geometry
+    from paper_2111_10743_b200.sharding import morton_patch_order, permute_geometry
+    g = np.load(os.path.join(GOLD, "opset_torus_o3.npz"))
+    geom = Geometry.from_arrays(g)
+    nb = geom.nodes_per_patch
+    order = morton_patch_order(geom.nodes, nb)
+    assert sorted(order.tolist()) == list(range(geom.npatches))
+    pg, ix = permute_geometry(geom, order)
+    assert np.array_equal(pg.nodes, geom.nodes[ix])
+    assert np.array_equal(pg.over_nodes.reshape(-1, pg.over_interp.shape[0], 3),
+                          geom.over_nodes.reshape(-1, pg.over_interp.shape[0], 3)[order])
+    assert np.array_equal(pg.coeffs_x, geom.coeffs_x[order])
+    # consecutive patches in the new order are close: the mean centroid step
+    # is far below the random-order step
+    c = geom.nodes.reshape(-1, nb, 3).mean(1)
+    step = np.linalg.norm(np.diff(c[order], axis=0), axis=1).mean()
+    rnd = np.linalg.norm(np.diff(c[np.random.default_rng(0).permutation(len(c))], axis=0),
+                         axis=1).mean()
+    assert step < 0.6 * rnd
+
+
+def test_rows_near_map_keeps_only_owned_rows():
+    from paper_2111_10743_b200.quadrature import NearMap
+    from paper_2111_10743_b200.sharding import _rows_near_map
+    g = np.load(os.path.join(GOLD, "opset_torus_o3.npz"))
+    near = NearMap(2.0, 128, g["near_offsets"], g["near_patches"])
+    n = len(near.offsets) - 1
+    r0, nr = n // 3, n // 3
+    sub = _rows_near_map(near, r0, nr)
+    cnt = np.diff(sub.offsets)
+    assert cnt[:r0].sum() == 0 and cnt[r0 + nr:].sum() == 0
+    assert np.array_equal(cnt[r0:r0 + nr], np.diff(near.offsets)[r0:r0 + nr])
+    assert np.array_equal(sub.patches, near.patches[near.offsets[r0]:near.offsets[r0 + nr]])

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, fixture, form, far, q):
+def _worker(rank, world, port, fixture, form, far, q, device_corr=False):
     import torch
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
@@ -38,8 +38,9 @@ def _worker(rank, world, port, fixture, form, far, q):
         from paper_2111_10743_b200 import CorrectionSet, Geometry
         from paper_2111_10743_b200.sharding import ShardedOperatorSet
         g = dict(np.load(os.path.join(GOLD, fixture)))
-        op = ShardedOperatorSet(Geometry.from_arrays(g), form, 1e-10,
-                                CorrectionSet.from_arrays(g), far=far)
+        corr = None if device_corr else CorrectionSet.from_arrays(g)
+        op = ShardedOperatorSet(Geometry.from_arrays(g), form, float(g["eps"]) if device_corr
+                                else 1e-10, corr, far=far)
         y = op.apply(np.asarray(g["tau"]))
         q.put((rank, np.asarray(y), None))
     except Exception as exc:  # noqa: BLE001 - report to the parent
@@ -48,19 +49,27 @@ def _worker(rank, world, port, fixture, form, far, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fixture,form,far", [("opset_torus_o3.npz", "a3", "direct"),
-                                              ("opset_sphere_o3.npz", "a2", "direct"),
-                                              ("opset_torus_o3.npz", "a3", "fmm")])
-def test_sharded_operator_set_two_ranks(cuda, fixture, form, far):
+@pytest.mark.parametrize("fixture,form,far,device_corr", [
+    ("opset_torus_o3.npz", "a3", "direct", False), ("opset_sphere_o3.npz", "a2", "direct", False),
+    ("opset_torus_o3.npz", "a3", "fmm", False), ("opset_torus_o3.npz", "a3", "fmm", True),
+    ("opset_torus_o3.npz", "a3", "direct", True)])
+def test_sharded_operator_set_two_ranks(cuda, fixture, form, far, device_corr):
+    """Morton-range target shards; per-rank corrections (device_corr: built on
+    the device for the rank's rows only); with the FMM, the upward pass split
+    by source range and all-reduced over the group between M2M and M2L."""
     from paper_2111_10743_b200 import CorrectionSet, Geometry, LayerOperatorSet
     g = dict(np.load(os.path.join(GOLD, fixture)))
-    ref = LayerOperatorSet(Geometry.from_arrays(g), form, 1e-10,
-                           corrections=CorrectionSet.from_arrays(g), far=far).apply(g["tau"])
+    if device_corr:
+        ref = LayerOperatorSet(Geometry.from_arrays(g), form, float(g["eps"]),
+                               far=far).apply(g["tau"])
+    else:
+        ref = LayerOperatorSet(Geometry.from_arrays(g), form, 1e-10,
+                               corrections=CorrectionSet.from_arrays(g), far=far).apply(g["tau"])
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, fixture, form, far, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fixture, form, far, q, device_corr))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -77,4 +86,5 @@ def test_sharded_operator_set_two_ranks(cuda, fixture, form, far):
                 p.terminate()
     for rank, y, err in res:
         rel = np.abs(y - ref).max() / np.abs(ref).max()
-        assert rel < 1e-12, (rank, rel)
+        # the distributed upward pass sums partial expansions in another order
+        assert rel < (1e-11 if far == "fmm" else 1e-12), (rank, rel)

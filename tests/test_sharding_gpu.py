@@ -82,3 +82,65 @@ def test_emulated_shards_match_unsharded(cuda, fixture, form, far):
         err = (got - ref).abs().max().item() / ref.abs().max().item()
         # FMM shards share the unsharded tree: the same approximation
         assert err < 1e-12, (world, err)
+
+
+@pytest.mark.parametrize("far", ["direct", "fmm"])
+def test_sharded_set_world1_morton_device_corrections(cuda, far):
+    """ShardedOperatorSet's own path on one rank: Morton-permuted patches,
+    corrections built on the device for its rows, inputs / outputs in the
+    caller's order -- equal to the plain LayerOperatorSet."""
+    from paper_2111_10743_b200 import Geometry, LayerOperatorSet
+    from paper_2111_10743_b200.sharding import ShardedOperatorSet
+    g = golden("opset_torus_o3.npz")
+    geom = Geometry.from_arrays(g)
+    eps = float(g["eps"])
+    ref = LayerOperatorSet(geom, "a3", eps, far=far).apply(g["tau"])
+    op = ShardedOperatorSet(geom, "a3", eps, None, far=far)
+    got = op.apply(g["tau"])
+    assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_distributed_upward_pass_emulated(cuda):
+    """The FMM's upward pass split by source range (lb_fmm_plan_set_source_range)
+    with the partial expansions summed by the upward hook: G plans on one GPU,
+    each with its rank's sources; pass 1 records every rank's partial
+    expansions, pass 2 hands each rank the sum (what the all-reduce does) --
+    the result equals the unsplit FMM."""
+    torch = cuda
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(5)
+    s = rng.standard_normal((40000, 3))
+    s /= np.linalg.norm(s, axis=1)[:, None]
+    t = s[::3].copy()
+    q = torch.from_numpy(rng.standard_normal((2, len(s)))).cuda()
+    nt = len(t)
+
+    def run(plan):
+        pot = torch.zeros((2, nt), dtype=torch.float64, device="cuda")
+        grad = torch.zeros((2, nt, 3), dtype=torch.float64, device="cuda")
+        plan.apply_device(q, None, 2, 3, 0, 1, pot, grad)
+        torch.cuda.synchronize()
+        return pot, grad
+    for eps in (1e-6, 1e-9):
+        ref = run(FmmPlan(s, t, eps))
+        G = 3
+        cuts = [0, 13000, 27000, len(s)]
+        plans, partial = [], [None] * G
+        for r in range(G):
+            p = FmmPlan(s, t, eps)
+            p.set_source_range(cuts[r], cuts[r + 1])
+            plans.append(p)
+        for r, p in enumerate(plans):  # pass 1: record the partials
+            def rec(up, nd, stream, r=r):
+                partial[r] = up.clone()
+            p.set_upward_hook(rec)
+            run(p)
+        total = sum(partial)
+        for r, p in enumerate(plans):  # pass 2: the all-reduced expansions
+            p.set_upward_hook(lambda up, nd, stream: up.copy_(total))
+            pot, grad = run(p)
+            assert p._hook_error is None
+            for a, b in ((pot, ref[0]), (grad, ref[1])):
+                err = (a - b).abs().max().item() / b.abs().max().item()
+                assert err < 1e-11, (eps, r, err)
+        assert not torch.equal(partial[0], total)  # the split really was partial
