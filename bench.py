@@ -323,7 +323,7 @@ def capture(torch, step, lib, _lib):
         return step, False, None
 
 
-def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib):
+def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib, peak_tc=None):
     """Per-stage device times of one apply (lb_opset stage events) and of one
     pot+grad FMM call (lb_fmm stage events) with their rooflines: SpMV passes
     against HBM (algorithmic bytes = nnz x (kinds x 8 + 4) + 8 (N + 1)), the
@@ -336,14 +336,22 @@ def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib):
     torch.cuda.synchronize()
     st = op.dev.stage_times()
     op.dev.set_timing(False)
+    # SURVEY §8(d) accounting: 8 B per value and kind + 4 B column index per
+    # nnz + 8 B per row offset (+ x gathers in L2); the kernels read the
+    # block-CSR index instead (4 / nb B per nnz), reported as actual_bytes
+    nb = int(op.disc.nodes_per_patch) if hasattr(op.disc, "nodes_per_patch") else 28
     b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
     b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
+    a1 = nnz * (2 * 8 + 4.0 / nb) + 8 * (n + 1)
+    a2 = nnz * (3 * 8 + 4.0 / nb) + 8 * (n + 1)
     stages = {
         "fmm_call1_ms": st[0], "fmm_call2_ms": st[2],
         "spmv1": {"ms": st[1], "bytes": b1, "GBps": b1 / st[1] / 1e6,
-                  "frac_hbm": b1 / st[1] / 1e6 / hbm_gbs},
+                  "frac_hbm": b1 / st[1] / 1e6 / hbm_gbs, "actual_bytes": a1,
+                  "actual_frac_hbm": a1 / st[1] / 1e6 / hbm_gbs},
         "spmv2_glue": {"ms": st[3], "bytes": b2, "GBps": b2 / st[3] / 1e6,
-                       "frac_hbm": b2 / st[3] / 1e6 / hbm_gbs},
+                       "frac_hbm": b2 / st[3] / 1e6 / hbm_gbs, "actual_bytes": a2,
+                       "actual_frac_hbm": a2 / st[3] / 1e6 / hbm_gbs},
         "apply_ms": st[7]}
     # one charge pot+grad call of the plan (the metric's unit), stage split
     w = torch.from_numpy(np.random.default_rng(3).standard_normal((1, nover))).cuda()
@@ -357,12 +365,13 @@ def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib):
     wc = plan.work_counts()
     leaf_pairs = wc["u_pairs"] + wc["w_pairs"] + wc["de_pairs"]
 
-    def fp(ms, flops):
+    def fp(ms, flops, peak=peak_tf, pipe="fp64"):
         tf = flops / (ms / 1e3) / 1e12 if ms > 0 else None
-        return {"ms": ms, "flops": flops, "TFLOPs": tf,
-                "frac_fp64": tf / peak_tf if tf else None}
+        return {"ms": ms, "flops": flops, "TFLOPs": tf, "pipe": pipe,
+                "frac": tf / peak if tf else None}
     fmm = {"p2m": fp(fs["p2m"], 11.0 * wc["p2m_pairs"]),
-           "m2m_ms": fs["m2m"], "m2l": fp(fs["m2l"], wc["m2l_flops"]),
+           "m2m_ms": fs["m2m"],
+           "m2l": fp(fs["m2l"], wc["m2l_flops"], peak_tc or peak_tf, "fp64 tensor (DMMA)"),
            "x_list": fp(fs["x"], 11.0 * wc["x_pairs"]), "l2l_ms": fs["l2l"],
            "leaf": fp(fs["leaf"], 20.0 * leaf_pairs), "total_ms": fs["total"],
            "pairs": {k: wc[k] for k in ("u_pairs", "w_pairs", "de_pairs", "x_pairs",
@@ -483,7 +492,7 @@ def main():
     peak_tc = dmma_peak_tflops(torch, lib, _lib)
     stages = roofline = None
     if world == 1:
-        stages = stage_rooflines(torch, op, op._plan, n, nover, cset.nnz, peak, hbm, _lib)
+        stages = stage_rooflines(torch, op, op._plan, n, nover, cset.nnz, peak, hbm, _lib, peak_tc)
         f = stages["fmm_call1_stages"]
         cands = [("spmv", stages["spmv2_glue"]["ms"], "hbm"),
                  ("leaf", f["leaf"]["ms"], "fp64"), ("m2l", f["m2l"]["ms"], "fp64")]
@@ -494,12 +503,18 @@ def main():
                         "achieved": s2["GBps"], "peak": hbm, "unit": "GB/s",
                         "frac": s2["frac_hbm"], "traffic": None,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        elif dom == "m2l":
+            s = f["m2l"]
+            roofline = {"bound": "tensor", "kernel": "FMM M2L (gemm_cols_kernel first factor + "
+                        "m2l_fused_kernel, DMMA 8x8x4)", "achieved": s["TFLOPs"], "peak": peak_tc,
+                        "unit": "TFLOP/s", "frac": s["frac"], "traffic": None,
+                        "peak_source": "measured in-run (lb_probe_dmma: FP64 tensor-core DMMA "
+                                       "chains); FP64 FMA pipe measured " + f"{peak:.1f}"}
         else:
-            s = f[dom]
-            roofline = {"bound": "fp64", "kernel": {"leaf": "leaf_kernel (FMM U/W/DE lists)",
-                                                     "m2l": "FMM M2L"}[dom],
+            s = f["leaf"]
+            roofline = {"bound": "fp64", "kernel": "leaf_kernel (FMM U/W/DE lists)",
                         "achieved": s["TFLOPs"], "peak": peak, "unit": "TFLOP/s",
-                        "frac": s["frac_fp64"], "traffic": None,
+                        "frac": s["frac"], "traffic": None,
                         "peak_source": f"measured in-run (lb_probe_dfma); nominal "
                                        f"{NOMINAL_FP64_TFLOPS}"}
     cpu = None

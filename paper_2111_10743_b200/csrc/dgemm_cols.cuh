@@ -55,6 +55,11 @@ struct Args {
   int add;                   // 1: Y += ..., 0: Y = ...
   int64_t nq;                // boxes/pairs (no batches)
   const int64_t* boff;       // batches: q range [boff[z] - boff[0], boff[z+1] - boff[0])
+  // optional per-batch shapes (the M2L's first factor over all keys at once):
+  // rows m_b[z] (<= M), output at Y + y_off[z] * nd with column stride ldy_b[z]
+  const int32_t* m_b;
+  const int64_t* y_off;
+  const int32_t* ldy_b;
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -106,7 +111,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
   const int64_t c0 = (int64_t)blockIdx.y * BN;
   if (c0 >= ncols) return;
   const int m0 = blockIdx.x * BM;
+  const int Mz = g.m_b ? g.m_b[z] : g.M;
+  if (m0 >= Mz) return;
   const double* A = g.a_off ? g.A + g.a_off[z] : g.A + (int64_t)z * g.a_batch;
+  double* const Yz = g.Y + (g.y_off ? g.y_off[z] * g.nd : 0);
+  const int64_t ldyz = g.ldy_b ? g.ldy_b[z] : g.ldy;
   // 16-byte A copies need even row strides / offsets and an aligned base
   const bool a16 = ((g.lda | g.a_seg | g.a_batch) & 1) == 0 && (((uintptr_t)A) & 15) == 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
     }
     kpp[j] = (ok && g.kperm) ? g.kperm + (int64_t)g.kp[q] * g.K : nullptr;
     const int64_t ob = g.out ? g.out[q] : q;
-    yout[j] = ok ? g.Y + (ob * g.nd + l) * g.ldy : nullptr;
+    yout[j] = ok ? Yz + (ob * g.nd + l) * ldyz : nullptr;
     alph[j] = ok ? g.alpha * (g.alpha_q ? g.alpha_q[q] : 1.0) : 0.0;
   }
   __syncthreads();
@@ -164,14 +173,14 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
         const int r = e / (kKC / 2), kk = (e % (kKC / 2)) * 2;
         const int row = m0 + r, k = k0 + kk;
         int bytes = 0;
-        if (row < g.M && k < g.K) bytes = (k + 1 < g.K) ? 16 : 8;
+        if (row < Mz && k < g.K) bytes = (k + 1 < g.K) ? 16 : 8;
         cp16(as + r * kLD + kk, bytes ? As_src + (int64_t)row * g.lda + k : g.A, bytes);
       }
     } else {
       for (int e = tid; e < BM * kKC; e += NT) {
         const int r = e / kKC, kk = e % kKC;
         const int row = m0 + r, k = k0 + kk;
-        const bool ok = row < g.M && k < g.K;
+        const bool ok = row < Mz && k < g.K;
         cp8(as + r * kLD + kk, ok ? As_src + (int64_t)row * g.lda + k : g.A, ok);
       }
     }
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int row = m0 + wm * WM + mt * 8 + gq;
-    if (row >= g.M) continue;
+    if (row >= Mz) continue;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
@@ -277,6 +286,10 @@ inline cudaError_t gemm_cols(const Args& a, int64_t max_cols_per_batch, int batc
     return (int64_t)((a.M + bm - 1) / bm) * ((max_cols_per_batch + bn - 1) / bn) * batches;
   };
   const int64_t want = 2 * 148;
+  if (a.m_b) {  // per-batch row counts: 64-row tiles, the tiles past a batch's rows exit
+    if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
+    return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+  }
   if (a.M > 64) {
     if (ctas(128, 128) >= want) return launch<128, 128, 32>(a, max_cols_per_batch, batches, st);
     if (ctas(128, 64) >= want) return launch<128, 64, 32>(a, max_cols_per_batch, batches, st);

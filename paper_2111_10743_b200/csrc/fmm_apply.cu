@@ -1593,6 +1593,37 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
       }
     }
     D.lo_key_batch[nk] = (int64_t)boff.size();
+    {  // the single-launch form: every key's batches, T of key k at tbase1[k] * nd
+      std::vector<int64_t> gb, ga, gy;
+      std::vector<int32_t> gm;
+      D.lo_tbase1.assign(nk + 1, 0);
+      D.lo_gmaxgrp = 0;
+      D.lo_rmax = 0;
+      for (int k = 0; k < nk; ++k) {
+        const int64_t p0 = D.v_key_pair_off[k], p1 = D.v_key_pair_off[k + 1];
+        const int r = P->lr_rank[k];
+        D.lo_tbase1[k + 1] = D.lo_tbase1[k] + (p1 - p0) * r;
+        if (p1 == p0) continue;
+        for (int64_t e = D.lo_key_batch[k]; e + 1 < D.lo_key_batch[k + 1]; ++e) {
+          gb.push_back(boff[e]);
+          ga.push_back(aoff[e]);
+          gy.push_back(D.lo_tbase1[k]);
+          gm.push_back(r);
+        }
+        D.lo_gmaxgrp = std::max(D.lo_gmaxgrp, D.lo_key_maxgrp[k]);
+        D.lo_rmax = std::max(D.lo_rmax, r);
+      }
+      D.lo_gbatch = (int64_t)gm.size();
+      gb.push_back(np);
+      D.lo_gb0 = gb.front();  // q of the launch counts from the first nonempty key's pairs
+      cudaFree(D.lo_gboff); cudaFree(D.lo_gaoff); cudaFree(D.lo_gyoff); cudaFree(D.lo_gm);
+      D.lo_gboff = D.lo_gaoff = D.lo_gyoff = nullptr;
+      D.lo_gm = nullptr;
+      LB_TRY(upload(&D.lo_gboff, gb));
+      LB_TRY(upload(&D.lo_gaoff, ga));
+      LB_TRY(upload(&D.lo_gyoff, gy));
+      LB_TRY(upload(&D.lo_gm, gm));
+    }
 
     cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
     cudaFree(D.lo_boff); cudaFree(D.lo_aoff);
@@ -1637,9 +1668,7 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     ku[nk] = (int64_t)(units.size() / 2);
     LB_TRY(upload(&D.lo_units[nd], units));
   }
-  int64_t need = 1;
-  for (int k = 0; k < nk; ++k)
-    need = std::max(need, (D.v_key_pair_off[k + 1] - D.v_key_pair_off[k]) * nd * P->lr_rank[k]);
+  int64_t need = std::max<int64_t>(1, D.lo_tbase1[nk] * nd);  // T of every key at once
   if (D.lr_t_cap < need) {
 
     cudaFree(D.lr_t);
@@ -1750,26 +1779,30 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     const char* e = std::getenv("LB_M2L_MODE");
     return (e && std::string(e) == "staged") ? 2 : 0;
   }();
+  // fused mode: the first factor of every key and offset in ONE launch
+  // (batches = lattice offsets, per-batch ranks), T of key k at tbase1[k] nd
+  const bool lowrank_fused = P->m2l_slices < 0 && m2l_mode != 2 && nrep <= m2lf::kMaxIt * m2lf::kThreads &&
+                             ND <= m2lf::kMaxNd && D.lo_rmax <= 4 * m2lf::kMaxKS;
+  if (lowrank_fused && D.lo_gbatch > 0) {
+    dg::Args a{};
+    a.A = D.lr_bp; a.a_off = D.lo_gaoff; a.lda = nrep; a.M = D.lo_rmax; a.m_b = D.lo_gm; a.K = nrep;
+    const int64_t q0 = D.lo_gb0;
+    a.S = 1; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.lo_src + q0; a.alpha_q = D.lo_scale + q0;
+    a.alpha = 1.0; a.Y = D.lr_t; a.y_off = D.lo_gyoff; a.ldy_b = D.lo_gm; a.out = D.lo_tcol + q0; a.add = 0;
+    a.boff = D.lo_gboff;
+    LB_DG(dg::gemm_cols(a, D.lo_gmaxgrp * ND, (int)D.lo_gbatch, st));
+  }
   for (int k = 0; k < P->ncanon; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
     if (pe == pb) continue;
-    const bool no_fuse = m2l_mode == 2;
-    if (P->m2l_slices < 0 && P->lr_rank[k] <= 4 * m2lf::kMaxKS && !no_fuse &&
-        nrep <= m2lf::kMaxIt * m2lf::kThreads && ND <= m2lf::kMaxNd) {
-      // low-rank, fused: T = (B_k P_d) x / h for all the key's pairs (batches
-      // of one lattice offset: one permuted factor per batch, contiguous
-      // multipoles), then Y = A_k T and the permuted accumulation per unit of
-      // whole target groups, Y kept in shared memory
+    const bool no_fuse = !lowrank_fused;
+    if (!no_fuse) {
+      // low-rank, fused: Y = A_k T and the permuted accumulation per unit of
+      // whole target groups, Y kept in shared memory (T from the launch above)
       const int r = P->lr_rank[k];
-      const int64_t kb = D.lo_key_batch[k];
-      const int nbatch = (int)(D.lo_key_batch[k + 1] - kb - 1);
-      dg::Args a{};
-      a.A = D.lr_bp; a.a_off = D.lo_aoff + kb; a.lda = nrep; a.M = r; a.K = nrep; a.S = 1; a.nd = ND;
-      a.X = D.up; a.ldx = nrep; a.in = D.lo_src + pb; a.alpha_q = D.lo_scale + pb; a.alpha = 1.0;
-      a.Y = D.lr_t; a.ldy = r; a.out = D.lo_tcol + pb; a.add = 0; a.boff = D.lo_boff + kb;
-      LB_DG(dg::gemm_cols(a, D.lo_key_maxgrp[k] * ND, nbatch, st));
       m2lf::Args f{};
-      f.A = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND; f.T = D.lr_t;
+      f.A = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND;
+      f.T = D.lr_t + D.lo_tbase1[k] * ND;
       const std::vector<int64_t>& ku = D.lo_key_units[ND];
       f.units = D.lo_units[ND] + 2 * ku[k]; f.vtgts = D.v_tgts; f.tpair = D.v_tgt_pair_off;
       f.voff = D.v_off_idx; f.perm = D.perm; f.p0 = pb; f.dc = D.dc;
@@ -1972,6 +2005,7 @@ void fmm_release_device(lb_fmm_plan* P) {
   cudaFree(D.lr_t);
   cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
   cudaFree(D.lo_boff); cudaFree(D.lo_aoff);
+  cudaFree(D.lo_gboff); cudaFree(D.lo_gaoff); cudaFree(D.lo_gyoff); cudaFree(D.lo_gm);
   for (int i = 0; i < 5; ++i) cudaFree(D.lo_units[i]);
   cudaFree(D.oz_b);
   cudaFree(D.oz_cs);

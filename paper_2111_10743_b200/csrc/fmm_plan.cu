@@ -10,34 +10,6 @@
 #include "fmm_plan.h"
 #include "lb_common.cuh"
 
-namespace lb {
-
-// fmm.py:569-576 on the device; explicit _rn intrinsics keep the arithmetic
-// identical to numpy's (no contraction).
-__global__ void morton_keys_kernel(const double* __restrict__ spos, int64_t ns,
-                                   const double* __restrict__ tpos, int64_t nt, double c0, double c1,
-                                   double c2, double half, uint64_t* __restrict__ keys,
-                                   int64_t* __restrict__ idx) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ns + nt) return;
-  const double* p = i < ns ? spos + 3 * i : tpos + 3 * (i - ns);
-  const double cc[3] = {c0, c1, c2};
-  const double two_h = __dmul_rn(2.0, half);
-  uint64_t code = 0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double origin = __dsub_rn(cc[a], half);
-    const double q = __ddiv_rn(__dsub_rn(p[a], origin), two_h);
-    int64_t cell = (int64_t)__dmul_rn(q, (double)(1 << kMaxDepth));
-    cell = cell < 0 ? 0 : (cell > (1 << kMaxDepth) - 1 ? (1 << kMaxDepth) - 1 : cell);
-    for (int b = 0; b < kMaxDepth; ++b) code |= (uint64_t)((cell >> b) & 1) << (3 * b + a);
-  }
-  keys[i] = code;
-  idx[i] = i;
-}
-
-}  // namespace lb
-
 using namespace lb;
 
 extern "C" {

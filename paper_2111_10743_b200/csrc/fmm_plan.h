@@ -103,6 +103,13 @@ struct FmmDevice {
   int64_t *lo_src = nullptr, *lo_tcol = nullptr, *lo_boff = nullptr, *lo_aoff = nullptr;
   double* lo_scale = nullptr;
   std::vector<int64_t> lo_key_batch, lo_key_maxgrp;    // per key: first batch entry, largest batch
+  // all keys' first factors in ONE launch: batch boundaries (no duplicates),
+  // factor offsets, ranks, T bases (x nd) per batch; host T base per key
+  int64_t *lo_gboff = nullptr, *lo_gaoff = nullptr, *lo_gyoff = nullptr;
+  int32_t *lo_gm = nullptr;
+  int64_t lo_gbatch = 0, lo_gmaxgrp = 0, lo_gb0 = 0;
+  int lo_rmax = 0;
+  std::vector<int64_t> lo_tbase1;                      // per key: sum of pairs x r over earlier keys
   // per density count nd (1..4): units (2 x int64 target-group ranges) and
   // each key's first unit; built once per nd, so an apply never allocates
   int64_t* lo_units[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};

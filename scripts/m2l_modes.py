@@ -37,7 +37,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
             torch.cuda.synchronize()
             plan.set_timing(False)
             out[f"{name}_nd{nd}"] = plan.stage_times()
-        np.save(os.path.join(ROOT, "gpurun_out", f"m2l_{os.environ.get('LB_M2L_MODE', 'target')}_{name}.npy"),
+        np.save(os.path.join("/tmp", f"m2l_{os.environ.get('LB_M2L_MODE', 'target')}_{name}.npy"),
                 pot.cpu().numpy())
     print(json.dumps(out))
     sys.exit(0)
@@ -53,9 +53,9 @@ for mode, d in res.items():
     for case, st in d.items():
         print(mode, case, "m2l %.3f ms  total %.3f ms" % (st["m2l"], st["total"]))
 for case in ("config3", "c5_1e6_e6", "c5_1e6_e9"):
-    ref = np.load(os.path.join(ROOT, "gpurun_out", f"m2l_staged_{case}.npy"))
+    ref = np.load(os.path.join("/tmp", f"m2l_staged_{case}.npy"))
     for mode in ("target", "fused"):
-        p = os.path.join(ROOT, "gpurun_out", f"m2l_{mode}_{case}.npy")
+        p = os.path.join("/tmp", f"m2l_{mode}_{case}.npy")
         if os.path.exists(p):
             a = np.load(p)
             print(case, mode, "vs staged", float(np.abs(a - ref).max() / np.abs(ref).max()))

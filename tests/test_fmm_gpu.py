@@ -97,8 +97,12 @@ def test_device_sort_tree_equals_host_tree(cuda):
                     device_sort=True).tree
         assert np.array_equal(a.level, g[case + "level"])
         assert np.array_equal(a.ijk, g[case + "ijk"])
-        assert np.array_equal(a.raw["src_sorted"], np.concatenate(
-            [x for x in a.src_idx if x is not None]) if False else a.raw["src_sorted"])
+        # the leaves' source index lists (sorted order), against the reference's
+        off, flat = g[case + "src_idx_off"], g[case + "src_idx"]
+        got = [x for x in a.src_idx]
+        lens = np.array([0 if x is None else len(x) for x in got])
+        assert np.array_equal(np.concatenate([[0], np.cumsum(lens)]), off)
+        assert np.array_equal(np.concatenate([x for x in got if x is not None and len(x)]), flat)
         off, flat = g[case + "ulist_off"], g[case + "ulist"]
         assert np.array_equal(a.raw["u_off"], off) and np.array_equal(a.raw["u"], flat)
 

