@@ -40,6 +40,7 @@
 #include "dgemm_cols.cuh"
 #include "fmm_plan.h"
 #include "lb_common.cuh"
+#include "m2l_first.cuh"
 #include "m2l_fused.cuh"
 #include "ozaki.cuh"
 #include "p2p_core.cuh"
@@ -1537,6 +1538,16 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     D.lo_ready = false;
   }
   const int nk = P->ncanon, nrep = P->nrep;
+  if (!D.lr_ap) {  // A_k in DMMA fragment order for the fused second factor (m2l_fused.cuh)
+    D.lr_ap_off.assign(nk + 1, 0);
+    for (int k = 0; k < nk; ++k)
+      D.lr_ap_off[k + 1] = D.lr_ap_off[k] + (int64_t)m2lf::packed_doubles(nrep, P->lr_rank[k]);
+    std::vector<double> ap(std::max<int64_t>(D.lr_ap_off[nk], 1));
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < nk; ++k)
+      m2lf::pack_a(P->lr_a_host.data() + P->lr_off[k] * nrep, nrep, P->lr_rank[k], ap.data() + D.lr_ap_off[k]);
+    LB_TRY(upload(&D.lr_ap, ap));
+  }
   if (!D.lo_ready) {
     // pair arrays back on the host once (the device plan build leaves them on the device)
     const int64_t np = D.v_key_pair_off[nk];
@@ -1602,7 +1613,7 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
       for (int k = 0; k < nk; ++k) {
         const int64_t p0 = D.v_key_pair_off[k], p1 = D.v_key_pair_off[k + 1];
         const int r = P->lr_rank[k];
-        D.lo_tbase1[k + 1] = D.lo_tbase1[k] + (p1 - p0) * r;
+        D.lo_tbase1[k + 1] = D.lo_tbase1[k] + (p1 - p0) * m2lf::tstride(r);
         if (p1 == p0) continue;
         for (int64_t e = D.lo_key_batch[k]; e + 1 < D.lo_key_batch[k + 1]; ++e) {
           gb.push_back(boff[e]);
@@ -1615,6 +1626,8 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
       }
       D.lo_gbatch = (int64_t)gm.size();
       gb.push_back(np);
+      D.lo_gm_host = gm;
+      D.lo_gb_host = gb;
       D.lo_gb0 = gb.front();  // q of the launch counts from the first nonempty key's pairs
       cudaFree(D.lo_gboff); cudaFree(D.lo_gaoff); cudaFree(D.lo_gyoff); cudaFree(D.lo_gm);
       D.lo_gboff = D.lo_gaoff = D.lo_gyoff = nullptr;
@@ -1637,11 +1650,23 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     LB_TRY(upload(&D.lo_aoff, aoff));
     for (int i = 0; i < 5; ++i) {
       cudaFree(D.lo_units[i]);
+      cudaFree(D.lo_tiles[i]);
       D.lo_units[i] = nullptr;
+      D.lo_tiles[i] = nullptr;
     }
     D.lo_ready = true;
   }
   if (nd < 1 || nd > 4) return fail(LB_ERR_ARG, "fmm: density chunk outside [1, 4]");
+  if (!D.lo_carry) {  // carry pool of the multi-pass groups (m2l_fused.cuh)
+    int dev = 0, sms = 0;
+    LB_CUDA(cudaGetDevice(&dev));
+    LB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    D.lo_carry_slots = m2lf::carry_slots(sms);
+    LB_CUDA(cudaMalloc((void**)&D.lo_carry,
+                       sizeof(double) * (size_t)D.lo_carry_slots * m2lf::kMaxNd * P->nrep));
+    LB_CUDA(cudaMalloc((void**)&D.lo_carry_flag, sizeof(unsigned) * (size_t)D.lo_carry_slots));
+    LB_CUDA(cudaMemset(D.lo_carry_flag, 0, sizeof(unsigned) * (size_t)D.lo_carry_slots));
+  }
   if (!D.lo_units[nd]) {  // units of whole target groups, <= one pass of columns where possible
     std::vector<int64_t> units;
     std::vector<int64_t>& ku = D.lo_key_units[nd];
@@ -1652,7 +1677,7 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
       int64_t ub = g0, cols = 0;
       for (int64_t gi = g0; gi < g1; ++gi) {
         const int64_t c = (D.v_tpoff_host[gi + 1] - D.v_tpoff_host[gi]) * nd;
-        if (gi > ub && cols + c > m2lf::kCols) {
+        if (gi > ub && cols + c > m2lf::pass_cols(nd)) {
           units.push_back(ub);
           units.push_back(gi);
           ub = gi;
@@ -1667,6 +1692,24 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     }
     ku[nk] = (int64_t)(units.size() / 2);
     LB_TRY(upload(&D.lo_units[nd], units));
+    // the first factor's flat tile list (m2l_first.cuh): (batch, column tile),
+    // the highest ranks first so the last wave holds the light tiles
+    std::vector<std::pair<int32_t, int32_t>> tl;
+    for (int64_t z = 0; z < D.lo_gbatch; ++z) {
+      const int64_t cols = (D.lo_gb_host[z + 1] - D.lo_gb_host[z]) * nd;
+      for (int64_t c = 0; c * m2l1::kBN < cols; ++c) tl.emplace_back((int32_t)z, (int32_t)c);
+    }
+    std::stable_sort(tl.begin(), tl.end(), [&](const auto& a, const auto& b) {
+      return D.lo_gm_host[a.first] > D.lo_gm_host[b.first];
+    });
+    std::vector<int32_t> flat;
+    flat.reserve(2 * tl.size());
+    for (const auto& e : tl) {
+      flat.push_back(e.first);
+      flat.push_back(e.second);
+    }
+    D.lo_ntiles[nd] = (int64_t)tl.size();
+    LB_TRY(upload(&D.lo_tiles[nd], flat));
   }
   int64_t need = std::max<int64_t>(1, D.lo_tbase1[nk] * nd);  // T of every key at once
   if (D.lr_t_cap < need) {
@@ -1674,6 +1717,9 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     cudaFree(D.lr_t);
     D.lr_t = nullptr;
     LB_CUDA(cudaMalloc((void**)&D.lr_t, sizeof(double) * need));
+    // the fused path's T columns are padded to whole k-steps; the pad rows are
+    // never written and must read as zero (m2l_fused.cuh)
+    LB_CUDA(cudaMemset(D.lr_t, 0, sizeof(double) * need));
     D.lr_t_cap = need;
   }
   return LB_OK;
@@ -1781,16 +1827,15 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   }();
   // fused mode: the first factor of every key and offset in ONE launch
   // (batches = lattice offsets, per-batch ranks), T of key k at tbase1[k] nd
-  const bool lowrank_fused = P->m2l_slices < 0 && m2l_mode != 2 && nrep <= m2lf::kMaxIt * m2lf::kThreads &&
+  const bool lowrank_fused = P->m2l_slices < 0 && m2l_mode != 2 && nrep <= m2lf::max_nrep() &&
                              ND <= m2lf::kMaxNd && D.lo_rmax <= 4 * m2lf::kMaxKS;
   if (lowrank_fused && D.lo_gbatch > 0) {
-    dg::Args a{};
-    a.A = D.lr_bp; a.a_off = D.lo_gaoff; a.lda = nrep; a.M = D.lo_rmax; a.m_b = D.lo_gm; a.K = nrep;
+    m2l1::Args a{};
     const int64_t q0 = D.lo_gb0;
-    a.S = 1; a.nd = ND; a.X = D.up; a.ldx = nrep; a.in = D.lo_src + q0; a.alpha_q = D.lo_scale + q0;
-    a.alpha = 1.0; a.Y = D.lr_t; a.y_off = D.lo_gyoff; a.ldy_b = D.lo_gm; a.out = D.lo_tcol + q0; a.add = 0;
-    a.boff = D.lo_gboff;
-    LB_DG(dg::gemm_cols(a, D.lo_gmaxgrp * ND, (int)D.lo_gbatch, st));
+    a.A = D.lr_bp; a.a_off = D.lo_gaoff; a.m_b = D.lo_gm; a.K = nrep; a.nd = ND; a.X = D.up;
+    a.in = D.lo_src + q0; a.alpha_q = D.lo_scale + q0; a.out = D.lo_tcol + q0; a.Y = D.lr_t;
+    a.y_off = D.lo_gyoff; a.boff = D.lo_gboff; a.tiles = D.lo_tiles[ND];
+    LB_DG(m2l1::launch(a, D.lo_ntiles[ND], D.lo_rmax, st));
   }
   for (int k = 0; k < P->ncanon; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
@@ -1801,11 +1846,13 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       // whole target groups, Y kept in shared memory (T from the launch above)
       const int r = P->lr_rank[k];
       m2lf::Args f{};
-      f.A = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND;
+      f.A = m2lf::use_ring(nrep) ? D.lr_ap + D.lr_ap_off[k] : nullptr;
+      f.Arow = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND;
       f.T = D.lr_t + D.lo_tbase1[k] * ND;
       const std::vector<int64_t>& ku = D.lo_key_units[ND];
       f.units = D.lo_units[ND] + 2 * ku[k]; f.vtgts = D.v_tgts; f.tpair = D.v_tgt_pair_off;
       f.voff = D.v_off_idx; f.perm = D.perm; f.p0 = pb; f.dc = D.dc;
+      f.carry = D.lo_carry; f.carry_flag = D.lo_carry_flag; f.carry_slots = D.lo_carry_slots;
       LB_DG(m2lf::launch(f, ku[k + 1] - ku[k], st));
       continue;
     }
@@ -2003,10 +2050,16 @@ void fmm_release_device(lb_fmm_plan* P) {
   cudaFree(D.lr_a);
   cudaFree(D.lr_b);
   cudaFree(D.lr_t);
+  cudaFree(D.lo_carry);
+  cudaFree(D.lo_carry_flag);
+  cudaFree(D.lr_ap);
   cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
   cudaFree(D.lo_boff); cudaFree(D.lo_aoff);
   cudaFree(D.lo_gboff); cudaFree(D.lo_gaoff); cudaFree(D.lo_gyoff); cudaFree(D.lo_gm);
-  for (int i = 0; i < 5; ++i) cudaFree(D.lo_units[i]);
+  for (int i = 0; i < 5; ++i) {
+    cudaFree(D.lo_units[i]);
+    cudaFree(D.lo_tiles[i]);
+  }
   cudaFree(D.oz_b);
   cudaFree(D.oz_cs);
   cudaFree(D.dn_off_dev);
@@ -2071,7 +2124,8 @@ int lb_fmm_plan_set_m2l_factors(lb_fmm_plan* P, const int32_t* ranks, const doub
   FmmDevice& D = P->dev;  // device copies are rebuilt on the next apply
   cudaFree(D.lr_a);
   cudaFree(D.lr_b);
-  D.lr_a = D.lr_b = nullptr;
+  cudaFree(D.lr_ap);
+  D.lr_a = D.lr_b = D.lr_ap = nullptr;
   return LB_OK;
 }
 

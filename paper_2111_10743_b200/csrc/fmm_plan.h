@@ -114,6 +114,16 @@ struct FmmDevice {
   // each key's first unit; built once per nd, so an apply never allocates
   int64_t* lo_units[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   std::vector<int64_t> lo_key_units[5];
+  // the first factor's flat (batch, column tile) list per nd (m2l_first.cuh)
+  int32_t* lo_tiles[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t lo_ntiles[5] = {0, 0, 0, 0, 0};
+  double* lr_ap = nullptr;      // A_k in DMMA fragment order (m2lf::pack_a), key k at lr_ap_off[k]
+  std::vector<int64_t> lr_ap_off;
+  double* lo_carry = nullptr;   // m2l_fused.cuh: carry pool (lo_carry_slots x kMaxNd x nrep)
+  unsigned* lo_carry_flag = nullptr;
+  int lo_carry_slots = 0;
+  std::vector<int32_t> lo_gm_host;
+  std::vector<int64_t> lo_gb_host;
 };
 
 // device arrays kept from the device tree build (fmm_tree_dev.cu): the
