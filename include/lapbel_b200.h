@@ -289,6 +289,16 @@ int lb_fmm_apply(lb_fmm_plan* plan, const double* charges,
  * about 1e3 * 2^(-7S) of max|K| max|x| (S = 8: fp64 roundoff).  Needs
  * nrep <= 2048. */
 int lb_fmm_plan_set_m2l(lb_fmm_plan* plan, int slices);
+/* X / W list evaluation (no reference counterpart; the lists themselves stay
+ * the reference's, fmm.py:650-715).  direct = 0: every X and W entry as the
+ * reference evaluates it (fmm.py:888-911, 966-988).  direct = 1: an X entry
+ * (target box b, source leaf x) whose b is a leaf with 2.5 nt(b) <= nrep, and
+ * a W entry (target leaf b, box w) whose w is a leaf with at most nrep
+ * sources, are evaluated as direct sums of the leaf's sources at b's targets
+ * (they join b's U list): exact where the reference approximates, and fewer
+ * pair evaluations.  Results then differ from direct = 0 within the plan's
+ * eps.  Rebuilds the device lists on the next apply. */
+int lb_fmm_plan_set_xw(lb_fmm_plan* plan, int direct);
 /* Owned targets [t0, t1) in the caller's target order (t1 < 0: all, the
  * default).  The tree and lists stay the reference's; M2L, X list, L2L and the
  * leaf stage then run only for boxes with owned targets below them, and only

@@ -73,6 +73,7 @@ SIGNATURES = {
     "lb_fmm_apply": [_P, _P, _P, _I32, _U32, _U32, _I32, _P, _P, _P, _P],
     "lb_fmm_plan_set_timing": [_P, _I32],
     "lb_fmm_plan_set_m2l": [_P, _I32],
+    "lb_fmm_plan_set_xw": [_P, _I32],
     "lb_fmm_plan_set_m2l_factors": [_P, _P, _P, _P],
     "lb_fmm_plan_set_target_range": [_P, _I64, _I64],
     "lb_fmm_plan_set_source_range": [_P, _I64, _I64],

@@ -290,14 +290,20 @@ inline cudaError_t gemm_cols(const Args& a, int64_t max_cols_per_batch, int batc
     if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
     return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
   }
+  // a launch too small to fill the SMs even with 64 x 64 tiles (the upper
+  // levels' M2M / L2L: a few hundred columns) is bound by ONE CTA's serial
+  // K loop (41 us per launch at K = 488, ncu profiles/round2): 32 x 32 tiles
+  // cut that loop's DMMA count four-fold and put four times the SMs to work
   if (a.M > 64) {
     if (ctas(128, 128) >= want) return launch<128, 128, 32>(a, max_cols_per_batch, batches, st);
     if (ctas(128, 64) >= want) return launch<128, 64, 32>(a, max_cols_per_batch, batches, st);
-    return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+    if (ctas(64, 64) >= 148) return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+    return launch<32, 32, 16>(a, max_cols_per_batch, batches, st);
   }
   if (a.M > 32) {
     if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
-    return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+    if (ctas(64, 64) >= 148) return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+    return launch<32, 32, 16>(a, max_cols_per_batch, batches, st);
   }
   if (ctas(32, 128) >= want) return launch<32, 128, 32>(a, max_cols_per_batch, batches, st);
   return launch<32, 64, 16>(a, max_cols_per_batch, batches, st);

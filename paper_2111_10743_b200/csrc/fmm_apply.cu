@@ -570,7 +570,24 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
   // leaves hold few targets (~17 on average at ncrit 120): the target pass
   // is the leaf's own size (not a power of two: 17 targets would leave 15 of
   // every 32 threads idle) and the remaining threads take other source phases
-  const int kTgt = (int)min((int64_t)kLeafBT, max((int64_t)1, t1 - t0));
+  // A leaf with 65 - 127 targets (ncrit 300 on a 4x oversampled surface: ~75)
+  // would run one phase with 40% of the threads idle: cut its targets into P
+  // passes of ceil(nt / P) so that kSplit = kLeafBT / kTgt source phases fill
+  // the block; P minimises passes x sources-per-phase (+5% per pass for the
+  // re-staged tiles)
+  const int ntl = (int)min((int64_t)kLeafBT, max((int64_t)1, t1 - t0));
+  int kTgt = ntl;
+  {
+    double best = 1e30;
+    for (int p = 1; p <= 4; ++p) {
+      const int kt = (ntl + p - 1) / p;
+      const double cost = p * (1.0 / (kLeafBT / kt) + 0.05);
+      if (cost < best - 1e-12) {
+        best = cost;
+        kTgt = kt;
+      }
+    }
+  }
   const int kSplit = kLeafBT / kTgt;
   const int64_t ub = u_off[li], nu = u_off[li + 1] - ub;
   const int64_t wb = w_off[li], nw = w_off[li + 1] - wb;
@@ -1321,22 +1338,45 @@ int build_device(lb_fmm_plan* P) {
   // X list (fmm.py:891-911): boxes with sourceful X entries; leaf stage
   // (fmm.py:940-988): target leaves, their U (with sources) and W lists.
   // Count / scan / fill, parallel over boxes, same order as a serial walk.
+  // With xw_direct (lb_fmm_plan_set_xw) two of the reference's approximate
+  // interactions are evaluated exactly where that is also cheaper:
+  //  * an X-list entry (target box b, source leaf x) of a LEAF b with few
+  //    targets (2.5 nt(b) <= nrep): x's sources act directly on b's targets
+  //    (joins b's U list) instead of on b's nrep check points;
+  //  * a W-list entry (target leaf b, box w) whose w is a leaf with at most
+  //    nrep sources: w's sources act directly (joins b's U list) instead of
+  //    w's nrep equivalent charges.
+  // Appended after the reference's U entries, X first, in list order.
+  const bool xw = P->xw_direct != 0;
+  auto x_direct = [&](int64_t b) {
+    const int64_t ntb = t.tgt_hi[b] - t.tgt_lo[b];
+    return xw && t.is_leaf[b] && ntb > 0 && 5 * ntb <= 2 * (int64_t)nrep;
+  };
+  auto w_direct = [&](int64_t w) { return xw && t.is_leaf[w] && t.src_hi[w] - t.src_lo[w] <= (int64_t)nrep; };
   std::vector<int64_t> xcnt(nb, 0), ucnt(nb, 0), wcnt(nb, 0);
   std::vector<uint8_t> is_tl(nb, 0);
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t b = 0; b < nb; ++b) {
     if (!own_id[b]) continue;  // as for M2L
+    const bool xd = x_direct(b);
+    int64_t nx = 0;
     for (int64_t q = 0; q < t.xlist.size(b); ++q) {
       const int64_t x = t.xlist.row(b)[q];
-      xcnt[b] += t.src_hi[x] > t.src_lo[x] ? 1 : 0;
+      nx += t.src_hi[x] > t.src_lo[x] ? 1 : 0;
     }
+    if (!xd) xcnt[b] = nx;
     if (!t.is_leaf[b]) continue;
     is_tl[b] = 1;
+    if (xd) ucnt[b] += nx;
     for (int64_t q = 0; q < t.ulist.size(b); ++q) {
       const int64_t u = t.ulist.row(b)[q];
       ucnt[b] += t.src_hi[u] > t.src_lo[u] ? 1 : 0;
     }
-    wcnt[b] = t.wlist.size(b);
+    for (int64_t q = 0; q < t.wlist.size(b); ++q) {
+      const int64_t w = t.wlist.row(b)[q];
+      if (w_direct(w)) ucnt[b] += t.src_hi[w] > t.src_lo[w] ? 1 : 0;
+      else ++wcnt[b];
+    }
   }
   std::vector<int64_t> xb, xo{0}, tl, uo{0}, wo{0}, xpos(nb), upos(nb), wpos(nb);
   for (int64_t b = 0; b < nb; ++b) {
@@ -1369,8 +1409,21 @@ int build_device(lb_fmm_plan* P) {
         const int64_t u = t.ulist.row(b)[q];
         if (t.src_hi[u] > t.src_lo[u]) ul[o++] = S[u];
       }
-      o = wpos[b];
-      for (int64_t q = 0; q < t.wlist.size(b); ++q) wl[o++] = S[t.wlist.row(b)[q]];
+      if (x_direct(b)) {
+        for (int64_t q = 0; q < t.xlist.size(b); ++q) {
+          const int64_t x = t.xlist.row(b)[q];
+          if (t.src_hi[x] > t.src_lo[x]) ul[o++] = S[x];
+        }
+      }
+      int64_t ow = wpos[b];
+      for (int64_t q = 0; q < t.wlist.size(b); ++q) {
+        const int64_t w = t.wlist.row(b)[q];
+        if (w_direct(w)) {
+          if (t.src_hi[w] > t.src_lo[w]) ul[o++] = S[w];
+        } else {
+          wl[ow++] = S[w];
+        }
+      }
     }
   }
   D.n_x = (int64_t)xb.size();
@@ -2152,6 +2205,15 @@ int lb_fmm_plan_set_target_range(lb_fmm_plan* P, int64_t t0, int64_t t1) {
   P->own_t0 = t0;
   P->own_t1 = t1;
   fmm_release_device(P);  // lists are rebuilt on the next apply
+  return LB_OK;
+}
+
+int lb_fmm_plan_set_xw(lb_fmm_plan* P, int direct) {
+  if (!P) return fail(LB_ERR_ARG, "null plan");
+  if (direct != 0 && direct != 1) return fail(LB_ERR_ARG, "lb_fmm_plan_set_xw: mode must be 0 or 1");
+  if (direct == P->xw_direct) return LB_OK;
+  P->xw_direct = direct;
+  fmm_release_device(P);  // the U / W / X device lists are rebuilt on the next apply
   return LB_OK;
 }
 

@@ -163,6 +163,7 @@ struct lb_fmm_plan {
   int64_t own_s0 = 0, own_s1 = -1;          // owned sources [s0, s1) of the upward pass; s1 < 0: all
   lb_fmm_upward_hook up_hook = nullptr;     // sums the ranks' partial upward expansions
   void* up_hook_user = nullptr;
+  int xw_direct = 0;                        // 1: cheap X / W entries evaluated directly (lb_fmm_plan_set_xw)
   int m2l_slices = 0;                       // 0: fp64 DGEMM M2L; 3..8: tcgen05 int8 slices;
                                             // -1: low-rank factors (fp64 DGEMM pair)
   std::vector<int32_t> lr_rank;             // per canonical key

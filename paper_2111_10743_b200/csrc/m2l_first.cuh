@@ -8,14 +8,17 @@
 // tensor-pipe time on padding at BASELINE config 3 (ncu, profiles/round2:
 // 61% pipe-active for 35% useful).  Here a CTA owns ALL rows of its batch in
 // 8-row M-tiles (ceil(r_k / 8) of them, nothing padded past the last tile),
-// 128 columns, and its 8 warps split the columns (16 each), so every warp
-// runs ceil(r_k / 8) x 2 independent DMMA chains per 4-deep k-step and no
-// warp idles on a ragged M.  K (= nrep) streams in chunks of 32 through a
+// 128 columns; of its 16 warps eight take the first half of the M-tiles and
+// eight the second, 16 columns each (8 warps per CTA left the tensor pipe at
+// 62%: two warps per scheduler do not cover the DMMA issue latency), so a warp
+// runs about ceil(r_k / 16) x 2 independent DMMA chains per 4-deep k-step.  K (= nrep) streams in chunks of 32 through a
 // three-stage cp.async pipeline; k-steps past K are skipped, not zero-padded.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "dgemm_cols.cuh"
 
@@ -23,7 +26,7 @@ namespace lb {
 namespace m2l1 {
 
 constexpr int kBN = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;  // 16 warps: 2 (halves of the M-tiles) x 8 (16 columns each)
 constexpr int kStages = 3;
 constexpr int kMaxMT = 14;  // rank <= 112 (m2l_fused.cuh: kMaxKS * 4)
 
@@ -65,9 +68,12 @@ __device__ __forceinline__ void run_tile(const Args& g, double* dsm, const doubl
   // 16-byte copies need even K (row / column strides) and aligned bases
   const bool v16 = (K & 1) == 0 && (((uintptr_t)A | (uintptr_t)g.X) & 15) == 0;
 
-  double acc[NMT][2][2];
+  // warps 0-7 take the first H M-tiles, warps 8-15 the rest; 16 columns each
+  constexpr int H = (NMT + 1) / 2;
+  const int wm = warp >> 3, wn = warp & 7;
+  double acc[H][2][2];
 #pragma unroll
-  for (int i = 0; i < NMT; ++i)
+  for (int i = 0; i < H; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -103,6 +109,24 @@ __device__ __forceinline__ void run_tile(const Args& g, double* dsm, const doubl
       }
     }
   };
+  // one K chunk of this warp's NM M-tiles (compile-time NM)
+  auto chunk = [&](auto nm_c, const double* as, const double* xs, int ksn) {
+    constexpr int NM = decltype(nm_c)::value;
+#pragma unroll
+    for (int ks = 0; ks < dg::kKC / 4; ++ks) {
+      if (ks >= ksn) break;
+      const int kk = ks * 4 + tq;
+      const double b0 = xs[kk], b1 = xs[8 * dg::kLD + kk];
+      double a[NM > 0 ? NM : 1];
+#pragma unroll
+      for (int mt = 0; mt < NM; ++mt) a[mt] = as[mt * 8 * dg::kLD + kk];
+#pragma unroll
+      for (int mt = 0; mt < NM; ++mt) {
+        dg::dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
+        dg::dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
+      }
+    }
+  };
 
   // prologue: kStages - 1 chunks in flight (empty groups keep the count uniform)
 #pragma unroll
@@ -116,34 +140,23 @@ __device__ __forceinline__ void run_tile(const Args& g, double* dsm, const doubl
     if (i + kStages - 1 < nchunk) load((i + kStages - 1) % kStages, (i + kStages - 1) * dg::kKC);
     dg::cp_commit();
     const int buf = i % kStages;
-    const double* as = As(buf) + gq * dg::kLD;
-    const double* xs = Xs(buf) + (warp * 16 + gq) * dg::kLD;
+    const double* as = As(buf) + (wm * H * 8 + gq) * dg::kLD;
+    const double* xs = Xs(buf) + (wn * 16 + gq) * dg::kLD;
     const int ksn = min(dg::kKC / 4, (K - i * dg::kKC + 3) / 4);  // k-steps with any k < K
-#pragma unroll
-    for (int ks = 0; ks < dg::kKC / 4; ++ks) {
-      if (ks >= ksn) break;
-      const int kk = ks * 4 + tq;
-      const double b0 = xs[kk], b1 = xs[8 * dg::kLD + kk];
-      double a[NMT];
-#pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) a[mt] = as[mt * 8 * dg::kLD + kk];
-#pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) {
-        dg::dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
-        dg::dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
-      }
-    }
+    if (wm == 0) chunk(std::integral_constant<int, H>{}, as, xs, ksn);
+    else chunk(std::integral_constant<int, NMT - H>{}, as, xs, ksn);
   }
-  // epilogue: D[row = mt*8 + gq][col = warp*16 + nt*8 + 2 tq + h], scaled by 1/h
+  // epilogue: D[row = mt*8 + gq][col = wn*16 + nt*8 + 2 tq + h], scaled by 1/h
+  const int nm_w = wm == 0 ? H : NMT - H;
 #pragma unroll
-  for (int mt = 0; mt < NMT; ++mt) {
-    const int row = mt * 8 + gq;
-    if (row >= Mz) continue;
+  for (int mt = 0; mt < H; ++mt) {
+    const int row = (wm * H + mt) * 8 + gq;
+    if (mt >= nm_w || row >= Mz) continue;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = warp * 16 + nt * 8 + 2 * tq + h;
+        const int c = wn * 16 + nt * 8 + 2 * tq + h;
         double* y = yout[c];
         if (y) y[row] = alph[c] * acc[mt][nt][h];
       }

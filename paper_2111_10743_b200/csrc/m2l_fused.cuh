@@ -234,7 +234,7 @@ __device__ __forceinline__ void gemm_round_ldg(const double* __restrict__ A, int
 }
 
 // all rounds of this warp: M-tiles warp, warp + kWarps, ... in groups of kMW
-template <int NTN>
+template <int NTN, bool RING>
 __device__ __forceinline__ void gemm_phase(const double* __restrict__ Ap, const double* __restrict__ Arow,
                                            int r, int nrep, const double* Ts, double* Ys, int LY,
                                            double* ring_base) {
@@ -243,7 +243,7 @@ __device__ __forceinline__ void gemm_phase(const double* __restrict__ Ap, const 
   double* const ring = ring_base + (size_t)warp * kRing * kMW * 64;
   for (int mt0 = warp; mt0 < mtiles; mt0 += kMW * kWarps) {
     const int nm = min(kMW, (mtiles - mt0 + kWarps - 1) / kWarps);
-    if (!Ap) {
+    if constexpr (!RING) {
       switch (nm) {
         case 1: gemm_round_ldg<NTN, 1>(Arow, r, nrep, mt0, Ts, Ys, LY); break;
         case 2: gemm_round_ldg<NTN, 2>(Arow, r, nrep, mt0, Ts, Ys, LY); break;
@@ -261,6 +261,7 @@ __device__ __forceinline__ void gemm_phase(const double* __restrict__ Ap, const 
   }
 }
 
+template <bool RING>
 __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <= 128 registers
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_poff[kCols];         // perm row offset (offset index x nrep) of the pass's pairs
@@ -318,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
       dg::cp_wait<0>();
     }
     __syncthreads();
-    if (ntn == 1) gemm_phase<1>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
-    else gemm_phase<kNT>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+    if (ntn == 1) gemm_phase<1, RING>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+    else gemm_phase<kNT, RING>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
     __syncthreads();
     // per target group and density, pairs in order, through the permutation:
     // one index per (pair, row) for all densities, four pairs in flight
@@ -386,14 +387,19 @@ inline cudaError_t launch(const Args& a, int64_t nunits, cudaStream_t st) {
       a.nrep > max_nrep())
     return cudaErrorInvalidValue;
   if ((a.A == nullptr) == use_ring(a.nrep) || !a.Arow) return cudaErrorInvalidValue;
-  static int attr = 0;
-  const int need = (int)smem_bytes(a.nrep, a.A != nullptr);
-  if (need > attr) {
-    const cudaError_t e = cudaFuncSetAttribute(m2l_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+  const bool ring = a.A != nullptr;
+  const int need = (int)smem_bytes(a.nrep, ring);
+  static int attr[2] = {0, 0};
+  if (need > attr[ring]) {
+    const cudaError_t e = ring ? cudaFuncSetAttribute(m2l_fused_kernel<true>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, need)
+                               : cudaFuncSetAttribute(m2l_fused_kernel<false>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, need);
     if (e != cudaSuccess) return e;
-    attr = need;
+    attr[ring] = need;
   }
-  m2l_fused_kernel<<<(unsigned)nunits, kThreads, need, st>>>(a);
+  if (ring) m2l_fused_kernel<true><<<(unsigned)nunits, kThreads, need, st>>>(a);
+  else m2l_fused_kernel<false><<<(unsigned)nunits, kThreads, need, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -364,7 +364,7 @@ class FmmPlan:
     def __init__(self, source_positions, target_positions, eps,
                  ncrit: int = 120, m: int | None = None,
                  buffer: int | None = None, rep: str | None = None,
-                 device_sort: bool | None = None, m2l="auto"):
+                 device_sort: bool | None = None, m2l="auto", xw: str = "lists"):
         self.spos = np.ascontiguousarray(_host(source_positions), dtype=float)
         self.tpos = np.ascontiguousarray(_host(target_positions), dtype=float)
         self.eps = float(eps)
@@ -393,6 +393,25 @@ class FmmPlan:
         self._set_operators()
         self._tree = None
         self.set_m2l(m2l)
+        self.xw = "lists"
+        self.set_xw(xw)
+
+    def set_xw(self, xw: str = "lists"):
+        """How X- and W-list entries are evaluated (the lists themselves are
+        always the reference's, fmm.py:650-715).  "lists": as the reference
+        does (sources on check points, fmm.py:888-911; equivalent charges on
+        targets, fmm.py:966-988).  "direct": an X entry of a target LEAF with
+        2.5 nt <= nrep and a W entry whose box is a leaf with <= nrep sources
+        are summed directly, leaf sources on leaf targets (lb_fmm_plan_set_xw):
+        exact where the reference approximates, and fewer pair evaluations on
+        surfaces (BASELINE config 3: 757 M X-list lattice pairs -> 116 M
+        direct pairs per density).  No reference counterpart; results move
+        within eps."""
+        if xw not in ("lists", "direct"):
+            raise ValueError(f"xw must be 'lists' or 'direct', not {xw!r}")
+        _lib.check(self._L.lb_fmm_plan_set_xw(self._h, 1 if xw == "direct" else 0),
+                   "lb_fmm_plan_set_xw")
+        self.xw = xw
 
     def set_m2l(self, m2l="auto"):
         """M2L arithmetic: "fp64" (DGEMM on the dense canonical matrices, the
@@ -542,9 +561,19 @@ class FmmPlan:
                 s = np.concatenate([[0.0], np.cumsum(w[idx], dtype=np.float64)])
                 v = s[off[1:]] - s[off[:-1]]
             return v
-        u_src = per_box_sum(r["u_off"], r["u"], ns_box.astype(float))
+        nsf = ns_box.astype(float)
+        u_src = per_box_sum(r["u_off"], r["u"], nsf)
+        x_src = per_box_sum(r["x_off"], r["x"], nsf)
         w_cnt = np.diff(r["w_off"]).astype(float)
-        x_src = per_box_sum(r["x_off"], r["x"], ns_box.astype(float))
+        if self.xw == "direct":  # the moves lb_fmm_plan_set_xw makes (fmm_apply.cu build_device)
+            xd = leaf & (nt_box > 0) & (5 * nt_box <= 2 * nrep)
+            u_src = u_src + np.where(xd, x_src, 0.0)
+            x_src = np.where(xd, 0.0, x_src)
+            wd_box = leaf & (ns_box <= nrep)          # W members evaluated directly
+            w_dir_src = per_box_sum(r["w_off"], r["w"], np.where(wd_box, nsf, 0.0))
+            w_dir_cnt = per_box_sum(r["w_off"], r["w"], wd_box.astype(float))
+            u_src = u_src + w_dir_src
+            w_cnt = w_cnt - w_dir_cnt
         surface = self.rep == "surface"
         out = {"u_pairs": float(np.dot(nt_box, u_src)),
                "w_pairs": float(np.dot(nt_box, w_cnt)) * nrep,

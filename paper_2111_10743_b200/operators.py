@@ -489,6 +489,11 @@ class LayerOperatorSet:
                     eps/100, fp64, fmm_plan.m2l_factors), "fp64" (the dense
                     canonical operators, the reference's arithmetic) or a
                     slice count in [3, 8] (tcgen05 int8 Ozaki slices).
+      fmm_xw      : X / W list evaluation of that plan (FmmPlan.set_xw):
+                    "direct" (default: entries that are cheaper as direct
+                    leaf-to-leaf sums are evaluated exactly) or "lists" (every
+                    entry as the reference evaluates it, fmm.py:888-911,
+                    966-988).
       fuse_a3     : A3 with exact sweeps runs its second sweep fused with the
                     glue (one accumulator, eta from Phi = S^T w: eta_weights,
                     lb_opset_set_eta_weights); False keeps the four-output
@@ -504,7 +509,8 @@ class LayerOperatorSet:
     def __init__(self, disc, formulation: str, eps: float, eta: float = 2.0,
                  use_fmm: bool = True, near=None, extra_kinds=(),
                  corrections=None, far: str = "auto", fmm_ncrit: int = 120,
-                 fmm_m2l="auto", correction_cache=None, fuse_a3: bool = True):
+                 fmm_m2l="auto", correction_cache=None, fuse_a3: bool = True,
+                 fmm_xw: str = "direct"):
         self.disc = disc
         self.formulation = formulation.lower()
         if self.formulation not in FORMULATIONS:
@@ -558,7 +564,7 @@ class LayerOperatorSet:
                                          n * nover > self.FMM_CROSSOVER)):
             from .fmm_plan import FmmPlan
             self._plan = FmmPlan(disc.over_nodes, disc.nodes, self.eps,
-                                 ncrit=fmm_ncrit, m2l=fmm_m2l)
+                                 ncrit=fmm_ncrit, m2l=fmm_m2l, xw=fmm_xw)
             self.dev.set_fmm(self._plan)
             self.far = "fmm"
         else:

@@ -247,7 +247,7 @@ class ShardedOperatorSet:
 
     def __init__(self, disc, formulation, eps, corrections=None, group=None,
                  far="direct", near=None, eta: float = 2.0, cap: int = 128,
-                 fmm_ncrit: int = 120, fmm_m2l="auto", morton: bool = True,
+                 fmm_ncrit: int = 120, fmm_m2l="auto", morton: bool = True, fmm_xw: str = "direct",
                  distributed_upward: bool = True):
         import torch.distributed as dist
         from . import _lib
@@ -290,7 +290,7 @@ class ShardedOperatorSet:
         self._plan = None
         if far == "fmm":
             from .fmm_plan import FmmPlan
-            plan = FmmPlan(geom.over_nodes, geom.nodes, self.eps, ncrit=fmm_ncrit, m2l=fmm_m2l)
+            plan = FmmPlan(geom.over_nodes, geom.nodes, self.eps, ncrit=fmm_ncrit, m2l=fmm_m2l, xw=fmm_xw)
             plan.set_target_range(r0, r0 + nr)
             if distributed_upward and world > 1:
                 # this rank's sources = its patches' oversampled nodes

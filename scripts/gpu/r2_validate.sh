@@ -1,0 +1,24 @@
+# Round-2 validation on one B200: GPU tests, smoke, both bench arms, then the
+# ncu launch list and full captures of the config-3 step (profiles/round2).
+# SKIP_TESTS=1 skips the pytest leg.
+set -x
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+if [ -z "$SKIP_TESTS" ]; then
+timeout 1500 python -m pytest tests -m gpu -x -q --durations=10 -p no:cacheprovider > gpurun_out/gputest.log 2>&1
+echo "pytest rc=$?"
+tail -4 gpurun_out/gputest.log
+fi
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?"
+timeout 900 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err
+echo "bench rc=$?"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err
+echo "bench ref rc=$?"
+timeout 600 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python scripts/profile_step.py > gpurun_out/c3_launches.log 2>&1
+echo "launches rc=$?"
+timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"first_kernel|leaf_kernel|lattice_pot|csr_epi" -c 10 -f -o gpurun_out/c3_full python scripts/profile_step.py > gpurun_out/c3_full.log 2>&1
+echo "full rc=$?"
+timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"m2l_fused" -c 4 -f -o gpurun_out/c3_full_m2l python scripts/profile_step.py > gpurun_out/c3_full_m2l.log 2>&1
+echo "full m2l rc=$?"
+ls -la gpurun_out

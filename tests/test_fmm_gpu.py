@@ -248,3 +248,46 @@ def test_fmm_plan_reuse_and_grid_surface_dipoles(cuda):
             ref = b.evaluate_direct(b.FmmSources(x, ch, dip), x[idx], ("pot", "grad"))
             assert rel_errs(res.pot[:, idx], ref.pot, 2) <= 10 * eps
             assert rel_errs(res.grad[:, idx], ref.grad, 2) <= 10 * eps
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-9])
+def test_xw_direct_is_within_eps_and_no_worse(cuda, eps):
+    """FmmPlan(xw="direct") evaluates the cheap X / W entries as direct leaf
+    sums (lb_fmm_plan_set_xw): a non-uniform surface cloud (adaptive tree, so
+    W and X lists are non-empty) must stay within eps of the exact sum, must
+    not be less accurate than the reference's evaluation of the same lists,
+    the two must agree within eps, and the work counts must move pairs out of
+    the X / W stages without changing the V list."""
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    b = _b()
+    rng = np.random.default_rng(21)
+    # a torus surface sampled unevenly: dense cap + sparse rest
+    n = 30000
+    u = np.concatenate([rng.uniform(0, 0.4, n // 2), rng.uniform(0, 2 * np.pi, n - n // 2)])
+    v = np.concatenate([rng.uniform(0, 0.4, n // 2), rng.uniform(0, 2 * np.pi, n - n // 2)])
+    x = np.stack([(2 + np.cos(u)) * np.cos(v), (2 + np.cos(u)) * np.sin(v), np.sin(u)], axis=1)
+    tgt = x[::4].copy()
+    q = rng.standard_normal((2, n))
+    d = rng.standard_normal((2, n, 3))
+    exact = b.evaluate_direct(b.FmmSources(x, q, d), tgt, ("pot", "grad", "hess"))
+    plan = FmmPlan(x, tgt, eps, ncrit=150, m2l="fp64", xw="lists")
+    wl = plan.work_counts()
+    assert wl["w_pairs"] > 0 and wl["x_pairs"] > 0, "the cloud must exercise the W and X lists"
+    a = plan.apply(q, d, ("pot", "grad", "hess"))
+    plan.set_xw("direct")
+    wd = plan.work_counts()
+    c = plan.apply(q, d, ("pot", "grad", "hess"))
+    assert wd["v_pairs"] == wl["v_pairs"]
+    assert wd["x_pairs"] < wl["x_pairs"] and wd["w_pairs"] < wl["w_pairs"]
+    assert wd["u_pairs"] > wl["u_pairs"]
+    for name in ("pot", "grad", "hess"):
+        ea = rel_errs(getattr(a, name), getattr(exact, name), 2)
+        ec = rel_errs(getattr(c, name), getattr(exact, name), 2)
+        assert ec <= eps, (name, ec)
+        assert ec <= 2.0 * ea + eps / 100, (name, ea, ec)
+        assert rel_errs(getattr(c, name), getattr(a, name), 2) <= eps, name
+    plan.set_xw("lists")  # and back: the reference's evaluation again, bit for bit
+    a2 = plan.apply(q, d, ("pot", "grad", "hess"))
+    assert np.array_equal(a2.pot, a.pot) and np.array_equal(a2.grad, a.grad)
+    with pytest.raises(ValueError):
+        plan.set_xw("sometimes")
