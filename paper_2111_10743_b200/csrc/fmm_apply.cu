@@ -570,22 +570,24 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
   // leaves hold few targets (~17 on average at ncrit 120): the target pass
   // is the leaf's own size (not a power of two: 17 targets would leave 15 of
   // every 32 threads idle) and the remaining threads take other source phases
-  // A leaf with 65 - 127 targets (ncrit 300 on a 4x oversampled surface: ~75)
-  // would run one phase with 40% of the threads idle: cut its targets into P
-  // passes of ceil(nt / P) so that kSplit = kLeafBT / kTgt source phases fill
-  // the block; P minimises passes x sources-per-phase (+5% per pass for the
+  // A leaf whose target count is not close to a divisor of the block (ncrit
+  // 300 on a 4x oversampled surface: ~75 of 128; a 150-target leaf: 128 + 22)
+  // would leave many threads idle: cut its targets into P balanced passes of
+  // ceil(nt / P) so that kSplit = kLeafBT / kTgt source phases fill the
+  // block; P minimises passes x sources-per-phase (+5% per pass for the
   // re-staged tiles)
-  const int ntl = (int)min((int64_t)kLeafBT, max((int64_t)1, t1 - t0));
-  int kTgt = ntl;
+  const int ntl = (int)max((int64_t)1, t1 - t0);
+  int kTgt = min(ntl, kLeafBT);
   {
     double best = 1e30;
-    for (int p = 1; p <= 4; ++p) {
+    for (int p = (ntl + kLeafBT - 1) / kLeafBT; p <= 16; ++p) {
       const int kt = (ntl + p - 1) / p;
       const double cost = p * (1.0 / (kLeafBT / kt) + 0.05);
       if (cost < best - 1e-12) {
         best = cost;
         kTgt = kt;
       }
+      if (kt == 1) break;
     }
   }
   const int kSplit = kLeafBT / kTgt;

@@ -1,6 +1,6 @@
-# Round-2 validation on one B200: GPU tests, smoke, both bench arms, then the
-# ncu launch list and full captures of the config-3 step (profiles/round2).
-# SKIP_TESTS=1 skips the pytest leg.
+# Round-2 validation on one B200: GPU tests, smoke, both bench arms, the ncu
+# launch list of the config-3 step and full captures of its top kernels
+# (copied into profiles/round2 by hand).  SKIP_TESTS=1 skips the pytest leg.
 set -x
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
@@ -17,8 +17,9 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 echo "bench ref rc=$?"
 timeout 600 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python scripts/profile_step.py > gpurun_out/c3_launches.log 2>&1
 echo "launches rc=$?"
-timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"first_kernel|leaf_kernel|lattice_pot|csr_epi" -c 10 -f -o gpurun_out/c3_full python scripts/profile_step.py > gpurun_out/c3_full.log 2>&1
+# first_kernel, leaf, csr pass 1 of call 1 + the largest fused launch: ~5 MB each
+timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"first_kernel|leaf_kernel|csr_epi" -c 3 -f -o gpurun_out/c3_full python scripts/profile_step.py > gpurun_out/c3_full.log 2>&1
 echo "full rc=$?"
-timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"m2l_fused" -c 4 -f -o gpurun_out/c3_full_m2l python scripts/profile_step.py > gpurun_out/c3_full_m2l.log 2>&1
+timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"m2l_fused" --launch-skip 2 -c 1 -f -o gpurun_out/c3_full_m2l python scripts/profile_step.py > gpurun_out/c3_full_m2l.log 2>&1
 echo "full m2l rc=$?"
-ls -la gpurun_out
+du -sh gpurun_out

@@ -18,7 +18,7 @@ q = torch.from_numpy(np.random.default_rng(3).standard_normal((2, len(s)))).cuda
 pot = torch.empty((2, len(t)), dtype=torch.float64, device="cuda")
 grad = torch.empty((2, len(t), 3), dtype=torch.float64, device="cuda")
 for ncrit in [int(a) for a in sys.argv[1:]] or [150, 200, 300, 400, 500, 700]:
-    plan = FmmPlan(s, t, 5e-8, ncrit=ncrit)
+    plan = FmmPlan(s, t, 5e-8, ncrit=ncrit, xw=os.environ.get("LB_XW", "direct"))
     row = {"ncrit": ncrit}
     for nd in (1, 2):
         for _ in range(2):
