@@ -202,6 +202,10 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the oracle has no FMM: this arm's far field is the exact sum (the reference's "
+                "use_fmm=False path).  The reference's own Python FmmPlan far field at this "
+                "config, timed in the build container on 8 vCPU: 59.7 s per apply "
+                "(profiles/round2/reference_fmm_config3_cpu.json)",
     }), flush=True)
 
 
