@@ -1175,6 +1175,52 @@ int build_device(lb_fmm_plan* P) {
   D.n_p2m = (int64_t)p2m.size();
   LB_TRY(upload(&D.p2m_leaves, p2m));
   if (src_range) LB_TRY(upload(&D.src_own, src_own));
+  // X / W entries evaluated directly (lb_fmm_plan_set_xw; the lists below)
+  const bool xw = P->xw_direct != 0;
+  auto x_direct = [&](int64_t b) {
+    const int64_t ntb = t.tgt_hi[b] - t.tgt_lo[b];
+    return xw && t.is_leaf[b] && ntb > 0 && 5 * ntb <= 2 * (int64_t)nrep;
+  };
+  auto w_direct = [&](int64_t w) { return xw && t.is_leaf[w] && t.src_hi[w] - t.src_lo[w] <= (int64_t)nrep; };
+  // Translations nobody reads are skipped (the reference computes them,
+  // fmm.py:853-871, 913-935; the results at the targets are unchanged):
+  //  * a box's multipole is NEEDED if it is a V-list source or a (non-direct)
+  //    W-list member of any box with targets -- on every rank: the ranks'
+  //    partial expansions are summed -- or if its parent's is; an M2M edge
+  //    child -> parent exists only for needed parents (the root's and level
+  //    1's expansions are never read);
+  //  * a box's local expansion is NONZERO if it has V-list sources or
+  //    (non-direct) X-list leaves, or its parent's is; an L2L edge parent ->
+  //    child exists only for nonzero parents, and a level without any nonzero
+  //    box gets its local expansions zeroed instead of computed.
+  std::vector<uint8_t> need_up(nb, 0), nz_dn(nb, 0);
+  for (int64_t b = 0; b < nb; ++b) {
+    if (t.tgt_hi[b] <= t.tgt_lo[b]) continue;
+    for (int64_t q = 0; q < t.vlist.size(b); ++q) need_up[t.vlist.row(b)[q]] = 1;
+    if (t.is_leaf[b])
+      for (int64_t q = 0; q < t.wlist.size(b); ++q) {
+        const int64_t w = t.wlist.row(b)[q];
+        if (!w_direct(w)) need_up[w] = 1;
+      }
+    bool dc = t.vlist.size(b) > 0;
+    if (!dc && !x_direct(b))
+      for (int64_t q = 0; q < t.xlist.size(b) && !dc; ++q) {
+        const int64_t x = t.xlist.row(b)[q];
+        dc = t.src_hi[x] > t.src_lo[x];
+      }
+    nz_dn[b] = dc ? 1 : 0;
+  }
+  std::vector<uint8_t> level_loc(t.nlev, 0);
+  for (int l = 0; l < t.nlev; ++l)
+    for (int64_t b : t.levels[l]) {
+      const int64_t p = t.parent[b];
+      if (l > 0 && nz_dn[p]) nz_dn[b] = 1;
+      if (nz_dn[b] && own_id[b]) level_loc[l] = 1;
+    }
+  for (int l = 1; l < t.nlev; ++l)  // a needed parent needs its children
+    for (int64_t b : t.levels[l])
+      if (need_up[t.parent[b]]) need_up[b] = 1;
+  D.level_loc.assign(level_loc.begin(), level_loc.end());
   std::vector<int64_t> uc, upar, dch, dpar, mpar, mch8;
   D.up_off.assign(1, 0);
   D.dn_off.assign(1, 0);
@@ -1190,12 +1236,12 @@ int build_device(lb_fmm_plan* P) {
           const int oct = (int)octant[s];
           const int64_t p = t.parent[b];
           // fmm.py:855-859 (with a source range: subtrees holding owned sources)
-          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0 && nsrc_own(b) > 0) bu[oct].push_back(b);
+          if (!t.is_leaf[p] && t.nsrc[p] > 0 && t.nsrc[b] > 0 && nsrc_own(b) > 0 && need_up[p]) bu[oct].push_back(b);
           // fmm.py:923-935 passes down to every child; children without targets
           // in their subtree never reach an L2T or a leaf, so they are skipped
           // (the results at the targets are unchanged; a plan whose targets are
           // one rank's rows skips most of the downward pass)
-          if (own_id[b]) bd[oct].push_back(b);
+          if (own_id[b] && nz_dn[p]) bd[oct].push_back(b);
         }
       const int64_t ubase = (int64_t)uc.size();
       for (int oct = 0; oct < 8; ++oct) {
@@ -1349,12 +1395,6 @@ int build_device(lb_fmm_plan* P) {
   //    nrep sources: w's sources act directly (joins b's U list) instead of
   //    w's nrep equivalent charges.
   // Appended after the reference's U entries, X first, in list order.
-  const bool xw = P->xw_direct != 0;
-  auto x_direct = [&](int64_t b) {
-    const int64_t ntb = t.tgt_hi[b] - t.tgt_lo[b];
-    return xw && t.is_leaf[b] && ntb > 0 && 5 * ntb <= 2 * (int64_t)nrep;
-  };
-  auto w_direct = [&](int64_t w) { return xw && t.is_leaf[w] && t.src_hi[w] - t.src_lo[w] <= (int64_t)nrep; };
   std::vector<int64_t> xcnt(nb, 0), ucnt(nb, 0), wcnt(nb, 0);
   std::vector<uint8_t> is_tl(nb, 0);
 #pragma omp parallel for schedule(dynamic, 1024)
@@ -1965,8 +2005,12 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     const int64_t s0 = D.level_slot_off[l], s1 = D.level_slot_off[l + 1];
     if (surface) {  // local = h pinv_dn @ dcheck over the level's slots (fmm.py:920)
       const double hl = t.half / std::ldexp(1.0, l);
-      LB_TRY(gemm_contig(D.pinv_dn, nrep, nrep, nrep, D.dc + s0 * ND * nrep, nrep,
-                         D.loc + s0 * ND * nrep, nrep, (s1 - s0) * ND, hl, st));
+      if (D.level_loc[l]) {
+        LB_TRY(gemm_contig(D.pinv_dn, nrep, nrep, nrep, D.dc + s0 * ND * nrep, nrep,
+                           D.loc + s0 * ND * nrep, nrep, (s1 - s0) * ND, hl, st));
+      } else if (s1 > s0) {  // no check values anywhere on this level: local = 0
+        LB_CUDA(cudaMemsetAsync(D.loc + s0 * ND * nrep, 0, sizeof(double) * (s1 - s0) * ND * nrep, st));
+      }
     }
     if (l + 1 >= t.nlev) break;
     if (surface) {

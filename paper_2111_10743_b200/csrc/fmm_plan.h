@@ -81,6 +81,7 @@ struct FmmDevice {
   double *tnrm = nullptr, *tproj = nullptr, *snrm = nullptr;
   int64_t* btgt_oct = nullptr;               // octant (x | y<<1 | z<<2) of every slot
   std::vector<int64_t> level_slot_off;       // slot range of every level
+  std::vector<uint8_t> level_loc;            // per level: any owned box with a nonzero local expansion
   std::vector<int64_t> v_tpoff_host;         // host copy of v_tgt_pair_off
   // emulated-fp64 M2L on the tensor cores (ozaki.cuh), built on first use
   int oz_S = 0;                              // slices the A packs were built for
