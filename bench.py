@@ -328,6 +328,41 @@ def capture(torch, step, lib, _lib):
         return step, False, None
 
 
+def count_sharded_launches(torch, op, mgs, lib, _lib):
+    """Kernel launches of one sharded step on this rank: every local phase of
+    the apply (lb_opset_apply_phase) and the MGS are captured into throw-away
+    CUDA graphs and their kernel nodes counted (lb_graph_kernel_nodes).  The
+    collectives between the phases are not ours and are not counted; the
+    FMM's upward hook (an all-reduce) is replaced by a no-op while capturing."""
+    import ctypes
+    from paper_2111_10743_b200.sharding import ShardedApply
+    plan = op._plan
+    fn0 = getattr(plan, "_hook_fn", None) if plan is not None else None
+    if fn0 is not None:
+        plan.set_upward_hook(lambda up, nd, stream: None)
+    total = 0
+    try:
+        steps = [lambda p=p: op.dev.apply_phase(op._code, p, op._tau_p, op._out_p)
+                 for p in range(ShardedApply.NPHASES[op._code])] + [mgs]
+        for fn in steps:
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(g):
+                fn()
+            nk, nn = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(lib.lb_graph_kernel_nodes(ctypes.c_void_p(g.raw_cuda_graph()),
+                                                 ctypes.byref(nk), ctypes.byref(nn)),
+                       "lb_graph_kernel_nodes")
+            total += int(nk.value)
+    except Exception as exc:  # noqa: BLE001 - the count is a report, not the measurement
+        print(f"bench: launch count by capture failed ({exc})", file=sys.stderr)
+        total = None
+    finally:
+        if fn0 is not None:
+            plan.set_upward_hook(fn0)
+        torch.cuda.synchronize()
+    return total
+
+
 def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib, peak_tc=None):
     """Per-stage device times of one apply (lb_opset stage events) and of one
     pot+grad FMM call (lb_fmm stage events) with their rooflines: SpMV passes
@@ -475,6 +510,8 @@ def main():
                 print("bench: graph replay differs from the eager step; timing eagerly",
                       file=sys.stderr)
                 run_step, graphed = step, False
+    if world > 1:  # the rank's own kernels per step, counted from throw-away captures
+        nkern = count_sharded_launches(torch, op, mgs, lib, _lib)
     timer = Timer(torch, world, local, flush)
     times, clocks = timer(run_step, args.steps)
     t_step = timer.max_over_ranks(sum(times) / len(times))

@@ -511,6 +511,7 @@ class FmmPlan:
         """fn(up, nd, stream): called on the apply's stream between the M2M and
         the M2L with the (nbox, nd, nrep) upward expansions as a CUDA tensor
         view (lb_fmm_plan_set_upward_hook); None removes it."""
+        self._hook_fn = fn  # kept so a caller can swap the hook and put it back
         if fn is None:
             self._hook = None
             _lib.check(self._L.lb_fmm_plan_set_upward_hook(self._h, None, None))
