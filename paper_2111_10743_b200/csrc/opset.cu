@@ -372,28 +372,53 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
     constexpr int K = Mix::K, X = Mix::X;
     // column of entry k: the block-CSR index (one int32 start per block of
     // nb consecutive columns, quadrature.py:693-700: 4/nb bytes per entry)
-    // when the handle has one, else the scalar index (4 bytes per entry)
-    const double inv_nb = bstart ? 1.0 / bnb : 0.0;
+    // when the handle has one, else the scalar index (4 bytes per entry).
+    // A row is whole blocks, so entry k sits in block kb / nb + (k - kb) / nb:
+    // one 64-bit division per row, then a 32-bit multiply-high per entry
+    // (exact for k - kb < 2^32 / nb; rows hold at most cap * nb entries)
+    const int64_t bbase = bstart ? kb / bnb : 0;
+    const unsigned magic = bstart ? (unsigned)((0x100000000ull + bnb - 1) / (unsigned)bnb) : 0u;
     auto col = [&](int64_t kk) -> int {
       if (!bstart) return __ldg(indices + kk);
-      int64_t b = (int64_t)((double)kk * inv_nb);
-      b += (b + 1) * bnb <= kk ? 1 : 0;
-      b -= b * bnb > kk ? 1 : 0;
-      return __ldg(bstart + b) + (int)(kk - b * bnb);
+      const unsigned rel = (unsigned)(kk - kb);
+      const unsigned q = __umulhi(rel, magic);
+      return __ldg(bstart + bbase + q) + (int)(rel - q * (unsigned)bnb);
     };
-    for (; k + 3 * stride < ke; k += 4 * stride) {
-      int c[4];
+    // loads in flight per lane: the value streams are the kernel's HBM
+    // traffic; with two streams (A3 pass 1) four entries per lane left DRAM at
+    // 63% (ncu, profiles/round2), so fewer streams unroll deeper
+    // (B200, config 3: two streams 4 / 6 / 8 / 12 entries -> 1.30 / 1.10 / 1.03 /
+    // 1.23 ms; three streams 1 / 2 / 3 / 4 / 8 -> 1.54 / 1.44 / 1.47 / 1.59 / 1.62 ms)
+    constexpr int UR = K >= 3 ? 2 : 8;
+    for (; k + (UR - 1) * stride < ke; k += UR * stride) {
+      int c[UR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = col(k + stride * u);
+      for (int u = 0; u < UR; ++u) c[u] = col(k + stride * u);
+      if constexpr (K >= 3) {  // three streams: per-entry loads
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double v[K], xv[X];
+        for (int u = 0; u < UR; ++u) {
+          double v[K], xv[X];
 #pragma unroll
-        for (int q = 0; q < K; ++q) v[q] = __ldg(jobs.val[q] + k + stride * u);
+          for (int q = 0; q < K; ++q) v[q] = __ldg(jobs.val[q] + k + stride * u);
 #pragma unroll
-        for (int q = 0; q < X; ++q) xv[q] = __ldg(jobs.x[q] + c[u]);
+          for (int q = 0; q < X; ++q) xv[q] = __ldg(jobs.x[q] + c[u]);
 #pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(v[Mix::vi(j)], xv[Mix::xi(j)], acc[j]);
+          for (int j = 0; j < J; ++j) acc[j] = fma(v[Mix::vi(j)], xv[Mix::xi(j)], acc[j]);
+        }
+      } else {
+        double v[UR][K];
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+#pragma unroll
+          for (int q = 0; q < K; ++q) v[u][q] = __ldg(jobs.val[q] + k + stride * u);
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          double xv[X];
+#pragma unroll
+          for (int q = 0; q < X; ++q) xv[q] = __ldg(jobs.x[q] + c[u]);
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[j] = fma(v[u][Mix::vi(j)], xv[Mix::xi(j)], acc[j]);
+        }
       }
     }
     for (; k < ke; k += stride) {
