@@ -614,10 +614,15 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
     int64_t vbase = 0;  // virtual index of this batch's first source
     for (int64_t sb0 = 0; sb0 < nsets_all && vbase < ve; sb0 += kLeafMaxSets) {
       const int nsets = (int)min((int64_t)kLeafMaxSets, nsets_all - sb0);
-      __syncthreads();
-      if (threadIdx.x == 0) {  // prefix sizes of this batch of source sets
-        int64_t e = 0;
-        for (int q = 0; q < nsets; ++q) {
+      // prefix sizes of this batch of source sets: every thread looks its
+      // sets up (the list entry and its box's source range are two dependent
+      // global loads: one thread walking ~50 sets serially stalled the whole
+      // block), then warp 0 scans the counts.  One batch covers the whole
+      // list in all but the largest leaves, and it is the same for every
+      // target pass: built once then.
+      if (sb0 > 0 || nsets_all > kLeafMaxSets || tb == t0) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < nsets; q += kLeafBT) {
           const int64_t g = sb0 + q;
           int64_t box, cnt;
           if (g < nu) {
@@ -631,8 +636,22 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
             cnt = nrep;
           }
           set_box[q] = box;
-          e += cnt;
-          set_end[q] = e;
+          set_end[q] = cnt;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          int64_t carry = 0;
+          for (int q0 = 0; q0 < nsets; q0 += 32) {
+            const int q = q0 + threadIdx.x;
+            int64_t v = q < nsets ? set_end[q] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int64_t up = __shfl_up_sync(0xffffffffu, v, o);
+              if ((int)threadIdx.x >= o) v += up;
+            }
+            if (q < nsets) set_end[q] = carry + v;
+            carry += __shfl_sync(0xffffffffu, v, 31);
+          }
         }
       }
       __syncthreads();
