@@ -506,7 +506,10 @@ inline size_t l2t_smem(int n, int level) {
 // (surface) and its W-list boxes' upward-equivalent charges -- are walked as
 // ONE virtual list so every shared-memory tile is full; the block's threads
 // are split into kSplit source phases per target and combined at the end.
-constexpr int kLeafBT = 128;
+#ifndef LB_LEAF_BT
+#define LB_LEAF_BT 128
+#endif
+constexpr int kLeafBT = LB_LEAF_BT;
 constexpr int kLeafTS = 256;
 constexpr int kLeafMaxSets = 512;
 

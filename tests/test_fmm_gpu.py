@@ -291,3 +291,37 @@ def test_xw_direct_is_within_eps_and_no_worse(cuda, eps):
     assert np.array_equal(a2.pot, a.pot) and np.array_equal(a2.grad, a.grad)
     with pytest.raises(ValueError):
         plan.set_xw("sometimes")
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-9])
+def test_m2l_kernels_density_count_invariance(cuda, eps):
+    """The low-rank M2L kernels (csrc/m2l_first.cuh, csrc/m2l_fused.cuh) pack
+    kCols / nd whole pairs per pass, so the number of densities changes which
+    target groups run in several passes (their sums parked in the carry pool
+    between passes) -- but never the order in which a target's pairs are
+    added: a density's result is bit-identical whether it is evaluated alone
+    or as one of 2, 3 or 4.  eps 1e-6: surface lattice (the cp.async ring
+    variant); 1e-9: Chebyshev grid, nrep 729 (the register-prefetch variant)."""
+    torch = cuda
+    from paper_2111_10743_b200.fmm_plan import FmmPlan
+    rng = np.random.default_rng(31)
+    n = 30000
+    x = rng.standard_normal((n, 3))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    x[: n // 3] *= 0.6          # two shells: a volume-like V list (many pairs per target and key)
+    q = torch.from_numpy(rng.standard_normal((4, n))).cuda()
+    plan = FmmPlan(x, x, eps)   # default low-rank M2L
+    assert plan.m2l_slices == -1
+
+    def run(nd):
+        pot = torch.zeros((nd, n), dtype=torch.float64, device="cuda")
+        grad = torch.zeros((nd, n, 3), dtype=torch.float64, device="cuda")
+        plan.apply_device(q[:nd].contiguous(), None, nd, (1 << nd) - 1, 0, 1, pot, grad)
+        torch.cuda.synchronize()
+        return pot.cpu().numpy(), grad.cpu().numpy()
+    p1, g1 = run(1)
+    exact = _b().evaluate_direct(_b().FmmSources(x, q[:1].cpu().numpy()), x[:500], ("pot",))
+    assert rel_errs(p1[:, :500], exact.pot, 1) <= eps
+    for nd in (2, 3, 4):
+        p, g = run(nd)
+        assert np.array_equal(p[0], p1[0]) and np.array_equal(g[0], g1[0]), nd
