@@ -1768,12 +1768,32 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     for (int i = 0; i < 5; ++i) {
       cudaFree(D.lo_units[i]);
       cudaFree(D.lo_tiles[i]);
+      cudaFree(D.lo_unit_key[i]);
       D.lo_units[i] = nullptr;
       D.lo_tiles[i] = nullptr;
+      D.lo_unit_key[i] = nullptr;
     }
+    cudaFree(D.lo_keytab); cudaFree(D.lo_rt_tgt); cudaFree(D.lo_rt_off); cudaFree(D.lo_rt_grp);
+    D.lo_keytab = D.lo_rt_tgt = D.lo_rt_off = D.lo_rt_grp = nullptr;
     D.lo_ready = true;
   }
   if (nd < 1 || nd > 4) return fail(LB_ERR_ARG, "fmm: density chunk outside [1, 4]");
+  if (!D.lo_fit_done) {  // the cube-symmetry permutations in closed form (m2l_fused.cuh)
+    std::vector<int32_t> aff;
+    std::vector<uint32_t> coords;
+    std::vector<uint16_t> lut;
+    int m = 0;
+    if (m2lf::fit_symmetries(P->pts.data(), nrep, P->off_perm.data(), P->noff, aff, coords, lut, m)) {
+      LB_TRY(upload(&D.lo_aff, aff));
+      LB_TRY(upload(&D.lo_coords, coords));
+      LB_TRY(upload(&D.lo_lut, lut));
+      D.lo_lut_n = m * m * m;
+    }
+    if (std::getenv("LB_FMM_DEBUG"))
+      std::fprintf(stderr, "fmm: closed-form M2L permutations %s (nrep %d, %d offsets, lattice %d^3)\n",
+                   D.lo_aff ? "fitted" : "NOT fitted, table lookups", nrep, P->noff, m);
+    D.lo_fit_done = true;
+  }
   if (!D.lo_carry) {  // carry pool of the multi-pass groups (m2l_fused.cuh)
     int dev = 0, sms = 0;
     LB_CUDA(cudaGetDevice(&dev));
@@ -1784,31 +1804,100 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
     LB_CUDA(cudaMalloc((void**)&D.lo_carry_flag, sizeof(unsigned) * (size_t)D.lo_carry_slots));
     LB_CUDA(cudaMemset(D.lo_carry_flag, 0, sizeof(unsigned) * (size_t)D.lo_carry_slots));
   }
-  if (!D.lo_units[nd]) {  // units of whole target groups, <= one pass of columns where possible
-    std::vector<int64_t> units;
-    std::vector<int64_t>& ku = D.lo_key_units[nd];
-    ku.assign(nk + 1, 0);
+  if (!D.lo_keytab) {  // per key: A_k offsets, T offset per density, first pair, rank (m2l_fused.cuh)
+    std::vector<int64_t> ktab(5 * (size_t)std::max(nk, 1), 0);
     for (int k = 0; k < nk; ++k) {
-      ku[k] = (int64_t)(units.size() / 2);
+      ktab[5 * k] = D.lr_ap_off[k];
+      ktab[5 * k + 1] = P->lr_off[k] * nrep;
+      ktab[5 * k + 2] = D.lo_tbase1[k];
+      ktab[5 * k + 3] = D.v_key_pair_off[k];
+      ktab[5 * k + 4] = P->lr_rank[k];
+    }
+    LB_TRY(upload(&D.lo_keytab, ktab));
+    // every target's (target, key) groups by ascending key, for the ordered
+    // reduction of the groups' partial sums into the check values
+    const int64_t ng = D.v_key_tgt_off[nk];
+    std::vector<int64_t> vt(std::max<int64_t>(ng, 1));
+    if (ng) LB_CUDA(cudaMemcpy(vt.data(), D.v_tgts, 8 * ng, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> order(ng);
+    for (int64_t i = 0; i < ng; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return vt[a] < vt[b]; });
+    std::vector<int64_t> rt_tgt, rt_off{0};
+    for (int64_t i = 0; i < ng; ++i) {  // group indices ascend with the key: the stable sort keeps key order
+      if (i == 0 || vt[order[i]] != vt[order[i - 1]]) {
+        if (i) rt_off.push_back(i);
+        rt_tgt.push_back(vt[order[i]]);
+      }
+    }
+    rt_off.push_back(ng);
+    if (ng == 0) rt_off.assign(1, 0);
+    D.lo_rt_n = (int64_t)rt_tgt.size();
+    LB_TRY(upload(&D.lo_rt_tgt, rt_tgt));
+    LB_TRY(upload(&D.lo_rt_off, rt_off));
+    LB_TRY(upload(&D.lo_rt_grp, order));
+  }
+  if (!D.lo_units[nd]) {  // units of whole target groups, <= one pass of columns where possible
+    // Units in (key, group) order are cut into batches whose groups' partial
+    // sums fit the scratch buffer (LB_M2L_PART_MB, default 3072 MB); a
+    // batch's units run in ONE launch, the highest ranks first, and are then
+    // reduced into the check values before the next batch starts.
+    static const int64_t cap_bytes = [] {
+      const char* e = std::getenv("LB_M2L_PART_MB");
+      const int64_t mb = e ? std::atoll(e) : 3072;
+      return std::max<int64_t>(mb, 16) << 20;
+    }();
+    const int64_t cap_groups = std::max<int64_t>(1, cap_bytes / ((int64_t)nd * nrep * 8));
+    struct U { int64_t a, b; int32_t key; };
+    std::vector<U> us;
+    for (int k = 0; k < nk; ++k) {
       const int64_t g0 = D.v_key_tgt_off[k], g1 = D.v_key_tgt_off[k + 1];
       int64_t ub = g0, cols = 0;
       for (int64_t gi = g0; gi < g1; ++gi) {
         const int64_t c = (D.v_tpoff_host[gi + 1] - D.v_tpoff_host[gi]) * nd;
         if (gi > ub && cols + c > m2lf::pass_cols(nd)) {
-          units.push_back(ub);
-          units.push_back(gi);
+          us.push_back({ub, gi, (int32_t)k});
           ub = gi;
           cols = 0;
         }
         cols += c;
       }
-      if (g1 > ub) {
-        units.push_back(ub);
-        units.push_back(g1);
-      }
+      if (g1 > ub) us.push_back({ub, g1, (int32_t)k});
     }
-    ku[nk] = (int64_t)(units.size() / 2);
+    std::vector<int64_t>& bo = D.lo_batch_off[nd];   // per batch: first unit; + end
+    std::vector<int64_t>& bg = D.lo_batch_grp[nd];   // per batch: first group; + end
+    bo.assign(1, 0);
+    bg.assign(1, us.empty() ? 0 : us.front().a);
+    int64_t maxg = 1;
+    for (size_t i = 0; i < us.size(); ++i) {
+      if (us[i].b - bg.back() > cap_groups && (int64_t)i > bo.back()) {
+        bo.push_back((int64_t)i);
+        bg.push_back(us[i].a);
+      }
+      maxg = std::max(maxg, us[i].b - bg.back());
+    }
+    bo.push_back((int64_t)us.size());
+    bg.push_back(us.empty() ? 0 : us.back().b);
+    for (size_t bi = 0; bi + 1 < bo.size(); ++bi)
+      std::stable_sort(us.begin() + bo[bi], us.begin() + bo[bi + 1], [&](const U& x, const U& y) {
+        return P->lr_rank[x.key] > P->lr_rank[y.key];
+      });
+    std::vector<int64_t> units;
+    std::vector<int32_t> ukey;
+    units.reserve(2 * us.size());
+    for (const U& u : us) {
+      units.push_back(u.a);
+      units.push_back(u.b);
+      ukey.push_back(u.key);
+    }
     LB_TRY(upload(&D.lo_units[nd], units));
+    LB_TRY(upload(&D.lo_unit_key[nd], ukey));
+    const int64_t need_part = maxg * nd * nrep;
+    if (D.lo_part_cap < need_part) {
+      cudaFree(D.lo_part);
+      D.lo_part = nullptr;
+      LB_CUDA(cudaMalloc((void**)&D.lo_part, sizeof(double) * need_part));
+      D.lo_part_cap = need_part;
+    }
     // the first factor's flat tile list (m2l_first.cuh): (batch, column tile),
     // the highest ranks first so the last wave holds the light tiles
     std::vector<std::pair<int32_t, int32_t>> tl;
@@ -1954,25 +2043,34 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     a.y_off = D.lo_gyoff; a.boff = D.lo_gboff; a.tiles = D.lo_tiles[ND];
     LB_DG(m2l1::launch(a, D.lo_ntiles[ND], D.lo_rmax, st));
   }
-  for (int k = 0; k < P->ncanon; ++k) {
+  if (lowrank_fused) {
+    // low-rank, fused: Y = A_k T and the permuted accumulation per unit of
+    // whole target groups, Y kept in shared memory (T from the launch above);
+    // every batch of units in one launch, its groups' sums then added to the
+    // check values in key order
+    const std::vector<int64_t>& bo = D.lo_batch_off[ND];
+    const std::vector<int64_t>& bg = D.lo_batch_grp[ND];
+    const int lut_n = D.lo_aff ? D.lo_lut_n : 0;
+    for (size_t bi = 0; bi + 1 < bo.size(); ++bi) {
+      if (bo[bi + 1] == bo[bi]) continue;
+      m2lf::Args f{};
+      f.A = m2lf::use_ring(nrep, lut_n) ? D.lr_ap : nullptr;
+      f.Arow = D.lr_a; f.nrep = nrep; f.nd = ND; f.T = D.lr_t;
+      f.keytab = D.lo_keytab; f.unit_key = D.lo_unit_key[ND] + bo[bi];
+      f.units = D.lo_units[ND] + 2 * bo[bi]; f.tpair = D.v_tgt_pair_off;
+      f.voff = D.v_off_idx; f.perm = D.perm;
+      f.aff = reinterpret_cast<const int4*>(D.lo_aff); f.coords = D.lo_coords; f.lut = D.lo_lut;
+      f.lut_n = D.lo_lut_n;
+      f.part = D.lo_part; f.g0 = bg[bi];
+      f.carry = D.lo_carry; f.carry_flag = D.lo_carry_flag; f.carry_slots = D.lo_carry_slots;
+      LB_DG(m2lf::launch(f, bo[bi + 1] - bo[bi], D.lo_rmax, st));
+      LB_DG(m2lf::reduce(D.lo_rt_tgt, D.lo_rt_off, D.lo_rt_grp, D.lo_rt_n, bg[bi], bg[bi + 1], D.lo_part, ND,
+                         nrep, D.dc, st));
+    }
+  }
+  for (int k = 0; k < P->ncanon && !lowrank_fused; ++k) {
     const int64_t pb = D.v_key_pair_off[k], pe = D.v_key_pair_off[k + 1];
     if (pe == pb) continue;
-    const bool no_fuse = !lowrank_fused;
-    if (!no_fuse) {
-      // low-rank, fused: Y = A_k T and the permuted accumulation per unit of
-      // whole target groups, Y kept in shared memory (T from the launch above)
-      const int r = P->lr_rank[k];
-      m2lf::Args f{};
-      f.A = m2lf::use_ring(nrep) ? D.lr_ap + D.lr_ap_off[k] : nullptr;
-      f.Arow = D.lr_a + P->lr_off[k] * nrep; f.nrep = nrep; f.r = r; f.nd = ND;
-      f.T = D.lr_t + D.lo_tbase1[k] * ND;
-      const std::vector<int64_t>& ku = D.lo_key_units[ND];
-      f.units = D.lo_units[ND] + 2 * ku[k]; f.vtgts = D.v_tgts; f.tpair = D.v_tgt_pair_off;
-      f.voff = D.v_off_idx; f.perm = D.perm; f.p0 = pb; f.dc = D.dc;
-      f.carry = D.lo_carry; f.carry_flag = D.lo_carry_flag; f.carry_slots = D.lo_carry_slots;
-      LB_DG(m2lf::launch(f, ku[k + 1] - ku[k], st));
-      continue;
-    }
     const std::vector<int64_t> tp(D.v_tpoff_host.begin() + D.v_key_tgt_off[k],
                                   D.v_tpoff_host.begin() + D.v_key_tgt_off[k + 1] + 1);
     int64_t ti = 0;
@@ -2173,6 +2271,9 @@ void fmm_release_device(lb_fmm_plan* P) {
   cudaFree(D.lr_t);
   cudaFree(D.lo_carry);
   cudaFree(D.lo_carry_flag);
+  cudaFree(D.lo_aff); cudaFree(D.lo_coords); cudaFree(D.lo_lut);
+  cudaFree(D.lo_keytab); cudaFree(D.lo_rt_tgt); cudaFree(D.lo_rt_off); cudaFree(D.lo_rt_grp); cudaFree(D.lo_part);
+  for (int i = 0; i < 5; ++i) cudaFree(D.lo_unit_key[i]);
   cudaFree(D.lr_ap);
   cudaFree(D.lr_bp); cudaFree(D.lo_src); cudaFree(D.lo_tcol); cudaFree(D.lo_scale);
   cudaFree(D.lo_boff); cudaFree(D.lo_aoff);

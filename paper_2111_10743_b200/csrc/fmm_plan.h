@@ -115,11 +115,27 @@ struct FmmDevice {
   // each key's first unit; built once per nd, so an apply never allocates
   int64_t* lo_units[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   std::vector<int64_t> lo_key_units[5];
+  // fused second factor: per-unit key, batches of units (first unit / first group per batch, + end),
+  // per-key table, partial-sum scratch, and every target's groups in key order for the reduction
+  int32_t* lo_unit_key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<int64_t> lo_batch_off[5], lo_batch_grp[5];
+  int64_t* lo_keytab = nullptr;
+  double* lo_part = nullptr;
+  int64_t lo_part_cap = 0;
+  int64_t *lo_rt_tgt = nullptr, *lo_rt_off = nullptr, *lo_rt_grp = nullptr;
+  int64_t lo_rt_n = 0;
   // the first factor's flat (batch, column tile) list per nd (m2l_first.cuh)
   int32_t* lo_tiles[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int64_t lo_ntiles[5] = {0, 0, 0, 0, 0};
   double* lr_ap = nullptr;      // A_k in DMMA fragment order (m2lf::pack_a), key k at lr_ap_off[k]
   std::vector<int64_t> lr_ap_off;
+  // closed-form M2L permutations (m2lf::fit_symmetries): per offset (A, B, C, D), per point its
+  // lattice coordinates, lattice index -> expansion index; lo_aff == nullptr: table lookups
+  bool lo_fit_done = false;
+  int32_t* lo_aff = nullptr;
+  uint32_t* lo_coords = nullptr;
+  uint16_t* lo_lut = nullptr;
+  int lo_lut_n = 0;
   double* lo_carry = nullptr;   // m2l_fused.cuh: carry pool (lo_carry_slots x kMaxNd x nrep)
   unsigned* lo_carry_flag = nullptr;
   int lo_carry_slots = 0;

@@ -8,10 +8,15 @@
 // cube-symmetry permutation in their fixed order:
 //   dc[t, l, i] += sum_{pairs of t} Y[perm[o, i], (pair, l)]
 // so Y never leaves the SM (the staged path wrote and re-read 2 x 8 nrep
-// bytes per pair and density).  One launch per key: a (target, key) group
-// belongs to exactly one unit, so within a launch no two CTAs touch the same
-// dc entry and the += is a plain read-modify-write; the keys' launches are
-// stream-ordered, which fixes the order of every target's sums.
+// bytes per pair and density).  A (target, key) group belongs to exactly one
+// unit and writes its sum, WRITE ONLY, to its own slot of a scratch buffer;
+// reduce_kernel then adds every target's slots to its check values in key
+// order.  So units of all keys run in ONE launch (heaviest ranks first; a
+// batch of units when the slots would not fit the scratch buffer), no CTA
+// waits on a read-modify-write of dc (the exposed L2 round trip per group was
+// the accumulation's largest stall), there are no atomics, and every check
+// value is the same left-to-right sum over the keys as a stream-ordered
+// launch per key gave: bit-identical results.
 //
 // A pass holds kCols / nd whole pairs (a pair's nd columns never straddle two
 // passes).  A target group with more pairs than one pass is the only group of
@@ -28,13 +33,18 @@
 // through a per-warp cp.async ring, L1 bypassed, one k-step pair ahead), two T
 // fragment loads (shared memory) and eight DMMAs.  M- and N-tile counts are compile-time in every
 // instantiation: a predicated-off DMMA still occupies the tensor pipe.  The
-// accumulation reads each pair's permutation index once for all its densities
-// with four pairs in flight; the dc rows a unit updates are prefetched into
-// L1 before the product.
+// accumulation computes each pair's permuted row once for all its densities
+// -- in closed form where the permutations are axis permutations and flips of
+// the expansion lattice (fit_symmetries; three IMADs and a shared-memory
+// table instead of a global index load), four pairs in flight.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "dgemm_cols.cuh"
 
@@ -53,17 +63,31 @@ constexpr int kMW = 4;       // M-tiles a warp holds at once
 __host__ __device__ inline int pass_cols(int nd) { return (kCols / nd) * nd; }
 
 struct Args {
-  const double* A;           // A_k in fragment order (pack_a), or nullptr: no ring, use Arow
-  const double* Arow;        // A_k (nrep x r) row-major, lda = r
-  int nrep, r, nd;
-  const double* T;           // T column c of the key at T + c * tstride(r), rows >= r zero
+  const double* A;           // all keys' A_k in fragment order (pack_a), or nullptr: no ring, use Arow
+  const double* Arow;        // all keys' A_k (nrep x r_k) row-major, lda = r_k
+  int nrep, nd;
+  const double* T;           // all keys' T; column c of key k at T + keytab[k].t_off * nd + c * tstride(r_k)
+  // per key: offset of A_k in A, in Arow, of its T (per density), its first pair, its rank
+  const int64_t* keytab;     // 5 int64 per key: a_off, arow_off, t_off, p0, r
+  const int32_t* unit_key;   // per unit: its key
   const int64_t* units;      // per unit: [first target group, end) (absolute group indices)
-  const int64_t* vtgts;      // per target group: target slot
   const int64_t* tpair;      // per target group: first pair (absolute); tpair[g + 1] = end
   const int32_t* voff;       // per pair: offset index
   const int32_t* perm;       // (noff x nrep) forward permutations
-  int64_t p0;                // absolute pair of T column 0 (the key's first pair)
-  double* dc;                // (nbox, nd, nrep)
+  // the same permutations in closed form (fit_symmetries below; nullptr: use
+  // the table): point i has lattice coordinates coords[i] = a | b << 8 | c << 16
+  // on the m^3 lattice, offset d maps them to the lattice index
+  // aff[d] = (A, B, C, D): A a + B b + C c + D, and lut turns that into the
+  // expansion index
+  const int4* aff;
+  const uint32_t* coords;
+  const uint16_t* lut;
+  int lut_n;                 // m^3
+  // every (target, key) group's sum goes to its own slot of `part`, write
+  // only: slot = group index - g0, nd x nrep doubles (reduce_kernel adds the
+  // slots into the check values in key order)
+  double* part;
+  int64_t g0;
   double* carry;             // multi-pass groups: pool of carry_slots x (kMaxNd * nrep) doubles
   unsigned* carry_flag;      // per slot: 0 free, 1 taken (zero-initialised)
   int carry_slots;
@@ -265,16 +289,22 @@ template <bool RING>
 __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <= 128 registers
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_poff[kCols];         // perm row offset (offset index x nrep) of the pass's pairs
+  __shared__ int4 s_aff[kCols];         // ... or their permutations in closed form
   __shared__ int64_t s_gq[kCols + 1];   // first pair of the unit's groups (one-pass units)
-  __shared__ int64_t s_gt[kCols];       // their target slots
   __shared__ int s_slot;                // a multi-pass unit's carry slot
   constexpr int LT = ldt();
-  const int nd = g.nd, nrep = g.nrep, r = g.r;
+  const int nd = g.nd, nrep = g.nrep;
   const int LY = ldy(nrep);
   double* Ys = sm;                          // [column][row], stride LY
   double* Ts = sm + (size_t)kCols * LY;     // [column][k], stride LT
   const int tid = threadIdx.x;
   const int64_t u = blockIdx.x;
+  const int64_t* const kt = g.keytab + 5 * (int64_t)g.unit_key[u];
+  const double* const Ap = g.A ? g.A + kt[0] : nullptr;
+  const double* const Arow = g.Arow + kt[1];
+  const double* const Tk = g.T + kt[2] * nd;
+  const int64_t p0 = kt[3];
+  const int r = (int)kt[4];
   const int64_t tg0 = g.units[2 * u], tg1 = g.units[2 * u + 1];
   const int ngrp = (int)(tg1 - tg0);
   const int64_t pa = g.tpair[tg0], pe = g.tpair[tg1];
@@ -282,20 +312,18 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
   const bool multi = (pe - pa) > ppp;  // one group in several passes
   const int K4 = tstride(r);
 
+  // lattice index -> expansion index, behind the tiles (and the ring)
+  uint16_t* const s_lut = reinterpret_cast<uint16_t*>(Ts + (size_t)kCols * LT + (RING ? kRingDoubles : 0));
+  if (g.aff)
+    for (int e = tid; e < g.lut_n; e += kThreads) s_lut[e] = g.lut[e];
   // group table (a multi-pass unit has one group)
   for (int e = tid; e <= ngrp && e <= kCols; e += kThreads) s_gq[e] = g.tpair[tg0 + e];
-  for (int e = tid; e < ngrp && e < kCols; e += kThreads) s_gt[e] = g.vtgts[tg0 + e];
   if (multi && tid == 0) {  // claim a carry slot (the pool outnumbers the resident CTAs)
     unsigned s = (unsigned)((u * 2654435761ull) % (unsigned)g.carry_slots);
     while (atomicCAS(g.carry_flag + s, 0u, 1u) != 0u) s = (s + 1) % (unsigned)g.carry_slots;
     s_slot = (int)s;
   }
   __syncthreads();
-  // the dc rows this unit updates, towards L1 while the product runs
-  for (int e = 0; e < ngrp && e < kCols; ++e) {
-    const double* d = g.dc + s_gt[e] * nd * (int64_t)nrep;
-    for (int i = tid * 4; i < nd * nrep; i += kThreads * 4) prefetch_l1(d + i);
-  }
   double* const carry = multi ? g.carry + (size_t)s_slot * kMaxNd * nrep : nullptr;
 
   for (int64_t pb = pa; pb < pe; pb += ppp) {
@@ -309,39 +337,52 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
     // columns past ncol of the last N-tile are zeroed
     {
       const int h4 = K4 / 2;  // 16-byte pieces per column
-      const double* Tc = g.T + (pb - g.p0) * nd * (int64_t)K4;
+      const double* Tc = Tk + (pb - p0) * nd * (int64_t)K4;
       for (int e = tid; e < h4 * ntn * 8; e += kThreads) {
         const int c = e / h4, k = (e - c * h4) * 2;
         dg::cp16(Ts + c * LT + k, c < ncol ? Tc + (int64_t)c * K4 + k : g.T, c < ncol ? 16 : 0);
       }
       dg::cp_commit();
-      if (tid < np) s_poff[tid] = g.voff[pb + tid] * nrep;
+      if (tid < np) {
+        const int d = g.voff[pb + tid];
+        s_poff[tid] = d * nrep;
+        if (g.aff) s_aff[tid] = g.aff[d];
+      }
       dg::cp_wait<0>();
     }
     __syncthreads();
-    if (ntn == 1) gemm_phase<1, RING>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
-    else gemm_phase<kNT, RING>(g.A, g.Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+    if (ntn == 1) gemm_phase<1, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+    else gemm_phase<kNT, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
     __syncthreads();
     // per target group and density, pairs in order, through the permutation:
     // one index per (pair, row) for all densities, four pairs in flight
-    for (int e = 0; e < (multi ? 1 : ngrp); ++e) {
-      const int64_t q0 = multi ? pa : s_gq[e], q1 = multi ? pe : s_gq[e + 1];
-      const int ja = (int)(max(q0, pb) - pb), jb = (int)(min(q1, pb + np) - pb);
-      if (ja >= jb) continue;
-      const bool first = (pb + ja) == q0, last = (pb + jb) == q1;
-      double* const d0 = g.dc + s_gt[e] * nd * (int64_t)nrep;
-      for (int i = tid; i < nrep; i += kThreads) {
-        double s[kMaxNd], old[kMaxNd];
+    for (int i = tid; i < nrep; i += kThreads) {
+      int ca = 0, cb = 0, cc = 0;
+      if (g.aff) {
+        const uint32_t cw = g.coords[i];
+        ca = cw & 255;
+        cb = (cw >> 8) & 255;
+        cc = cw >> 16;
+      }
+      const int32_t* pi = g.perm + i;
+      auto index = [&](int jp) -> int {  // row of pair jp's Y column this thread adds
+        if (!g.aff) return pi[s_poff[jp]];
+        const int4 af = s_aff[jp];
+        return s_lut[af.x * ca + af.y * cb + af.z * cc + af.w];
+      };
+      for (int e = 0; e < (multi ? 1 : ngrp); ++e) {
+        const int64_t q0 = multi ? pa : s_gq[e], q1 = multi ? pe : s_gq[e + 1];
+        const int ja = (int)(max(q0, pb) - pb), jb = (int)(min(q1, pb + np) - pb);
+        if (ja >= jb) continue;
+        const bool first = (pb + ja) == q0, last = (pb + jb) == q1;
+        double* const d0 = g.part + (tg0 + e - g.g0) * nd * (int64_t)nrep;
+        double s[kMaxNd];
 #pragma unroll
-        for (int l = 0; l < kMaxNd; ++l) {
-          s[l] = (first || l >= nd) ? 0.0 : carry[(size_t)l * nrep + i];
-          old[l] = (last && l < nd) ? d0[(int64_t)l * nrep + i] : 0.0;
-        }
-        const int32_t* pi = g.perm + i;
+        for (int l = 0; l < kMaxNd; ++l) s[l] = (first || l >= nd) ? 0.0 : carry[(size_t)l * nrep + i];
         for (int jp = ja; jp < jb; jp += 4) {
           int id[4];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) id[v] = (jp + v < jb) ? pi[s_poff[jp + v]] : 0;
+          for (int v = 0; v < 4; ++v) id[v] = (jp + v < jb) ? index(jp + v) : 0;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             if (jp + v >= jb) break;
@@ -354,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
 #pragma unroll
         for (int l = 0; l < kMaxNd; ++l) {
           if (l >= nd) break;
-          if (last) d0[(int64_t)l * nrep + i] = old[l] + s[l];
+          if (last) d0[(int64_t)l * nrep + i] = s[l];
           else carry[(size_t)l * nrep + i] = s[l];
         }
       }
@@ -369,26 +410,161 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
   }
 }
 
-inline size_t smem_bytes(int nrep, bool ring) {
-  return sizeof(double) * ((size_t)kCols * ldy(nrep) + (size_t)kCols * ldt() + (ring ? kRingDoubles : 0));
+// lut_n: entries of the lattice-index table (m^3; 0 without closed-form permutations)
+inline size_t smem_bytes(int nrep, bool ring, int lut_n) {
+  return sizeof(double) * ((size_t)kCols * ldy(nrep) + (size_t)kCols * ldt() + (ring ? kRingDoubles : 0)) +
+         ((sizeof(uint16_t) * (size_t)lut_n + 15) / 16) * 16;
 }
 // the ring variant when two CTAs with a ring fit one SM (227 KB, 1 KB reserved per CTA)
-inline bool use_ring(int nrep) { return 2 * (smem_bytes(nrep, true) + 1024 + 512) <= 227 * 1024; }
+inline bool use_ring(int nrep, int lut_n) {
+  return 2 * (smem_bytes(nrep, true, lut_n) + 1024 + 512) <= 227 * 1024;
+}
+
+// The cube-symmetry permutations in closed form.  pts: the expansion points
+// on [-1, 1]^3 (nrep x 3); they sit on an m x m x m tensor lattice (uniform
+// surface lattice or Chebyshev grid, both symmetric), so every permutation
+// perm[d] (noff x nrep) is "permute the axes, flip some": lattice coordinates
+// (a, b, c) -> index A a + B b + C c + D of the image on the m^3 lattice.
+// Returns false (outputs untouched) if any permutation is not of that form.
+inline bool fit_symmetries(const double* pts, int nrep, const int32_t* perm, int noff,
+                           std::vector<int32_t>& aff, std::vector<uint32_t>& coords,
+                           std::vector<uint16_t>& lut, int& m_out) {
+  std::vector<double> vals;
+  for (int i = 0; i < nrep; ++i) {
+    bool seen = false;
+    for (double v : vals) seen = seen || std::fabs(v - pts[3 * i]) < 1e-9;
+    if (!seen) vals.push_back(pts[3 * i]);
+  }
+  std::sort(vals.begin(), vals.end());
+  const int m = (int)vals.size();
+  if (m < 2 || m > 16 || nrep > 65535) return false;
+  auto rank = [&](double x) {
+    for (int k = 0; k < m; ++k)
+      if (std::fabs(vals[k] - x) < 1e-9) return k;
+    return -1;
+  };
+  std::vector<uint32_t> co(nrep);
+  std::vector<int> c3(3 * nrep);
+  std::vector<uint16_t> lu((size_t)m * m * m, 0);
+  std::vector<uint8_t> used((size_t)m * m * m, 0);
+  for (int i = 0; i < nrep; ++i) {
+    const int a = rank(pts[3 * i]), b = rank(pts[3 * i + 1]), c = rank(pts[3 * i + 2]);
+    if (a < 0 || b < 0 || c < 0) return false;
+    c3[3 * i] = a; c3[3 * i + 1] = b; c3[3 * i + 2] = c;
+    co[i] = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)c << 16);
+    lu[((size_t)a * m + b) * m + c] = (uint16_t)i;
+    used[((size_t)a * m + b) * m + c] = 1;
+  }
+  static const int P6[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  const int stride[3] = {m * m, m, 1};
+  std::vector<int32_t> af(4 * (size_t)noff);
+  for (int d = 0; d < noff; ++d) {
+    bool found = false;
+    for (int p = 0; p < 6 && !found; ++p)
+      for (int f = 0; f < 8 && !found; ++f) {
+        // image coordinate k = (flip_k ? m - 1 - x[P6[p][k]] : x[P6[p][k]])
+        int A[3] = {0, 0, 0}, D = 0;
+        for (int k = 0; k < 3; ++k) {
+          const int sgn = (f >> k) & 1 ? -1 : 1;
+          A[P6[p][k]] += sgn * stride[k];
+          if (sgn < 0) D += (m - 1) * stride[k];
+        }
+        bool ok = true;
+        for (int i = 0; i < nrep && ok; ++i) {
+          const int t = A[0] * c3[3 * i] + A[1] * c3[3 * i + 1] + A[2] * c3[3 * i + 2] + D;
+          ok = t >= 0 && t < m * m * m && used[t] && lu[t] == perm[(size_t)d * nrep + i];
+        }
+        if (ok) {
+          af[4 * (size_t)d] = A[0]; af[4 * (size_t)d + 1] = A[1]; af[4 * (size_t)d + 2] = A[2];
+          af[4 * (size_t)d + 3] = D;
+          found = true;
+        }
+      }
+    if (!found) return false;
+  }
+  aff.swap(af);
+  coords.swap(co);
+  lut.swap(lu);
+  m_out = m;
+  return true;
+}
+
+// dc[t, l, i] += the slots of t's (target, key) groups in [g0, g1), in key
+// order (rt_grp lists every target's groups by ascending key): with the
+// batches of keys processed in order, every check value is the same
+// left-to-right sum over the keys as a stream-ordered launch per key gave.
+// One CTA per target with V pairs; rows strided over the threads.
+__global__ void __launch_bounds__(256) reduce_kernel(const int64_t* __restrict__ rt_tgt,
+                                                     const int64_t* __restrict__ rt_off,
+                                                     const int64_t* __restrict__ rt_grp, int64_t g0,
+                                                     int64_t g1, const double* __restrict__ part, int nd,
+                                                     int nrep, double* __restrict__ dc) {
+  __shared__ int s_lo, s_n;
+  const int64_t ti = blockIdx.x;
+  const int64_t q0 = rt_off[ti], q1 = rt_off[ti + 1];
+  // the target's groups ascend (by key, hence by group index): those of this
+  // batch are one contiguous run [lo, lo + n) of its list
+  if (threadIdx.x < 32) {
+    int lo = -1, n = 0;
+    for (int64_t qb = q0; qb < q1; qb += 32) {
+      const int64_t q = qb + threadIdx.x;
+      const bool in = q < q1 && rt_grp[q] >= g0 && rt_grp[q] < g1;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        if (lo < 0) lo = (int)(qb - q0) + __ffs(m) - 1;
+        n += __popc(m);
+      }
+    }
+    if (threadIdx.x == 0) {
+      s_lo = lo;
+      s_n = n;
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n == 0) return;  // nothing of this batch lands on the target: its check values stay untouched
+  const int64_t* const gl = rt_grp + q0 + s_lo;
+  double* const d = dc + rt_tgt[ti] * nd * (int64_t)nrep;
+  const int len = nd * nrep;
+  for (int e = threadIdx.x; e < len; e += 256) {
+    double v = d[e];
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {  // four slots in flight, added left to right
+      const double p0 = part[(gl[j] - g0) * len + e], p1 = part[(gl[j + 1] - g0) * len + e];
+      const double p2 = part[(gl[j + 2] - g0) * len + e], p3 = part[(gl[j + 3] - g0) * len + e];
+      v += p0;
+      v += p1;
+      v += p2;
+      v += p3;
+    }
+    for (; j < n; ++j) v += part[(gl[j] - g0) * len + e];
+    d[e] = v;
+  }
+}
+
+inline cudaError_t reduce(const int64_t* rt_tgt, const int64_t* rt_off, const int64_t* rt_grp, int64_t ntgt,
+                          int64_t g0, int64_t g1, const double* part, int nd, int nrep, double* dc,
+                          cudaStream_t st) {
+  if (ntgt <= 0 || g1 <= g0) return cudaSuccess;
+  reduce_kernel<<<(unsigned)ntgt, 256, 0, st>>>(rt_tgt, rt_off, rt_grp, g0, g1, part, nd, nrep, dc);
+  return cudaGetLastError();
+}
 
 // slots of the carry pool: four per SM (two CTAs are resident per SM)
 inline int carry_slots(int sm_count) { return 4 * sm_count; }
 
 // largest nrep one CTA's tile fits in shared memory for
-inline int max_nrep() { return (int)((226 * 1024 / sizeof(double) - (size_t)kCols * ldt()) / kCols) - 8; }
+inline int max_nrep() { return (int)((216 * 1024 / sizeof(double) - (size_t)kCols * ldt()) / kCols) - 8; }
 
-inline cudaError_t launch(const Args& a, int64_t nunits, cudaStream_t st) {
+inline cudaError_t launch(const Args& a, int64_t nunits, int rmax, cudaStream_t st) {
   if (nunits <= 0) return cudaSuccess;
-  if (a.r > 4 * kMaxKS || a.nd > kMaxNd || a.nd < 1 || !a.carry || !a.carry_flag || a.carry_slots < 1 ||
+  if (rmax > 4 * kMaxKS || a.nd > kMaxNd || a.nd < 1 || !a.keytab || !a.unit_key || !a.part || !a.carry || !a.carry_flag || a.carry_slots < 1 ||
       a.nrep > max_nrep())
     return cudaErrorInvalidValue;
-  if ((a.A == nullptr) == use_ring(a.nrep) || !a.Arow) return cudaErrorInvalidValue;
+  const int lut_n = a.aff ? a.lut_n : 0;
+  if ((a.A == nullptr) == use_ring(a.nrep, lut_n) || !a.Arow) return cudaErrorInvalidValue;
   const bool ring = a.A != nullptr;
-  const int need = (int)smem_bytes(a.nrep, ring);
+  const int need = (int)smem_bytes(a.nrep, ring, lut_n);
   static int attr[2] = {0, 0};
   if (need > attr[ring]) {
     const cudaError_t e = ring ? cudaFuncSetAttribute(m2l_fused_kernel<true>,
