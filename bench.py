@@ -47,7 +47,7 @@ NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
 K_ARNOLDI = 8               # MGS basis size in the timed step
 CONFIG3 = {"order": 7, "nu": 64, "nv": 32, "R": 2.0, "r": 1.0, "eps": 5e-8,
            "eta": 2.0, "cap": 256, "ncrit": 400}
-M2L_DRAM_BYTES_NCU = 530.5e6  # first 89.8 + 74.2 MB, 16 fused launches 366.5 MB (ncu launch list)
+M2L_DRAM_BYTES_NCU = 763.6e6  # first factor 89.3 + 73.0 MB, fused 102.0 + 202.6 MB, reduce 283.6 + 13.1 MB (ncu launch list)
 ROW_STRIDE = 128            # CPU arms: every 128th target (896 rows of 114,688)
 WORKLOAD = "config3-torus64x32-o7-A3-fmm5e-8-apply+MGS(k=8)"
 
@@ -547,11 +547,11 @@ def main():
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
         elif dom == "m2l":
             s = f["m2l"]
-            roofline = {"bound": "tensor", "kernel": "FMM M2L (m2l1::first_kernel + 16 x "
-                        "m2lf::m2l_fused_kernel, DMMA 8x8x4), pot+grad call", "achieved": s["TFLOPs"],
+            roofline = {"bound": "tensor", "kernel": "FMM M2L (m2l1::first_kernel + m2lf::m2l_fused_kernel, "
+                        "DMMA 8x8x4, + m2lf::reduce_kernel), pot+grad call", "achieved": s["TFLOPs"],
                         "peak": peak_tc, "unit": "TFLOP/s", "frac": s["frac"],
                         "traffic": M2L_DRAM_BYTES_NCU,
-                        "traffic_note": "dram read+write of the 17 launches, ncu "
+                        "traffic_note": "dram read+write of its 3 launches, ncu "
                                         "(profiles/round2/config3_step_launches.md); algorithmic: one "
                                         "488 x 8 B multipole per V pair = 0.83 GB",
                         "peak_source": "measured in-run (lb_probe_dmma: FP64 tensor-core DMMA "

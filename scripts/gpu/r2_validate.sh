@@ -20,6 +20,6 @@ echo "launches rc=$?"
 # first_kernel, leaf, csr pass 1 of call 1 + the largest fused launch: ~5 MB each
 timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"first_kernel|leaf_kernel|csr_epi" -c 3 -f -o gpurun_out/c3_full python scripts/profile_step.py > gpurun_out/c3_full.log 2>&1
 echo "full rc=$?"
-timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"m2l_fused" --launch-skip 2 -c 1 -f -o gpurun_out/c3_full_m2l python scripts/profile_step.py > gpurun_out/c3_full_m2l.log 2>&1
+timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none -k regex:"m2l_fused|reduce_kernel" -c 2 -f -o gpurun_out/c3_full_m2l python scripts/profile_step.py > gpurun_out/c3_full_m2l.log 2>&1
 echo "full m2l rc=$?"
 du -sh gpurun_out
