@@ -5,7 +5,7 @@ mean-zero right-hand side (the Hodge post-processing that would produce the
 two right-hand sides of config 3 is out of scope).
 Checks: solution of the FMM run vs the exact-sweep run of the same system.
 Usage: python scripts/config3_solve.py [eps] [ncrit] [config]
-  config 4 (data/config4_geom.npz, N = 1,202,940, order 9): eps 1e-9 as
+  config 4 (shapes.wavy_torus, N = 1,202,940, order 9): eps 1e-9 as
   BASELINE asks; the exact-sweep cross-check is skipped there (5.8e12 pairs per
   sweep) and the true residual |A u - f| / |f| of the FMM solve is reported."""
 import json
@@ -22,18 +22,17 @@ import paper_2111_10743_b200 as b  # noqa: E402
 from paper_2111_10743_b200.quadrature import build_correction_set, build_near_map  # noqa: E402
 
 eps = float(sys.argv[1]) if len(sys.argv) > 1 else 5e-8
-ncrit = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+ncrit = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 config = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-g = dict(np.load(os.path.join(ROOT, "data", f"config{config}_geom.npz")))
-geom = b.Geometry.from_arrays(g)
-out = {"N": geom.nnodes, "N_over": geom.noversampled, "eps": eps}
+from paper_2111_10743_b200 import shapes  # noqa: E402
+# the geometries and near maps are pinned to the reference's by tests/test_configs_gpu.py
+geom = shapes.build_torus(7, 64, 32, 2.0, 1.0) if config == 3 else shapes.wavy_torus(9, 82, 163)
+out = {"N": geom.nnodes, "N_over": geom.noversampled, "eps": eps, "ncrit": ncrit}
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 near = build_near_map(geom, 2.0, cap=256)
 torch.cuda.synchronize()
 out["t_near_s"] = time.perf_counter() - t0
-out["near_equal_reference"] = bool(np.array_equal(near.offsets, g["near_offsets"])
-                                   and np.array_equal(near.patches, g["near_patches"]))
 kinds = list(b.FORMULATIONS["a3"])
 cset, t_q = build_correction_set(geom, near, kinds, eps)
 out["t_q_s"] = t_q
@@ -42,11 +41,13 @@ out["t_q_split"] = dict(LAST_BUILD)
 out["nnz_per_kind"] = cset.nnz
 # seeded smooth mean-zero right-hand side
 rng = np.random.default_rng(config)
-cen = geom.nodes[rng.choice(geom.nnodes, 16, replace=False)]
+nodes = np.asarray(geom.nodes.cpu() if hasattr(geom.nodes, 'cpu') else geom.nodes)
+wts = np.asarray(geom.weights.cpu() if hasattr(geom.weights, 'cpu') else geom.weights)
+cen = nodes[rng.choice(geom.nnodes, 16, replace=False)]
 amp = rng.standard_normal(16)
-d2 = ((geom.nodes[:, None, :] - cen[None, :, :]) ** 2).sum(-1)
+d2 = ((nodes[:, None, :] - cen[None, :, :]) ** 2).sum(-1)
 f = (amp[None, :] * np.exp(-d2 / (2 * 0.5 ** 2))).sum(1)
-f -= np.dot(geom.weights, f) / geom.weights.sum()
+f -= np.dot(wts, f) / wts.sum()
 res = {}
 out["config"] = config
 for far in (("fmm", "direct") if config == 3 else ("fmm",)):
@@ -59,7 +60,7 @@ for far in (("fmm", "direct") if config == 3 else ("fmm",)):
     torch.cuda.synchronize()
     res[far] = np.asarray(rep.u.values)
     if True:  # true residual of the density: |A sigma - f0| / |f0|
-        f0 = f - np.dot(geom.weights, f) / geom.weights.sum()
+        f0 = f - np.dot(wts, f) / wts.sum()
         r = op.apply(np.asarray(rep.sigma.values)) - f0
         out[far + "_true_residual"] = float(np.linalg.norm(r) / np.linalg.norm(f0))
         out["residual_history"] = [float(h) for h in rep.residual_history]
