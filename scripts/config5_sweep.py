@@ -80,19 +80,22 @@ for n, eps in ((1_000_000, 1e-6), (1_000_000, 1e-9), (10_000_000, 1e-6), (10_000
     qd = torch.from_numpy(q).cuda()
     pot = torch.empty((1, n), dtype=torch.float64, device="cuda")
     grad = torch.empty((1, n, 3), dtype=torch.float64, device="cuda")
-    t = ev_time(lambda: plan.apply_device(qd, None, 1, 1, 0, 1, pot, grad), 2)
-    plan.set_timing(True)
-    plan.apply_device(qd, None, 1, 1, 0, 1, pot, grad)
-    st = plan.stage_times()
-    idx = rng.choice(n, 200, replace=False)
-    ref = b.evaluate_direct(b.FmmSources(x, q), x[idx], ("pot", "grad"))
-    err = max(np.abs(pot.cpu().numpy()[:, idx] - ref.pot).max() / np.abs(ref.pot).max(),
-              np.abs(grad.cpu().numpy()[:, idx] - ref.grad).max() / np.abs(ref.grad).max())
-    print(json.dumps({"case": f"fmm N={n} eps={eps}", "rep": plan.rep, "m": plan.m,
-                      "plan_s": t_plan, "apply_s": t,
-                      "effective_interactions_per_s": n * (n - 1) / t,
-                      "err_vs_direct_200_targets": err, "stages_ms": st,
-                      "nbox": int(plan.tree.sizes[0]), "V": int(plan.tree.sizes[6]),
-                      "U": int(plan.tree.sizes[7])}), flush=True)
+    for xw in ("lists", "direct"):  # the reference's list evaluation, then lb_fmm_plan_set_xw(1)
+        plan.set_xw(xw)
+        plan.set_timing(False)
+        t = ev_time(lambda: plan.apply_device(qd, None, 1, 1, 0, 1, pot, grad), 2)
+        plan.set_timing(True)
+        plan.apply_device(qd, None, 1, 1, 0, 1, pot, grad)
+        st = plan.stage_times()
+        idx = np.random.default_rng(7).choice(n, 200, replace=False)
+        ref = b.evaluate_direct(b.FmmSources(x, q), x[idx], ("pot", "grad"))
+        err = max(np.abs(pot.cpu().numpy()[:, idx] - ref.pot).max() / np.abs(ref.pot).max(),
+                  np.abs(grad.cpu().numpy()[:, idx] - ref.grad).max() / np.abs(ref.grad).max())
+        print(json.dumps({"case": f"fmm N={n} eps={eps}", "xw": xw, "rep": plan.rep, "m": plan.m,
+                          "plan_s": t_plan, "apply_s": t,
+                          "effective_interactions_per_s": n * (n - 1) / t,
+                          "err_vs_direct_200_targets": err, "stages_ms": st,
+                          "nbox": int(plan.tree.sizes[0]), "V": int(plan.tree.sizes[6]),
+                          "U": int(plan.tree.sizes[7])}), flush=True)
     del plan
     torch.cuda.empty_cache()
