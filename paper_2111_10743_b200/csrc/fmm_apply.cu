@@ -1881,16 +1881,22 @@ int ensure_lowrank(lb_fmm_plan* P, int nd) {
       std::stable_sort(us.begin() + bo[bi], us.begin() + bo[bi + 1], [&](const U& x, const U& y) {
         return P->lr_rank[x.key] > P->lr_rank[y.key];
       });
-    std::vector<int64_t> units;
-    std::vector<int32_t> ukey;
-    units.reserve(2 * us.size());
+    // one 64-byte record per unit (m2l_fused.cuh)
+    std::vector<int64_t> urec;
+    urec.reserve(m2lf::kRec * us.size());
     for (const U& u : us) {
-      units.push_back(u.a);
-      units.push_back(u.b);
-      ukey.push_back(u.key);
+      const int k = u.key, r = P->lr_rank[k];
+      const int64_t pa = D.v_tpoff_host[u.a], pe = D.v_tpoff_host[u.b];
+      urec.push_back(D.lr_ap_off[k]);
+      urec.push_back(P->lr_off[k] * nrep);
+      urec.push_back(D.lo_tbase1[k] * nd + (pa - D.v_key_pair_off[k]) * nd * m2lf::tstride(r));
+      urec.push_back(r);
+      urec.push_back(u.a);
+      urec.push_back(u.b - u.a);
+      urec.push_back(pa);
+      urec.push_back(pe);
     }
-    LB_TRY(upload(&D.lo_units[nd], units));
-    LB_TRY(upload(&D.lo_unit_key[nd], ukey));
+    LB_TRY(upload(&D.lo_units[nd], urec));
     const int64_t need_part = maxg * nd * nrep;
     if (D.lo_part_cap < need_part) {
       cudaFree(D.lo_part);
@@ -2056,8 +2062,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
       m2lf::Args f{};
       f.A = m2lf::use_ring(nrep, lut_n) ? D.lr_ap : nullptr;
       f.Arow = D.lr_a; f.nrep = nrep; f.nd = ND; f.T = D.lr_t;
-      f.keytab = D.lo_keytab; f.unit_key = D.lo_unit_key[ND] + bo[bi];
-      f.units = D.lo_units[ND] + 2 * bo[bi]; f.tpair = D.v_tgt_pair_off;
+      f.urec = D.lo_units[ND] + m2lf::kRec * bo[bi]; f.tpair = D.v_tgt_pair_off;
       f.voff = D.v_off_idx; f.perm = D.perm;
       f.aff = reinterpret_cast<const int4*>(D.lo_aff); f.coords = D.lo_coords; f.lut = D.lo_lut;
       f.lut_n = D.lo_lut_n;

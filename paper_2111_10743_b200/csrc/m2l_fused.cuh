@@ -58,6 +58,7 @@ constexpr int kNT = kCols / 8;
 constexpr int kMaxKS = 28;   // rank <= 112
 constexpr int kMaxNd = 4;    // densities per FMM chunk
 constexpr int kMW = 4;       // M-tiles a warp holds at once
+constexpr int kRec = 8;      // int64 per unit record
 
 // columns one pass holds for nd densities (whole pairs)
 __host__ __device__ inline int pass_cols(int nd) { return (kCols / nd) * nd; }
@@ -66,11 +67,14 @@ struct Args {
   const double* A;           // all keys' A_k in fragment order (pack_a), or nullptr: no ring, use Arow
   const double* Arow;        // all keys' A_k (nrep x r_k) row-major, lda = r_k
   int nrep, nd;
-  const double* T;           // all keys' T; column c of key k at T + keytab[k].t_off * nd + c * tstride(r_k)
-  // per key: offset of A_k in A, in Arow, of its T (per density), its first pair, its rank
-  const int64_t* keytab;     // 5 int64 per key: a_off, arow_off, t_off, p0, r
-  const int32_t* unit_key;   // per unit: its key
-  const int64_t* units;      // per unit: [first target group, end) (absolute group indices)
+  const double* T;           // all keys' T (first factor)
+  // per unit ONE 64-byte record, so a CTA's start is one dependent load deep
+  // (key -> key table -> group range -> pair range was four: ncu showed 45% of
+  // the grid-representation kernel's samples on those loads and the T tile's):
+  // offset of its key's A_k in A and in Arow, offset of its first T column in
+  // T, the key's rank, its first target group, its group count, its pair
+  // range [pa, pe)
+  const int64_t* urec;       // kRec int64 per unit
   const int64_t* tpair;      // per target group: first pair (absolute); tpair[g + 1] = end
   const int32_t* voff;       // per pair: offset index
   const int32_t* perm;       // (noff x nrep) forward permutations
@@ -299,19 +303,36 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
   double* Ts = sm + (size_t)kCols * LY;     // [column][k], stride LT
   const int tid = threadIdx.x;
   const int64_t u = blockIdx.x;
-  const int64_t* const kt = g.keytab + 5 * (int64_t)g.unit_key[u];
-  const double* const Ap = g.A ? g.A + kt[0] : nullptr;
-  const double* const Arow = g.Arow + kt[1];
-  const double* const Tk = g.T + kt[2] * nd;
-  const int64_t p0 = kt[3];
-  const int r = (int)kt[4];
-  const int64_t tg0 = g.units[2 * u], tg1 = g.units[2 * u + 1];
-  const int ngrp = (int)(tg1 - tg0);
-  const int64_t pa = g.tpair[tg0], pe = g.tpair[tg1];
+  const longlong2* const rp = reinterpret_cast<const longlong2*>(g.urec + kRec * u);
+  const longlong2 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
+  const double* const Ap = g.A ? g.A + r0.x : nullptr;
+  const double* const Arow = g.Arow + r0.y;
+  const double* const Tu = g.T + r1.x;  // the unit's first T column
+  const int r = (int)r1.y;
+  const int64_t tg0 = r2.x;
+  const int ngrp = (int)r2.y;
+  const int64_t pa = r3.x, pe = r3.y;
   const int ppp = kCols / nd;  // pairs per pass
   const bool multi = (pe - pa) > ppp;  // one group in several passes
   const int K4 = tstride(r);
 
+  // T columns of a pass (global columns are tstride(r) doubles, zero past r):
+  // 16-byte cp.async copies into Ts[c][k] at stride LT (LT = 4 mod 16 doubles:
+  // conflict-free fragment reads, as in dgemm_cols.cuh); the columns past ncol
+  // of the last N-tile are zeroed.  The first pass's copies are issued before
+  // anything else so that they fly under the rest of the CTA's set-up.
+  auto issue_T = [&](int64_t pb) {
+    const int ncol = (int)min((int64_t)ppp, pe - pb) * nd;
+    const int ntn = (ncol + 7) / 8;
+    const int h4 = K4 / 2;  // 16-byte pieces per column
+    const double* Tc = Tu + (pb - pa) * nd * (int64_t)K4;
+    for (int e = tid; e < h4 * ntn * 8; e += kThreads) {
+      const int c = e / h4, k = (e - c * h4) * 2;
+      dg::cp16(Ts + c * LT + k, c < ncol ? Tc + (int64_t)c * K4 + k : g.T, c < ncol ? 16 : 0);
+    }
+    dg::cp_commit();
+  };
+  issue_T(pa);
   // lattice index -> expansion index, behind the tiles (and the ring)
   uint16_t* const s_lut = reinterpret_cast<uint16_t*>(Ts + (size_t)kCols * LT + (RING ? kRingDoubles : 0));
   if (g.aff)
@@ -330,26 +351,16 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
     const int np = (int)min((int64_t)ppp, pe - pb);
     const int ncol = np * nd;
     const int ntn = (ncol + 7) / 8;  // N-tiles in use
-    __syncthreads();  // the previous pass's accumulation is done with Ys / s_poff
-    // T columns of this pass (global columns are tstride(r) doubles, zero past
-    // r): 16-byte cp.async copies into Ts[c][k] at stride LT (LT = 4 mod 16
-    // doubles: conflict-free fragment reads, as in dgemm_cols.cuh); the
-    // columns past ncol of the last N-tile are zeroed
-    {
-      const int h4 = K4 / 2;  // 16-byte pieces per column
-      const double* Tc = Tk + (pb - p0) * nd * (int64_t)K4;
-      for (int e = tid; e < h4 * ntn * 8; e += kThreads) {
-        const int c = e / h4, k = (e - c * h4) * 2;
-        dg::cp16(Ts + c * LT + k, c < ncol ? Tc + (int64_t)c * K4 + k : g.T, c < ncol ? 16 : 0);
-      }
-      dg::cp_commit();
-      if (tid < np) {
-        const int d = g.voff[pb + tid];
-        s_poff[tid] = d * nrep;
-        if (g.aff) s_aff[tid] = g.aff[d];
-      }
-      dg::cp_wait<0>();
+    if (pb != pa) {
+      __syncthreads();  // the previous pass's accumulation is done with Ys / s_poff
+      issue_T(pb);
     }
+    if (tid < np) {
+      const int d = g.voff[pb + tid];
+      s_poff[tid] = d * nrep;
+      if (g.aff) s_aff[tid] = g.aff[d];
+    }
+    dg::cp_wait<0>();
     __syncthreads();
     if (ntn == 1) gemm_phase<1, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
     else gemm_phase<kNT, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
@@ -558,7 +569,7 @@ inline int max_nrep() { return (int)((216 * 1024 / sizeof(double) - (size_t)kCol
 
 inline cudaError_t launch(const Args& a, int64_t nunits, int rmax, cudaStream_t st) {
   if (nunits <= 0) return cudaSuccess;
-  if (rmax > 4 * kMaxKS || a.nd > kMaxNd || a.nd < 1 || !a.keytab || !a.unit_key || !a.part || !a.carry || !a.carry_flag || a.carry_slots < 1 ||
+  if (rmax > 4 * kMaxKS || a.nd > kMaxNd || a.nd < 1 || !a.urec || !a.part || !a.carry || !a.carry_flag || a.carry_slots < 1 ||
       a.nrep > max_nrep())
     return cudaErrorInvalidValue;
   const int lut_n = a.aff ? a.lut_n : 0;
