@@ -446,6 +446,10 @@ int lb_dgemm_cols(const double* A, int lda, int M, int K, const double* X, int64
 int lb_probe_dfma(double* scratch, int blocks, int iters, void* stream);
 /* FP64 tensor-core peak: DMMA 8x8x4 chains, flops = blocks*8*iters*8*512. */
 int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream);
+/* The same chains with a different A fragment register per DMMA (mode 1) or
+ * different A and B fragment registers (mode 2): what a GEMM inner loop
+ * feeds the pipe. */
+int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, void* stream);
 int lb_probe_rsqrt(const double* x, double* y, int64_t n, int mode,
                    void* stream);
 

@@ -43,6 +43,28 @@ __global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters, 
   if (s == 12345.678) out[blockIdx.x] = s;
 }
 
+// operand-delivery variants of the DMMA peak probe: MODE 1 changes the A
+// fragment register with every DMMA (B fixed), MODE 2 changes both -- a real
+// GEMM's inner loop (the peak kernel above feeds every DMMA the same A / B)
+template <int MODE>
+__global__ void __launch_bounds__(256) dmma_operand_kernel(double* out, int iters, double a) {
+  double c[8][2], av[8], bv[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    c[t][0] = c[t][1] = threadIdx.x * 1e-3 + t;
+    av[t] = a + (threadIdx.x + t) * 1e-9;
+    bv[t] = a - (threadIdx.x + 3 * t) * 1e-9;
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dmma_884(c[t][0], c[t][1], av[t], MODE == 2 ? bv[t] : bv[0]);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 __global__ void rsqrt_seed_kernel(const double* x, double* y, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = rsqrt_seed(x[i]);
@@ -67,6 +89,15 @@ int lb_probe_dfma(double* scratch, int blocks, int iters, void* stream) {
 // flops executed = blocks * 8 warps * iters * 8 mma * 512
 int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream) {
   lb::dmma_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+// as lb_probe_dmma with a different A fragment (mode 1) or A and B fragment
+// (mode 2) register per DMMA
+int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, void* stream) {
+  if (mode == 1) lb::dmma_operand_kernel<1><<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
+  else lb::dmma_operand_kernel<2><<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }
