@@ -450,6 +450,10 @@ int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream);
  * different A and B fragment registers (mode 2): what a GEMM inner loop
  * feeds the pipe. */
 int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, void* stream);
+/* Warps 0..nw_mma-1 of every 8-warp block run DMMA chains (it_mma iterations
+ * of 8 DMMAs), the others DFMA chains (it_fma iterations of 128 DFMAs per
+ * thread): do the FP64 tensor cores and the FP64 FMA pipe overlap? */
+int lb_probe_mixed(double* scratch, int blocks, int it_mma, int it_fma, int nw_mma, void* stream);
 int lb_probe_rsqrt(const double* x, double* y, int64_t n, int mode,
                    void* stream);
 

@@ -544,7 +544,7 @@ __device__ __forceinline__ void pair_a3(double tx, double ty, double tz, double 
 
 template <int ND, bool HD, int LEVEL, bool A3P = false>
 __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
-    const int64_t* __restrict__ items, double* __restrict__ part,
+    const int64_t* __restrict__ order, const int64_t* __restrict__ items, double* __restrict__ part,
     const int64_t* __restrict__ leaves, const int64_t* __restrict__ u_off,
     const int64_t* __restrict__ u_list, const int64_t* __restrict__ w_off,
     const int64_t* __restrict__ w_list, const double* __restrict__ bctr,
@@ -566,8 +566,9 @@ __global__ void __launch_bounds__(kLeafBT) leaf_kernel(
   __shared__ int64_t set_box[kLeafMaxSets];
   __shared__ double red[kLeafBT];
   // work item: target leaf li, virtual sources [vb, ve), partial slot (or -1)
-  const int64_t li = items[4 * blockIdx.x], vb = items[4 * blockIdx.x + 1];
-  const int64_t ve = items[4 * blockIdx.x + 2], poff = items[4 * blockIdx.x + 3];
+  const int64_t it = order[blockIdx.x];
+  const int64_t li = items[4 * it], vb = items[4 * it + 1];
+  const int64_t ve = items[4 * it + 2], poff = items[4 * it + 3];
   const int64_t b = leaves[li];
   const int64_t t0 = btgt[2 * b], t1 = btgt[2 * b + 1];
   // leaves hold few targets (~17 on average at ncrit 120): the target pass
@@ -1194,6 +1195,13 @@ int build_device(lb_fmm_plan* P) {
   std::vector<int64_t> p2m;
   for (int64_t b = 0; b < nb; ++b)
     if (t.is_leaf[b] && t.src_hi[b] > t.src_lo[b] && nsrc_own(b) > 0) p2m.push_back(S[b]);
+  // heaviest leaves first: one CTA per leaf with very uneven source counts,
+  // so the launch's tail is its lightest leaves (tmpA is indexed by position
+  // and scattered through this same list: results unchanged)
+  std::stable_sort(p2m.begin(), p2m.end(), [&](int64_t a, int64_t c) {
+    const int64_t ba = P->id_of[a], bc = P->id_of[c];
+    return t.src_hi[ba] - t.src_lo[ba] > t.src_hi[bc] - t.src_lo[bc];
+  });
   D.n_p2m = (int64_t)p2m.size();
   LB_TRY(upload(&D.p2m_leaves, p2m));
   if (src_range) LB_TRY(upload(&D.src_own, src_own));
@@ -1502,7 +1510,7 @@ int build_device(lb_fmm_plan* P) {
   // is the kernel's critical path (measured: SMs idle half of the leaf stage
   // on config 3 without this); split leaves reduce their partials in order
   {
-    std::vector<int64_t> items, islot, sleaf, srange;
+    std::vector<int64_t> items, islot, sleaf, srange, weight;
     int64_t slots = 0;
     for (int64_t li = 0; li < D.n_tleaf; ++li) {
       const int64_t b = P->id_of[tl[li]];
@@ -1524,6 +1532,7 @@ int build_device(lb_fmm_plan* P) {
         items.push_back(k * seg);
         items.push_back(k + 1 == nseg ? vtot : (k + 1) * seg);
         items.push_back(-1);
+        weight.push_back(std::max<int64_t>(ntl, 1) * ((k + 1 == nseg ? vtot : (k + 1) * seg) - k * seg));
         islot.push_back(nseg == 1 ? -1 : slots);
         if (nseg > 1) slots += ntl;
       }
@@ -1534,6 +1543,13 @@ int build_device(lb_fmm_plan* P) {
     D.part_width = -1;
     LB_TRY(upload(&D.leaf_items, items));
     LB_TRY(upload(&D.leaf_item_slot, islot));
+    // launch order: heaviest item first (block i runs item order[i]), so the
+    // stage does not end on a few 2^20-pair items that started last; every
+    // item still writes its own outputs / slots, results unchanged
+    std::vector<int64_t> order(D.n_items);
+    for (int64_t i = 0; i < D.n_items; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t c) { return weight[a] > weight[c]; });
+    LB_TRY(upload(&D.leaf_order, order));
     LB_TRY(upload(&D.split_leaf, sleaf));
     LB_TRY(upload(&D.split_item_off, srange));  // [first item, end) per split leaf
   }
@@ -2212,7 +2228,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     }
 #define LB_LEAF(HD, LV)                                                                        \
   leaf_kernel<ND, HD, LV><<<(unsigned)D.n_items, kLeafBT, 0, st>>>(                                 \
-      D.leaf_items, D.leaf_part,                                                                \
+      D.leaf_order, D.leaf_items, D.leaf_part,                                                  \
       D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,       \
       D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,      \
       surface ? P->ue_scale : 1.0, D.loc, D.up, D.tout);                                      \
@@ -2223,7 +2239,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
     if constexpr (ND == 2) {
       if (proj_out) {  // projected leaf (fmm_apply_a3proj): writes tproj, not tout
         leaf_kernel<2, true, 2, true><<<(unsigned)D.n_items, kLeafBT, 0, st>>>(
-            D.leaf_items, D.leaf_part,
+            D.leaf_order, D.leaf_items, D.leaf_part,
             D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.bctr, D.bhalf, D.bsrc, D.btgt,
             D.spos, D.tpos, D.cs, D.vs, t.ns, t.nt, D.pts, nrep, surface ? 1 : 0, P->de_scale,
             surface ? P->ue_scale : 1.0, D.loc, D.up, D.tproj, D.tnrm, D.snrm);
@@ -2266,7 +2282,7 @@ void fmm_release_device(lb_fmm_plan* P) {
                   D.v_tgt_pair_off, D.v_tgts, D.v_off_idx, D.v_scale, D.x_boxes, D.x_off,
                   D.x_leaves, D.t_leaves, D.u_off, D.u_list, D.w_off, D.w_list, D.cs, D.vs, D.up,
                   D.dc, D.tmpA, D.tmpB, D.tout, D.btgt_oct, D.tnrm, D.tproj, D.snrm,
-                  D.leaf_items, D.leaf_item_slot, D.split_leaf, D.split_item_off, D.leaf_part};
+                  D.leaf_items, D.leaf_item_slot, D.split_leaf, D.split_item_off, D.leaf_part, D.leaf_order};
   for (void* p : ptrs) cudaFree(p);
   if (P->rep == 0) cudaFree(D.loc);
   cudaFree(D.oz_a);

@@ -65,6 +65,7 @@ struct FmmDevice {
   int64_t *split_leaf = nullptr, *split_item_off = nullptr;  // split leaves, their item ranges
   int64_t n_split = 0, part_doubles = 0;     // partial slots (targets x items) of split leaves
   int64_t* leaf_item_slot = nullptr;        // per item: first partial target slot, or -1
+  int64_t* leaf_order = nullptr;            // launch order of the items (heaviest first)
   double* leaf_part = nullptr;
   int64_t leaf_part_cap = 0, part_width = -1;
   // work arrays (per nd)

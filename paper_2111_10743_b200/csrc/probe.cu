@@ -65,6 +65,39 @@ __global__ void __launch_bounds__(256) dmma_operand_kernel(double* out, int iter
   if (s == 12345.678) out[blockIdx.x] = s;
 }
 
+// do the FP64 tensor cores and the FP64 FMA pipe run side by side?  warps
+// 0..NW_MMA-1 of the block run DMMA chains, the rest DFMA chains (iteration
+// counts separate, either may be 0); compare the time with each half alone
+__global__ void __launch_bounds__(256) mixed_peak_kernel(double* out, int it_mma, int it_fma,
+                                                          int nw_mma, double a, double b) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0.0;
+  if (warp < nw_mma) {
+    double c[8][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = threadIdx.x * 1e-3 + t;
+    double av = a + threadIdx.x * 1e-9, bv = a - threadIdx.x * 1e-9;
+    for (int i = 0; i < it_mma; ++i) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) dmma_884(c[t][0], c[t][1], av, bv);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  } else {
+    double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < it_fma; ++i) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+      }
+    }
+    s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  }
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 __global__ void rsqrt_seed_kernel(const double* x, double* y, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = rsqrt_seed(x[i]);
@@ -98,6 +131,14 @@ int lb_probe_dmma(double* scratch, int blocks, int iters, void* stream) {
 int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, void* stream) {
   if (mode == 1) lb::dmma_operand_kernel<1><<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
   else lb::dmma_operand_kernel<2><<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, iters, 1e-3);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+// DMMA flops = blocks * nw_mma * it_mma * 8 * 512; DFMA flops = blocks * (8 - nw_mma) * 32 * it_fma * 256
+int lb_probe_mixed(double* scratch, int blocks, int it_mma, int it_fma, int nw_mma, void* stream) {
+  lb::mixed_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, it_mma, it_fma, nw_mma,
+                                                                    0.999999, 1e-7);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }
