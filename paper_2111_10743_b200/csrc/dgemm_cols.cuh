@@ -20,11 +20,12 @@
 // low-rank factors, or the dense canonical operators).
 //
 // Tiles: BM x BN per CTA, warps of WM x 32 (WM/8 M-tiles x 4 N-tiles of 8x8,
-// WM/8 * 4 DMMAs per 4-deep k-step).  K runs in chunks of 32 through a
-// two-stage cp.async pipeline (A rows 16-byte coalesced when aligned, X 16 B
-// per contiguous pair or 8 B per gathered element, zero-filled past K);
-// fragments come from shared memory at a 36-double stride (two wavefronts per
-// 8-byte fragment load, the minimum for 32 x 8 B).
+// WM/8 * 4 DMMAs per 4-deep k-step).  K runs in chunks of KC through an
+// NS-stage cp.async ring with one block barrier per chunk (A rows 16-byte
+// coalesced when aligned, X 16 B per contiguous pair or 8 B per gathered
+// element, zero-filled past K); fragments come from shared memory at a
+// (KC + 4)-double stride (two wavefronts per 8-byte fragment load, the
+// minimum for 32 x 8 B).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,8 +34,8 @@
 namespace lb {
 namespace dg {
 
-constexpr int kKC = 32;      // K chunk
-constexpr int kLD = 36;      // smem row stride (doubles)
+constexpr int kKC = 32;      // K chunk and smem row stride (doubles) of m2l_first.cuh's tiles
+constexpr int kLD = 36;
 constexpr int kMaxSeg = 8;
 
 struct Args {
@@ -81,22 +82,25 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int BM, int BN, int WM>
+template <int BM, int BN, int WM, int KC, int NS>
 struct Cfg {
   static constexpr int kWarpsM = BM / WM, kWarpsN = BN / 32;
   static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
   static constexpr int kMT = WM / 8;
-  static constexpr size_t kSmem = sizeof(double) * 2 * (BM + BN) * kLD;
+  static constexpr int kLD = KC + 4;  // smem row stride (doubles)
+  static constexpr size_t kSmem = sizeof(double) * NS * (BM + BN) * kLD;
 };
 
-template <int BM, int BN, int WM>
-__global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Args g) {
-  using C = Cfg<BM, BN, WM>;
+template <int BM, int BN, int WM, int KC, int NS>
+__global__ void __launch_bounds__(Cfg<BM, BN, WM, KC, NS>::kThreads) gemm_cols_kernel(Args g) {
+  using C = Cfg<BM, BN, WM, KC, NS>;
   constexpr int NT = C::kThreads, MT = C::kMT;
+  constexpr int kKC = KC, kLD = C::kLD;  // (shadow the namespace's m2l_first constants)
+  static_assert(KC % 4 == 0 && NS >= 2, "K chunk in 4-deep k-steps, at least two stages");
   extern __shared__ __align__(16) double dsm[];
-  // stage b: A tile at dsm + b * BM * kLD, X tile at dsm + 2 * BM * kLD + b * BN * kLD
-  auto As = [&](int b) { return dsm + b * BM * kLD; };
-  auto Xs = [&](int b) { return dsm + 2 * BM * kLD + b * BN * kLD; };
+  // stage b: A tile at dsm + b * (BM + BN) * kLD, X tile BM * kLD behind it
+  auto As = [&](int b) { return dsm + b * (BM + BN) * kLD; };
+  auto Xs = [&](int b) { return dsm + b * (BM + BN) * kLD + BM * kLD; };
   __shared__ const double* xin[kMaxSeg][BN];
   __shared__ const int32_t* kpp[BN];
   __shared__ double* yout[BN];
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
       }
     } else {
       for (int e = tid; e < BN * kKC; e += NT) {
-        const int c = e >> 5, kk = e & 31, k = k0 + kk;
+        const int c = e / kKC, kk = e % kKC, k = k0 + kk;
         const double* base = xin[s][c];
         const bool ok = base != nullptr && k < g.K;
         const int32_t* pp = kpp[c];
@@ -205,22 +209,28 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
     cp_commit();
   };
 
-  if (nstep > 0) {
-    int s, k0;
-    step_at(0, s, k0);
-    load(0, s, k0);
+  // ring: steps i .. i + NS - 2 in flight while step i is multiplied; one
+  // commit group per step (empty past the end) keeps the wait count fixed
+  for (int p = 0; p < NS - 1; ++p) {
+    if (p < nstep) {
+      int s, k0;
+      step_at(p, s, k0);
+      load(p, s, k0);
+    } else {
+      cp_commit();
+    }
   }
   for (int i = 0; i < nstep; ++i) {
-    const int buf = i & 1;
-    if (i + 1 < nstep) {
+    const int buf = i % NS;
+    cp_wait<NS - 2>();
+    __syncthreads();  // step i has landed for every thread; buffer (i - 1) % NS is free
+    if (i + NS - 1 < nstep) {
       int s, k0;
-      step_at(i + 1, s, k0);
-      load(buf ^ 1, s, k0);
-      cp_wait<1>();
+      step_at(i + NS - 1, s, k0);
+      load((i + NS - 1) % NS, s, k0);
     } else {
-      cp_wait<0>();
+      cp_commit();
     }
-    __syncthreads();
     const double* as = As(buf) + (wm * WM + gq) * kLD;
     const double* xs = Xs(buf) + (wn * 32 + gq) * kLD;
 #pragma unroll
@@ -236,7 +246,6 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
-    __syncthreads();
   }
   // epilogue: D[row][col] with row = gq, cols = 2 tq, 2 tq + 1 of each tile
 #pragma unroll
@@ -257,12 +266,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM>::kThreads) gemm_cols_kernel(Ar
   }
 }
 
-template <int BM, int BN, int WM>
+template <int BM, int BN, int WM, int KC = 32, int NS = 2>
 inline cudaError_t launch(const Args& a, int64_t max_cols, int batches, cudaStream_t st) {
-  using C = Cfg<BM, BN, WM>;
+  using C = Cfg<BM, BN, WM, KC, NS>;
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(gemm_cols_kernel<BM, BN, WM>,
+    const cudaError_t e = cudaFuncSetAttribute(gemm_cols_kernel<BM, BN, WM, KC, NS>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)C::kSmem);
     if (e != cudaSuccess) return e;
@@ -270,7 +279,7 @@ inline cudaError_t launch(const Args& a, int64_t max_cols, int batches, cudaStre
   }
   const dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((max_cols + BN - 1) / BN),
                   (unsigned)batches);
-  gemm_cols_kernel<BM, BN, WM><<<grid, C::kThreads, C::kSmem, st>>>(a);
+  gemm_cols_kernel<BM, BN, WM, KC, NS><<<grid, C::kThreads, C::kSmem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -290,15 +299,41 @@ inline cudaError_t gemm_cols(const Args& a, int64_t max_cols_per_batch, int batc
     if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
     return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
   }
-  // a launch too small to fill the SMs even with 64 x 64 tiles (the upper
-  // levels' M2M / L2L: a few hundred columns) is bound by ONE CTA's serial
-  // K loop (41 us per launch at K = 488, ncu profiles/round2): 32 x 32 tiles
-  // cut that loop's DMMA count four-fold and put four times the SMs to work
+  // Translation shapes (M > 64, K = M = nrep): the tile is chosen by a wave
+  // model measured on a B200 at M = K = 488 (profiles/round2/
+  // leaf_overlap_and_tiles.md).  A CTA's time is set by its own K loop
+  // (DMMA latency x accumulators per warp, one barrier per chunk), not by
+  // how many CTAs share the SM, so a launch costs (full waves) x tw + the
+  // last wave (t1 if it fits one CTA per SM, else tw), in units that scale
+  // with K alike for every tile: what matters is how the CTA count falls on
+  // the 148 x occupancy slots.  The FMM's bottom levels are one to three
+  // waves, where the best tile beats the old fixed choice by 20-30%.
   if (a.M > 64) {
-    if (ctas(128, 128) >= want) return launch<128, 128, 32>(a, max_cols_per_batch, batches, st);
-    if (ctas(128, 64) >= want) return launch<128, 64, 32>(a, max_cols_per_batch, batches, st);
-    if (ctas(64, 64) >= 148) return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
-    return launch<32, 32, 16>(a, max_cols_per_batch, batches, st);
+    struct Cand { int id; int bm, bn; double t1, tw; int slots; };
+    static const Cand cands[] = {{0, 64, 64, 39.0, 52.0, 296},
+                                 {1, 64, 96, 60.0, 70.0, 296},
+                                 {2, 64, 128, 60.0, 93.0, 296},
+                                 {3, 128, 128, 93.0, 93.0, 148}};
+    // a launch too small to put a 64 x 64 CTA on most SMs is bound by ONE
+    // CTA's serial K loop: 32 x 32 tiles cut that loop's DMMA count four-fold
+    if (ctas(64, 64) <= 100) return launch<32, 32, 16>(a, max_cols_per_batch, batches, st);
+    int best = 0;
+    double best_t = 1e300;
+    for (const Cand& c : cands) {
+      const int64_t n = ctas(c.bm, c.bn);
+      const int64_t full = n / c.slots, rem = n % c.slots;
+      const double t = full * c.tw + (rem == 0 ? 0.0 : (rem <= 148 ? c.t1 : c.tw));
+      if (t < best_t - 1e-9) {
+        best_t = t;
+        best = c.id;
+      }
+    }
+    switch (best) {
+      case 0: return launch<64, 64, 32>(a, max_cols_per_batch, batches, st);
+      case 1: return launch<64, 96, 32, 16, 4>(a, max_cols_per_batch, batches, st);
+      case 2: return launch<64, 128, 32, 16, 3>(a, max_cols_per_batch, batches, st);
+      default: return launch<128, 128, 32>(a, max_cols_per_batch, batches, st);
+    }
   }
   if (a.M > 32) {
     if (ctas(64, 128) >= want) return launch<64, 128, 32>(a, max_cols_per_batch, batches, st);
