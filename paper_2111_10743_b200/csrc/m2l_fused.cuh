@@ -355,15 +355,22 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
       __syncthreads();  // the previous pass's accumulation is done with Ys / s_poff
       issue_T(pb);
     }
-    if (tid < np) {
-      const int d = g.voff[pb + tid];
-      s_poff[tid] = d * nrep;
-      if (g.aff) s_aff[tid] = g.aff[d];
-    }
+    // the pairs' offsets (and their closed-form permutations: a dependent
+    // load) are only needed by the accumulation: loaded here, parked in
+    // registers under the product, stored after it -- the barrier before the
+    // product does not wait for them
+    int pd = 0;
+    int4 paf = make_int4(0, 0, 0, 0);
+    if (tid < np) pd = g.voff[pb + tid];
     dg::cp_wait<0>();
     __syncthreads();
+    if (tid < np && g.aff) paf = g.aff[pd];
     if (ntn == 1) gemm_phase<1, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
     else gemm_phase<kNT, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+    if (tid < np) {
+      s_poff[tid] = pd * nrep;
+      if (g.aff) s_aff[tid] = paf;
+    }
     __syncthreads();
     // per target group and density, pairs in order, through the permutation:
     // one index per (pair, row) for all densities, four pairs in flight
