@@ -14,7 +14,13 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("M,K,n,gather,perm,add", [
     (296, 296, 1000, False, False, 0), (488, 488, 777, True, False, 1),
     (729, 729, 300, True, True, 0), (37, 729, 513, True, True, 0),
-    (729, 37, 129, False, False, 1), (5, 3, 7, False, False, 0), (64, 488, 1, True, True, 1)])
+    (729, 37, 129, False, False, 1), (5, 3, 7, False, False, 0), (64, 488, 1, True, True, 1),
+    # one column count per tile of gemm_cols' wave model at the translation
+    # shape (dgemm_cols.cuh: 32x32, 64x64, 64x96 with the 4-stage ring,
+    # 64x128 with the 3-stage ring, 128x128), gathered and in place
+    (488, 488, 740, True, False, 0), (488, 488, 1500, True, False, 1), (488, 488, 3001, True, False, 1),
+    (488, 488, 4380, False, False, 0), (488, 488, 8760, True, False, 1), (729, 729, 2200, True, True, 1),
+    (296, 296, 6001, True, False, 0)])
 def test_dgemm_cols_matches_torch(cuda, M, K, n, gather, perm, add):
     torch = cuda
     from paper_2111_10743_b200 import _lib
