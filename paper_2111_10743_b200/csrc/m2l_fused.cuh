@@ -95,6 +95,7 @@ struct Args {
   double* carry;             // multi-pass groups: pool of carry_slots x (kMaxNd * nrep) doubles
   unsigned* carry_flag;      // per slot: 0 free, 1 taken (zero-initialised)
   int carry_slots;
+  int64_t nunits;            // units of this launch (set by launch(); urec holds that many records)
 };
 
 // T's column stride in global memory: whole 4-deep k-steps (32-byte columns)
@@ -289,8 +290,13 @@ __device__ __forceinline__ void gemm_phase(const double* __restrict__ Ap, const 
   }
 }
 
-template <bool RING>
-__global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <= 128 registers
+// One CTA per unit, no A_k ring: the kernel of the expansion sizes whose Y
+// tile leaves no shared memory for a ring at two CTAs per SM (grid
+// representations, nrep >= 729).  Kept beside the persistent kernel below
+// because that one is slower here (10^6 points, eps 1e-9: M2L 66.3 ms with
+// this kernel, 67.5-69.3 ms persistent, with or without cross-unit prefetch).
+__global__ void __launch_bounds__(kThreads, 2) m2l_fused_unit_kernel(Args g) {  // <= 128 registers
+  constexpr bool RING = false;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_poff[kCols];         // perm row offset (offset index x nrep) of the pass's pairs
   __shared__ int4 s_aff[kCols];         // ... or their permutations in closed form
@@ -425,6 +431,183 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
       __threadfence();
       atomicExch(g.carry_flag + s_slot, 0u);
     }
+  }
+}
+
+template <bool RING>  // (instantiated with the ring only; see launch())
+__global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <= 128 registers
+  // Persistent CTAs (two per SM): CTA b runs units b, b + gridDim.x, ... of
+  // the heaviest-first list.  What a freshly launched CTA would wait for at
+  // its start -- the unit record (one L2 round trip) and the first T tile
+  // (another) -- is fetched during the previous unit instead: the next
+  // record by cp.async into shared memory under the product, the next T tile
+  // right after the product's barrier (Ts is free then) under the
+  // accumulation.  Per-unit tables are double-buffered by unit parity, so a
+  // unit's set-up never waits for the previous unit's stragglers.
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_poff[kCols];            // perm row offset (offset index x nrep) of the pass's pairs
+  __shared__ int4 s_aff[kCols];            // ... or their permutations in closed form
+  __shared__ int64_t s_gq[2][kCols + 1];   // first pair of the unit's groups (one-pass units)
+  __shared__ int s_slot[2];                // a multi-pass unit's carry slot
+  __shared__ __align__(16) int64_t s_rec[2][kRec];  // prefetched unit records
+  constexpr int LT = ldt();
+  const int nd = g.nd, nrep = g.nrep;
+  const int LY = ldy(nrep);
+  double* Ys = sm;                          // [column][row], stride LY
+  double* Ts = sm + (size_t)kCols * LY;     // [column][k], stride LT
+  const int tid = threadIdx.x;
+  const int ppp = kCols / nd;  // pairs per pass
+
+  // T columns of a pass (global columns are tstride(r) doubles, zero past r):
+  // 16-byte cp.async copies into Ts[c][k] at stride LT (LT = 4 mod 16 doubles:
+  // conflict-free fragment reads, as in dgemm_cols.cuh); the columns past ncol
+  // of the last N-tile are zeroed.
+  auto issue_T = [&](const double* Tu, int K4, int64_t pa, int64_t pe, int64_t pb) {
+    const int ncol = (int)min((int64_t)ppp, pe - pb) * nd;
+    const int ntn = (ncol + 7) / 8;
+    const int h4 = K4 / 2;  // 16-byte pieces per column
+    const double* Tc = Tu + (pb - pa) * nd * (int64_t)K4;
+    for (int e = tid; e < h4 * ntn * 8; e += kThreads) {
+      const int c = e / h4, k = (e - c * h4) * 2;
+      dg::cp16(Ts + c * LT + k, c < ncol ? Tc + (int64_t)c * K4 + k : g.T, c < ncol ? 16 : 0);
+    }
+    dg::cp_commit();
+  };
+  int64_t u = blockIdx.x;
+  if (u >= g.nunits) return;
+  // the first unit's record straight from global memory, and its T tile's
+  // copies before anything else so that they fly under the CTA's set-up
+  const int64_t* rec = g.urec + kRec * u;
+  issue_T(g.T + __ldg(rec + 2), tstride((int)__ldg(rec + 3)), __ldg(rec + 6), __ldg(rec + 7), __ldg(rec + 6));
+  // lattice index -> expansion index, behind the tiles (and the ring): once per CTA
+  uint16_t* const s_lut = reinterpret_cast<uint16_t*>(Ts + (size_t)kCols * LT + (RING ? kRingDoubles : 0));
+  if (g.aff)
+    for (int e = tid; e < g.lut_n; e += kThreads) s_lut[e] = g.lut[e];
+  for (int par = 0;; par ^= 1) {
+    // (one volatile generic load per field: the record sits in global memory
+    // for a CTA's first unit, in shared memory afterwards, and must not be
+    // re-read once the copy of the next record may be in flight)
+    auto field = [&](int k) -> int64_t {
+      int64_t v;
+      asm volatile("ld.b64 %0, [%1];\n" : "=l"(v) : "l"(rec + k));
+      return v;
+    };
+    const double* const Ap = g.A ? g.A + field(0) : nullptr;
+    const double* const Arow = g.Arow + field(1);
+    const double* const Tu = g.T + field(2);  // the unit's first T column
+    const int r = (int)field(3);
+    const int64_t tg0 = field(4);
+    const int ngrp = (int)field(5);
+    const int64_t pa = field(6), pe = field(7);
+    const bool multi = (pe - pa) > ppp;  // one group in several passes
+    const int K4 = tstride(r);
+    const int64_t un = u + gridDim.x;
+    const bool more = un < g.nunits;
+    // group table (a multi-pass unit has one group); read after the first
+    // pass's barriers
+    for (int e = tid; e <= ngrp && e <= kCols; e += kThreads) s_gq[par][e] = g.tpair[tg0 + e];
+    if (multi && tid == 0) {  // claim a carry slot (the pool outnumbers the resident CTAs)
+      unsigned s = (unsigned)((u * 2654435761ull) % (unsigned)g.carry_slots);
+      while (atomicCAS(g.carry_flag + s, 0u, 1u) != 0u) s = (s + 1) % (unsigned)g.carry_slots;
+      s_slot[par] = (int)s;
+    }
+    double* carry = nullptr;
+
+    for (int64_t pb = pa; pb < pe; pb += ppp) {
+      const int np = (int)min((int64_t)ppp, pe - pb);
+      const int ncol = np * nd;
+      const int ntn = (ncol + 7) / 8;  // N-tiles in use
+      // the pairs' offsets (and their closed-form permutations: a dependent
+      // load) are only needed by the accumulation: loaded here, parked in
+      // registers under the product, stored after it -- the barrier before the
+      // product does not wait for them
+      int pd = 0;
+      int4 paf = make_int4(0, 0, 0, 0);
+      if (tid < np) pd = g.voff[pb + tid];
+      dg::cp_wait<0>();
+      __syncthreads();  // this pass's T has landed; the previous accumulation is done with Ys / s_poff
+      if (pb == pa) {
+        if (multi) carry = g.carry + (size_t)s_slot[par] * kMaxNd * nrep;
+        // the next unit's record, under the product
+        if (more && tid < kRec / 2)
+          dg::cp16(reinterpret_cast<double*>(s_rec[par ^ 1]) + 2 * tid,
+                   reinterpret_cast<const double*>(g.urec + kRec * un) + 2 * tid, 16);
+        dg::cp_commit();
+      }
+      if (tid < np && g.aff) paf = g.aff[pd];
+      if (ntn == 1) gemm_phase<1, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+      else gemm_phase<kNT, RING>(Ap, Arow, r, nrep, Ts, Ys, LY, Ts + (size_t)kCols * LT);
+      if (tid < np) {
+        s_poff[tid] = pd * nrep;
+        if (g.aff) s_aff[tid] = paf;
+      }
+      dg::cp_wait<0>();  // (the record copy; the ring's groups are done)
+      __syncthreads();   // Y complete, Ts free, the next record visible
+      // the next pass's T tile under the accumulation: this unit's next pass,
+      // or the next unit's first
+      if (pb + ppp < pe) {
+        issue_T(Tu, K4, pa, pe, pb + ppp);
+      } else if (more) {
+        const int64_t* const nr = s_rec[par ^ 1];
+        issue_T(g.T + nr[2], tstride((int)nr[3]), nr[6], nr[7], nr[6]);
+      }
+      // per target group and density, pairs in order, through the permutation:
+      // one index per (pair, row) for all densities, four pairs in flight
+      for (int i = tid; i < nrep; i += kThreads) {
+        int ca = 0, cb = 0, cc = 0;
+        if (g.aff) {
+          const uint32_t cw = g.coords[i];
+          ca = cw & 255;
+          cb = (cw >> 8) & 255;
+          cc = cw >> 16;
+        }
+        const int32_t* pi = g.perm + i;
+        auto index = [&](int jp) -> int {  // row of pair jp's Y column this thread adds
+          if (!g.aff) return pi[s_poff[jp]];
+          const int4 af = s_aff[jp];
+          return s_lut[af.x * ca + af.y * cb + af.z * cc + af.w];
+        };
+        for (int e = 0; e < (multi ? 1 : ngrp); ++e) {
+          const int64_t q0 = multi ? pa : s_gq[par][e], q1 = multi ? pe : s_gq[par][e + 1];
+          const int ja = (int)(max(q0, pb) - pb), jb = (int)(min(q1, pb + np) - pb);
+          if (ja >= jb) continue;
+          const bool first = (pb + ja) == q0, last = (pb + jb) == q1;
+          double* const d0 = g.part + (tg0 + e - g.g0) * nd * (int64_t)nrep;
+          double s[kMaxNd];
+#pragma unroll
+          for (int l = 0; l < kMaxNd; ++l) s[l] = (first || l >= nd) ? 0.0 : carry[(size_t)l * nrep + i];
+          for (int jp = ja; jp < jb; jp += 4) {
+            int id[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) id[v] = (jp + v < jb) ? index(jp + v) : 0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (jp + v >= jb) break;
+              const double* y = Ys + (size_t)((jp + v) * nd) * LY + id[v];
+#pragma unroll
+              for (int l = 0; l < kMaxNd; ++l)
+                if (l < nd) s[l] += y[(size_t)l * LY];
+            }
+          }
+#pragma unroll
+          for (int l = 0; l < kMaxNd; ++l) {
+            if (l >= nd) break;
+            if (last) d0[(int64_t)l * nrep + i] = s[l];
+            else carry[(size_t)l * nrep + i] = s[l];
+          }
+        }
+      }
+    }
+    if (multi) {  // hand the carry slot back
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicExch(g.carry_flag + s_slot[par], 0u);
+      }
+    }
+    if (!more) break;
+    u = un;
+    rec = s_rec[par ^ 1];
   }
 }
 
@@ -587,13 +770,25 @@ inline cudaError_t launch(const Args& a, int64_t nunits, int rmax, cudaStream_t 
   if (need > attr[ring]) {
     const cudaError_t e = ring ? cudaFuncSetAttribute(m2l_fused_kernel<true>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, need)
-                               : cudaFuncSetAttribute(m2l_fused_kernel<false>,
+                               : cudaFuncSetAttribute(m2l_fused_unit_kernel,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, need);
     if (e != cudaSuccess) return e;
     attr[ring] = need;
   }
-  if (ring) m2l_fused_kernel<true><<<(unsigned)nunits, kThreads, need, st>>>(a);
-  else m2l_fused_kernel<false><<<(unsigned)nunits, kThreads, need, st>>>(a);
+  // ring variant: persistent CTAs, two per SM (what the tile is sized for),
+  // striding the heaviest-first unit list (config 3 M2L 1.48 -> 1.43 ms per
+  // pot+grad call, 10^6 points at eps 1e-6 10.6 -> 10.2 ms); the no-ring
+  // variant keeps one CTA per unit (see m2l_fused_unit_kernel)
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  Args b = a;
+  b.nunits = nunits;
+  if (ring) m2l_fused_kernel<true><<<(unsigned)std::min<int64_t>(nunits, 2 * (int64_t)sms), kThreads, need, st>>>(b);
+  else m2l_fused_unit_kernel<<<(unsigned)nunits, kThreads, need, st>>>(b);
   return cudaGetLastError();
 }
 
