@@ -363,6 +363,29 @@ def count_sharded_launches(torch, op, mgs, lib, _lib):
     return total
 
 
+def read_rows_gbs(torch, _lib, nrows, rowlen):
+    """Best of 5 runs of lb_probe_read_rows (two streams of nrows x rowlen
+    doubles, L2 flushed before each run), GB/s."""
+    lib = _lib.load()
+    nrows = int(min(nrows, (3 << 30) // (8 * rowlen)))  # <= 3 GB per stream
+    a = torch.ones(nrows * rowlen, dtype=torch.float64, device="cuda")
+    b = torch.ones(nrows * rowlen, dtype=torch.float64, device="cuda")
+    out = torch.empty(nrows, dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    best = None
+    for _ in range(5):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.lb_probe_read_rows(_lib.ptr(a), _lib.ptr(b), nrows, rowlen, _lib.ptr(out),
+                                          _lib.stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return 2.0 * nrows * rowlen * 8 / best / 1e6
+
+
 def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib, peak_tc=None):
     """Per-stage device times of one apply (lb_opset stage events) and of one
     pot+grad FMM call (lb_fmm stage events) with their rooflines: SpMV passes
@@ -378,20 +401,29 @@ def stage_rooflines(torch, op, plan, n, nover, nnz, peak_tf, hbm_gbs, _lib, peak
     op.dev.set_timing(False)
     # SURVEY §8(d) accounting: 8 B per value and kind + 4 B column index per
     # nnz + 8 B per row offset (+ x gathers in L2); the kernels read the
-    # block-CSR index instead (4 / nb B per nnz), reported as actual_bytes
+    # block-CSR index instead (4 / nb B per nnz): the bytes reported
     nb = int(op.disc.nodes_per_patch) if hasattr(op.disc, "nodes_per_patch") else 28
     b1 = nnz * (2 * 8 + 4) + 8 * (n + 1)
     b2 = nnz * (3 * 8 + 4) + 8 * (n + 1)
     a1 = nnz * (2 * 8 + 4.0 / nb) + 8 * (n + 1)
     a2 = nnz * (3 * 8 + 4.0 / nb) + 8 * (n + 1)
+    # pure two-stream read in the SpMV's row shape (lb_probe_read_rows): the
+    # read-only ceiling beside MEASURED_PEAKS.json's copy bandwidth
+    read_gbs = read_rows_gbs(torch, _lib, n, max(nnz // max(n, 1), 1))
+
+    def spmv(ms, actual, formula):
+        # the kernels move the block-CSR bytes (ncu: 5.24 GB DRAM read for pass
+        # 1 at config 3); the SURVEY formula charges a 4-byte
+        # column index per nnz that they do not read, so its GB/s is a derived
+        # figure that can exceed the copy bandwidth
+        return {"ms": ms, "bytes": actual, "GBps": actual / ms / 1e6,
+                "frac_hbm": actual / ms / 1e6 / hbm_gbs,
+                "frac_of_read_ceiling": actual / ms / 1e6 / read_gbs if read_gbs else None,
+                "survey_formula_bytes": formula, "survey_formula_GBps": formula / ms / 1e6}
     stages = {
         "fmm_call1_ms": st[0], "fmm_call2_ms": st[2],
-        "spmv1": {"ms": st[1], "bytes": b1, "GBps": b1 / st[1] / 1e6,
-                  "frac_hbm": b1 / st[1] / 1e6 / hbm_gbs, "actual_bytes": a1,
-                  "actual_frac_hbm": a1 / st[1] / 1e6 / hbm_gbs},
-        "spmv2_glue": {"ms": st[3], "bytes": b2, "GBps": b2 / st[3] / 1e6,
-                       "frac_hbm": b2 / st[3] / 1e6 / hbm_gbs, "actual_bytes": a2,
-                       "actual_frac_hbm": a2 / st[3] / 1e6 / hbm_gbs},
+        "spmv1": spmv(st[1], a1, b1), "spmv2_glue": spmv(st[3], a2, b2),
+        "hbm_read_ceiling_GBps": read_gbs,
         "apply_ms": st[7]}
     # one charge pot+grad call of the plan (the metric's unit), stage split
     w = torch.from_numpy(np.random.default_rng(3).standard_normal((1, nover))).cuda()
@@ -543,7 +575,9 @@ def main():
             s2 = stages["spmv2_glue"]
             roofline = {"bound": "hbm", "kernel": "csr_epi_kernel (A3 pass 2: 3 kinds + glue)",
                         "achieved": s2["GBps"], "peak": hbm, "unit": "GB/s",
-                        "frac": s2["frac_hbm"], "traffic": None,
+                        "frac": s2["frac_hbm"], "traffic": s2["bytes"],
+                        "traffic_note": "block-CSR bytes the kernel reads (= ncu dram__bytes_read, "
+                                        "profiles/round2/config3_step_launches.md)",
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
         elif dom == "m2l":
             s = f["m2l"]

@@ -454,6 +454,11 @@ int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, voi
  * of 8 DMMAs), the others DFMA chains (it_fma iterations of 128 DFMAs per
  * thread): do the FP64 tensor cores and the FP64 FMA pipe overlap? */
 int lb_probe_mixed(double* scratch, int blocks, int it_mma, int it_fma, int nw_mma, void* stream);
+/* HBM read ceiling in the correction SpMV's access shape: one warp per row of
+ * rowlen doubles in each of two streams (a, b: nrows * rowlen doubles each),
+ * 256-byte warp loads, eight in flight per stream; out[row] = the row's sum. */
+int lb_probe_read_rows(const double* a, const double* b, int64_t nrows, int64_t rowlen, double* out,
+                       void* stream);
 int lb_probe_rsqrt(const double* x, double* y, int64_t n, int mode,
                    void* stream);
 

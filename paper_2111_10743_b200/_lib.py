@@ -88,6 +88,7 @@ SIGNATURES = {
     "lb_probe_dmma": [_P, _I32, _I32, _P],
     "lb_probe_dmma_operands": [_P, _I32, _I32, _I32, _P],
     "lb_probe_mixed": [_P, _I32, _I32, _I32, _I32, _P],
+    "lb_probe_read_rows": [_P, _P, _I64, _I64, _P, _P],
     "lb_dgemm_cols": [_P, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
                       ctypes.c_double, _I32, _P],
     "lb_probe_rsqrt": [_P, _P, _I64, _I32, _P],

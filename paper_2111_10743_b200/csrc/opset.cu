@@ -317,8 +317,17 @@ struct EpiA1p2 : EpiBase {
 // picked from the mean row length so every warp has ~4 chunks of 32 nnz in
 // flight: the row loop is latency-bound otherwise).  Segment warps of a row
 // combine their partial sums in a fixed order through shared memory.
+// Three CTAs per SM by launch bounds (<= 85 registers).  Left to itself ptxas
+// builds the row loop in 48 registers by interleaving the value loads with
+// the FMAs that consume them, so an in-order warp has ~6 of its 16-24 loads
+// in flight; with the larger budget it issues a whole unrolled iteration's
+// loads first.  Config 3 (B200): pass 1 1.027 -> 0.947 ms, pass 2 1.439 ->
+// 1.271 ms (5.5 / 6.1 TB/s of actual bytes; a pure two-stream read in the
+// same row shape, lb_probe_read_rows, runs at 6.9).  Two CTAs per SM (96
+// registers) lose it again (1.047 / 1.330), four (64) match three.
+constexpr int kCsrMinBlocks = 3;
 template <int J, class E, class Mix = MixId<J>>
-__global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restrict__ indptr,
+__global__ void __launch_bounds__(kCsrBT, kCsrMinBlocks) csr_epi_kernel(const int64_t* __restrict__ indptr,
                                                          const int32_t* __restrict__ indices,
                                                          const int32_t* __restrict__ bstart, int bnb,
                                                          int64_t grow0, int64_t nrows, int wpr,
@@ -385,11 +394,11 @@ __global__ void __launch_bounds__(kCsrBT) csr_epi_kernel(const int64_t* __restri
       return __ldg(bstart + bbase + q) + (int)(rel - q * (unsigned)bnb);
     };
     // loads in flight per lane: the value streams are the kernel's HBM
-    // traffic; with two streams (A3 pass 1) four entries per lane left DRAM at
-    // 63% (ncu, profiles/round2), so fewer streams unroll deeper
-    // (B200, config 3: two streams 4 / 6 / 8 / 12 entries -> 1.30 / 1.10 / 1.03 /
-    // 1.23 ms; three streams 1 / 2 / 3 / 4 / 8 -> 1.54 / 1.44 / 1.47 / 1.59 / 1.62 ms)
-    constexpr int UR = K >= 3 ? 2 : 8;
+    // traffic, and fewer streams unroll deeper.  B200, config 3, with the
+    // launch bounds above: two streams 6 / 8 / 10 / 12 / 16 entries -> 1.10 /
+    // 0.947 / 0.981 / 1.07 / 1.35 ms; three streams 2 / 3 / 4 / 5 / 6 / 8 ->
+    // 1.32 / 1.33 / 1.27 / 1.55 / 1.31 / 1.38 ms
+    constexpr int UR = K >= 3 ? 4 : 8;
     for (; k + (UR - 1) * stride < ke; k += UR * stride) {
       int c[UR];
 #pragma unroll

@@ -98,6 +98,43 @@ __global__ void __launch_bounds__(256) mixed_peak_kernel(double* out, int it_mma
   if (s == 12345.678) out[blockIdx.x] = s;
 }
 
+// HBM read ceiling for the correction SpMV's access shape: one warp per
+// "row" of rowlen doubles in each of two streams, 256-byte warp loads, eight
+// in flight per stream and lane, rows dealt to 8-warp blocks as csr_epi_kernel
+// deals them; no index, no gather, no epilogue
+__global__ void __launch_bounds__(256) read_rows_kernel(const double* __restrict__ a,
+                                                         const double* __restrict__ b, int64_t nrows,
+                                                         int64_t rowlen, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  if (row >= nrows) return;
+  const int64_t kb = row * rowlen, ke = kb + rowlen;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t k = kb + lane;
+  for (; k + 7 * 32 < ke; k += 8 * 32) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) va[u] = __ldg(a + k + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vb[u] = __ldg(b + k + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s0 += va[u];
+      s1 += vb[u];
+    }
+  }
+  for (; k < ke; k += 32) {
+    s0 += __ldg(a + k);
+    s1 += __ldg(b + k);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if (lane == 0) out[row] = s0 + s1;
+}
+
 __global__ void rsqrt_seed_kernel(const double* x, double* y, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = rsqrt_seed(x[i]);
@@ -139,6 +176,15 @@ int lb_probe_dmma_operands(double* scratch, int blocks, int iters, int mode, voi
 int lb_probe_mixed(double* scratch, int blocks, int it_mma, int it_fma, int nw_mma, void* stream) {
   lb::mixed_peak_kernel<<<blocks, 256, 0, lb::as_stream(stream)>>>(scratch, it_mma, it_fma, nw_mma,
                                                                     0.999999, 1e-7);
+  LB_CHECK_LAUNCH();
+  return LB_OK;
+}
+
+// bytes read = 2 * nrows * rowlen * 8
+int lb_probe_read_rows(const double* a, const double* b, int64_t nrows, int64_t rowlen, double* out,
+                       void* stream) {
+  if (nrows <= 0) return LB_OK;
+  lb::read_rows_kernel<<<(unsigned)lb::ceil_div(nrows, 8), 256, 0, lb::as_stream(stream)>>>(a, b, nrows, rowlen, out);
   LB_CHECK_LAUNCH();
   return LB_OK;
 }
