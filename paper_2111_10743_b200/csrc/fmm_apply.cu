@@ -88,13 +88,17 @@ __global__ void gather_sources_kernel(const double* __restrict__ charges,
 // and barriers of a one-point-per-thread pass.
 constexpr int kLatBT = 128;
 
-template <int ND, int kLatLPT>
+// DM: compile-time mask of the chunk's densities that carry dipoles (the A3
+// projected call has them on its first density only: the second skips the
+// dipole dot product instead of multiplying zeros -- the sums are the same
+// bit for bit, fma(0, x, acc) = acc)
+template <int ND, int kLatLPT, unsigned DM>
 __global__ void __launch_bounds__(kLatBT) lattice_pot_kernel(
     const int64_t* __restrict__ boxes, const int64_t* __restrict__ src_off,
     const int64_t* __restrict__ src_boxes, int single, const double* __restrict__ bctr,
     const double* __restrict__ bhalf, const int64_t* __restrict__ bsrc,
     const double* __restrict__ spos, const double* __restrict__ cs, const double* __restrict__ vs,
-    int64_t ns, int hd, const double* __restrict__ pts, int nrep, double fac, int scale_by_h,
+    int64_t ns, int dm, const double* __restrict__ pts, int nrep, double fac, int scale_by_h,
     double* __restrict__ out, int out_by_box, int add) {
   constexpr int TS = 64;
   constexpr int W = 3 + 4 * ND;
@@ -132,39 +136,31 @@ __global__ void __launch_bounds__(kLatBT) lattice_pot_kernel(
 #pragma unroll
           for (int l = 0; l < ND; ++l) {
             r[3 + l] = cs[(int64_t)l * ns + j];
-            const bool on = hd != 0;
-            r[3 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3] : 0.0;
-            r[4 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3 + 1] : 0.0;
-            r[5 + ND + 3 * l] = on ? vs[((int64_t)l * ns + j) * 3 + 2] : 0.0;
+            if ((DM >> l) & 1u) {
+              r[3 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3];
+              r[4 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 1];
+              r[5 + ND + 3 * l] = vs[((int64_t)l * ns + j) * 3 + 2];
+            }
           }
         }
         __syncthreads();
-        if (hd) {
-          for (int k = 0; k < n; ++k) {
-            const double* r = sh + k * W;
+        for (int k = 0; k < n; ++k) {
+          const double* r = sh + k * W;
 #pragma unroll
-            for (int j = 0; j < kLatLPT; ++j) {
-              const double r0 = px[j] - r[0], r1 = py[j] - r[1], r2 = pz[j] - r[2];
-              const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
-              const double invr = inv_sqrt_skip(rr);
-              const double invr3 = invr * invr * invr;
+          for (int j = 0; j < kLatLPT; ++j) {
+            const double r0 = px[j] - r[0], r1 = py[j] - r[1], r2 = pz[j] - r[2];
+            const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+            const double invr = inv_sqrt_skip(rr);
+            double invr3 = 0.0;
+            if constexpr (DM != 0u) invr3 = invr * invr * invr;
 #pragma unroll
-              for (int l = 0; l < ND; ++l) {
+            for (int l = 0; l < ND; ++l) {
+              if ((DM >> l) & 1u) {
                 const double vr = fma(r[5 + ND + 3 * l], r2, fma(r[4 + ND + 3 * l], r1, r[3 + ND + 3 * l] * r0));
                 acc[j][l] = fma(r[3 + l], invr, fma(vr, invr3, acc[j][l]));
+              } else {
+                acc[j][l] = fma(r[3 + l], invr, acc[j][l]);
               }
-            }
-          }
-        } else {
-          for (int k = 0; k < n; ++k) {
-            const double* r = sh + k * W;
-#pragma unroll
-            for (int j = 0; j < kLatLPT; ++j) {
-              const double r0 = px[j] - r[0], r1 = py[j] - r[1], r2 = pz[j] - r[2];
-              const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
-              const double invr = inv_sqrt_skip(rr);
-#pragma unroll
-              for (int l = 0; l < ND; ++l) acc[j][l] = fma(r[3 + l], invr, acc[j][l]);
             }
           }
         }
@@ -187,20 +183,36 @@ __global__ void __launch_bounds__(kLatBT) lattice_pot_kernel(
 }
 
 // lattice points per thread sized to the lattice (296 surface points: 3;
-// 488: 4; 729 grid points: 6; larger lattices loop)
-template <int ND, class... A>
-int launch_lattice(unsigned grid, cudaStream_t st, const int64_t* boxes, A... a) {
-  if (grid == 0) return LB_OK;
+// 488: 4; 729 grid points: 6; larger lattices loop); dipole mask exact for
+// one or two densities, all-or-none for more
+template <int ND, unsigned DM, class... A>
+int launch_lattice_dm(unsigned grid, cudaStream_t st, const int64_t* boxes, A... a) {
   // nrep is argument 12 after boxes (see lattice_pot_kernel's parameter list)
   const int nrep = std::get<12>(std::make_tuple(a...));
   static_assert(std::is_same<typename std::tuple_element<12, std::tuple<A...>>::type, int>::value,
                 "launch_lattice: argument 12 must be nrep");
-  if (nrep <= 2 * kLatBT) lattice_pot_kernel<ND, 2><<<grid, kLatBT, 0, st>>>(boxes, a...);
-  else if (nrep <= 3 * kLatBT) lattice_pot_kernel<ND, 3><<<grid, kLatBT, 0, st>>>(boxes, a...);
-  else if (nrep <= 4 * kLatBT) lattice_pot_kernel<ND, 4><<<grid, kLatBT, 0, st>>>(boxes, a...);
-  else lattice_pot_kernel<ND, 6><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  if (nrep <= 2 * kLatBT) lattice_pot_kernel<ND, 2, DM><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else if (nrep <= 3 * kLatBT) lattice_pot_kernel<ND, 3, DM><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else if (nrep <= 4 * kLatBT) lattice_pot_kernel<ND, 4, DM><<<grid, kLatBT, 0, st>>>(boxes, a...);
+  else lattice_pot_kernel<ND, 6, DM><<<grid, kLatBT, 0, st>>>(boxes, a...);
   LB_CHECK_LAUNCH();
   return LB_OK;
+}
+
+template <int ND, class... A>
+int launch_lattice(unsigned grid, cudaStream_t st, const int64_t* boxes, A... a) {
+  if (grid == 0) return LB_OK;
+  // the dipole mask of the chunk's densities is argument 10 after boxes
+  static_assert(std::is_same<typename std::tuple_element<10, std::tuple<A...>>::type, int>::value,
+                "launch_lattice: argument 10 must be the dipole mask");
+  const unsigned dm = (unsigned)std::get<10>(std::make_tuple(a...)) & ((1u << ND) - 1u);
+  constexpr unsigned ALL = (1u << ND) - 1u;
+  if (dm == 0u) return launch_lattice_dm<ND, 0u>(grid, st, boxes, a...);
+  if constexpr (ND == 2) {
+    if (dm == 1u) return launch_lattice_dm<ND, 1u>(grid, st, boxes, a...);
+    if (dm == 2u) return launch_lattice_dm<ND, 2u>(grid, st, boxes, a...);
+  }
+  return launch_lattice_dm<ND, ALL>(grid, st, boxes, a...);
 }
 
 // ---------------------------------------------------------------------------
@@ -1964,7 +1976,8 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   const int64_t nb = t.nbox();
   const bool surface = P->rep == 0;
   const int n = P->m;
-  const bool hd = ((dmask >> d0) & ((1u << ND) - 1u)) != 0;
+  const unsigned dm_chunk = (dmask >> d0) & ((1u << ND) - 1u);  // the chunk's densities with dipoles
+  const bool hd = dm_chunk != 0;
   auto mark = [&](int i) { if (!ev.empty()) cudaEventRecord(ev[i], st); };
   mark(0);
   // gather into sorted source order
@@ -1989,7 +2002,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   if (D.n_p2m > 0) {
     if (surface) {
       LB_TRY(launch_lattice<ND>((unsigned)D.n_p2m, st, D.p2m_leaves, nullptr, nullptr, 1, D.bctr, D.bhalf,
-                                D.bsrc, D.spos, p2m_cs, p2m_vs, t.ns, hd ? 1 : 0, D.pts, nrep, P->uc_scale, 1,
+                                D.bsrc, D.spos, p2m_cs, p2m_vs, t.ns, (int)dm_chunk, D.pts, nrep, P->uc_scale, 1,
                                 D.tmpA, 0, 0));
       // upward[b] = pinv_up @ (h phi) straight into the leaves' slots (fmm.py:852)
       dg::Args a{};
@@ -2137,7 +2150,7 @@ int apply_chunk(lb_fmm_plan* P, int d0, uint32_t cmask, uint32_t dmask, const do
   // ---- X list (fmm.py:888-911)
   if (D.n_x > 0) {
     LB_TRY(launch_lattice<ND>((unsigned)D.n_x, st, D.x_boxes, D.x_off, D.x_leaves, 0, D.bctr, D.bhalf, D.bsrc,
-                              D.spos, D.cs, D.vs, t.ns, hd ? 1 : 0, D.pts, nrep,
+                              D.spos, D.cs, D.vs, t.ns, (int)dm_chunk, D.pts, nrep,
                               surface ? P->dc_scale : 1.0, 0, D.dc, 1, 1));
   }
   mark(4);
