@@ -503,6 +503,21 @@ __global__ void __launch_bounds__(kThreads, 2) m2l_fused_kernel(Args g) {  // <=
     const int K4 = tstride(r);
     const int64_t un = u + gridDim.x;
     const bool more = un < g.nunits;
+    if (pa >= pe) {  // a unit without pairs (the host builds none): only hand over to the next one
+      if (!more) break;
+      __syncthreads();  // everyone is done with the previous unit's tables and record
+      if (tid < kRec / 2)
+        dg::cp16(reinterpret_cast<double*>(s_rec[par ^ 1]) + 2 * tid,
+                 reinterpret_cast<const double*>(g.urec + kRec * un) + 2 * tid, 16);
+      dg::cp_commit();
+      dg::cp_wait<0>();
+      __syncthreads();
+      const int64_t* const nr = s_rec[par ^ 1];
+      issue_T(g.T + nr[2], tstride((int)nr[3]), nr[6], nr[7], nr[6]);
+      u = un;
+      rec = s_rec[par ^ 1];
+      continue;
+    }
     // group table (a multi-pass unit has one group); read after the first
     // pass's barriers
     for (int e = tid; e <= ngrp && e <= kCols; e += kThreads) s_gq[par][e] = g.tpair[tg0 + e];
